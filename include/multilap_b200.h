@@ -1,0 +1,168 @@
+/*
+ * multilap_b200.h -- C ABI of libmlb.so, the B200 (sm_100a) NFFT
+ * normalized-Laplacian matvec path of arXiv 2007.05239 ("multilap").
+ *
+ * The reference (/root/reference/pkg/src/multilap, pure Python) has no FFI;
+ * its seam is Python duck typing.  Every entry point
+ * below replaces one reference function, cited as file:line; the Python
+ * package paper_2007_05239_b200 binds them with ctypes (INTEGRATION.md shows
+ * the binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *   - Return 0 (MLB_OK) on success, otherwise an MLB_ERR_* code; the message
+ *     is in mlb_last_error() (thread-local).  MLB_ERR_CONFIG maps to the
+ *     reference's ConfigError, MLB_ERR_NUMERICAL to NumericalError.
+ *   - All vectors are fp64.  "dev" pointers are CUDA device pointers, "host"
+ *     pointers are CPU memory.  Inputs are never written.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - Handles own their device buffers until *_destroy.  A binding may be
+ *     used from one stream at a time; plans are read-only and shareable.
+ *   - No torch types: plain pointers, sizes and C structs only.
+ */
+#ifndef MULTILAP_B200_H
+#define MULTILAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLB_ABI_VERSION 1
+
+#define MLB_OK 0
+#define MLB_ERR_CONFIG 1      /* reference ConfigError    (errors.py:11-12) */
+#define MLB_ERR_NUMERICAL 2   /* reference NumericalError (errors.py:19-21) */
+#define MLB_ERR_CUDA 3        /* CUDA runtime failure */
+#define MLB_ERR_ARG 4         /* NULL handle / bad size */
+
+/* flags for mlb_apply */
+#define MLB_USE_ISD 1u        /* s = D^-1/2 (set by mlb_binding_set_isd), else s = 1 */
+#define MLB_ACCUMULATE 2u     /* y += result instead of y = result */
+#define MLB_SORTED 4u         /* v and y are in the binding's sorted (cell) order */
+
+typedef struct mlb_plan mlb_plan;
+typedef struct mlb_binding mlb_binding;
+
+/* Plan description: the host computes the plan math (fastsum.py:256-313)
+ * and passes the device-facing tables.  Layouts:
+ *   fused_band : (K,)*(d-1) x Kh real, K = N+1 (k = -N/2..N/2), Kh = N/2+1
+ *                (k = 0..N/2 on the last axis); the reference's
+ *                fused_weights / ng^d restricted to the band |k| <= N/2.
+ *   twiddle    : L x K complex (re,im interleaved): exp(-2 pi i k u / ng)
+ *                for the active cells u = u_lo..u_lo+L-1, k = -N/2..N/2.
+ *   win_coef   : (2m+1) x (win_deg+1): monomial coefficients in s = 2f-1 of
+ *                phi(f - o), o = -m..m, f in [0,1) (the Kaiser-Bessel window
+ *                of fastsum.py:158-167 as an exact-to-1e-14 polynomial).   */
+typedef struct mlb_plan_desc {
+    int d, N, m, ng;
+    int bin_lo, bin_hi;       /* admissible floor(ng*x) range per axis */
+    int win_deg;
+    double K0;                /* kernel value at 0 (kernels.py:38-39) */
+    const double* fused_band; /* host */
+    const double* twiddle;    /* host */
+    const double* win_coef;   /* host */
+} mlb_plan_desc;
+
+int mlb_abi_version(void);
+const char* mlb_last_error(void);
+int mlb_device_count(void);
+
+/* build_plan (fastsum.py:256-313): upload plan tables to `device`. */
+int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out);
+int mlb_plan_destroy(mlb_plan* plan);
+
+/* bind_points / _make_binding (fastsum.py:333-386): bin the n points
+ * (row-major n x d box coordinates, host memory) by cell floor(ng*x*scale)
+ * with `scale` = 1/sqrt(d) (1 for the bare torus transforms), counting-sort
+ * them by (brick, cell), build the chunk/segment tables and upload.  The box
+ * check is the caller's (validate_box, fastsum.py:66-80).  `node_ids_host`
+ * (nullable) maps point i to its node index in the vectors passed to
+ * mlb_apply -- one binding per component block (graphs.py:99-129). */
+int mlb_bind(const mlb_plan* plan, const double* points_host, int64_t n, double scale,
+             const int32_t* node_ids_host, mlb_binding** out);
+int mlb_binding_destroy(mlb_binding* b);
+int64_t mlb_binding_n(const mlb_binding* b);
+/* sorted position -> original node index (int32, host out, n entries) */
+int mlb_binding_perm(const mlb_binding* b, int32_t* perm_host);
+/* binding statistics: [n, nchunks, nsegments, nbricks, tile_cells, grid_cells] */
+int mlb_binding_stats(const mlb_binding* b, int64_t* out6);
+
+/* Store D^-1/2 (graphs.py:159-165) for the fused Laplacian; node order, device. */
+int mlb_binding_set_isd(mlb_binding* b, const double* isd_dev, void* stream);
+
+/* The hot path.  With s = isd (MLB_USE_ISD) or 1 and acc = W~(s.v) -- the
+ * spread / rFFT * fused / irFFT / gather chain of fastsum_apply
+ * (fastsum.py:475-497) without the diagonal removal:
+ *     y (=|+=) alpha*v + s.(beta*acc + gamma*s.v)
+ *   W v              (fastsum_apply, fastsum.py:475-497):   1, 0, alpha=-K0, beta=1, gamma=0
+ *   L_sym+delta v    (apply_sym_laplacian, graphs.py:197-201): USE_ISD, 1+delta, -1, K0
+ *   D^-1/2 W D^-1/2 v (apply_one_minus_L1 term, powermean.py:75-76): USE_ISD, 0, 1, -K0
+ * v, y: device, node order (or sorted order with MLB_SORTED). */
+int mlb_apply(mlb_binding* b, const double* v_dev, double* y_dev, double alpha, double beta,
+              double gamma, unsigned flags, void* stream);
+
+/* Test hooks on the three stages (sub-box grid of L^d cells, row-major):
+ * spread (fastsum.py:389-391), convolution rfftn*fused*irfftn
+ * (fastsum.py:492-495), gather (fastsum.py:400-406). */
+int mlb_grid_cells(const mlb_binding* b, int64_t* cells, int* L, int* u_lo);
+int mlb_spread(mlb_binding* b, const double* v_dev, double* grid_dev, unsigned flags, void* stream);
+int mlb_convolve(mlb_binding* b, const double* grid_in_dev, double* grid_out_dev, void* stream);
+int mlb_gather(mlb_binding* b, const double* grid_dev, double* y_dev, unsigned flags, void* stream);
+
+/* Permutations between node order and the binding's sorted order. */
+int mlb_to_sorted(const mlb_binding* b, const double* v_node_dev, double* v_sorted_dev, void* stream);
+int mlb_to_node(const mlb_binding* b, const double* v_sorted_dev, double* v_node_dev, int accumulate,
+                void* stream);
+
+/* ---- Krylov kernels (krylov.py:65-71, :172-216) -------------------------
+ * V is column-major n x ldcols (column j at V + j*ld).  Deterministic
+ * fixed-order reductions; `work` is device scratch of mlb_krylov_work_size. */
+int64_t mlb_krylov_work_size(int64_t n, int maxcols);
+/* h[0..cols) = V[:, :cols]^T w (device out) */
+int mlb_gemv_t(const double* V, int64_t ld, int64_t n, int cols, const double* w, double* h,
+               double* work, void* stream);
+/* two-pass classical Gram-Schmidt of w against V[:, :cols] (krylov.py:65-71):
+ * h_out = h1+h2 (device, cols), h1_out = first-pass projections (device,
+ * cols, nullable; h1[cols-1] is the Lanczos alpha of krylov.py:198),
+ * nrm2_out = ||w||^2 after (device, 1, nullable) */
+int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out,
+             double* h1_out, double* nrm2_out, double* work, void* stream);
+/* y = V[:, :cols] c  (c device) ; out may alias nothing */
+int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c, double* y,
+               double scale, int accumulate, void* stream);
+/* Out[:, :k] = V[:, :s] S[:s, :k]  (S column-major s x k, device); Out must not alias V */
+int mlb_gemm_vs(const double* V, int64_t ld, int64_t n, int s, const double* S, int k, double* Out,
+                int64_t ldo, void* stream);
+/* dot products / norms (device scalar out) */
+int mlb_dot(const double* x, const double* y, int64_t n, double* out, double* work, void* stream);
+/* y = a*x + b*y */
+int mlb_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream);
+/* y = x * scale_dev[0]^pow  (pow = -0.5 -> normalise by sqrt of a norm^2) */
+int mlb_scale_by(const double* x, double* y, int64_t n, const double* s_dev, double pw, void* stream);
+
+/* z = x .* y */
+int mlb_hadamard(const double* x, const double* y, double* z, int64_t n, void* stream);
+
+/* Exact dense kernel sums (direct_apply, fastsum.py:500-553) with the same
+ * epilogue as mlb_apply: y (=|+=) alpha v + s.(beta sum_j K(x_i-x_j) s_j v_j
+ * + gamma s.v), the sum INCLUDING j = i.  X: n x d row-major (device);
+ * family 0 = gaussian, 1 = laplacian; s nullable (= 1). */
+int mlb_direct(const double* X, int64_t n, int d, int family, double sigma, const double* v, const double* s,
+               double* y, double alpha, double beta, double gamma, int accumulate, void* stream);
+
+/* ---- Allen-Cahn (allencahn.py:172-223) ----------------------------------
+ * Phi: n x k row-major, U/F: n x m row-major, fid: n.  One iteration:
+ *   R = (1+c dt) U - dt/(2 eps) T(U) - dt fid (U-F);  Vc = Phi^T R / denom;
+ *   U_next = proj_simplex(Phi Vc);  stats = [max_i |dU_i|^2, max_i |U_next_i|^2]. */
+int64_t mlb_ac_work_size(int64_t n, int k, int m);
+int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, const double* F,
+                const double* fid, const double* denom, double c_dt, double dt_2eps, double dt,
+                double* U_next, double* stats, double* work, void* stream);
+/* argmax per row, ties to the lowest class (allencahn.py:226-229) */
+int mlb_argmax_rows(const double* U, int64_t n, int m, int32_t* labels, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MULTILAP_B200_H */

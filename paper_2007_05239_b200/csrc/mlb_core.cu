@@ -1,0 +1,414 @@
+// libmlb.so C ABI: errors, plans, bindings (host counting sort), apply.
+//
+// bind_points / _make_binding (fastsum.py:333-386) on the reference build the
+// full (2m+1)^d tensor product of flat indices and weights per point (16 C
+// bytes per point) and stable-argsort it.  Here the binding is geometry only:
+// per point the fractional offsets f = ng*x - floor(ng*x) (8d bytes), the
+// permutation to cell order, and chunk/segment tables; window weights are
+// recomputed by the kernels on every apply.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mlb_internal.cuh"
+
+namespace mlb {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+// Restores the caller's current device (torch keeps its own notion of it).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+static int dev_upload(T** dst, const T* src, size_t count) {
+    if (count == 0) count = 1;
+    MLB_CUDA_TRY(cudaMalloc((void**)dst, count * sizeof(T)));
+    if (src) MLB_CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return MLB_OK;
+}
+
+template <typename T>
+static void dev_free(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+static int ipow_h(int b, int e) {
+    int r = 1;
+    for (int i = 0; i < e; ++i) r *= b;
+    return r;
+}
+
+}  // namespace mlb
+
+using namespace mlb;
+
+extern "C" {
+
+int mlb_abi_version(void) { return MLB_ABI_VERSION; }
+
+const char* mlb_last_error(void) { return g_err.c_str(); }
+
+int mlb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
+    if (!desc || !out) return fail(MLB_ERR_ARG, "null argument");
+    const int d = desc->d, N = desc->N, m = desc->m, ng = desc->ng;
+    if (d < 1 || d > 3) return fail(MLB_ERR_CONFIG, "fastsum supports d in {1, 2, 3}");
+    if (N < 4 || N % 2) return fail(MLB_ERR_CONFIG, "N must be even and >= 4");
+    if (m < 2 || m > kMaxM)
+        return fail(MLB_ERR_CONFIG, "m_nfft must lie in [2, " + std::to_string(kMaxM) + "] on the GPU path");
+    if (ng < N + 2 || ng % 2) return fail(MLB_ERR_CONFIG, "invalid oversampled grid size");
+    if (desc->bin_hi < desc->bin_lo) return fail(MLB_ERR_CONFIG, "empty bin range");
+    const int want_deg = (m <= 3) ? 16 : 14;
+    if (desc->win_deg != want_deg)
+        return fail(MLB_ERR_CONFIG, "window polynomial degree must be " + std::to_string(want_deg));
+    DeviceGuard guard(device);
+    mlb_plan* p = new mlb_plan();
+    p->device = device;
+    Geom& g = p->g;
+    g.d = d;
+    g.N = N;
+    g.m = m;
+    g.ng = ng;
+    g.S = 2 * m + 1;
+    g.nb = desc->bin_hi - desc->bin_lo + 1;
+    g.L = g.nb + 2 * m;
+    g.ulo = desc->bin_lo - m;
+    g.K = N + 1;
+    g.Kh = N / 2 + 1;
+    g.K0 = desc->K0;
+    if (d <= 2) {
+        g.Tb = g.nb;  // the whole sub-box is one brick
+    } else {
+        g.Tb = (m >= 6) ? 2 : 4;
+        if (g.Tb > g.nb) g.Tb = g.nb;
+    }
+    g.TL = g.Tb + 2 * m;
+    g.nbr = (g.nb + g.Tb - 1) / g.Tb;
+    // window coefficients: split P_q (q=1..m) into even/odd parts in s
+    const int nc = desc->win_deg + 1;
+    p->win_coef_host.assign(desc->win_coef, desc->win_coef + (size_t)(2 * m + 1) * nc);
+    std::memset(&p->wc, 0, sizeof(WinCoef));
+    p->wc.deg = desc->win_deg;
+    for (int q = 1; q <= m; ++q) {
+        const double* c = desc->win_coef + (size_t)(q + m) * nc;  // o = q
+        for (int j = 0; j < nc; ++j) {
+            if (j % 2 == 0) p->wc.e[q - 1][j / 2] = c[j];
+            else p->wc.o[q - 1][j / 2] = c[j];
+        }
+    }
+    for (int j = 0; j < nc; ++j) p->wc.mm[j] = desc->win_coef[j];  // o = -m
+    // device tables
+    size_t nf = (size_t)g.Kh;
+    for (int i = 1; i < d; ++i) nf *= g.K;
+    int rc = dev_upload(&p->fused, desc->fused_band, nf);
+    if (rc == MLB_OK) {
+        std::vector<double2> tw((size_t)g.L * g.K);
+        for (size_t i = 0; i < tw.size(); ++i) tw[i] = make_double2(desc->twiddle[2 * i], desc->twiddle[2 * i + 1]);
+        rc = dev_upload(&p->twid, tw.data(), tw.size());
+    }
+    if (rc != MLB_OK) {
+        dev_free(p->fused);
+        dev_free(p->twid);
+        delete p;
+        return rc;
+    }
+    *out = p;
+    return MLB_OK;
+}
+
+int mlb_plan_destroy(mlb_plan* p) {
+    if (!p) return MLB_OK;
+    DeviceGuard guard(p->device);
+    dev_free(p->fused);
+    dev_free(p->twid);
+    delete p;
+    return MLB_OK;
+}
+
+int mlb_binding_destroy(mlb_binding* b) {
+    if (!b) return MLB_OK;
+    DeviceGuard guard(b->plan->device);
+    dev_free(b->perm);
+    dev_free(b->frac);
+    dev_free(b->chunk_start);
+    dev_free(b->chunk_cell);
+    dev_free(b->seg_chunk);
+    dev_free(b->seg_brick);
+    dev_free(b->brick_seg);
+    dev_free(b->isd);
+    dev_free(b->partial);
+    dev_free(b->grid);
+    dev_free(b->grid2);
+    dev_free(b->stage_a);
+    dev_free(b->stage_b);
+    delete b;
+    return MLB_OK;
+}
+
+int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
+             mlb_binding** out) {
+    if (!plan || !out || (n > 0 && !pts)) return fail(MLB_ERR_ARG, "null argument");
+    if (n < 0 || n >= (int64_t)1 << 31) return fail(MLB_ERR_ARG, "n out of range");
+    const Geom& g = plan->g;
+    const int d = g.d, Tb = g.Tb, nbr = g.nbr, TL = g.TL;
+    const int bin_lo = g.ulo + g.m;
+    // 1. cells and fractional offsets, exactly as _make_binding computes
+    //    tx = ng * (x * scale); u = floor(tx) (fastsum.py:343-353, :386)
+    std::vector<int32_t> key((size_t)n);
+    std::vector<double> f((size_t)n * d);
+    std::vector<int32_t> cell_local((size_t)n);
+    const int nloc = ipow_h(Tb, d);
+    const int nbricks = ipow_h(nbr, d);
+    for (int64_t i = 0; i < n; ++i) {
+        int brick = 0, local = 0, tcell = 0;
+        for (int a = 0; a < d; ++a) {
+            const double xt = pts[i * d + a] * scale;
+            const double tx = (double)g.ng * xt;
+            const double fl = std::floor(tx);
+            const int bin = (int)fl - bin_lo;
+            if (!(bin >= 0 && bin < g.nb)) {
+                return fail(MLB_ERR_CONFIG, "point " + std::to_string(i) + " lies outside the plan's admissible box");
+            }
+            f[(size_t)i * d + a] = tx - fl;
+            brick = brick * nbr + bin / Tb;
+            local = local * Tb + bin % Tb;
+            tcell = tcell * TL + bin % Tb;
+        }
+        key[i] = brick * nloc + local;
+        cell_local[i] = tcell;
+    }
+    // 2. stable counting sort by key
+    const int64_t nkeys = (int64_t)nbricks * nloc;
+    std::vector<int64_t> cnt(nkeys + 1, 0);
+    for (int64_t i = 0; i < n; ++i) cnt[key[i] + 1]++;
+    for (int64_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+    std::vector<int32_t> perm((size_t)n);
+    {
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (int64_t i = 0; i < n; ++i) perm[pos[key[i]]++] = (int32_t)i;
+    }
+    std::vector<int32_t> perm_node(perm);
+    if (node_ids)
+        for (int64_t j = 0; j < n; ++j) perm_node[j] = node_ids[perm[j]];
+    // 3. chunks (<= kChunk points of one cell) and segments (<= maxseg chunks of one brick)
+    std::vector<int32_t> chunk_start, chunk_cell, chunk_brick;
+    for (int64_t k = 0; k < nkeys; ++k) {
+        const int64_t lo = cnt[k], hi = cnt[k + 1];
+        for (int64_t s = lo; s < hi; s += kChunk) {
+            chunk_start.push_back((int32_t)s);
+            chunk_cell.push_back(cell_local[perm[s]]);
+            chunk_brick.push_back((int32_t)(k / nloc));
+        }
+    }
+    const int nch = (int)chunk_cell.size();
+    chunk_start.push_back((int32_t)n);
+    // aim for ~8 CTAs per SM worth of segments, but never fewer than 4 chunks each
+    int maxseg = (int)((nch + 148 * 8 - 1) / (148 * 8));
+    if (maxseg < 4) maxseg = 4;
+    if (maxseg > 512) maxseg = 512;
+    std::vector<int32_t> seg_chunk, seg_brick, brick_seg(nbricks + 1, 0);
+    for (int c = 0; c < nch;) {
+        const int br = chunk_brick[c];
+        int e = c;
+        while (e < nch && chunk_brick[e] == br && e - c < maxseg) ++e;
+        seg_chunk.push_back(c);
+        seg_brick.push_back(br);
+        brick_seg[br + 1]++;
+        c = e;
+    }
+    const int nseg = (int)seg_brick.size();
+    seg_chunk.push_back(nch);
+    for (int br = 0; br < nbricks; ++br) brick_seg[br + 1] += brick_seg[br];
+    // frac in sorted order, SoA
+    std::vector<double> fs((size_t)n * d);
+    for (int64_t j = 0; j < n; ++j)
+        for (int a = 0; a < d; ++a) fs[(size_t)a * n + j] = f[(size_t)perm[j] * d + a];
+
+    DeviceGuard guard(plan->device);
+    mlb_binding* b = new mlb_binding();
+    b->plan = plan;
+    b->n = n;
+    b->nchunks = nch;
+    b->nseg = nseg;
+    b->nbricks = nbricks;
+    b->max_seg_chunks = maxseg;
+    b->tile_cells = ipow_h(TL, d);
+    b->grid_cells = 1;
+    for (int a = 0; a < d; ++a) b->grid_cells *= g.L;
+    int64_t st = (int64_t)g.Kh;
+    if (d == 2) st = std::max((int64_t)g.L * g.Kh, (int64_t)g.K * g.Kh);
+    if (d == 3) {
+        st = std::max((int64_t)g.L * g.L * g.Kh, (int64_t)g.L * g.K * g.Kh);
+        st = std::max(st, (int64_t)g.K * g.K * g.Kh);
+    }
+    b->stage_elems = 2 * st;
+    int rc = MLB_OK;
+    if (rc == MLB_OK) rc = dev_upload(&b->perm, perm_node.data(), (size_t)n);
+    if (rc == MLB_OK) rc = dev_upload(&b->frac, fs.data(), (size_t)n * d);
+    if (rc == MLB_OK) rc = dev_upload(&b->chunk_start, chunk_start.data(), chunk_start.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->chunk_cell, chunk_cell.data(), chunk_cell.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->seg_chunk, seg_chunk.data(), seg_chunk.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->seg_brick, seg_brick.data(), seg_brick.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->brick_seg, brick_seg.data(), brick_seg.size());
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, (size_t)nseg * b->tile_cells);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_a, nullptr, (size_t)b->stage_elems);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_b, nullptr, (size_t)b->stage_elems);
+    if (rc != MLB_OK) {
+        std::string msg = g_err;
+        mlb_binding_destroy(b);
+        return fail(rc, msg);
+    }
+    *out = b;
+    return MLB_OK;
+}
+
+int64_t mlb_binding_n(const mlb_binding* b) { return b ? b->n : -1; }
+
+int mlb_binding_perm(const mlb_binding* b, int32_t* perm_host) {
+    if (!b || !perm_host) return fail(MLB_ERR_ARG, "null argument");
+    DeviceGuard guard(b->plan->device);
+    if (b->n) MLB_CUDA_TRY(cudaMemcpy(perm_host, b->perm, b->n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return MLB_OK;
+}
+
+int mlb_binding_stats(const mlb_binding* b, int64_t* o) {
+    if (!b || !o) return fail(MLB_ERR_ARG, "null argument");
+    o[0] = b->n;
+    o[1] = b->nchunks;
+    o[2] = b->nseg;
+    o[3] = b->nbricks;
+    o[4] = b->tile_cells;
+    o[5] = b->grid_cells;
+    return MLB_OK;
+}
+
+int mlb_grid_cells(const mlb_binding* b, int64_t* cells, int* L, int* ulo) {
+    if (!b) return fail(MLB_ERR_ARG, "null argument");
+    if (cells) *cells = b->grid_cells;
+    if (L) *L = b->plan->g.L;
+    if (ulo) *ulo = b->plan->g.ulo;
+    return MLB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ permutations --
+namespace mlb {
+__global__ void gather_perm_kernel(const int32_t* __restrict__ perm, const double* __restrict__ src,
+                                   double* __restrict__ dst, int64_t n) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        dst[j] = src[perm[j]];
+}
+__global__ void scatter_perm_kernel(const int32_t* __restrict__ perm, const double* __restrict__ src,
+                                    double* __restrict__ dst, int64_t n, int acc) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = perm[j];
+        dst[i] = acc ? dst[i] + src[j] : src[j];
+    }
+}
+static int grid_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)(b < 1 ? 1 : b);
+}
+}  // namespace mlb
+
+extern "C" {
+
+int mlb_binding_set_isd(mlb_binding* b, const double* isd_dev, void* stream) {
+    if (!b || (!isd_dev && b->n)) return fail(MLB_ERR_ARG, "null argument");
+    if (!b->n) return MLB_OK;
+    DeviceGuard guard(b->plan->device);
+    gather_perm_kernel<<<grid_for(b->n), 256, 0, (cudaStream_t)stream>>>(b->perm, isd_dev, b->isd, b->n);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_to_sorted(const mlb_binding* b, const double* v, double* vs, void* stream) {
+    if (!b) return fail(MLB_ERR_ARG, "null argument");
+    if (!b->n) return MLB_OK;
+    DeviceGuard guard(b->plan->device);
+    gather_perm_kernel<<<grid_for(b->n), 256, 0, (cudaStream_t)stream>>>(b->perm, v, vs, b->n);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_to_node(const mlb_binding* b, const double* vs, double* v, int accumulate, void* stream) {
+    if (!b) return fail(MLB_ERR_ARG, "null argument");
+    if (!b->n) return MLB_OK;
+    DeviceGuard guard(b->plan->device);
+    scatter_perm_kernel<<<grid_for(b->n), 256, 0, (cudaStream_t)stream>>>(b->perm, vs, v, b->n, accumulate);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_spread(mlb_binding* b, const double* v, double* grid, unsigned flags, void* stream) {
+    if (!b || !grid) return fail(MLB_ERR_ARG, "null argument");
+    DeviceGuard guard(b->plan->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = launch_spread(b, v, flags, st);
+    if (rc != MLB_OK) return rc;
+    if (b->nseg == 0) {
+        MLB_CUDA_TRY(cudaMemsetAsync(grid, 0, b->grid_cells * sizeof(double), st));
+        return MLB_OK;
+    }
+    return launch_reduce(b, grid, st);
+}
+
+int mlb_convolve(mlb_binding* b, const double* gin, double* gout, void* stream) {
+    if (!b || !gin || !gout) return fail(MLB_ERR_ARG, "null argument");
+    DeviceGuard guard(b->plan->device);
+    return launch_convolve(b, gin, gout, (cudaStream_t)stream);
+}
+
+int mlb_gather(mlb_binding* b, const double* grid, double* y, unsigned flags, void* stream) {
+    if (!b || !grid || !y) return fail(MLB_ERR_ARG, "null argument");
+    DeviceGuard guard(b->plan->device);
+    return launch_gather(b, grid, nullptr, y, 0.0, 1.0, 0.0, flags & (MLB_SORTED | MLB_ACCUMULATE),
+                         (cudaStream_t)stream);
+}
+
+int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double beta, double gamma, unsigned flags,
+              void* stream) {
+    if (!b || (b->n && (!v || !y))) return fail(MLB_ERR_ARG, "null argument");
+    if (!b->n) return MLB_OK;
+    DeviceGuard guard(b->plan->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = launch_spread(b, v, flags, st);
+    if (rc == MLB_OK) rc = launch_reduce(b, b->grid, st);
+    if (rc == MLB_OK) rc = launch_convolve(b, b->grid, b->grid2, st);
+    if (rc == MLB_OK) rc = launch_gather(b, b->grid2, v, y, alpha, beta, gamma, flags, st);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Internal declarations of libmlb.so (B200 / sm_100a NFFT Laplacian path).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/multilap_b200.h"
+
+namespace mlb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define MLB_CUDA_TRY(expr)                                                              \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return ::mlb::fail(MLB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
+constexpr int kChunk = 32;        // points per chunk (one warp lane each)
+constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
+
+// Window polynomial coefficients, passed by value as a kernel parameter
+// (lives in constant bank 0 so the DFMAs read coefficients as c[] operands).
+// Even/odd split of the pairs P_q / P_{1-q}, q = 1..m, plus P_{-m}.
+struct WinCoef {
+    double e[kMaxM][9];   // even part of P_q in s^2 (up to 9 terms)
+    double o[kMaxM][8];   // odd part of P_q: P_q = E(s^2) + s*O(s^2)
+    double mm[kMaxWinCoef];  // P_{-m}, monomial in s
+    int deg;
+};
+
+// Geometry shared by all kernels of one plan.
+struct Geom {
+    int d, N, m, ng;
+    int S;        // 2m+1 stencil width
+    int nb;       // bins per axis
+    int L;        // active cells per axis = nb + 2m
+    int ulo;      // first active cell (signed torus index) = bin_lo - m
+    int K, Kh;    // N+1, N/2+1
+    int Tb, TL;   // brick bins per axis, brick tile cells per axis (Tb + 2m)
+    int nbr;      // bricks per axis
+    double K0;
+};
+
+}  // namespace mlb
+
+struct mlb_plan {
+    int device;
+    mlb::Geom g;
+    mlb::WinCoef wc;
+    double* fused = nullptr;     // band weights (K^(d-1) x Kh)
+    double2* twid = nullptr;     // L x K
+    std::vector<double> win_coef_host;
+};
+
+struct mlb_binding {
+    const mlb_plan* plan;
+    int64_t n;
+    int nchunks, nseg, nbricks;
+    // device tables
+    int32_t* perm = nullptr;         // sorted -> node
+    double* frac = nullptr;          // d x n (SoA) fractional cell offsets f in [0,1)
+    int32_t* chunk_start = nullptr;  // nchunks+1
+    int32_t* chunk_cell = nullptr;   // nchunks: flat tile index of the chunk's bin base cell
+    int32_t* seg_chunk = nullptr;    // nseg+1
+    int32_t* seg_brick = nullptr;    // nseg
+    int32_t* brick_seg = nullptr;    // nbricks+1 (CSR, bricks lexicographic)
+    double* isd = nullptr;           // sorted order
+    // scratch
+    double* partial = nullptr;       // nseg x TL^d
+    double* grid = nullptr;          // L^d (spread result)
+    double* grid2 = nullptr;         // L^d (convolved)
+    double* stage_a = nullptr;       // complex DFT intermediates
+    double* stage_b = nullptr;
+    int64_t stage_elems = 0;         // doubles per stage buffer
+    int tile_cells = 0;              // TL^d
+    int64_t grid_cells = 0;          // L^d
+    int max_seg_chunks = 0;
+};
+
+namespace mlb {
+// kernels launchers (mlb_fastsum.cu)
+int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st);
+int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st);
+int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_t st);
+int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
+                  double beta, double gamma, unsigned flags, cudaStream_t st);
+}  // namespace mlb

@@ -1,0 +1,258 @@
+// Krylov vector kernels: tall-skinny GEMV (V^T w, V c), CGS2, restart GEMM,
+// dot products, axpby, elementwise.  Replaces the OpenBLAS calls of
+// krylov.py:65-71 (CGS2), :147 / :160 (restart V S), :208 (y = V c).
+//
+// All reductions are two-level with a FIXED partition of rows into blocks and
+// a fixed-order final sum, so repeated runs are bitwise identical (the
+// reference pins seed determinism: test_krylov.py:62-71).  V is column-major:
+// column j starts at V + j*ld (coalesced reads down each column).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "mlb_internal.cuh"
+
+namespace mlb {
+
+constexpr int kRedThreads = 256;
+constexpr int kMaxRowBlocks = 256;
+
+static int row_blocks(int64_t n) {
+    int64_t b = (n + 2047) / 2048;
+    if (b > kMaxRowBlocks) b = kMaxRowBlocks;
+    return (int)(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+    return s;  // valid in thread 0
+}
+
+// partial[j * nb + blockIdx.x] = sum_{rows of block} V[j][i] w[i]; grid (nb, cols)
+__global__ void gemv_t_partial(const double* __restrict__ V, int64_t ld, int64_t n, const double* __restrict__ w,
+                               double* __restrict__ partial) {
+    __shared__ double sh[32];
+    const int nb = gridDim.x, j = blockIdx.y;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    const double* col = V + (int64_t)j * ld;
+    double s = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) s = fma(col[i], w[i], s);
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) partial[(int64_t)j * nb + blockIdx.x] = s;
+}
+
+// out[j] = sum_b partial[j*nb + b] (+ add[j])
+__global__ void finish_partial(const double* __restrict__ partial, int nb, int cols, double* __restrict__ out,
+                               const double* __restrict__ add) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += partial[(int64_t)j * nb + b];
+    if (add) s += add[j];
+    out[j] = s;
+}
+
+// y[i] (=|+=) scale * sum_j V[j][i] c[j]; optional per-block partial of y_new^2
+__global__ void gemv_n_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                              const double* __restrict__ c, double* __restrict__ y, double scale, int accumulate,
+                              double* __restrict__ nrm_partial) {
+    extern __shared__ double csh[];
+    __shared__ double sh[32];
+    for (int j = threadIdx.x; j < cols; j += blockDim.x) csh[j] = c[j];
+    __syncthreads();
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    double ss = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < cols; ++j) acc = fma(V[(int64_t)j * ld + i], csh[j], acc);
+        const double r = accumulate ? fma(scale, acc, y[i]) : scale * acc;
+        y[i] = r;
+        ss = fma(r, r, ss);
+    }
+    if (nrm_partial) {
+        ss = block_sum(ss, sh);
+        if (threadIdx.x == 0) nrm_partial[blockIdx.x] = ss;
+    }
+}
+
+__global__ void dot_partial(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                            double* __restrict__ partial) {
+    __shared__ double sh[32];
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    double s = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) s = fma(x[i], y[i], s);
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void axpby_kernel(double a, const double* __restrict__ x, double b, double* __restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (b == 0.0) ? a * x[i] : fma(a, x[i], b * y[i]);
+}
+
+__global__ void scale_by_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n,
+                                const double* __restrict__ s, double pw) {
+    const double f = (pw == -0.5) ? 1.0 / sqrt(s[0]) : pow(s[0], pw);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] * f;
+}
+
+__global__ void hadamard_kernel(const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ z,
+                                int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        z[i] = x[i] * y[i];
+}
+
+// Out[:, j] = sum_l V[:, l] S[l, j]: 64-row x 32-col tiles, K-steps of 16 via smem.
+__global__ void gemm_vs_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int s,
+                               const double* __restrict__ S, int k, double* __restrict__ Out, int64_t ldo) {
+    __shared__ double Vt[16][65];
+    __shared__ double St[16][33];
+    const int64_t row0 = blockIdx.x * 64;
+    const int col0 = blockIdx.y * 32;
+    const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;  // 16 x 16 threads, each 4 rows x 2 cols
+    double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    for (int l0 = 0; l0 < s; l0 += 16) {
+        for (int e = threadIdx.x; e < 16 * 64; e += blockDim.x) {
+            const int l = e / 64, r = e % 64;
+            const int64_t gi = row0 + r;
+            Vt[l][r] = (l0 + l < s && gi < n) ? V[(int64_t)(l0 + l) * ld + gi] : 0.0;
+        }
+        for (int e = threadIdx.x; e < 16 * 32; e += blockDim.x) {
+            const int l = e / 32, c = e % 32;
+            St[l][c] = (l0 + l < s && col0 + c < k) ? S[(int64_t)(col0 + c) * s + l0 + l] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int l = 0; l < 16; ++l) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) acc[a][b] = fma(Vt[l][tr + 16 * a], St[l][tc + 16 * b], acc[a][b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int64_t gi = row0 + tr + 16 * a;
+            const int c = col0 + tc + 16 * b;
+            if (gi < n && c < k) Out[(int64_t)c * ldo + gi] = acc[a][b];
+        }
+}
+
+static int ew_grid(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace mlb
+
+using namespace mlb;
+
+extern "C" {
+
+int64_t mlb_krylov_work_size(int64_t n, int maxcols) {
+    (void)n;
+    return (int64_t)kMaxRowBlocks * (maxcols + 2) + 2 * (maxcols + 2);
+}
+
+int mlb_gemv_t(const double* V, int64_t ld, int64_t n, int cols, const double* w, double* h, double* work,
+               void* stream) {
+    if (cols <= 0) return MLB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = row_blocks(n);
+    gemv_t_partial<<<dim3(nb, cols), kRedThreads, 0, st>>>(V, ld, n, w, work);
+    finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(work, nb, cols, h, nullptr);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c, double* y, double scale,
+               int accumulate, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = std::max(1, std::min(148 * 4, (int)((n + 255) / 256)));
+    gemv_n_kernel<<<nb, 256, cols * sizeof(double), st>>>(V, ld, n, cols, c, y, scale, accumulate, nullptr);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out, double* h1_out,
+             double* nrm2_out, double* work, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = row_blocks(n);
+    double* part = work;                                     // kMaxRowBlocks * cols
+    double* h1 = work + (int64_t)kMaxRowBlocks * (cols + 2);  // cols
+    const int nbn = std::max(1, std::min(kMaxRowBlocks, (int)((n + 255) / 256)));
+    // pass 1: h1 = V^T w ; w -= V h1
+    gemv_t_partial<<<dim3(nb, cols), kRedThreads, 0, st>>>(V, ld, n, w, part);
+    finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(part, nb, cols, h1, nullptr);
+    gemv_n_kernel<<<nbn, 256, cols * sizeof(double), st>>>(V, ld, n, cols, h1, w, -1.0, 1, nullptr);
+    // pass 2: h2 = V^T w ; w -= V h2 ; h_out = h1 + h2 ; ||w||^2
+    gemv_t_partial<<<dim3(nb, cols), kRedThreads, 0, st>>>(V, ld, n, w, part);
+    finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(part, nb, cols, h_out, h1);
+    // h2 = h_out - h1 is needed for the update: recompute it into h1's slot
+    double* h2 = h1 + cols + 1;
+    finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(part, nb, cols, h2, nullptr);
+    double* npart = part + (int64_t)nb * cols;
+    gemv_n_kernel<<<nbn, 256, cols * sizeof(double), st>>>(V, ld, n, cols, h2, w, -1.0, 1, npart);
+    if (nrm2_out) finish_partial<<<1, 64, 0, st>>>(npart, nbn, 1, nrm2_out, nullptr);
+    if (h1_out) MLB_CUDA_TRY(cudaMemcpyAsync(h1_out, h1, cols * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_gemm_vs(const double* V, int64_t ld, int64_t n, int s, const double* S, int k, double* Out, int64_t ldo,
+                void* stream) {
+    if (k <= 0 || n <= 0) return MLB_OK;
+    dim3 grid((unsigned)((n + 63) / 64), (unsigned)((k + 31) / 32));
+    gemm_vs_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(V, ld, n, s, S, k, Out, ldo);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_dot(const double* x, const double* y, int64_t n, double* out, double* work, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = row_blocks(n);
+    dot_partial<<<nb, kRedThreads, 0, st>>>(x, y, n, work);
+    finish_partial<<<1, 64, 0, st>>>(work, nb, 1, out, nullptr);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream) {
+    if (n <= 0) return MLB_OK;
+    axpby_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(a, x, b, y, n);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_scale_by(const double* x, double* y, int64_t n, const double* s_dev, double pw, void* stream) {
+    if (n <= 0) return MLB_OK;
+    scale_by_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(x, y, n, s_dev, pw);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_hadamard(const double* x, const double* y, double* z, int64_t n, void* stream) {
+    if (n <= 0) return MLB_OK;
+    hadamard_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(x, y, z, n);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+"""Graph layers and the shifted normalized Laplacian -- drop-in for multilap.graphs.
+
+    L_{sym,delta} v = (1 + delta) v - D^-1/2 W D^-1/2 v      (graphs.py:197-201)
+
+Kernel weights (points + fastsum plan) are bound on the GPU once; each
+Laplacian matvec is ONE fused libmlb call: spread of D^-1/2 v, pruned-DFT
+convolution, gather with the (1+delta) v - D^-1/2 (.) + K0 D^-1 v epilogue
+(the K(0) diagonal removal folded in).
+
+Vectors may be numpy arrays (copied to / from the device -- the reference's
+calling convention) or float64 CUDA tensors (stay on the device).
+"""
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib, fastsum
+from .errors import ConfigError, FormatError, NumericalError
+from .kernels import KernelSpec
+
+_SYM_TOL = 1e-12
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _is_tensor(v):
+    try:
+        import torch
+        return isinstance(v, torch.Tensor)
+    except Exception:
+        return False
+
+
+def _current_device():
+    return _torch().cuda.current_device()
+
+
+def to_device(v, device):
+    """fp64 contiguous CUDA tensor view/copy of v."""
+    torch = _torch()
+    if isinstance(v, torch.Tensor):
+        return v.to(device=f"cuda:{device}", dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=float))).to(f"cuda:{device}")
+
+
+class KernelWeights:
+    """W_ij = K(x_i - x_j), zero diagonal, from a point cloud (graphs.py:80-144).
+
+    With a plan every component block is bound on the device (one binding per
+    block; cross-block weights are zero).  Without a plan the exact O(n^2)
+    device kernel (direct.py) is used.
+    """
+
+    def __init__(self, points, kernel, plan=None, components=None, device=None):
+        points = np.asarray(points, dtype=float)
+        if points.ndim != 2:
+            raise ConfigError(f"points must be a 2-d array, got {points.shape}")
+        if not np.all(np.isfinite(points)):
+            raise ConfigError("points contain non-finite values")
+        self.points = points
+        self.kernel = kernel
+        self.plan = plan
+        self.n = points.shape[0]
+        self.device = _current_device() if device is None else int(device)
+        if components is None:
+            self._blocks = [np.arange(self.n)]
+        else:
+            components = np.asarray(components)
+            if components.shape != (self.n,):
+                raise ConfigError("components must be one label per point")
+            self._blocks = [np.flatnonzero(components == c) for c in np.unique(components)]
+        self._isd_dev = None
+        if plan is not None:
+            if plan.d != points.shape[1]:
+                raise ConfigError(f"plan dimension {plan.d} does not match points ({points.shape[1]})")
+            self._bindings = [fastsum.bind_points(plan, points[idx], device=self.device,
+                                                  node_ids=idx.astype(np.int32)) for idx in self._blocks]
+        else:
+            self._bindings = None
+
+    # -- device interface ---------------------------------------------------
+    @property
+    def fused(self):
+        """True when matvecs run through libmlb bindings (the NFFT hot path)."""
+        return self._bindings is not None
+
+    def set_isd(self, isd_dev):
+        self._isd_dev = isd_dev
+        if self._bindings is not None:
+            for b in self._bindings:
+                _lib.check(_lib.lib().mlb_binding_set_isd(b.ptr, _lib.ptr(isd_dev), _lib.stream_ptr()))
+
+    def apply_dev(self, v, y, alpha, beta, gamma, flags=0):
+        """y (=|+=) alpha v + s (beta W~(s v) + gamma s v) on device tensors (node order)."""
+        if self._bindings is not None:
+            for b in self._bindings:
+                fastsum.apply_binding(b, v, y, alpha, beta, gamma, flags)
+            return y
+        from .direct import direct_apply_dev
+        s = self._isd_dev if flags & _lib.MLB_USE_ISD else None
+        direct_apply_dev(self, v, y, alpha, beta, gamma, s, bool(flags & _lib.MLB_ACCUMULATE))
+        return y
+
+    # -- weights protocol (graphs.py:119-144) ---------------------------------
+    def matvec(self, v):
+        torch = _torch()
+        host = not _is_tensor(v)
+        vd = to_device(v, self.device)
+        if tuple(vd.shape) != (self.n,):
+            raise ConfigError("v must be a vector matching the number of points")
+        y = torch.empty_like(vd)
+        if self.n:
+            self.apply_dev(vd, y, -self.kernel.value_at_zero(), 1.0, 0.0, 0)
+        return y.cpu().numpy() if host else y
+
+    def materialize(self):
+        W = np.zeros((self.n, self.n))
+        for idx in self._blocks:
+            pts = self.points[idx]
+            sq = np.sum(pts ** 2, axis=1)
+            d2 = np.maximum(sq[:, None] + sq[None, :] - 2.0 * pts @ pts.T, 0.0)
+            blk = self.kernel.of_sqdist(d2)
+            np.fill_diagonal(blk, 0.0)
+            W[np.ix_(idx, idx)] = blk
+        return W
+
+
+class DenseWeights:
+    """Explicit symmetric weights (graphs.py:27-50); matvec on the device GEMV."""
+
+    def __init__(self, W, device=None):
+        W = np.asarray(W, dtype=float)
+        if W.ndim != 2 or W.shape[0] != W.shape[1]:
+            raise ConfigError(f"weight matrix must be square, got {W.shape}")
+        if not np.all(np.isfinite(W)):
+            raise ConfigError("weight matrix contains non-finite entries")
+        scale = max(1.0, np.abs(W).max(initial=0.0))
+        if np.abs(W - W.T).max(initial=0.0) > _SYM_TOL * scale:
+            raise ConfigError("weight matrix is not symmetric")
+        if W.min(initial=0.0) < 0:
+            raise ConfigError("weight matrix has negative entries")
+        if np.abs(np.diag(W)).max(initial=0.0) > 0:
+            raise ConfigError("weight matrix must have a zero diagonal")
+        self.W = W
+        self.n = W.shape[0]
+        self.device = _current_device() if device is None else int(device)
+        self._Wd = None
+
+    def _dev(self):
+        if self._Wd is None:
+            self._Wd = to_device(self.W, self.device)  # symmetric: row-major == column-major
+        return self._Wd
+
+    def matvec(self, v):
+        from .krylov import gemv_n
+        host = not _is_tensor(v)
+        vd = to_device(v, self.device)
+        y = _torch().empty_like(vd)
+        if self.n:
+            gemv_n(self._dev(), self.n, self.n, vd, y)
+        return y.cpu().numpy() if host else y
+
+    def materialize(self):
+        return self.W.copy()
+
+
+class SparseWeights:
+    """CSR weights (graphs.py:53-77).  Not on the NFFT path: kept host-side for
+    API compatibility (edge-list graphs have no kernel structure to exploit)."""
+
+    def __init__(self, W):
+        import scipy.sparse as sp
+        W = sp.csr_array(W, dtype=float)
+        if W.shape[0] != W.shape[1]:
+            raise ConfigError(f"weight matrix must be square, got {W.shape}")
+        if W.nnz and not np.all(np.isfinite(W.data)):
+            raise ConfigError("weight matrix contains non-finite entries")
+        scale = max(1.0, np.abs(W.data).max(initial=0.0) if W.nnz else 0.0)
+        asym = W - W.T
+        if asym.nnz and np.abs(asym.data).max() > _SYM_TOL * scale:
+            raise ConfigError("weight matrix is not symmetric")
+        if W.nnz and W.data.min() < 0:
+            raise ConfigError("weight matrix has negative entries")
+        if np.abs(W.diagonal()).max(initial=0.0) > 0:
+            raise ConfigError("weight matrix must have a zero diagonal")
+        self.W = W
+        self.n = W.shape[0]
+
+    def matvec(self, v):
+        if _is_tensor(v):
+            return to_device(self.W @ v.cpu().numpy(), v.device.index)
+        return self.W @ np.asarray(v, dtype=float)
+
+    def materialize(self):
+        return self.W.toarray()
+
+
+@dataclass(frozen=True)
+class Layer:
+    """One graph layer: weights, cached degrees, diagonal shift (graphs.py:147-165)."""
+
+    weights: object
+    degrees: np.ndarray
+    shift: float = 0.0
+
+    @property
+    def n(self):
+        return self.weights.n
+
+    @property
+    def inv_sqrt_degrees(self):
+        isd = self.__dict__.get("_isd")
+        if isd is None:
+            isd = 1.0 / np.sqrt(self.degrees)
+            self.__dict__["_isd"] = isd
+        return isd
+
+    def isd_device(self, device):
+        key = ("_isd_dev", int(device))
+        t = self.__dict__.get(key)
+        if t is None:
+            t = to_device(self.inv_sqrt_degrees, device)
+            self.__dict__[key] = t
+        return t
+
+    @property
+    def on_device(self):
+        return isinstance(self.weights, (KernelWeights, DenseWeights))
+
+
+def build_layer(weights, shift=0.0):
+    """Degrees by one matvec on ones; reject degree <= 1e-300 (graphs.py:168-183)."""
+    if shift < 0:
+        raise ConfigError(f"shift must be nonnegative, got {shift}")
+    degrees = np.asarray(_as_host(weights.matvec(np.ones(weights.n))), dtype=float)
+    bad = np.flatnonzero(degrees <= 1e-300)
+    if bad.size:
+        raise NumericalError(f"node {bad[0]} has zero degree; the normalized Laplacian is undefined")
+    layer = Layer(weights=weights, degrees=degrees, shift=float(shift))
+    if isinstance(weights, KernelWeights):
+        weights.set_isd(layer.isd_device(weights.device))
+    return layer
+
+
+def _as_host(x):
+    return x.cpu().numpy() if _is_tensor(x) else x
+
+
+def with_shift(layer, shift):
+    if shift < 0:
+        raise ConfigError(f"shift must be nonnegative, got {shift}")
+    new = replace(layer, shift=float(shift))
+    for k, v in layer.__dict__.items():  # share cached isd
+        if isinstance(k, tuple) or k == "_isd":
+            new.__dict__[k] = v
+    return new
+
+
+def apply_weight(layer, v):
+    return layer.weights.matvec(v if _is_tensor(v) else np.asarray(v, dtype=float))
+
+
+def apply_sym_laplacian_dev(layer, v, y, accumulate=False, scale=1.0):
+    """Device form: y (=|+=) scale * L_{sym,delta} v on CUDA tensors."""
+    w = layer.weights
+    flags = _lib.MLB_ACCUMULATE if accumulate else 0
+    if isinstance(w, KernelWeights):
+        if w._isd_dev is None:
+            w.set_isd(layer.isd_device(w.device))
+        K0 = w.kernel.value_at_zero()
+        w.apply_dev(v, y, scale * (1.0 + layer.shift), -scale, scale * K0, flags | _lib.MLB_USE_ISD)
+        return y
+    from .krylov import axpby, hadamard
+    isd = layer.isd_device(v.device.index)
+    t = hadamard(isd, v)
+    Wt = w.matvec(t)
+    Wt = to_device(Wt, v.device.index)
+    r = hadamard(isd, Wt)
+    # y = scale*((1+shift) v - r) (+ y)
+    if accumulate:
+        axpby(scale * (1.0 + layer.shift), v, 1.0, y)
+    else:
+        y.copy_(v).mul_(scale * (1.0 + layer.shift))
+    axpby(-scale, r, 1.0, y)
+    return y
+
+
+def apply_sym_laplacian(layer, v):
+    """(1 + shift) v - D^-1/2 W D^-1/2 v (graphs.py:197-201)."""
+    if not layer.on_device:
+        v = np.asarray(_as_host(v), dtype=float)
+        isd = layer.inv_sqrt_degrees
+        return (1.0 + layer.shift) * v - isd * np.asarray(_as_host(layer.weights.matvec(isd * v)))
+    torch = _torch()
+    host = not _is_tensor(v)
+    dev = layer.weights.device
+    vd = to_device(v, dev)
+    if tuple(vd.shape) != (layer.n,):
+        raise ConfigError("v must match the layer size")
+    y = torch.empty_like(vd)
+    apply_sym_laplacian_dev(layer, vd, y)
+    return y.cpu().numpy() if host else y
+
+
+def materialize_sym_laplacian(layer):
+    W = layer.weights.materialize()
+    isd = layer.inv_sqrt_degrees
+    L = -(isd[:, None] * W * isd[None, :])
+    L[np.diag_indices_from(L)] += 1.0 + layer.shift
+    return L
+
+
+@dataclass(frozen=True)
+class MultilayerGraph:
+    """Layers over one node set (graphs.py:213-238)."""
+
+    layers: tuple
+
+    def __post_init__(self):
+        if not self.layers:
+            raise ConfigError("a multilayer graph needs at least one layer")
+        sizes = {layer.n for layer in self.layers}
+        if len(sizes) != 1:
+            raise ConfigError(f"layers disagree on node count: {sorted(sizes)}")
+
+    @property
+    def n(self):
+        return self.layers[0].n
+
+    @property
+    def T(self):
+        return len(self.layers)
+
+    def with_shift(self, shift):
+        return MultilayerGraph(tuple(with_shift(s, shift) for s in self.layers))
+
+    def subgraph(self, layer_indices):
+        return MultilayerGraph(tuple(self.layers[i] for i in layer_indices))
+
+
+def load_edge_list(path, n=None):
+    """`i j w` edge list -> SparseWeights (graphs.py:241-279)."""
+    import scipy.sparse as sp
+    rows, cols, vals = [], [], []
+    with open(path) as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            line = raw.split("#", 1)[0].strip()
+            if not line:
+                continue
+            parts = line.split()
+            if len(parts) != 3:
+                raise FormatError(f"{path}:{lineno}: expected 'i j w', got {raw.strip()!r}")
+            try:
+                i, j, w = int(parts[0]), int(parts[1]), float(parts[2])
+            except ValueError as exc:
+                raise FormatError(f"{path}:{lineno}: {exc}") from exc
+            if i < 0 or j < 0:
+                raise FormatError(f"{path}:{lineno}: node ids must be >= 0")
+            if not np.isfinite(w) or w < 0:
+                raise FormatError(f"{path}:{lineno}: weight must be finite and >= 0")
+            if i != j:
+                rows.append(i)
+                cols.append(j)
+                vals.append(w)
+    if n is None:
+        if not rows:
+            raise FormatError(f"{path}: empty edge list and no node count given")
+        n = max(max(rows), max(cols)) + 1
+    elif rows and max(max(rows), max(cols)) >= n:
+        raise FormatError(f"{path}: node id exceeds declared node count {n}")
+    W = sp.coo_array((vals, (rows, cols)), shape=(n, n)).tocsr()
+    return SparseWeights(W.maximum(W.T))

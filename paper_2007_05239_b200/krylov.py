@@ -1,0 +1,442 @@
+"""Device-resident Krylov solvers -- drop-in for multilap.krylov.
+
+* lanczos_largest_eigs: thick-restart Lanczos (krylov.py:74-169)
+* lanczos_fn_apply / pksm_apply: Lanczos f(A) v with f = lambda^p (krylov.py:172-244)
+
+The basis V lives on the GPU (column-major: one contiguous row of a torch
+(dim, n) tensor per Krylov vector); every O(n) operation -- the operator
+apply, the CGS2 reorthogonalisation, norms, the final V c -- runs in
+libmlb.so.  Only the O(s^2) projected problems (tridiagonal / small dense
+eigh, the stopping logic) run on the host, one small device->host read per
+Krylov step.  PKSM keeps the layer's vectors in its binding's cell order so
+spread and gather read them coalesced.
+
+PKSM stopping test: the reference forms y_s = |v| V_s Q f(L) Q[0,:] every
+step and stops when |y_s - y_{s-1}| <= tol |y_s| (krylov.py:208-211).  With
+V orthonormal that equals the same test on the coefficient vectors, so y is
+formed once at the end.  Borderline steps (ratio within
+1e-3 of the threshold) are re-tested on the exact device y's.
+"""
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, ConvergenceError, NumericalError
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ------------------------------------------------------------ device ops ---
+class _Work:
+    """Per-device scratch for the reduction kernels."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, device, cols):
+        torch = _torch()
+        need = int(_lib.lib().mlb_krylov_work_size(0, int(cols) + 2))
+        key = int(device)
+        buf = cls._cache.get(key)
+        if buf is None or buf.numel() < need:
+            buf = torch.empty(max(need, 1 << 16), dtype=torch.float64, device=f"cuda:{device}")
+            cls._cache[key] = buf
+        return buf
+
+
+def _sp():
+    return _lib.stream_ptr()
+
+
+def gemv_n(V, ld, cols, c, y, scale=1.0, accumulate=False):
+    """y (=|+=) scale * V[:, :cols] c   (V column-major with leading dim ld)."""
+    n = y.numel()
+    _lib.check(_lib.lib().mlb_gemv_n(_lib.ptr(V), ld, n, cols, _lib.ptr(c), _lib.ptr(y), float(scale),
+                                     int(accumulate), _sp()))
+    return y
+
+
+def gemv_t(V, ld, cols, w, h):
+    n = w.numel()
+    work = _Work.get(w.device.index, cols)
+    _lib.check(_lib.lib().mlb_gemv_t(_lib.ptr(V), ld, n, cols, _lib.ptr(w), _lib.ptr(h), _lib.ptr(work), _sp()))
+    return h
+
+
+def cgs2(V, cols, w, h_out, h1_out=None, nrm2_out=None):
+    """Two-pass classical Gram-Schmidt of w against V[:cols] in place (krylov.py:65-71)."""
+    n = w.numel()
+    work = _Work.get(w.device.index, cols)
+    _lib.check(_lib.lib().mlb_cgs2(_lib.ptr(V), n, n, cols, _lib.ptr(w), _lib.ptr(h_out), _lib.ptr(h1_out),
+                                   _lib.ptr(nrm2_out), _lib.ptr(work), _sp()))
+
+
+def dot(x, y, out):
+    work = _Work.get(x.device.index, 1)
+    _lib.check(_lib.lib().mlb_dot(_lib.ptr(x), _lib.ptr(y), x.numel(), _lib.ptr(out), _lib.ptr(work), _sp()))
+    return out
+
+
+def axpby(a, x, b, y):
+    _lib.check(_lib.lib().mlb_axpby(float(a), _lib.ptr(x), float(b), _lib.ptr(y), y.numel(), _sp()))
+    return y
+
+
+def hadamard(x, y, out=None):
+    out = _torch().empty_like(x) if out is None else out
+    _lib.check(_lib.lib().mlb_hadamard(_lib.ptr(x), _lib.ptr(y), _lib.ptr(out), x.numel(), _sp()))
+    return out
+
+
+def scale_by(x, y, s_dev, pw):
+    _lib.check(_lib.lib().mlb_scale_by(_lib.ptr(x), _lib.ptr(y), x.numel(), _lib.ptr(s_dev), float(pw), _sp()))
+    return y
+
+
+def gemm_vs(V, ld, s, S_dev, k, Out, ldo):
+    """Out[:k] = (V[:, :s] S[:s, :k]) column blocks; S column-major s x k on device."""
+    n = ld
+    _lib.check(_lib.lib().mlb_gemm_vs(_lib.ptr(V), ld, n, s, _lib.ptr(S_dev), k, _lib.ptr(Out), ldo, _sp()))
+    return Out
+
+
+def _to_dev(x, device):
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x.to(device=f"cuda:{device}", dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=float))).to(f"cuda:{device}")
+
+
+def _host(x):
+    torch = _torch()
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+# ------------------------------------------------------------- operators ---
+class SymmetricOperator:
+    """A symmetric linear map (krylov.py:19-37).
+
+    `apply` keeps the reference meaning (numpy in, numpy out, any callable);
+    `apply_dev` (optional) maps a CUDA fp64 tensor to a new CUDA tensor and is
+    what the device solvers call -- the GPU layers provide it.
+    """
+
+    def __init__(self, n, apply, name="operator", apply_dev=None, device=None):
+        self.n = n
+        self.apply = apply
+        self.name = name
+        self._apply_dev = apply_dev
+        self.device = _torch().cuda.current_device() if device is None else int(device)
+
+    def apply_dev(self, v):
+        if self._apply_dev is not None:
+            return self._apply_dev(v)
+        return _to_dev(self.apply(v.cpu().numpy()), v.device.index)
+
+    def selftest_symmetry(self, rng=None, probes=2, tol=1e-8):
+        """<Ax, y> == <x, Ay> on default_rng(0) probe pairs (krylov.py:27-37)."""
+        rng = np.random.default_rng(0) if rng is None else rng
+        for _ in range(probes):
+            x = rng.standard_normal(self.n)
+            y = rng.standard_normal(self.n)
+            xd, yd = _to_dev(x, self.device), _to_dev(y, self.device)
+            ax, ay = self.apply_dev(xd), self.apply_dev(yd)
+            out = _torch().empty(4, dtype=_torch().float64, device=xd.device)
+            dot(ax, yd, out[0:1])
+            dot(xd, ay, out[1:2])
+            dot(ax, ax, out[2:3])
+            dot(yd, yd, out[3:4])
+            a, b, nax2, ny2 = out.cpu().numpy()
+            scale = max(np.sqrt(nax2) * np.sqrt(ny2), 1e-300)
+            if abs(a - b) > tol * scale:
+                raise NumericalError(f"{self.name} fails the symmetry probe")
+
+
+def operator_from_layer(layer):
+    from .graphs import apply_sym_laplacian, apply_sym_laplacian_dev
+    torch = _torch()
+
+    def apply_dev(v):
+        y = torch.empty_like(v)
+        return apply_sym_laplacian_dev(layer, v, y)
+
+    dev = layer.weights.device if layer.on_device else None
+    return SymmetricOperator(layer.n, lambda v: apply_sym_laplacian(layer, v), "sym-laplacian",
+                             apply_dev=apply_dev if layer.on_device else None, device=dev)
+
+
+@dataclass
+class EigenResult:
+    """Largest eigenpairs: values descending, vectors column-aligned (krylov.py:46-54)."""
+
+    values: np.ndarray
+    vectors: np.ndarray
+    residuals: np.ndarray
+    matvecs: int
+    restarts: int
+
+
+def _start_vector(n, seed):
+    rng = np.random.default_rng(seed)                 # krylov.py:57-62
+    v = np.ones(n) + 1e-2 * rng.standard_normal(n)
+    return v / np.linalg.norm(v)
+
+
+# ------------------------------------------------------------- Lanczos -----
+def lanczos_largest_eigs(op, k, tol=1e-8, max_subspace=None, max_restarts=60, seed=0, return_device=False):
+    """k largest eigenpairs of a symmetric operator via restarted Lanczos (krylov.py:74-169)."""
+    torch = _torch()
+    n = op.n
+    if not 1 <= k < n:
+        raise ConfigError(f"need 1 <= k < n, got k={k}, n={n}")
+    op.selftest_symmetry()
+    if max_subspace is None:
+        max_subspace = max(2 * k + 10, 20)
+    ms = int(min(max_subspace, n))
+    if ms < k + 2:
+        ms = min(n, k + 2)
+    keep = min(ms - 1, k + max(2, k // 2))
+    dev = f"cuda:{op.device}"
+    V = torch.empty((ms, n), dtype=torch.float64, device=dev)
+    Vtmp = torch.empty((ms, n), dtype=torch.float64, device=dev)
+    H = np.zeros((ms, ms))
+    V[0] = _to_dev(_start_vector(n, seed), op.device)
+    u = V[0].clone()
+    s = 0
+    matvecs = 0
+    rng_fill = np.random.default_rng(seed + 1)
+    best = None
+    hbuf = torch.empty(ms + 2, dtype=torch.float64, device=dev)
+    beta = 0.0
+    for restart in range(max_restarts + 1):
+        j = s
+        while j < ms:
+            V[j] = u
+            w = op.apply_dev(u)
+            if w.data_ptr() == u.data_ptr():
+                w = w.clone()
+            matvecs += 1
+            cgs2(V, j + 1, w, hbuf[: j + 1], None, hbuf[ms:ms + 1])
+            hh = hbuf.cpu().numpy()
+            h = hh[: j + 1]
+            H[: j + 1, j] = h
+            H[j, : j + 1] = h
+            beta = float(np.sqrt(max(hh[ms], 0.0)))
+            j += 1
+            if beta <= 1e-13 * max(1.0, np.abs(H[:j, :j]).max()):
+                if j >= n:
+                    break
+                ud = _to_dev(rng_fill.standard_normal(n), op.device)
+                cgs2(V, j, ud, hbuf[:j], None, hbuf[ms:ms + 1])
+                nu = float(np.sqrt(max(hbuf[ms:ms + 1].cpu().item(), 0.0)))
+                if nu <= 1e-13:
+                    break
+                u = axpby(1.0 / nu, ud, 0.0, ud)
+                beta = 0.0
+            else:
+                u = axpby(1.0 / beta, w, 0.0, w)
+        sd = j
+        theta, S = np.linalg.eigh(H[:sd, :sd])
+        order = np.argsort(theta)[::-1]
+        theta, S = theta[order], S[:, order]
+        scale = max(abs(theta[0]), abs(theta[-1]), 1e-300)
+        res = np.abs(beta * S[sd - 1, :])
+        best = res[:k]
+        if np.all(res[:k] <= tol * scale) or sd >= n:
+            Sd = _to_dev(np.asfortranarray(S[:, :k]).ravel(order="F"), op.device)
+            gemm_vs(V, n, sd, Sd, k, Vtmp, n)
+            vec = Vtmp[:k].T
+            vectors = vec if return_device else vec.cpu().numpy()
+            return EigenResult(values=theta[:k], vectors=vectors, residuals=res[:k], matvecs=matvecs,
+                               restarts=restart)
+        if restart == max_restarts:
+            break
+        Sd = _to_dev(np.asfortranarray(S[:, :keep]).ravel(order="F"), op.device)
+        gemm_vs(V, n, sd, Sd, keep, Vtmp, n)
+        V[:keep] = Vtmp[:keep]
+        H[:, :] = 0.0
+        H[:keep, :keep] = np.diag(theta[:keep])
+        s = keep
+    raise ConvergenceError(
+        f"Lanczos did not converge: {matvecs} matvecs, best residuals {np.array2string(best, precision=2)}",
+        residuals=best)
+
+
+# -------------------------------------------------- Lanczos matrix function -
+class PksmStats:
+    """Counts of the last solves (inner steps / matvecs), for benches."""
+
+    steps = []
+
+    @classmethod
+    def reset(cls):
+        cls.steps = []
+
+
+def lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None, out_scale=1.0,
+                         accumulate=False):
+    """Device Lanczos f(A) v; v is a CUDA tensor (not modified).
+
+    Returns y (or writes out (=|+=) out_scale * y).
+    """
+    torch = _torch()
+    if tuple(v.shape) != (n,):
+        raise ConfigError("v must match the operator dimension")
+    dim = int(min(krylov_dim, n))
+    if dim < 1:
+        raise ConfigError(f"krylov_dim must be >= 1, got {krylov_dim}")
+    buf = torch.empty(2, dtype=torch.float64, device=v.device)
+    dot(v, v, buf[0:1])
+    nv = float(np.sqrt(buf[0].item()))
+    if nv == 0.0:
+        if out is None:
+            return torch.zeros_like(v)
+        if not accumulate:
+            out.zero_()
+        return out
+    V = torch.empty((dim, n), dtype=torch.float64, device=v.device)
+    axpby(1.0 / nv, v, 0.0, V[0])
+    alphas = np.empty(dim)
+    betas = np.empty(dim)
+    hbuf = torch.empty(2 * dim + 3, dtype=torch.float64, device=v.device)
+    c_prev = None
+    s = 0
+    while True:
+        w = apply_dev(V[s])
+        cgs2(V, s + 1, w, hbuf[: s + 1], hbuf[dim:dim + s + 1], hbuf[dim + s + 1:dim + s + 2])
+        # alpha = V[:, s] . w before orthogonalisation (krylov.py:198) and ||w||^2 after
+        pair = hbuf[dim + s:dim + s + 2].cpu().numpy()
+        alphas[s] = pair[0]
+        beta = float(np.sqrt(max(pair[1], 0.0)))
+        betas[s] = beta
+        s += 1
+        T = np.diag(alphas[:s])
+        if s > 1:
+            off = betas[: s - 1]
+            T += np.diag(off, 1) + np.diag(off, -1)
+        lam, Q = np.linalg.eigh(T)
+        c = nv * (Q @ (fn(lam) * Q[0, :]))
+        stop = False
+        if c_prev is not None:
+            diff = c.copy()
+            diff[: s - 1] -= c_prev
+            lhs = np.linalg.norm(diff)
+            rhs = tol * max(np.linalg.norm(c), 1e-300)
+            if rhs > 0 and abs(lhs / rhs - 1.0) < 1e-3:
+                # borderline: exact test on the device vectors (krylov.py:208-211)
+                y = torch.zeros(n, dtype=torch.float64, device=v.device)
+                yp = torch.zeros(n, dtype=torch.float64, device=v.device)
+                gemv_n(V, n, s, _to_dev(c, v.device.index), y)
+                gemv_n(V, n, s - 1, _to_dev(c_prev, v.device.index), yp)
+                nb = torch.empty(2, dtype=torch.float64, device=v.device)
+                d = axpby(1.0, y, -1.0, yp)
+                dot(d, d, nb[0:1])
+                dot(y, y, nb[1:2])
+                a2, b2 = nb.cpu().numpy()
+                lhs, rhs = np.sqrt(a2), tol * max(np.sqrt(b2), 1e-300)
+            stop = lhs <= rhs
+        happy = beta <= 1e-13 * max(1.0, np.abs(alphas[:s]).max())
+        if stop or happy or s >= dim:
+            PksmStats.steps.append(s)
+            cd = _to_dev(c, v.device.index)
+            if out is None:
+                y = torch.empty(n, dtype=torch.float64, device=v.device)
+                gemv_n(V, n, s, cd, y)
+                return y
+            gemv_n(V, n, s, cd, out, out_scale, accumulate)
+            return out
+        c_prev = c
+        axpby(1.0 / beta, w, 0.0, V[s])
+
+
+def lanczos_fn_apply(op, v, fn, krylov_dim=50, tol=1e-8):
+    """y ~= f(A) v via the Lanczos relation (krylov.py:172-216)."""
+    torch = _torch()
+    host = not isinstance(v, torch.Tensor)
+    if host:
+        v = np.asarray(v, dtype=float)
+        if v.shape != (op.n,):
+            raise ConfigError("v must match the operator dimension")
+    vd = _to_dev(v, op.device)
+    y = lanczos_fn_apply_dev(op.apply_dev, op.n, vd, fn, krylov_dim, tol)
+    return y.cpu().numpy() if host else y
+
+
+def power_fn(p):
+    """lambda^p with the PSD / positivity checks of pksm_apply (krylov.py:230-242)."""
+    def fn(lam):
+        low = lam.min()
+        if low < -1e-10:
+            raise NumericalError(f"operator is not positive semidefinite (eigenvalue {low:.3e})")
+        lam = np.maximum(lam, 0.0)
+        if p < 0 and lam.min() <= 0.0:
+            raise NumericalError("zero eigenvalue encountered with a negative power; "
+                                 "a positive shift delta is required")
+        return lam ** p
+    return fn
+
+
+def pksm_layer_dev(layer, p, v_node, out, out_scale=1.0, accumulate=True, krylov_dim=50, tol=1e-8):
+    """out (+)= out_scale * (L_sym + delta)^p v for a GPU kernel layer.
+
+    Runs in the layer binding's cell order when the layer has one binding
+    (vectors coalesced for spread/gather), node order otherwise.
+    """
+    from .graphs import KernelWeights, apply_sym_laplacian_dev
+    torch = _torch()
+    fn = power_fn(p)
+    w = layer.weights
+    if isinstance(w, KernelWeights) and w.fused and len(w._bindings) == 1:
+        b = w._bindings[0]
+        if w._isd_dev is None:
+            w.set_isd(layer.isd_device(w.device))
+        lib = _lib.lib()
+        vs = torch.empty_like(v_node)
+        _lib.check(lib.mlb_to_sorted(b.ptr, _lib.ptr(v_node), _lib.ptr(vs), _sp()))
+        K0 = w.kernel.value_at_zero()
+        a = 1.0 + layer.shift
+        flags = _lib.MLB_USE_ISD | _lib.MLB_SORTED
+
+        def apply_sorted(x):
+            y = torch.empty_like(x)
+            _lib.check(lib.mlb_apply(b.ptr, _lib.ptr(x), _lib.ptr(y), a, -1.0, K0, flags, _sp()))
+            return y
+
+        ys = lanczos_fn_apply_dev(apply_sorted, layer.n, vs, fn, krylov_dim, tol)
+        if out_scale != 1.0:
+            ys.mul_(out_scale)
+        _lib.check(lib.mlb_to_node(b.ptr, _lib.ptr(ys), _lib.ptr(out), int(accumulate), _sp()))
+        return out
+
+    def apply_node(x):
+        y = torch.empty_like(x)
+        return apply_sym_laplacian_dev(layer, x, y)
+
+    return lanczos_fn_apply_dev(apply_node, layer.n, v_node, fn, krylov_dim, tol, out=out, out_scale=out_scale,
+                                accumulate=accumulate)
+
+
+def pksm_apply(target, p, v, krylov_dim=50, tol=1e-8):
+    """(L_{sym,delta})^p v, or A^p v for a SymmetricOperator (krylov.py:219-244)."""
+    from .graphs import Layer
+    torch = _torch()
+    if p == 0:
+        raise ConfigError("p must be nonzero")
+    if isinstance(target, Layer) and target.on_device:
+        host = not isinstance(v, torch.Tensor)
+        if host:
+            v = np.asarray(v, dtype=float)
+            if v.shape != (target.n,):
+                raise ConfigError("v must match the operator dimension")
+        vd = _to_dev(v, target.weights.device)
+        out = torch.zeros_like(vd)
+        pksm_layer_dev(target, p, vd, out, 1.0, False, krylov_dim, tol)
+        return out.cpu().numpy() if host else out
+    op = operator_from_layer(target) if isinstance(target, Layer) else target
+    return lanczos_fn_apply(op, v, power_fn(p), krylov_dim=krylov_dim, tol=tol)
