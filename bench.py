@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark: normalized-Laplacian matvecs/s (node*layers/s), fp64, on B200.
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+512x512 synthetic segmentation image (n = 262,144 nodes), T = 2 kernel layers
+-- RGB d=3 sigma=0.1 (N=64, m=4, p=8; the reference rejects N=32 for this
+layer) and xy d=2 sigma=0.15 (N=32, m=4, p=8) -- shifted by
+delta = ln 2 as in the p = -1 PKSM solves.  One STEP = one shifted
+normalized-Laplacian matvec y = (1+delta) v - D^-1/2 W D^-1/2 v on every
+layer (2 x 262,144 node*layers), vectors in node order (the drop-in
+`apply_sym_laplacian` semantics).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W warm-up steps; then K steps, each bracketed by CUDA events on the
+launching stream, with a 256 MB L2 flush between steps (outside the events);
+barrier + synchronize around the loop; max over ranks.  Multi-GPU (torchrun):
+layers are independent, each rank owns the 2 layers of its own seeded image
+(round-robin layer ownership, no data-path collective) -> weak scaling.
+
+`--impl reference` times the CPU reference algorithm (the numpy oracle port
+of multilap's fastsum/graphs path: bincount spread/gather + scipy.fft) on a
+bounded subsample of the same layers, rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "normalized-Laplacian matvecs/sec (node*layers/s) fp64"
+UNIT = "node*layers/s"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_layers(workload, device, delta):
+    import synth
+    from paper_2007_05239_b200 import with_shift
+    G = synth.build_graph(workload, device=device)
+    return [with_shift(l, delta) for l in G.layers]
+
+
+def algorithmic_bytes(d):
+    """B(d) = 16 d + 40 bytes per node per normalized-Laplacian matvec."""
+    return 16 * d + 40
+
+
+def algorithmic_flops(d, m):
+    """F(d, m) = 4 (2m+1)^d fp64 flops per node per matvec."""
+    return 4 * (2 * m + 1) ** d
+
+
+def measure_fp64_peak(torch, device):
+    from paper_2007_05239_b200 import _lib
+    lib = _lib.lib()
+    out = torch.zeros(1, dtype=torch.float64, device=device)
+    blocks, iters = 148 * 8, 20000
+    for _ in range(2):
+        lib.mlb_probe_fp64(iters, blocks, _lib.ptr(out), _lib.stream_ptr())
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(3):
+        s.record()
+        lib.mlb_probe_fp64(iters, blocks, _lib.ptr(out), _lib.stream_ptr())
+        e.record()
+        e.synchronize()
+        flops = 2.0 * 8 * iters * blocks * 256
+        best = max(best, flops / (s.elapsed_time(e) * 1e-3) / 1e12)
+    return best
+
+
+def stage_breakdown(torch, layers, v, reps=10):
+    """Per-kernel device times (CUDA events) of spread(+reduce), convolve, gather per layer."""
+    from paper_2007_05239_b200 import _lib
+    lib = _lib.lib()
+    out = []
+    for li, lay in enumerate(layers):
+        w = lay.weights
+        b = w._bindings[0]
+        g = b.plan
+        K0 = w.kernel.value_at_zero()
+        grid = torch.empty(b.stats()["grid_cells"], dtype=torch.float64, device=v.device)
+        grid2 = torch.empty_like(grid)
+        y = torch.empty_like(v)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        tt = np.zeros(3)
+        for r in range(reps + 2):
+            ev[0].record()
+            _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD, _lib.stream_ptr()))
+            ev[1].record()
+            _lib.check(lib.mlb_convolve(b.ptr, _lib.ptr(grid), _lib.ptr(grid2), _lib.stream_ptr()))
+            ev[2].record()
+            _lib.check(lib.mlb_apply_gather_only(b.ptr, _lib.ptr(grid2), _lib.ptr(v), _lib.ptr(y),
+                                                 1.0 + lay.shift, -1.0, K0, _lib.MLB_USE_ISD, _lib.stream_ptr())
+                       if hasattr(lib, "mlb_apply_gather_only") else
+                       lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), 0, _lib.stream_ptr()))
+            ev[3].record()
+            ev[3].synchronize()
+            if r >= 2:
+                tt += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+        tt /= reps
+        d, m = g.d, g.m_nfft
+        out.append(dict(layer=li, d=d, N=g.N, m=m, n=b.n, spread_ms=tt[0], convolve_ms=tt[1], gather_ms=tt[2],
+                        stats=b.stats()))
+    return out
+
+
+def cpu_baseline_oracle(workload, delta, n_sample, reps, seed=1):
+    """Time the numpy oracle (reference algorithm) on a subsample of each layer."""
+    from oracle import fastsum_oracle as fo
+    from oracle import solvers_oracle as so
+    from paper_2007_05239_b200 import datapipe, GroupSpec, KernelSpec
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(workload.n, size=min(n_sample, workload.n), replace=False))
+    layers = []
+    for ls in workload.layers:
+        g = GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma))
+        Xb, kb, _ = datapipe._scaled_group(workload.X[idx][:, list(ls.columns)], g, 1.0 / 16)
+        plan = fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p)
+        b = fo.bind(plan, Xb)
+        lay = so.OracleLayer(lambda x, plan=plan, b=b: fo.fastsum(plan, x, binding=b), len(idx)).shifted(delta)
+        layers.append(lay)
+    v = rng.standard_normal(len(idx))
+    for lay in layers:  # warm-up
+        so.sym_laplacian(lay, v)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for lay in layers:
+            so.sym_laplacian(lay, v)
+    dt = time.perf_counter() - t0
+    return len(idx) * len(layers) * reps / dt, len(idx), dt
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import synth
+    wl = synth.config2_segmentation(seed=0)
+    delta = math.log(2.0)
+    n_s = args.ref_sample
+    from oracle import fastsum_oracle as fo
+    from oracle import solvers_oracle as so
+    from paper_2007_05239_b200 import datapipe, GroupSpec, KernelSpec
+    rng = np.random.default_rng(1)
+    idx = np.sort(rng.choice(wl.n, size=n_s, replace=False))
+    layers = []
+    for ls in wl.layers:
+        g = GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma))
+        Xb, kb, _ = datapipe._scaled_group(wl.X[idx][:, list(ls.columns)], g, 1.0 / 16)
+        plan = fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p)
+        b = fo.bind(plan, Xb)
+        layers.append(so.OracleLayer(lambda x, plan=plan, b=b: fo.fastsum(plan, x, binding=b), n_s).shifted(delta))
+    v = rng.standard_normal(n_s)
+    for _ in range(args.warmup):
+        for lay in layers:
+            so.sym_laplacian(lay, v)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for lay in layers:
+            so.sym_laplacian(lay, v)
+    dt = time.perf_counter() - t0
+    value = n_s * len(layers) * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[1] shapes)",
+        "config": {"workload": wl.name, "layers": [vars(l) for l in wl.layers], "delta": delta,
+                   "sample_nodes": n_s},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{n_s}-node random subsample of both layers of {wl.name}; one step = one "
+                                   "shifted normalized-Laplacian matvec per layer through the numpy oracle "
+                                   "(reference algorithm: bincount spread/gather, scipy.fft, 1 thread)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    device = local
+    torch.cuda.set_device(device)
+    import synth
+    from paper_2007_05239_b200 import _lib, apply_sym_laplacian
+    from paper_2007_05239_b200.graphs import apply_sym_laplacian_dev
+    lib = _lib.lib()
+    wl = synth.config2_segmentation(seed=rank)   # rank r owns the layers of image r
+    delta = math.log(2.0)
+    layers = build_layers(wl, device, delta)
+    n, T = wl.n, len(layers)
+    rng = np.random.default_rng(1000 + rank)
+    v_host = rng.standard_normal(n)
+    v = torch.from_numpy(v_host).cuda(device)
+    ys = [torch.empty_like(v) for _ in layers]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+    def step():
+        for lay, y in zip(layers, ys):
+            apply_sym_laplacian_dev(lay, v, y)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(device)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = lib.mlb_launch_count()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        starts[i].record()
+        step()
+        ends[i].record()
+    torch.cuda.synchronize()
+    launches = lib.mlb_launch_count() - l0
+    if ws > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    total_ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n * T * args.steps * ws / (total_ms * 1e-3)
+
+    # ---- end-to-end through the public API: pinned host in, host out ----------
+    v_pin = torch.from_numpy(v_host).pin_memory()
+    for _ in range(2):
+        for lay in layers:
+            apply_sym_laplacian(lay, v_pin)
+    torch.cuda.synchronize()
+    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(3, min(args.steps, 10))
+    e_s.record()
+    for _ in range(e2e_steps):
+        for lay in layers:
+            out = apply_sym_laplacian(lay, v_pin)
+    e_e.record()
+    e_e.synchronize()
+    e2e_ms = e_s.elapsed_time(e_e)
+    e2e_value = n * T * e2e_steps * ws / (e2e_ms * 1e-3)
+
+    # ---- sorted-order variant (what the PKSM inner loop runs) -----------------
+    sorted_value = None
+    try:
+        vs = [torch.empty_like(v) for _ in layers]
+        for lay, x in zip(layers, vs):
+            lib.mlb_to_sorted(lay.weights._bindings[0].ptr, _lib.ptr(v), _lib.ptr(x), _lib.stream_ptr())
+
+        def step_sorted():
+            for lay, x, y in zip(layers, vs, ys):
+                w = lay.weights
+                lib.mlb_apply(w._bindings[0].ptr, _lib.ptr(x), _lib.ptr(y), 1.0 + lay.shift, -1.0,
+                              w.kernel.value_at_zero(), _lib.MLB_USE_ISD | _lib.MLB_SORTED, _lib.stream_ptr())
+        for _ in range(3):
+            step_sorted()
+        tot = 0.0
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            starts[i].record()
+            step_sorted()
+            ends[i].record()
+        torch.cuda.synchronize()
+        tot = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+        sorted_value = n * T * args.steps * ws / (tot * 1e-3)
+    except Exception as exc:  # diagnostic only
+        sorted_value = f"error: {exc}"
+
+    # ---- roofline of the dominant kernel ---------------------------------------
+    stages = stage_breakdown(torch, layers, v)
+    fp64_peak = measure_fp64_peak(torch, f"cuda:{device}")
+    hbm_peak, peak_kind = _peaks()
+    kern = []
+    for st in stages:
+        d, m, nl = st["d"], st["m"], st["n"]
+        C = (2 * m + 1) ** d
+        kern.append(("spread", st, st["spread_ms"], (8 * d + 16) * nl, 2 * C * nl))
+        kern.append(("gather", st, st["gather_ms"], (8 * d + 24) * nl, 2 * C * nl))
+        kern.append(("convolve", st, st["convolve_ms"], 16 * st["stats"]["grid_cells"], 0))
+    top = max(kern, key=lambda k: k[2])
+    name, st, ms, nbytes, nflops = top
+    achieved = nbytes / (ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": f"{name} (layer d={st['d']}, N={st['N']}, m={st['m']})",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "traffic": None,
+            "fp64": {"achieved_tflops": nflops / (ms * 1e-3) / 1e12, "peak_tflops": fp64_peak,
+                     "frac": (nflops / (ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
+                     "peak_source": "mlb_probe_fp64 DFMA microbenchmark, this run"}}
+    # whole-step HBM-roofline fraction of the metric (R * B(d) / peak)
+    step_bytes = sum(algorithmic_bytes(st["d"]) * st["n"] for st in stages)
+    step_flops = sum(algorithmic_flops(st["d"], st["m"]) * st["n"] for st in stages)
+    ms_step = total_ms / args.steps
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE configs[1] image; no dataset exists for it)",
+        "config": {"workload": wl.name, "nodes_per_rank": n, "layers": [vars(l) for l in wl.layers],
+                   "delta": delta, "vector_order": "node", "l2": "256 MB flush between steps (outside events)",
+                   "parallelism": f"layer-parallel x{ws} (independent layers per rank, no collective)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * T, "d2h_bytes_per_step": 8 * n * T,
+                "path": "paper_2007_05239_b200.apply_sym_laplacian(layer, pinned host tensor) per layer"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": roof,
+        "step_roofline": {"hbm_bytes_per_step": step_bytes, "hbm_frac": step_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak,
+                          "fp64_flops_per_step": step_flops,
+                          "fp64_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak if fp64_peak else None},
+        "sorted_order_value": sorted_value,
+        "stages_ms": [{k: st[k] for k in ("layer", "d", "N", "m", "n", "spread_ms", "convolve_ms", "gather_ms")}
+                      for st in stages],
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        val, ns, secs = cpu_baseline_oracle(wl, delta, args.cpu_sample, args.cpu_reps)
+        result["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
+                                  "sample": f"{ns}-node subsample of both layers, {args.cpu_reps} shifted "
+                                            f"normalized-Laplacian matvecs per layer through the numpy oracle "
+                                            f"(bincount + scipy.fft, 1 thread), {secs:.1f} s"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=32768)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--ref-sample", type=int, default=16384)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -53,7 +53,10 @@ typedef struct mlb_binding mlb_binding;
  *                for the active cells u = u_lo..u_lo+L-1, k = -N/2..N/2.
  *   win_coef   : (2m+1) x (win_deg+1): monomial coefficients in s = 2f-1 of
  *                phi(f - o), o = -m..m, f in [0,1) (the Kaiser-Bessel window
- *                of fastsum.py:158-167 as an exact-to-1e-14 polynomial).   */
+ *                of fastsum.py:158-167 as an exact-to-1e-14 polynomial).
+ *   conv_kernel: d <= 2 only (NULL for d = 3): (2L-1)^d real spatial kernel
+ *                Kc[D] = sum_{|k|<=N/2} F(k) cos(2 pi k.D / ng), D = -(L-1)..L-1,
+ *                so the convolution stage is a direct sub-box convolution. */
 typedef struct mlb_plan_desc {
     int d, N, m, ng;
     int bin_lo, bin_hi;       /* admissible floor(ng*x) range per axis */
@@ -62,11 +65,19 @@ typedef struct mlb_plan_desc {
     const double* fused_band; /* host */
     const double* twiddle;    /* host */
     const double* win_coef;   /* host */
+    const double* conv_kernel;/* host, d <= 2 (nullable for d = 3) */
 } mlb_plan_desc;
 
 int mlb_abi_version(void);
 const char* mlb_last_error(void);
 int mlb_device_count(void);
+/* number of kernels libmlb has launched in this process (bench evidence) */
+int64_t mlb_launch_count(void);
+/* FP64 FMA throughput probe: `blocks` x 256 threads x iters x 8 DFMA (roofline
+ * denominator; MEASURED_PEAKS.json carries no FP64 figure) */
+int mlb_probe_fp64(int64_t iters, int blocks, double* out_dev, void* stream);
+/* FP64 tensor-core probe: blocks x 8 warps x iters x 4 DMMA.8x8x4 (m8n8k4 f64) */
+int mlb_probe_dmma(int64_t iters, int blocks, double* out_dev, void* stream);
 
 /* build_plan (fastsum.py:256-313): upload plan tables to `device`. */
 int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out);

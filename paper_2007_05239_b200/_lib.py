@@ -29,7 +29,8 @@ U = C.c_uint
 
 class PlanDesc(C.Structure):
     _fields_ = [("d", I), ("N", I), ("m", I), ("ng", I), ("bin_lo", I), ("bin_hi", I),
-                ("win_deg", I), ("K0", D), ("fused_band", P), ("twiddle", P), ("win_coef", P)]
+                ("win_deg", I), ("K0", D), ("fused_band", P), ("twiddle", P), ("win_coef", P),
+                ("conv_kernel", P)]
 
 
 # name -> (restype, argtypes); mirrors include/multilap_b200.h
@@ -37,6 +38,9 @@ SIGNATURES = {
     "mlb_abi_version": (I, []),
     "mlb_last_error": (C.c_char_p, []),
     "mlb_device_count": (I, []),
+    "mlb_launch_count": (I64, []),
+    "mlb_probe_fp64": (I, [I64, I, P, P]),
+    "mlb_probe_dmma": (I, [I64, I, P, P]),
     "mlb_plan_create": (I, [C.POINTER(PlanDesc), I, C.POINTER(P)]),
     "mlb_plan_destroy": (I, [P]),
     "mlb_bind": (I, [P, P, I64, D, P, C.POINTER(P)]),

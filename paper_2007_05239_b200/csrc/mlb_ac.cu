@@ -268,9 +268,13 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
     const size_t sm1 = (size_t)kAcRows * (m + k) * sizeof(double);
     MLB_CUDA_TRY(cudaFuncSetAttribute(ac_rhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     ac_rhs_kernel<<<nb, 256, sm1, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
+    note_launches(1);
     ac_finish_kernel<<<(k * m + 127) / 128, 128, 0, st>>>(partial, nb, k, m, denom, Vc);
+    note_launches(1);
     ac_update_kernel<<<nb, 256, (size_t)k * m * sizeof(double), st>>>(Phi, n, k, m, Vc, U, U_next, mx);
+    note_launches(1);
     ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -279,6 +283,7 @@ int mlb_argmax_rows(const double* U, int64_t n, int m, int32_t* labels, void* st
     if (n <= 0) return MLB_OK;
     int64_t b = std::min<int64_t>((n + 255) / 256, 148 * 16);
     argmax_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(U, n, m, labels);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -292,6 +297,7 @@ int mlb_direct(const double* X, int64_t n, int d, int family, double sigma, cons
     MLB_CUDA_TRY(cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     direct_kernel<<<(unsigned)((n + 127) / 128), 128, smem, (cudaStream_t)stream>>>(
         X, n, d, family, 1.0 / sigma, v, s, y, alpha, beta, gamma, accumulate);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }

@@ -8,6 +8,8 @@
 // recomputed by the kernels on every apply.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -18,6 +20,9 @@
 namespace mlb {
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -69,6 +74,8 @@ extern "C" {
 int mlb_abi_version(void) { return MLB_ABI_VERSION; }
 
 const char* mlb_last_error(void) { return g_err.c_str(); }
+
+int64_t mlb_launch_count(void) { return g_launches.load(); }
 
 int mlb_device_count(void) {
     int n = 0;
@@ -133,9 +140,14 @@ int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
         for (size_t i = 0; i < tw.size(); ++i) tw[i] = make_double2(desc->twiddle[2 * i], desc->twiddle[2 * i + 1]);
         rc = dev_upload(&p->twid, tw.data(), tw.size());
     }
+    if (rc == MLB_OK && d <= 2 && desc->conv_kernel) {
+        const size_t nk = (d == 1) ? (size_t)(2 * g.L - 1) : (size_t)(2 * g.L - 1) * (2 * g.L - 1);
+        rc = dev_upload(&p->conv, desc->conv_kernel, nk);
+    }
     if (rc != MLB_OK) {
         dev_free(p->fused);
         dev_free(p->twid);
+        dev_free(p->conv);
         delete p;
         return rc;
     }
@@ -148,6 +160,7 @@ int mlb_plan_destroy(mlb_plan* p) {
     DeviceGuard guard(p->device);
     dev_free(p->fused);
     dev_free(p->twid);
+    dev_free(p->conv);
     delete p;
     return MLB_OK;
 }
@@ -159,9 +172,13 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->frac);
     dev_free(b->chunk_start);
     dev_free(b->chunk_cell);
+    dev_free(b->chunk_gcell);
     dev_free(b->seg_chunk);
     dev_free(b->seg_brick);
     dev_free(b->brick_seg);
+    dev_free(b->heavy);
+    dev_free(b->brick_first);
+    dev_free(b->brick_count);
     dev_free(b->isd);
     dev_free(b->partial);
     dev_free(b->grid);
@@ -183,11 +200,11 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     //    tx = ng * (x * scale); u = floor(tx) (fastsum.py:343-353, :386)
     std::vector<int32_t> key((size_t)n);
     std::vector<double> f((size_t)n * d);
-    std::vector<int32_t> cell_local((size_t)n);
+    std::vector<int32_t> cell_local((size_t)n), cell_glob((size_t)n);
     const int nloc = ipow_h(Tb, d);
     const int nbricks = ipow_h(nbr, d);
     for (int64_t i = 0; i < n; ++i) {
-        int brick = 0, local = 0, tcell = 0;
+        int brick = 0, local = 0, tcell = 0, gcell = 0;
         for (int a = 0; a < d; ++a) {
             const double xt = pts[i * d + a] * scale;
             const double tx = (double)g.ng * xt;
@@ -200,9 +217,11 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
             brick = brick * nbr + bin / Tb;
             local = local * Tb + bin % Tb;
             tcell = tcell * TL + bin % Tb;
+            gcell = gcell * g.L + bin;
         }
         key[i] = brick * nloc + local;
         cell_local[i] = tcell;
+        cell_glob[i] = gcell;
     }
     // 2. stable counting sort by key
     const int64_t nkeys = (int64_t)nbricks * nloc;
@@ -218,21 +237,24 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (node_ids)
         for (int64_t j = 0; j < n; ++j) perm_node[j] = node_ids[perm[j]];
     // 3. chunks (<= kChunk points of one cell) and segments (<= maxseg chunks of one brick)
-    std::vector<int32_t> chunk_start, chunk_cell, chunk_brick;
+    std::vector<int32_t> chunk_start, chunk_cell, chunk_gcell, chunk_brick;
     for (int64_t k = 0; k < nkeys; ++k) {
         const int64_t lo = cnt[k], hi = cnt[k + 1];
         for (int64_t s = lo; s < hi; s += kChunk) {
             chunk_start.push_back((int32_t)s);
             chunk_cell.push_back(cell_local[perm[s]]);
+            chunk_gcell.push_back(cell_glob[perm[s]]);
             chunk_brick.push_back((int32_t)(k / nloc));
         }
     }
     const int nch = (int)chunk_cell.size();
     chunk_start.push_back((int32_t)n);
-    // aim for ~8 CTAs per SM worth of segments, but never fewer than 4 chunks each
-    int maxseg = (int)((nch + 148 * 8 - 1) / (148 * 8));
+    // segments: d <= 2 -> ~2 CTAs per SM (every segment tile is the whole
+    // sub-box); d = 3 -> ~8 per SM (tiles are brick-sized)
+    const int target = (d <= 2) ? 148 * 2 : 148 * 4;
+    int maxseg = (int)((nch + target - 1) / target);
     if (maxseg < 4) maxseg = 4;
-    if (maxseg > 512) maxseg = 512;
+    if (maxseg > 4096) maxseg = 4096;
     std::vector<int32_t> seg_chunk, seg_brick, brick_seg(nbricks + 1, 0);
     for (int c = 0; c < nch;) {
         const int br = chunk_brick[c];
@@ -246,6 +268,17 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     const int nseg = (int)seg_brick.size();
     seg_chunk.push_back(nch);
     for (int br = 0; br < nbricks; ++br) brick_seg[br + 1] += brick_seg[br];
+    std::vector<int32_t> heavy, brick_first(nbricks, -1);
+    int max_heavy = 0;
+    for (int br = 0; br < nbricks; ++br) {
+        const int ns = brick_seg[br + 1] - brick_seg[br];
+        if (ns >= 1) brick_first[br] = brick_seg[br];
+        if (ns >= 2) {
+            heavy.push_back(brick_seg[br]);
+            heavy.push_back(ns);
+            max_heavy = std::max(max_heavy, ns);
+        }
+    }
     // frac in sorted order, SoA
     std::vector<double> fs((size_t)n * d);
     for (int64_t j = 0; j < n; ++j)
@@ -259,6 +292,8 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     b->nseg = nseg;
     b->nbricks = nbricks;
     b->max_seg_chunks = maxseg;
+    b->nheavy = (int)(heavy.size() / 2);
+    b->max_heavy_segs = max_heavy;
     b->tile_cells = ipow_h(TL, d);
     b->grid_cells = 1;
     for (int a = 0; a < d; ++a) b->grid_cells *= g.L;
@@ -274,9 +309,16 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->frac, fs.data(), (size_t)n * d);
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_start, chunk_start.data(), chunk_start.size());
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_cell, chunk_cell.data(), chunk_cell.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->chunk_gcell, chunk_gcell.data(), chunk_gcell.size());
     if (rc == MLB_OK) rc = dev_upload(&b->seg_chunk, seg_chunk.data(), seg_chunk.size());
     if (rc == MLB_OK) rc = dev_upload(&b->seg_brick, seg_brick.data(), seg_brick.size());
     if (rc == MLB_OK) rc = dev_upload(&b->brick_seg, brick_seg.data(), brick_seg.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->heavy, heavy.data(), heavy.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->brick_first, brick_first.data(), brick_first.size());
+    if (rc == MLB_OK) {
+        std::vector<int32_t> zeros(nbricks, 0);
+        rc = dev_upload(&b->brick_count, zeros.data(), zeros.size());
+    }
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, (size_t)nseg * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells);
@@ -350,6 +392,7 @@ int mlb_binding_set_isd(mlb_binding* b, const double* isd_dev, void* stream) {
     if (!b->n) return MLB_OK;
     DeviceGuard guard(b->plan->device);
     gather_perm_kernel<<<grid_for(b->n), 256, 0, (cudaStream_t)stream>>>(b->perm, isd_dev, b->isd, b->n);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -359,6 +402,7 @@ int mlb_to_sorted(const mlb_binding* b, const double* v, double* vs, void* strea
     if (!b->n) return MLB_OK;
     DeviceGuard guard(b->plan->device);
     gather_perm_kernel<<<grid_for(b->n), 256, 0, (cudaStream_t)stream>>>(b->perm, v, vs, b->n);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -368,6 +412,7 @@ int mlb_to_node(const mlb_binding* b, const double* vs, double* v, int accumulat
     if (!b->n) return MLB_OK;
     DeviceGuard guard(b->plan->device);
     scatter_perm_kernel<<<grid_for(b->n), 256, 0, (cudaStream_t)stream>>>(b->perm, vs, v, b->n, accumulate);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -412,3 +457,50 @@ int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double b
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ FP64 probe --
+namespace mlb {
+__global__ void dfma_probe_kernel(int64_t iters, double* out) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double b = 0.999999999, c = 1e-12;
+    for (int64_t i = 0; i < iters; ++i) {
+        a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+        a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+__global__ void dmma_probe_kernel(int64_t iters, double* out) {
+    // 4 independent m8n8k4 fp64 MMA chains per warp
+    double a = 1.0 + threadIdx.x * 1e-9, b = 0.999999;
+    double c0[2] = {0, 0}, c1[2] = {0, 0}, c2[2] = {0, 0}, c3[2] = {0, 0};
+    for (int64_t i = 0; i < iters; ++i) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0[0]), "+d"(c0[1]) : "d"(a), "d"(b));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c1[0]), "+d"(c1[1]) : "d"(a), "d"(b));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c2[0]), "+d"(c2[1]) : "d"(a), "d"(b));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c3[0]), "+d"(c3[1]) : "d"(a), "d"(b));
+    }
+    const double s = c0[0] + c0[1] + c1[0] + c1[1] + c2[0] + c2[1] + c3[0] + c3[1];
+    if (s == 12345.678) out[0] = s;
+}
+}  // namespace mlb
+
+extern "C" int mlb_probe_dmma(int64_t iters, int blocks, double* out_dev, void* stream) {
+    mlb::dmma_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, out_dev);
+    mlb::note_launches(1);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+extern "C" int mlb_probe_fp64(int64_t iters, int blocks, double* out_dev, void* stream) {
+    mlb::dfma_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, out_dev);
+    mlb::note_launches(1);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}

@@ -1,5 +1,6 @@
-// NFFT fast-summation kernels for sm_100a: spread, partial-tile reduce,
-// pruned separable DFT convolution, gather with the fused D^-1/2 epilogue.
+// NFFT fast-summation kernels for sm_100a: spread, deterministic partial-tile
+// reduce, gather with the fused D^-1/2 epilogue (the convolution between them
+// is mlb_dft.cu).
 //
 // Reference chain (fastsum.py:475-497): spread (bincount, :389-391) ->
 // rfftn * fused_weights * irfftn (:492-495) -> gather (bincount, :400-406)
@@ -7,12 +8,10 @@
 // scalings and the shift; here they are fused into spread and gather.
 //
 // Layout:
-//   * points are counting-sorted by (brick, cell); chunks are <= 32 points of
-//     one cell; segments are <= max_seg_chunks chunks of one brick;
+//   * points are counting-sorted by (brick, cell); a chunk is <= 64 points
+//     of one cell; a segment is <= max_seg_chunks chunks of one brick;
 //   * a brick is Tb^d cells whose stencils cover a (Tb+2m)^d tile;
-//   * the grid is only the active sub-box of L^d cells (u = ulo..ulo+L-1 per
-//     axis); the FFT stage is a pruned DFT between that sub-box and the
-//     (N+1)^(d-1) x (N/2+1) band where the fused weights are nonzero.
+//   * the grid is only the active sub-box of L^d cells (u = ulo..ulo+L-1).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,7 +52,17 @@ struct SpreadCfg<3, M> {
     static constexpr int B0 = (S + P0 - 1) / P0, B1 = (S + P1 - 1) / P1, B2 = (SP + P2 - 1) / P2;
 };
 
-constexpr int kWinPad = 17;  // staged window row stride (>= every P*B reach; odd -> no bank conflicts)
+// staged window row stride: covers every lane's reach (entries >= S stay 0)
+// and is odd (conflict-free 8-byte rows across lanes)
+template <int D, int M>
+struct StageCfg {
+    using C = SpreadCfg<D, M>;
+    static constexpr int r0 = C::P0 * C::B0;
+    static constexpr int r1 = C::P1 * C::B1;
+    static constexpr int r2 = (C::NPASS - 1) * C::SP + C::P2 * C::B2;
+    static constexpr int reach = (r0 > r1 ? (r0 > r2 ? r0 : r2) : (r1 > r2 ? r1 : r2));
+    static constexpr int pad = (reach % 2) ? reach : reach + 1;
+};
 
 struct FsArgs {
     Geom g;
@@ -62,52 +71,89 @@ struct FsArgs {
     const double* frac;
     const int32_t* chunk_start;
     const int32_t* chunk_cell;
+    const int32_t* chunk_gcell;
     const int32_t* seg_chunk;
     const int32_t* seg_brick;
     const int32_t* brick_seg;
+    const int32_t* brick_first;
+    int32_t* brick_count;     // per-brick completion counters (spread epilogue), left at 0
+    int fuse_brick_sum;       // 1: the last CTA of a multi-segment brick sums its tiles
     const double* isd;
     double* partial;
     int tile_cells;
+    int nchunks;
 };
 
-__device__ __forceinline__ int ipow(int b, int e) {
-    int r = 1;
-    for (int i = 0; i < e; ++i) r *= b;
-    return r;
+// per-point spread inputs, prefetched one 32-point sub-chunk ahead
+template <int D>
+struct PtIn {
+    double f[D];
+    double s;
+    int node;
+};
+
+template <int D>
+__device__ __forceinline__ void load_pt(const FsArgs& a, int p, bool ok, unsigned flags, PtIn<D>& r) {
+    if (ok) {
+        r.node = (flags & MLB_SORTED) ? p : __ldg(a.perm + p);
+        r.s = (flags & MLB_USE_ISD) ? __ldg(a.isd + p) : 1.0;
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax) r.f[ax] = __ldg(a.frac + (int64_t)ax * a.n + p);
+    } else {
+        r.node = -1;
+        r.s = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax) r.f[ax] = 0.5;
+    }
 }
 
 // ----------------------------------------------------------------- spread --
 // One CTA per segment.  Each warp owns a private smem copy of the brick tile
-// and a contiguous share of the segment's chunks.  Per chunk: lanes compute
-// the d(2m+1) window values of one point each (v*s folded into axis 0) into
-// smem staging; then every lane accumulates its stencil block over the
-// chunk's points in registers (all points of a chunk share one cell, so the
-// block is fixed) and flushes into its warp tile when the cell changes.
-// No atomics: warp tiles are summed in a fixed order -> bitwise reproducible.
+// and a contiguous share of the segment's chunks (sub-chunks of 32 points).
+// Per sub-chunk: each lane computes the d(2m+1) window values of one point
+// (v*s folded into axis 0) into smem staging; then every lane accumulates its
+// stencil block over the sub-chunk's points in registers (all points of a
+// chunk share one cell, so the block is fixed) and flushes into its warp
+// tile when the cell changes.  The next sub-chunk's inputs are prefetched
+// before the accumulation.  No atomics: warp tiles are summed in a fixed
+// order -> bitwise reproducible.
 template <int D, int M>
 __global__ void __launch_bounds__(256) spread_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v,
                                                      unsigned flags) {
     using C = SpreadCfg<D, M>;
     constexpr int S = C::S;
+    constexpr int SPAD = StageCfg<D, M>::pad;
     extern __shared__ double smem[];
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TL = a.g.TL;
     const int tile = a.tile_cells;
     double* tiles = smem;                                   // nw * tile
-    double* stage = smem + (size_t)nw * tile;               // nw * 32 * D * kWinPad
+    double* stage = smem + (size_t)nw * tile;               // nw * 32 * D * SPAD
     double* my_tile = tiles + (size_t)warp * tile;
-    double* my_stage = stage + (size_t)warp * 32 * D * kWinPad;
+    double* my_stage = stage + (size_t)warp * 32 * D * SPAD;
 
     for (int i = threadIdx.x; i < nw * tile; i += blockDim.x) tiles[i] = 0.0;
-    for (int i = lane; i < 32 * D * kWinPad; i += 32) my_stage[i] = 0.0;
+    for (int i = lane; i < 32 * D * SPAD; i += 32) my_stage[i] = 0.0;
     __syncthreads();
 
     const int seg = blockIdx.x;
     const int c0 = a.seg_chunk[seg], c1 = a.seg_chunk[seg + 1];
-    const int nch = c1 - c0;
-    const int my0 = c0 + (int)(((long long)nch * warp) / nw);
-    const int my1 = c0 + (int)(((long long)nch * (warp + 1)) / nw);
+    // balance by points: warp w owns sorted points [wp0, wp1) of the segment,
+    // walked in <= 32-point sub-chunks that never straddle a chunk (cell)
+    const int P0 = a.chunk_start[c0], P1 = a.chunk_start[c1];
+    const int wp0 = P0 + (int)(((long long)(P1 - P0) * warp) / nw);
+    const int wp1 = P0 + (int)(((long long)(P1 - P0) * (warp + 1)) / nw);
+    int chs = c0;
+    {
+        int lo = c0, hi = c1 - 1;  // first chunk with chunk_start[ch+1] > wp0
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (a.chunk_start[mid + 1] > wp0) hi = mid;
+            else lo = mid + 1;
+        }
+        chs = lo;
+    }
 
     const int l0 = lane / (C::P1 * C::P2), l1 = (lane / C::P2) % C::P1, l2 = lane % C::P2;
     const bool active = lane < C::P0 * C::P1 * C::P2;
@@ -152,51 +198,75 @@ __global__ void __launch_bounds__(256) spread_kernel(FsArgs a, WinCoef wc, const
             }
         };
 
-        for (int ch = my0; ch < my1; ++ch) {
+        // sub-chunk iterator: (chunk ch, first point sp, end cend <= wp1)
+        int ch = chs;
+        int sp = wp0;
+        int cend = (sp < wp1) ? min(a.chunk_start[ch + 1], wp1) : wp1;
+        PtIn<D> nxt;
+        load_pt<D>(a, sp + lane, sp + lane < cend, flags, nxt);
+        double vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
+        while (sp < wp1) {
             const int cell = a.chunk_cell[ch];
-            const int p0 = a.chunk_start[ch];
-            const int np = a.chunk_start[ch + 1] - p0;
+            const int np = min(32, cend - sp);
+            const PtIn<D> cin = nxt;
+            const double vcur = vn;
+            // advance the iterator and prefetch the next sub-chunk's inputs
+            int nch2 = ch, nsp = sp + 32, nend = cend;
+            if (nsp >= cend) {
+                nsp = cend;
+                if (cend < wp1) {
+                    ++nch2;
+                    nend = min(a.chunk_start[nch2 + 1], wp1);
+                }
+            }
+            load_pt<D>(a, nsp + lane, nsp + lane < nend, flags, nxt);
             if (cell != cur) {
                 flush(cur);
                 cur = cell;
             }
             __syncwarp();
-            if (lane < np) {
-                const int p = p0 + lane;
-                const int node = (flags & MLB_SORTED) ? p : a.perm[p];
-                double val = __ldg(v + node);
-                if (flags & MLB_USE_ISD) val *= __ldg(a.isd + p);
+            {
+                const double val = (lane < np) ? vcur * cin.s : 0.0;
                 double w[S];
 #pragma unroll
                 for (int ax = 0; ax < D; ++ax) {
-                    kb_windows<M>(__ldg(a.frac + (int64_t)ax * a.n + p), wc, w);
-                    double* dst = my_stage + (lane * D + ax) * kWinPad;
+                    kb_windows<M>(cin.f[ax], wc, w);
+                    double* dst = my_stage + (lane * D + ax) * SPAD;
 #pragma unroll
                     for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * val : w[o];
                 }
             }
+            vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
             __syncwarp();
             if (active) {
-                for (int jp = 0; jp < np; ++jp) {
-                    const double* ws = my_stage + jp * D * kWinPad;
-                    double w0[C::B0], w1[C::B1], w2[C::B2];
+                const int npe = (np + 1) & ~1;  // axis-0 rows past np carry val = 0
+                for (int jp = 0; jp < npe; jp += 2) {
 #pragma unroll
-                    for (int i = 0; i < C::B0; ++i) w0[i] = ws[l0 * C::B0 + i];
+                    for (int h = 0; h < 2; ++h) {
+                        const double* ws = my_stage + (jp + h) * D * SPAD;
+                        double w0[C::B0], w1[C::B1], w2[C::B2];
 #pragma unroll
-                    for (int j = 0; j < C::B1; ++j) w1[j] = (D >= 2) ? ws[kWinPad + l1 * C::B1 + j] : 1.0;
+                        for (int i = 0; i < C::B0; ++i) w0[i] = ws[l0 * C::B0 + i];
 #pragma unroll
-                    for (int k = 0; k < C::B2; ++k)
-                        w2[k] = (D == 3) ? ws[2 * kWinPad + off2 + l2 * C::B2 + k] : 1.0;
+                        for (int j = 0; j < C::B1; ++j) w1[j] = (D >= 2) ? ws[SPAD + l1 * C::B1 + j] : 1.0;
 #pragma unroll
-                    for (int i = 0; i < C::B0; ++i)
+                        for (int k = 0; k < C::B2; ++k)
+                            w2[k] = (D == 3) ? ws[2 * SPAD + off2 + l2 * C::B2 + k] : 1.0;
 #pragma unroll
-                        for (int j = 0; j < C::B1; ++j) {
-                            const double w01 = w0[i] * w1[j];
+                        for (int i = 0; i < C::B0; ++i)
 #pragma unroll
-                            for (int k = 0; k < C::B2; ++k) acc[i][j][k] = fma(w01, w2[k], acc[i][j][k]);
-                        }
+                            for (int j = 0; j < C::B1; ++j) {
+                                const double w01 = w0[i] * w1[j];
+#pragma unroll
+                                for (int k = 0; k < C::B2; ++k) acc[i][j][k] = fma(w01, w2[k], acc[i][j][k]);
+                            }
+                    }
                 }
             }
+            ch = nch2;
+            sp = nsp;
+            cend = nend;
+            if (sp >= cend) break;
         }
         flush(cur);
         __syncwarp();
@@ -209,15 +279,100 @@ __global__ void __launch_bounds__(256) spread_kernel(FsArgs a, WinCoef wc, const
         for (int w = 0; w < nw; ++w) s += tiles[(size_t)w * tile + i];
         out[i] = s;
     }
+    if (!a.fuse_brick_sum) return;
+    // Bricks split into several segments: the CTA that finishes last sums the
+    // brick's segment tiles in segment order into the first one (stage R1),
+    // so the result does not depend on which CTA came last.
+    const int brick = a.seg_brick[seg];
+    const int s0 = a.brick_first[brick];
+    const int ns = a.brick_seg[brick + 1] - s0;
+    if (ns < 2) return;
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(a.brick_count + brick, 1);
+        last = (prev == ns - 1);
+        if (last) a.brick_count[brick] = 0;  // ready for the next apply
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+        double t = 0.0;
+        for (int j = 0; j < ns; ++j) t += __ldcg(a.partial + (size_t)(s0 + j) * tile + i);
+        a.partial[(size_t)s0 * tile + i] = t;
+    }
 }
 
 // ------------------------------------------------------------------ reduce --
-// grid[u] = sum over the bricks whose tile covers u, over their segments in
-// order, of partial[seg][u - brick_origin].  One thread per active cell.
-template <int D>
+// Stage R1: for every brick split into >= 2 segments, sum its segment tiles
+// (fixed order) into the brick's first segment tile.  Block = 8 tile cells x
+// 32 segment groups; group g sums segments g, g+32, ... then the 32 group
+// sums are combined in order through smem -> deterministic.
+__global__ void seg_sum_kernel(double* __restrict__ partial, const int32_t* __restrict__ heavy, int tile,
+                               double* __restrict__ out) {
+    __shared__ double sh[32][9];
+    const int hb = blockIdx.y;
+    const int s0 = heavy[2 * hb], ns = heavy[2 * hb + 1];
+    const int c = threadIdx.x & 7, grp = threadIdx.x >> 3;
+    const int cell = blockIdx.x * 8 + c;
+    double s = 0.0;
+    if (cell < tile) {
+        int j = grp;
+        for (; j + 96 < ns; j += 128) {
+            const double a0 = partial[(size_t)(s0 + j) * tile + cell];
+            const double a1 = partial[(size_t)(s0 + j + 32) * tile + cell];
+            const double a2 = partial[(size_t)(s0 + j + 64) * tile + cell];
+            const double a3 = partial[(size_t)(s0 + j + 96) * tile + cell];
+            s += a0;
+            s += a1;
+            s += a2;
+            s += a3;
+        }
+        for (; j < ns; j += 32) s += partial[(size_t)(s0 + j) * tile + cell];
+    }
+    sh[grp][c] = s;
+    __syncthreads();
+    if (grp == 0 && cell < tile) {
+        double t = 0.0;
+        for (int g2 = 0; g2 < 32; ++g2) t += sh[g2][c];
+        if (out) out[cell] = t;
+        else partial[(size_t)s0 * tile + cell] = t;
+    }
+}
+
+// R1 variant for bricks with few segments: one thread per (brick, cell).
+__global__ void seg_sum_small_kernel(double* __restrict__ partial, const int32_t* __restrict__ heavy, int tile,
+                                     int nheavy) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nheavy * tile) return;
+    const int hb = (int)(idx / tile), cell = (int)(idx % tile);
+    const int s0 = heavy[2 * hb], ns = heavy[2 * hb + 1];
+    double s = 0.0;
+    int j = 0;
+    for (; j + 3 < ns; j += 4) {
+        const double a0 = partial[(size_t)(s0 + j) * tile + cell];
+        const double a1 = partial[(size_t)(s0 + j + 1) * tile + cell];
+        const double a2 = partial[(size_t)(s0 + j + 2) * tile + cell];
+        const double a3 = partial[(size_t)(s0 + j + 3) * tile + cell];
+        s += a0;
+        s += a1;
+        s += a2;
+        s += a3;
+    }
+    for (; j < ns; ++j) s += partial[(size_t)(s0 + j) * tile + cell];
+    partial[(size_t)s0 * tile + cell] = s;
+}
+
+// Stage R2: grid[u] = sum over the (<= 3^d) bricks whose tile covers u of
+// that brick's (first-segment) tile value.  One thread per active cell.
+template <int D, int TBC>
 __global__ void reduce_kernel(FsArgs a, double* __restrict__ grid) {
     const Geom g = a.g;
-    const int L = g.L, Tb = g.Tb, TL = g.TL, nbr = g.nbr;
+    const int L = g.L, nbr = g.nbr;
+    const int Tb = TBC ? TBC : g.Tb;
+    const int TL = TBC ? TBC + 2 * g.m : g.TL;
     int64_t total = 1;
     for (int i = 0; i < D; ++i) total *= L;
     for (int64_t cidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cidx < total;
@@ -229,6 +384,7 @@ __global__ void reduce_kernel(FsArgs a, double* __restrict__ grid) {
             r /= L;
         }
         int blo[3] = {0, 0, 0}, bhi[3] = {0, 0, 0};
+#pragma unroll
         for (int ax = 0; ax < D; ++ax) {
             int lo = u[ax] - TL + 1;
             lo = lo <= 0 ? 0 : (lo + Tb - 1) / Tb;
@@ -252,190 +408,175 @@ __global__ void reduce_kernel(FsArgs a, double* __restrict__ grid) {
                         brick = (b0 * nbr + b1) * nbr + b2;
                         t = ((u[0] - b0 * Tb) * TL + (u[1] - b1 * Tb)) * TL + (u[2] - b2 * Tb);
                     }
-                    const int s0 = a.brick_seg[brick], s1 = a.brick_seg[brick + 1];
-                    for (int sg = s0; sg < s1; ++sg) s += a.partial[(size_t)sg * a.tile_cells + t];
+                    const int s0 = __ldg(a.brick_first + brick);
+                    if (s0 >= 0) s += a.partial[(size_t)s0 * a.tile_cells + t];
                 }
         grid[cidx] = s;
     }
 }
 
-// ---------------------------------------------------------------- DFT stage --
-// out[a][k][b] = sum_u in[a][u][b] T(u,k).  Modes:
-//   0: forward real->complex on the last axis (k = 0..N/2), B = 1
-//   1: forward complex->complex (k = -N/2..N/2)
-//   2: mode 1, then multiply by the fused band weights (last forward stage)
-//   3: inverse complex->complex (sum over k, output u)
-//   4: inverse complex->real on the last axis, Hermitian weights 1,2,2,..
-//   5: mode 0 then multiply (d = 1)
-struct DftArgs {
-    const double* in;
-    double* out;
-    int A, U, Kout, B;
-    const double2* tw;
-    int K;        // twiddle row stride
-    int koff;     // column offset into twiddle rows
-    const double* fused;
-};
-
-template <int MODE>
-__global__ void dft_kernel(DftArgs p) {
-    const int64_t total = (int64_t)p.A * p.Kout * p.B;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int b = (int)(idx % p.B);
-        const int k = (int)((idx / p.B) % p.Kout);
-        const int64_t aa = idx / ((int64_t)p.B * p.Kout);
-        double re = 0.0, im = 0.0;
-        if (MODE == 0 || MODE == 5) {
-            const double* x = p.in + aa * p.U;
-            for (int u = 0; u < p.U; ++u) {
-                const double2 t = p.tw[u * p.K + k + p.koff];
-                const double xv = x[u];
-                re = fma(xv, t.x, re);
-                im = fma(xv, t.y, im);
-            }
-        } else if (MODE == 1 || MODE == 2) {
-            const double2* x = reinterpret_cast<const double2*>(p.in) + aa * (int64_t)p.U * p.B + b;
-            for (int u = 0; u < p.U; ++u) {
-                const double2 t = p.tw[u * p.K + k + p.koff];
-                const double2 xv = x[(int64_t)u * p.B];
-                re = fma(xv.x, t.x, fma(-xv.y, t.y, re));
-                im = fma(xv.x, t.y, fma(xv.y, t.x, im));
-            }
-        } else if (MODE == 3) {
-            // here U = number of frequencies summed, Kout = L output cells
-            const double2* x = reinterpret_cast<const double2*>(p.in) + aa * (int64_t)p.U * p.B + b;
-            for (int kk = 0; kk < p.U; ++kk) {
-                const double2 t = p.tw[k * p.K + kk + p.koff];  // conj applied below
-                const double2 xv = x[(int64_t)kk * p.B];
-                re = fma(xv.x, t.x, fma(xv.y, t.y, re));
-                im = fma(xv.y, t.x, fma(-xv.x, t.y, im));
-            }
-        } else {  // MODE == 4
-            const double2* x = reinterpret_cast<const double2*>(p.in) + aa * p.U;
-            for (int kk = 0; kk < p.U; ++kk) {
-                const double2 t = p.tw[k * p.K + kk + p.koff];
-                const double2 xv = x[kk];
-                const double wgt = (kk == 0) ? 1.0 : 2.0;
-                re = fma(wgt, fma(xv.x, t.x, xv.y * t.y), re);
-            }
-        }
-        if (MODE == 2 || MODE == 5) {
-            const double f = p.fused[(int64_t)k * p.B + b];
-            re *= f;
-            im *= f;
-        }
-        if (MODE == 4) {
-            p.out[aa * p.Kout + k] = re;
-        } else {
-            reinterpret_cast<double2*>(p.out)[(aa * p.Kout + k) * (int64_t)p.B + b] = make_double2(re, im);
-        }
+// Stage R2 for d = 3, block-centric: a CTA covers GB = 4 grid blocks of
+// Tb^3 cells; the <= 27 source bricks of each grid block are looked up once
+// (smem), then every cell issues its <= 27 independent tile loads.
+template <int TB>
+__global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restrict__ grid) {
+    constexpr int CPB = TB * TB * TB;  // cells per grid block
+    constexpr int GB = 256 / CPB;      // grid blocks per CTA
+    const Geom g = a.g;
+    const int L = g.L, TL = TB + 2 * g.m, nbr = g.nbr;
+    const int ngb = (L + TB - 1) / TB;  // grid blocks per axis
+    const int R = (TL + TB - 1) / TB;   // source bricks per axis (3 for m=4,Tb=4)
+    __shared__ int src[GB][64];
+    const int lb = threadIdx.x / CPB, c = threadIdx.x % CPB;
+    const int gbid = blockIdx.x * GB + lb;
+    const int gb0 = gbid / (ngb * ngb), gb1 = (gbid / ngb) % ngb, gb2 = gbid % ngb;
+    const bool live = gbid < ngb * ngb * ngb;
+    if (c < R * R * R) {
+        const int s0 = c / (R * R), s1 = (c / R) % R, s2 = c % R;
+        const int b0 = gb0 - s0, b1 = gb1 - s1, b2 = gb2 - s2;
+        int f = -1;
+        if (live && b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 < nbr && b1 < nbr && b2 < nbr)
+            f = __ldg(a.brick_first + (b0 * nbr + b1) * nbr + b2);
+        src[lb][c] = f;
     }
-}
-
-template <int MODE>
-static void run_dft(const DftArgs& p, cudaStream_t st) {
-    const int64_t total = (int64_t)p.A * p.Kout * p.B;
-    int threads = 256;
-    int64_t blocks = (total + threads - 1) / threads;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    if (blocks < 1) blocks = 1;
-    dft_kernel<MODE><<<(int)blocks, threads, 0, st>>>(p);
+    __syncthreads();
+    if (!live) return;
+    const int c0 = c / (TB * TB), c1 = (c / TB) % TB, c2 = c % TB;
+    const int u0 = gb0 * TB + c0, u1 = gb1 * TB + c1, u2 = gb2 * TB + c2;
+    if (u0 >= L || u1 >= L || u2 >= L) return;
+    double sum = 0.0;
+    const int RRR = R * R * R;
+#pragma unroll 8
+    for (int q = 0; q < RRR; ++q) {
+        const int f = src[lb][q];
+        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
+        const int t0 = s0 * TB + c0, t1 = s1 * TB + c1, t2 = s2 * TB + c2;
+        const bool ok = f >= 0 && t0 < TL && t1 < TL && t2 < TL;
+        const double x = ok ? __ldcg(a.partial + (size_t)f * a.tile_cells + (t0 * TL + t1) * TL + t2) : 0.0;
+        sum += x;
+    }
+    grid[((int64_t)u0 * L + u1) * L + u2] = sum;
 }
 
 // ------------------------------------------------------------------ gather --
-// One CTA per segment: stage the brick tile of the convolved grid in smem,
-// then one point per lane: y = alpha v + s (beta acc + gamma s v).
+// Every warp owns a contiguous range of chunks; it stages the (2m+1)^d grid
+// neighbourhood of the current chunk's cell in shared memory (reloaded only
+// when the cell changes -- consecutive chunks usually share it) and each
+// lane owns TWO points of the chunk (p0+lane, p0+32+lane), so every staged
+// value read (a broadcast LDS: the whole chunk shares one cell) feeds two
+// FMAs.  Epilogue: y = alpha v + s (beta acc + gamma s v).
 template <int D, int M>
 __global__ void __launch_bounds__(256) gather_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
                                                      const double* __restrict__ v, double* __restrict__ y,
                                                      double alpha, double beta, double gamma, unsigned flags) {
     constexpr int S = 2 * M + 1;
-    extern __shared__ double smem[];
-    const Geom g = a.g;
-    const int L = g.L, TL = g.TL, Tb = g.Tb, nbr = g.nbr;
-    const int seg = blockIdx.x;
-    const int brick = a.seg_brick[seg];
-    int bo[3] = {0, 0, 0};
-    {
-        int r = brick;
-        for (int ax = D - 1; ax >= 0; --ax) {
-            bo[ax] = (r % nbr) * Tb;
-            r /= nbr;
-        }
-    }
-    double* tile = smem;
-    const int tile_cells = a.tile_cells;
-    for (int i = threadIdx.x; i < tile_cells; i += blockDim.x) {
-        int t[3] = {0, 0, 0};
-        int r = i;
-        for (int ax = D - 1; ax >= 0; --ax) {
-            t[ax] = r % TL;
-            r /= TL;
-        }
-        bool ok = true;
-        int64_t gi = 0;
-        for (int ax = 0; ax < D; ++ax) {
-            const int u = bo[ax] + t[ax];
-            ok = ok && (u < L);
-            gi = gi * L + u;
-        }
-        tile[i] = ok ? grid[gi] : 0.0;
-    }
-    __syncthreads();
-    const int nw = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c0 = a.seg_chunk[seg], c1 = a.seg_chunk[seg + 1];
-    const int TL1 = (D >= 2) ? TL : 1;
-    const int TL2 = (D == 3) ? TL * TL : 1;
-    for (int ch = c0 + warp; ch < c1; ch += nw) {
-        const int cell = a.chunk_cell[ch];
+    constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
+    extern __shared__ double nbs[];
+    const int L = a.g.L;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    double* nb = nbs + wl * NB;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwt = (gridDim.x * blockDim.x) >> 5;
+    const int c_lo = (int)(((long long)a.nchunks * gw) / nwt);
+    const int c_hi = (int)(((long long)a.nchunks * (gw + 1)) / nwt);
+    const int64_t rs = (D == 3) ? (int64_t)L * L : (int64_t)L;  // stride of axis 0
+    int cur = -1;
+    for (int ch = c_lo; ch < c_hi; ++ch) {
         const int p0 = a.chunk_start[ch];
         const int np = a.chunk_start[ch + 1] - p0;
-        if (lane >= np) continue;
-        const int p = p0 + lane;
-        double w0[S], w1[S], w2[S];
-        kb_windows<M>(__ldg(a.frac + p), wc, w0);
-        if (D >= 2) kb_windows<M>(__ldg(a.frac + a.n + p), wc, w1);
-        if (D == 3) kb_windows<M>(__ldg(a.frac + 2 * a.n + p), wc, w2);
-        double acc = 0.0;
-        const double* tb = tile + cell;
+        const int gbase = a.chunk_gcell[ch];
+        const bool okA = lane < np, okB = lane + 32 < np;
+        const int pA = p0 + lane, pB = p0 + 32 + lane;
+        // issue the point loads before (possibly) restaging the neighbourhood
+        const double fA0 = okA ? __ldg(a.frac + pA) : 0.5, fB0 = okB ? __ldg(a.frac + pB) : 0.5;
+        const double fA1 = (D >= 2 && okA) ? __ldg(a.frac + a.n + pA) : 0.5;
+        const double fB1 = (D >= 2 && okB) ? __ldg(a.frac + a.n + pB) : 0.5;
+        const double fA2 = (D == 3 && okA) ? __ldg(a.frac + 2 * a.n + pA) : 0.5;
+        const double fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
+        if (gbase != cur) {
+            __syncwarp();
+            for (int e = lane; e < NB; e += 32) {
+                int64_t off;
+                if (D == 1) off = e;
+                else if (D == 2) off = (e / S) * rs + e % S;
+                else off = (e / (S * S)) * rs + ((e / S) % S) * (int64_t)L + e % S;
+                nb[e] = __ldg(grid + gbase + off);
+            }
+            __syncwarp();
+            cur = gbase;
+        }
+        double wA0[S], wA1[S], wA2[S], wB0[S], wB1[S], wB2[S];
+        kb_windows<M>(fA0, wc, wA0);
+        kb_windows<M>(fB0, wc, wB0);
+        if (D >= 2) {
+            kb_windows<M>(fA1, wc, wA1);
+            kb_windows<M>(fB1, wc, wB1);
+        }
+        if (D == 3) {
+            kb_windows<M>(fA2, wc, wA2);
+            kb_windows<M>(fB2, wc, wB2);
+        }
+        double accA = 0.0, accB = 0.0;
         if (D == 1) {
 #pragma unroll
-            for (int i = 0; i < S; ++i) acc = fma(w0[i], tb[i], acc);
+            for (int i = 0; i < S; ++i) {
+                const double gv = nb[i];
+                accA = fma(wA0[i], gv, accA);
+                accB = fma(wB0[i], gv, accB);
+            }
         } else if (D == 2) {
 #pragma unroll
             for (int i = 0; i < S; ++i) {
-                double r1 = 0.0;
+                double rA = 0.0, rB = 0.0;
 #pragma unroll
-                for (int j = 0; j < S; ++j) r1 = fma(w1[j], tb[i * TL1 + j], r1);
-                acc = fma(w0[i], r1, acc);
+                for (int j = 0; j < S; ++j) {
+                    const double gv = nb[i * S + j];
+                    rA = fma(wA1[j], gv, rA);
+                    rB = fma(wB1[j], gv, rB);
+                }
+                accA = fma(wA0[i], rA, accA);
+                accB = fma(wB0[i], rB, accB);
             }
         } else {
 #pragma unroll 1
             for (int i = 0; i < S; ++i) {
-                const double* ti = tb + i * TL2;
-                double r1 = 0.0;
+                const double* gi = nb + i * S * S;
+                double rA = 0.0, rB = 0.0;
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
-                    double r2 = 0.0;
+                    double qA = 0.0, qB = 0.0;
 #pragma unroll
-                    for (int k = 0; k < S; ++k) r2 = fma(w2[k], ti[j * TL1 + k], r2);
-                    r1 = fma(w1[j], r2, r1);
+                    for (int k = 0; k < S; ++k) {
+                        const double gv = gi[j * S + k];
+                        qA = fma(wA2[k], gv, qA);
+                        qB = fma(wB2[k], gv, qB);
+                    }
+                    rA = fma(wA1[j], qA, rA);
+                    rB = fma(wB1[j], qB, rB);
                 }
-                // w0[i] with a runtime i: select through a small unrolled scan
-                double wi = 0.0;
+                double xA = 0.0, xB = 0.0;
 #pragma unroll
-                for (int q = 0; q < S; ++q) wi = (q == i) ? w0[q] : wi;
-                acc = fma(wi, r1, acc);
+                for (int q = 0; q < S; ++q) {
+                    xA = (q == i) ? wA0[q] : xA;
+                    xB = (q == i) ? wB0[q] : xB;
+                }
+                accA = fma(xA, rA, accA);
+                accB = fma(xB, rB, accB);
             }
         }
-        const int node = (flags & MLB_SORTED) ? p : a.perm[p];
-        const double vv = v ? __ldg(v + node) : 0.0;
-        const double s = (flags & MLB_USE_ISD) ? __ldg(a.isd + p) : 1.0;
-        double res = alpha * vv + s * (beta * acc + gamma * s * vv);
-        if (flags & MLB_ACCUMULATE) res += y[node];
-        y[node] = res;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool ok = h ? okB : okA;
+            if (!ok) continue;
+            const int p = h ? pB : pA;
+            const double acc = h ? accB : accA;
+            const int node = (flags & MLB_SORTED) ? p : __ldg(a.perm + p);
+            const double vv = v ? __ldg(v + node) : 0.0;
+            const double s = (flags & MLB_USE_ISD) ? __ldg(a.isd + p) : 1.0;
+            double res = alpha * vv + s * (beta * acc + gamma * s * vv);
+            if (flags & MLB_ACCUMULATE) res += y[node];
+            y[node] = res;
+        }
     }
 }
 
@@ -448,30 +589,35 @@ static FsArgs make_args(mlb_binding* b) {
     a.frac = b->frac;
     a.chunk_start = b->chunk_start;
     a.chunk_cell = b->chunk_cell;
+    a.chunk_gcell = b->chunk_gcell;
     a.seg_chunk = b->seg_chunk;
     a.seg_brick = b->seg_brick;
     a.brick_seg = b->brick_seg;
+    a.brick_first = b->brick_first;
+    a.brick_count = b->brick_count;
+    a.fuse_brick_sum = (b->plan->g.d == 3) ? 1 : 0;
     a.isd = b->isd;
     a.partial = b->partial;
     a.tile_cells = b->tile_cells;
+    a.nchunks = b->nchunks;
     return a;
 }
 
-static int spread_warps(int D, int tile_cells) {
-    // warp-private tiles + window staging must fit in ~200 KB of smem
-    const size_t per_warp = (size_t)tile_cells * 8 + 32 * D * kWinPad * 8;
-    int nw = (int)(200 * 1024 / per_warp);
-    return std::max(1, std::min(8, nw));
+template <int D, int M>
+static size_t spread_smem(int nw, int tile_cells) {
+    return (size_t)nw * tile_cells * 8 + (size_t)nw * 32 * D * StageCfg<D, M>::pad * 8;
 }
 
 template <int D, int M>
 static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st) {
     FsArgs a = make_args(b);
-    const int nw = spread_warps(D, b->tile_cells);
-    const size_t smem = (size_t)nw * b->tile_cells * 8 + (size_t)nw * 32 * D * kWinPad * 8;
+    int nw = 8;
+    while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 200 * 1024) --nw;
+    const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
     auto kern = spread_kernel<D, M>;
     MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<b->nseg, nw * 32, smem, st>>>(a, b->plan->wc, v, flags);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -479,11 +625,29 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
 template <int D, int M>
 static int gather_dm(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                      double beta, double gamma, unsigned flags, cudaStream_t st) {
+    constexpr int S = 2 * M + 1;
+    constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
     FsArgs a = make_args(b);
-    const size_t smem = (size_t)b->tile_cells * 8;
+    const size_t smem = (size_t)8 * NB * sizeof(double);
     auto kern = gather_kernel<D, M>;
-    MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<b->nseg, 256, smem, st>>>(a, b->plan->wc, grid, v, y, alpha, beta, gamma, flags);
+    static int per_sm = 0;  // resident blocks per SM for this instantiation
+    if (per_sm == 0) {
+        MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MLB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    int nsm = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int blocks = nsm * per_sm;
+    const int need = (b->nchunks + 7) / 8;  // at least one chunk per warp
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    kern<<<blocks, 256, smem, st>>>(a, b->plan->wc, grid, v, y, alpha, beta, gamma, flags);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -516,62 +680,46 @@ int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t 
 
 int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     FsArgs a = make_args(b);
-    const int64_t total = b->grid_cells;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    switch (b->plan->g.d) {
-        case 1: reduce_kernel<1><<<(int)blocks, 256, 0, st>>>(a, grid); break;
-        case 2: reduce_kernel<2><<<(int)blocks, 256, 0, st>>>(a, grid); break;
-        default: reduce_kernel<3><<<(int)blocks, 256, 0, st>>>(a, grid); break;
+    const Geom& G = b->plan->g;
+    if (G.d <= 2) {
+        // one brick covering the whole sub-box: R1 writes the grid directly
+        if (b->nseg == 1) {
+            MLB_CUDA_TRY(cudaMemcpyAsync(grid, b->partial, b->grid_cells * sizeof(double),
+                                         cudaMemcpyDeviceToDevice, st));
+            return MLB_OK;
+        }
+        dim3 g1((b->tile_cells + 7) / 8, 1);
+        seg_sum_kernel<<<g1, 256, 0, st>>>(b->partial, b->heavy, b->tile_cells, grid);
+        note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+        return MLB_OK;
     }
-    MLB_CUDA_TRY(cudaGetLastError());
-    return MLB_OK;
-}
-
-int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_t st) {
-    const Geom& g = b->plan->g;
-    const int L = g.L, K = g.K, Kh = g.Kh, half = g.N / 2;
-    DftArgs p;
-    p.tw = b->plan->twid;
-    p.K = K;
-    p.fused = b->plan->fused;
-    double* A = b->stage_a;
-    double* B = b->stage_b;
-    if (g.d == 1) {
-        p = {gin, A, 1, L, Kh, 1, b->plan->twid, K, half, b->plan->fused};
-        run_dft<5>(p, st);
-        p = {A, gout, 1, Kh, L, 1, b->plan->twid, K, half, nullptr};
-        run_dft<4>(p, st);
-    } else if (g.d == 2) {
-        p = {gin, A, L, L, Kh, 1, b->plan->twid, K, half, nullptr};  // [u0][k1]
-        run_dft<0>(p, st);
-        p = {A, B, 1, L, K, Kh, b->plan->twid, K, 0, b->plan->fused};  // [k0][k1] * F
-        run_dft<2>(p, st);
-        p = {B, A, 1, K, L, Kh, b->plan->twid, K, 0, nullptr};  // [u0][k1]
-        run_dft<3>(p, st);
-        p = {A, gout, L, Kh, L, 1, b->plan->twid, K, half, nullptr};  // [u0][u1]
-        run_dft<4>(p, st);
+    // d = 3: R1 ran inside the spread kernel (last CTA per brick)
+    const int Tb = G.Tb;
+    const int ngb = (G.L + Tb - 1) / Tb;
+    const int64_t nblk = (int64_t)ngb * ngb * ngb;
+    const int R = (G.TL + Tb - 1) / Tb;  // source bricks per axis
+    if (Tb == 4 && R * R * R <= 64) {
+        reduce3_kernel<4><<<(unsigned)((nblk + 3) / 4), 256, 0, st>>>(a, grid);
+    } else if (Tb == 2) {
+        const int64_t total = b->grid_cells;
+        int64_t blocks = (total + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        reduce_kernel<3, 2><<<(int)blocks, 256, 0, st>>>(a, grid);
     } else {
-        p = {gin, A, L * L, L, Kh, 1, b->plan->twid, K, half, nullptr};  // [u0][u1][k2]
-        run_dft<0>(p, st);
-        p = {A, B, L, L, K, Kh, b->plan->twid, K, 0, nullptr};  // [u0][k1][k2]
-        run_dft<1>(p, st);
-        p = {B, A, 1, L, K, K * Kh, b->plan->twid, K, 0, b->plan->fused};  // [k0][k1][k2] * F
-        run_dft<2>(p, st);
-        p = {A, B, 1, K, L, K * Kh, b->plan->twid, K, 0, nullptr};  // [u0][k1][k2]
-        run_dft<3>(p, st);
-        p = {B, A, L, K, L, Kh, b->plan->twid, K, 0, nullptr};  // [u0][u1][k2]
-        run_dft<3>(p, st);
-        p = {A, gout, L * L, Kh, L, 1, b->plan->twid, K, half, nullptr};  // [u0][u1][u2]
-        run_dft<4>(p, st);
+        const int64_t total = b->grid_cells;
+        int64_t blocks = (total + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        reduce_kernel<3, 0><<<(int)blocks, 256, 0, st>>>(a, grid);
     }
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
 
 int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha, double beta,
                   double gamma, unsigned flags, cudaStream_t st) {
-    if (b->nseg == 0) return MLB_OK;
+    if (b->nchunks == 0) return MLB_OK;
     const Geom& g = b->plan->g;
     MLB_DISPATCH_DM(gather_dm, g.d, g.m, b, grid, v, y, alpha, beta, gamma, flags, st);
 }

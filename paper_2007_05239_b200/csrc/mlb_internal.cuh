@@ -12,6 +12,7 @@
 namespace mlb {
 
 void set_error(const std::string& msg);
+void note_launches(int k);  // libmlb kernel-launch counter (bench evidence)
 int fail(int code, const std::string& msg);
 
 #define MLB_CUDA_TRY(expr)                                                              \
@@ -22,7 +23,7 @@ int fail(int code, const std::string& msg);
     } while (0)
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
-constexpr int kChunk = 32;        // points per chunk (one warp lane each)
+constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
 // Window polynomial coefficients, passed by value as a kernel parameter
@@ -56,6 +57,7 @@ struct mlb_plan {
     mlb::WinCoef wc;
     double* fused = nullptr;     // band weights (K^(d-1) x Kh)
     double2* twid = nullptr;     // L x K
+    double* conv = nullptr;      // d <= 2: (2L-1)^d spatial kernel (nullptr: use the DFT stages)
     std::vector<double> win_coef_host;
 };
 
@@ -68,9 +70,15 @@ struct mlb_binding {
     double* frac = nullptr;          // d x n (SoA) fractional cell offsets f in [0,1)
     int32_t* chunk_start = nullptr;  // nchunks+1
     int32_t* chunk_cell = nullptr;   // nchunks: flat tile index of the chunk's bin base cell
+    int32_t* chunk_gcell = nullptr;  // nchunks: flat sub-box (L^d) index of the bin base cell
     int32_t* seg_chunk = nullptr;    // nseg+1
     int32_t* seg_brick = nullptr;    // nseg
     int32_t* brick_seg = nullptr;    // nbricks+1 (CSR, bricks lexicographic)
+    int32_t* heavy = nullptr;        // nheavy x (first segment, segment count) of bricks with >= 2 segments
+    int nheavy = 0;
+    int max_heavy_segs = 0;
+    int32_t* brick_first = nullptr;  // nbricks: first segment of the brick, -1 if empty
+    int32_t* brick_count = nullptr;  // nbricks: completion counters of the spread epilogue (kept at 0)
     double* isd = nullptr;           // sorted order
     // scratch
     double* partial = nullptr;       // nseg x TL^d

@@ -177,7 +177,9 @@ int mlb_gemv_t(const double* V, int64_t ld, int64_t n, int cols, const double* w
     cudaStream_t st = (cudaStream_t)stream;
     const int nb = row_blocks(n);
     gemv_t_partial<<<dim3(nb, cols), kRedThreads, 0, st>>>(V, ld, n, w, work);
+    note_launches(1);
     finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(work, nb, cols, h, nullptr);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -187,6 +189,7 @@ int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c
     cudaStream_t st = (cudaStream_t)stream;
     const int nb = std::max(1, std::min(148 * 4, (int)((n + 255) / 256)));
     gemv_n_kernel<<<nb, 256, cols * sizeof(double), st>>>(V, ld, n, cols, c, y, scale, accumulate, nullptr);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -200,17 +203,27 @@ int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double
     const int nbn = std::max(1, std::min(kMaxRowBlocks, (int)((n + 255) / 256)));
     // pass 1: h1 = V^T w ; w -= V h1
     gemv_t_partial<<<dim3(nb, cols), kRedThreads, 0, st>>>(V, ld, n, w, part);
+    note_launches(1);
     finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(part, nb, cols, h1, nullptr);
+    note_launches(1);
     gemv_n_kernel<<<nbn, 256, cols * sizeof(double), st>>>(V, ld, n, cols, h1, w, -1.0, 1, nullptr);
+    note_launches(1);
     // pass 2: h2 = V^T w ; w -= V h2 ; h_out = h1 + h2 ; ||w||^2
     gemv_t_partial<<<dim3(nb, cols), kRedThreads, 0, st>>>(V, ld, n, w, part);
+    note_launches(1);
     finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(part, nb, cols, h_out, h1);
+    note_launches(1);
     // h2 = h_out - h1 is needed for the update: recompute it into h1's slot
     double* h2 = h1 + cols + 1;
     finish_partial<<<(cols + 63) / 64, 64, 0, st>>>(part, nb, cols, h2, nullptr);
+    note_launches(1);
     double* npart = part + (int64_t)nb * cols;
     gemv_n_kernel<<<nbn, 256, cols * sizeof(double), st>>>(V, ld, n, cols, h2, w, -1.0, 1, npart);
-    if (nrm2_out) finish_partial<<<1, 64, 0, st>>>(npart, nbn, 1, nrm2_out, nullptr);
+    note_launches(1);
+    if (nrm2_out) {
+        finish_partial<<<1, 64, 0, st>>>(npart, nbn, 1, nrm2_out, nullptr);
+        note_launches(1);
+    }
     if (h1_out) MLB_CUDA_TRY(cudaMemcpyAsync(h1_out, h1, cols * sizeof(double), cudaMemcpyDeviceToDevice, st));
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
@@ -221,6 +234,7 @@ int mlb_gemm_vs(const double* V, int64_t ld, int64_t n, int s, const double* S, 
     if (k <= 0 || n <= 0) return MLB_OK;
     dim3 grid((unsigned)((n + 63) / 64), (unsigned)((k + 31) / 32));
     gemm_vs_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(V, ld, n, s, S, k, Out, ldo);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -229,7 +243,9 @@ int mlb_dot(const double* x, const double* y, int64_t n, double* out, double* wo
     cudaStream_t st = (cudaStream_t)stream;
     const int nb = row_blocks(n);
     dot_partial<<<nb, kRedThreads, 0, st>>>(x, y, n, work);
+    note_launches(1);
     finish_partial<<<1, 64, 0, st>>>(work, nb, 1, out, nullptr);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -237,6 +253,7 @@ int mlb_dot(const double* x, const double* y, int64_t n, double* out, double* wo
 int mlb_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream) {
     if (n <= 0) return MLB_OK;
     axpby_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(a, x, b, y, n);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -244,6 +261,7 @@ int mlb_axpby(double a, const double* x, double b, double* y, int64_t n, void* s
 int mlb_scale_by(const double* x, double* y, int64_t n, const double* s_dev, double pw, void* stream) {
     if (n <= 0) return MLB_OK;
     scale_by_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(x, y, n, s_dev, pw);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
@@ -251,6 +269,7 @@ int mlb_scale_by(const double* x, double* y, int64_t n, const double* s_dev, dou
 int mlb_hadamard(const double* x, const double* y, double* z, int64_t n, void* stream) {
     if (n <= 0) return MLB_OK;
     hadamard_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(x, y, z, n);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }

@@ -245,8 +245,36 @@ class FastsumPlan:
         tw = np.empty((L, N + 1, 2))
         tw[..., 0] = np.cos(ph)
         tw[..., 1] = -np.sin(ph)
+        conv = None
+        if d <= 2:
+            # spatial kernel Kc[D] = sum_k F(k) exp(2 pi i k.D/ng) over the full
+            # band (F even -> real); D = -(L-1)..(L-1) per axis
+            idx_full = [np.mod(kfull, ng)] * d
+            Ffull = self.fused_weights_full()[np.ix_(*idx_full)] / float(ng) ** d
+            D = np.arange(-(L - 1), L)
+            A = np.exp(2j * math.pi * np.outer(kfull, D) / ng)       # K x (2L-1)
+            if d == 1:
+                Kc = (Ffull @ A).real
+            else:
+                Kc = (A.T @ Ffull @ A).real
+            conv = np.ascontiguousarray(Kc)
         return dict(bin_lo=blo, bin_hi=bhi, L=L, ulo=ulo, fused_band=np.ascontiguousarray(band),
-                    twiddle=np.ascontiguousarray(tw))
+                    twiddle=np.ascontiguousarray(tw), conv_kernel=conv)
+
+    def fused_weights_full(self):
+        """The full (ng,)*d fused weights (the reference keeps the R2C half; the
+        array is even, so the missing half is its reflection)."""
+        ng, d = self.n_grid, self.d
+        h = self.fused_weights
+        full = np.empty((ng,) * d)
+        full[..., : ng // 2 + 1] = h
+        k = np.arange(ng // 2 + 1, ng)
+        src = np.mod(-k, ng)
+        refl = h
+        for ax in range(d - 1):
+            refl = np.take(refl, np.mod(-np.arange(ng), ng), axis=ax)
+        full[..., ng // 2 + 1:] = refl[..., src]
+        return full
 
     def device_plan(self, device=0, domain="box"):
         key = (int(device), domain)
@@ -256,9 +284,11 @@ class FastsumPlan:
         lib = _lib.lib()
         t = self.device_tables(domain)
         wc = np.ascontiguousarray(self.win_coef)
+        conv = t["conv_kernel"]
         desc = _lib.PlanDesc(self.d, self.N, self.m_nfft, self.n_grid, t["bin_lo"], t["bin_hi"],
                              self.win_deg, float(self.K0), t["fused_band"].ctypes.data,
-                             t["twiddle"].ctypes.data, wc.ctypes.data)
+                             t["twiddle"].ctypes.data, wc.ctypes.data,
+                             None if conv is None else conv.ctypes.data)
         out = C.c_void_p()
         _lib.check(lib.mlb_plan_create(C.byref(desc), int(device), C.byref(out)))
         h = _PlanHandle(out, t)

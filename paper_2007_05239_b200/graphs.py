@@ -296,8 +296,18 @@ def apply_sym_laplacian(layer, v):
         isd = layer.inv_sqrt_degrees
         return (1.0 + layer.shift) * v - isd * np.asarray(_as_host(layer.weights.matvec(isd * v)))
     torch = _torch()
-    host = not _is_tensor(v)
     dev = layer.weights.device
+    if _is_tensor(v) and not v.is_cuda:
+        # host tensor (e.g. pinned): async copy in, compute, copy back to host
+        vd = v.to(device=f"cuda:{dev}", dtype=torch.float64, non_blocking=True)
+        if tuple(vd.shape) != (layer.n,):
+            raise ConfigError("v must match the layer size")
+        y = torch.empty_like(vd)
+        apply_sym_laplacian_dev(layer, vd, y)
+        out = torch.empty(y.shape, dtype=torch.float64, pin_memory=v.is_pinned())
+        out.copy_(y)
+        return out
+    host = not _is_tensor(v)
     vd = to_device(v, dev)
     if tuple(vd.shape) != (layer.n,):
         raise ConfigError("v must match the layer size")

@@ -1,0 +1,156 @@
+"""Seeded synthetic stand-ins for the BASELINE.json configs (bench / test data).
+
+The reference publishes no datasets for these configs; SURVEY.md section 8(d)
+restates them concretely and records the corrections the reference forces
+(N = 64 for sigma = 0.1 RGB layers, ball radius 0.21875 for config 5).
+Each generator returns a `Workload`: feature matrix, per-layer column groups
+with kernel / plan parameters, ground-truth labels and solver settings.
+"""
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class LayerSpec:
+    columns: tuple
+    sigma: float          # feature units ("fastsum-box" mode)
+    N: int
+    m: int
+    p: int = 8
+    family: str = "gaussian"
+
+
+@dataclass
+class Workload:
+    name: str
+    X: np.ndarray
+    layers: list
+    truth: np.ndarray
+    k: int
+    p_mean: float = -1.0
+    label_fraction: float = 0.01
+    ac_max_iter: int = 300
+    notes: dict = field(default_factory=dict)
+
+    @property
+    def n(self):
+        return self.X.shape[0]
+
+
+def _image_features(rgb, H, W):
+    yy, xx = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    xy = np.stack([yy.ravel() / (H - 1), xx.ravel() / (W - 1)], axis=1)
+    return np.concatenate([rgb.reshape(-1, 3), xy], axis=1)
+
+
+def config1_toy(seed=0):
+    """100x100, 3 classes (background + 2 rectangles); RGB d=3 sigma=0.1, xy d=2 sigma=0.2.
+
+    Correction: the RGB layer is rejected by the reference at N=16 (negative
+    NFFT degrees) -> N=64 for RGB, N=16 for xy.
+    """
+    rng = np.random.default_rng(seed)
+    H = W = 100
+    truth = np.zeros((H, W), dtype=np.int64)
+    for c in (1, 2):
+        y0, x0 = rng.integers(0, 60, 2)
+        h, w = rng.integers(20, 40, 2)
+        truth[y0:y0 + h, x0:x0 + w] = c
+    colors = rng.random((3, 3))
+    rgb = colors[truth] + rng.normal(0.0, 0.05, (H, W, 3))
+    X = _image_features(rgb, H, W)
+    layers = [LayerSpec((0, 1, 2), 0.1, 64, 4, 8), LayerSpec((3, 4), 0.2, 16, 4, 8)]
+    return Workload("cfg1_toy_100x100", X, layers, truth.ravel(), k=10, label_fraction=0.02)
+
+
+def config2_segmentation(seed=0, side=512):
+    """512x512, 5 Voronoi classes, class-mean RGB + N(0, 0.05^2); RGB d=3 sigma=0.1
+    (N=64 -- N=32 is rejected by the reference), xy d=2 sigma=0.15 (N=32); m=4, p=8."""
+    rng = np.random.default_rng(seed)
+    H = W = side
+    seeds = rng.random((5, 2))
+    yy, xx = np.meshgrid(np.arange(H) / (H - 1), np.arange(W) / (W - 1), indexing="ij")
+    d2 = (yy[..., None] - seeds[:, 0]) ** 2 + (xx[..., None] - seeds[:, 1]) ** 2
+    truth = np.argmin(d2, axis=-1)
+    colors = rng.random((5, 3))
+    rgb = colors[truth] + rng.normal(0.0, 0.05, (H, W, 3))
+    X = _image_features(rgb, H, W)
+    layers = [LayerSpec((0, 1, 2), 0.1, 64, 4, 8), LayerSpec((3, 4), 0.15, 32, 4, 8)]
+    return Workload(f"cfg2_segmentation_{side}x{side}", X, layers, truth.ravel(), k=20, label_fraction=0.01)
+
+
+def config3_feature_grouped(seed=0, side=200, bands=104):
+    """200x200, 16 blob classes, 104 smooth bands + N(0, 0.02^2), min-max scaled;
+    52 layers of consecutive band pairs (d=2, sigma=0.05, N=32, m=4)."""
+    rng = np.random.default_rng(seed)
+    H = W = side
+    cent = rng.random((16, 2))
+    yy, xx = np.meshgrid(np.arange(H) / (H - 1), np.arange(W) / (W - 1), indexing="ij")
+    d2 = (yy[..., None] - cent[:, 0]) ** 2 + (xx[..., None] - cent[:, 1]) ** 2
+    truth = np.argmin(d2, axis=-1).ravel()
+    bidx = np.arange(bands)
+    spectra = np.zeros((16, bands))
+    for c in range(16):
+        for _ in range(5):
+            mu, sd, a = rng.uniform(0, bands), rng.uniform(3, 20), rng.uniform(0.2, 1.0)
+            spectra[c] += a * np.exp(-0.5 * ((bidx - mu) / sd) ** 2)
+    X = spectra[truth] + rng.normal(0.0, 0.02, (H * W, bands))
+    X = (X - X.min(axis=0)) / (X.max(axis=0) - X.min(axis=0))
+    layers = [LayerSpec((2 * i, 2 * i + 1), 0.05, 32, 4, 8) for i in range(bands // 2)]
+    return Workload("cfg3_feature_grouped_200x200x104", X, layers, truth, k=10, label_fraction=0.05)
+
+
+def config4_large(seed=0, side=3162):
+    """3162x3162 (n ~ 1e7), 4 classes (background + 3 ellipses); RGB d=3 sigma=0.1,
+    xy d=2 sigma=0.1; N=64, m=5."""
+    rng = np.random.default_rng(seed)
+    H = W = side
+    yy, xx = np.meshgrid(np.arange(H) / (H - 1), np.arange(W) / (W - 1), indexing="ij")
+    truth = np.zeros((H, W), dtype=np.int64)
+    for c in (1, 2, 3):
+        cy, cx = rng.uniform(0.2, 0.8, 2)
+        ay, ax = rng.uniform(0.08, 0.2, 2)
+        th = rng.uniform(0, math.pi)
+        u = (yy - cy) * math.cos(th) + (xx - cx) * math.sin(th)
+        v = -(yy - cy) * math.sin(th) + (xx - cx) * math.cos(th)
+        truth[(u / ay) ** 2 + (v / ax) ** 2 <= 1.0] = c
+    colors = rng.random((4, 3))
+    rgb = colors[truth] + rng.normal(0.0, 0.05, (H, W, 3))
+    X = _image_features(rgb, H, W)
+    layers = [LayerSpec((0, 1, 2), 0.1, 64, 5, 8), LayerSpec((3, 4), 0.1, 64, 5, 8)]
+    return Workload(f"cfg4_large_{side}x{side}", X, layers, truth.ravel(), k=10, label_fraction=0.005)
+
+
+def ball_points(rng, n, d, radius=0.21875):
+    """Uniform in the d-ball (radius 0.21875: the reference rejects 0.25)."""
+    g = rng.standard_normal((n, d))
+    g /= np.linalg.norm(g, axis=1, keepdims=True)
+    return g * (radius * rng.random(n) ** (1.0 / d))[:, None]
+
+
+def config5_micro(n, d, seed=0):
+    """Matvec micro-benchmark points (box units) and v ~ N(0,1), x drawn before v."""
+    rng = np.random.default_rng(seed)
+    x = ball_points(rng, n, d)
+    v = rng.standard_normal(n)
+    return x, v
+
+
+CONFIGS = {1: config1_toy, 2: config2_segmentation, 3: config3_feature_grouped, 4: config4_large}
+
+
+def build_graph(workload, device=None, layer_ids=None):
+    """GPU multilayer graph of a workload: one feature_group call per layer so
+    each layer keeps its own plan parameters (N differs between layers)."""
+    from paper_2007_05239_b200 import GroupingSpec, GroupSpec, KernelSpec, MultilayerGraph, feature_group
+    layers = []
+    ids = range(len(workload.layers)) if layer_ids is None else layer_ids
+    for i in ids:
+        ls = workload.layers[i]
+        spec = GroupingSpec((GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma)),))
+        G = feature_group(workload.X, spec, fastsum_params=dict(N=ls.N, m_nfft=ls.m, p_nfft=ls.p), device=device)
+        layers.append(G.layers[0])
+    return MultilayerGraph(tuple(layers))

@@ -56,7 +56,7 @@ def test_two_point_hand_sum():
     assert_allclose(got, math.exp(-4.0) * np.array([2.0, 1.0]), rtol=1e-6)
 
 
-@pytest.mark.parametrize("d,N,m", [(1, 32, 4), (2, 32, 4), (3, 16, 4), (3, 32, 5), (2, 16, 6), (3, 16, 6)])
+@pytest.mark.parametrize("d,N,m", [(1, 32, 4), (2, 32, 4), (2, 64, 5), (3, 16, 4), (3, 32, 5), (2, 16, 6), (3, 16, 6), (3, 64, 4)])
 def test_stages_match_oracle(d, N, m):
     """spread grid, convolved grid and gather, each against the oracle."""
     import torch
