@@ -142,7 +142,10 @@ int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
     }
     if (rc == MLB_OK && d <= 2 && desc->conv_kernel) {
         const size_t nk = (d == 1) ? (size_t)(2 * g.L - 1) : (size_t)(2 * g.L - 1) * (2 * g.L - 1);
-        rc = dev_upload(&p->conv, desc->conv_kernel, nk);
+        // +2 doubles: TMA bulk copies round sizes up to 16 bytes
+        std::vector<double> kc(nk + 2, 0.0);
+        std::memcpy(kc.data(), desc->conv_kernel, nk * sizeof(double));
+        rc = dev_upload(&p->conv, kc.data(), kc.size());
     }
     if (rc != MLB_OK) {
         dev_free(p->fused);
@@ -177,8 +180,11 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->seg_brick);
     dev_free(b->brick_seg);
     dev_free(b->heavy);
+    dev_free(b->groups);
+    dev_free(b->gsum);
     dev_free(b->brick_first);
     dev_free(b->brick_count);
+    dev_free(b->work);
     dev_free(b->isd);
     dev_free(b->partial);
     dev_free(b->grid);
@@ -249,17 +255,17 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     }
     const int nch = (int)chunk_cell.size();
     chunk_start.push_back((int32_t)n);
-    // segments: d <= 2 -> ~2 CTAs per SM (every segment tile is the whole
-    // sub-box); d = 3 -> ~8 per SM (tiles are brick-sized)
-    const int target = (d <= 2) ? 148 * 2 : 148 * 4;
-    int maxseg = (int)((nch + target - 1) / target);
-    if (maxseg < 4) maxseg = 4;
-    if (maxseg > 4096) maxseg = 4096;
+    // segments (one warp's work unit): <= kSegPoints points of one brick,
+    // never splitting a chunk; a bit smaller when n is small so every SM
+    // gets work
+    // (large n: grow segments so the partial tiles stay ~ 148 x 16 of them)
+    int seg_points = (int)std::max<int64_t>(kSegPoints, n / (148 * 16));
+    while (seg_points > 64 && (n / seg_points) < 148 * 8) seg_points /= 2;
     std::vector<int32_t> seg_chunk, seg_brick, brick_seg(nbricks + 1, 0);
     for (int c = 0; c < nch;) {
         const int br = chunk_brick[c];
-        int e = c;
-        while (e < nch && chunk_brick[e] == br && e - c < maxseg) ++e;
+        int e = c + 1;
+        while (e < nch && chunk_brick[e] == br && chunk_start[e + 1] - chunk_start[c] <= seg_points) ++e;
         seg_chunk.push_back(c);
         seg_brick.push_back(br);
         brick_seg[br + 1]++;
@@ -268,14 +274,21 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     const int nseg = (int)seg_brick.size();
     seg_chunk.push_back(nch);
     for (int br = 0; br < nbricks; ++br) brick_seg[br + 1] += brick_seg[br];
-    std::vector<int32_t> heavy, brick_first(nbricks, -1);
+    std::vector<int32_t> heavy, groups, brick_first(nbricks, -1);
     int max_heavy = 0;
     for (int br = 0; br < nbricks; ++br) {
         const int ns = brick_seg[br + 1] - brick_seg[br];
         if (ns >= 1) brick_first[br] = brick_seg[br];
         if (ns >= 2) {
+            const int goff = (int)(groups.size() / 2);
+            int ng = 0;
+            for (int s0 = 0; s0 < ns; s0 += 16, ++ng) {
+                groups.push_back(brick_seg[br] + s0);
+                groups.push_back(std::min(16, ns - s0));
+            }
             heavy.push_back(brick_seg[br]);
-            heavy.push_back(ns);
+            heavy.push_back(goff);
+            heavy.push_back(ng);
             max_heavy = std::max(max_heavy, ns);
         }
     }
@@ -291,8 +304,9 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     b->nchunks = nch;
     b->nseg = nseg;
     b->nbricks = nbricks;
-    b->max_seg_chunks = maxseg;
-    b->nheavy = (int)(heavy.size() / 2);
+    b->max_seg_chunks = seg_points;
+    b->nheavy = (int)(heavy.size() / 3);
+    b->ngroups = (int)(groups.size() / 2);
     b->max_heavy_segs = max_heavy;
     b->tile_cells = ipow_h(TL, d);
     b->grid_cells = 1;
@@ -314,15 +328,21 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->seg_brick, seg_brick.data(), seg_brick.size());
     if (rc == MLB_OK) rc = dev_upload(&b->brick_seg, brick_seg.data(), brick_seg.size());
     if (rc == MLB_OK) rc = dev_upload(&b->heavy, heavy.data(), heavy.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->groups, groups.data(), groups.size());
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->gsum, nullptr, (size_t)b->ngroups * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload(&b->brick_first, brick_first.data(), brick_first.size());
     if (rc == MLB_OK) {
         std::vector<int32_t> zeros(nbricks, 0);
         rc = dev_upload(&b->brick_count, zeros.data(), zeros.size());
     }
+    if (rc == MLB_OK) rc = dev_upload<int>(&b->work, nullptr, 1);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
-    if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, (size_t)nseg * b->tile_cells);
-    if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells);
-    if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells);
+    // d <= 2: one partial grid per spread CTA (<= 2 per SM); d = 3: one per segment
+    b->spread_parts_max = 148 * 2;
+    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)nseg;
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, nparts * b->tile_cells);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells + 2);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_a, nullptr, (size_t)b->stage_elems);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_b, nullptr, (size_t)b->stage_elems);
     if (rc != MLB_OK) {

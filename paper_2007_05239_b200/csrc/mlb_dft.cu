@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "mlb_internal.cuh"
+#include "mlb_tma.cuh"
 
 namespace mlb {
 
@@ -167,13 +168,29 @@ static Operand op(const void* p, int64_t bstride, int ld, int koff = 0) {
 __global__ void conv2d_kernel(const double* __restrict__ gin, double* __restrict__ gout,
                               const double* __restrict__ Kc, int L) {
     // one warp per output cell; lanes stride the input columns, the 32 lane
-    // sums combine by a fixed shuffle tree -> deterministic
-    extern __shared__ double sm[];
+    // sums combine by a fixed shuffle tree -> deterministic.  The grid and the
+    // kernel table arrive by TMA bulk copies.
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint64_t bar;
     const int KL = 2 * L - 1;
-    double* sg = sm;            // L*L input grid
-    double* sk = sm + L * L;    // KL*KL kernel
-    for (int i = threadIdx.x; i < L * L; i += blockDim.x) sg[i] = __ldg(gin + i);
-    for (int i = threadIdx.x; i < KL * KL; i += blockDim.x) sk[i] = __ldg(Kc + i);
+    const int gsz = (L * L + 1) & ~1;
+    double* sg = sm;            // L*L input grid (padded to even)
+    double* sk = sm + gsz;      // KL*KL kernel
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // the grid may be a caller buffer: bulk-copy whole 16-byte units, the
+        // odd tail element separately; the kernel table is padded by the plan
+        const uint32_t b1 = (uint32_t)((L * L * 8) & ~15), b2 = (uint32_t)(((KL * KL * 8) + 15) & ~15);
+        mbar_arrive_expect_tx(&bar, b1 + b2);
+        if (b1) tma_load_1d(sg, gin, b1, &bar);
+        tma_load_1d(sk, Kc, b2, &bar);
+        if ((L * L) & 1) sg[L * L - 1] = __ldg(gin + L * L - 1);
+    }
+    mbar_wait(&bar, 0);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -239,12 +256,19 @@ __global__ void __launch_bounds__(256) f12_kernel(F3Args p) {
     double2* sE = sm3;                          // L*K
     double2* sA1 = sE + L * K;                  // L*T2
     double* sg = reinterpret_cast<double*>(sA1 + L * F12_T2);  // L*L
+    __shared__ uint64_t bar;
     const int u0 = blockIdx.y;
     const int k2_0 = blockIdx.x * F12_T2;
     const int nt = min(F12_T2, Kh - k2_0);
-    load_tw(sE, p.tw, L * K);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
     const double* slab = p.grid + (int64_t)u0 * L * L;
-    for (int i = threadIdx.x; i < L * L; i += blockDim.x) sg[i] = __ldg(slab + i);
+    for (int i = threadIdx.x; i < L * L; i += blockDim.x) cp_async8(sg + i, slab + i);
+    tma_stage(sE, p.tw, (uint32_t)(L * K * 16), &bar, 0);
+    cp_async_wait_all();
     __syncthreads();
     // A1[u1][j] = sum_u2 g[u1][u2] E[u2][k2_0 + j + half]
     for (int o = threadIdx.x; o < L * F12_T2; o += blockDim.x) {
@@ -252,12 +276,25 @@ __global__ void __launch_bounds__(256) f12_kernel(F3Args p) {
         double2 acc = make_double2(0.0, 0.0);
         if (j < nt) {
             const int kc = k2_0 + j + p.half;
-            for (int u2 = 0; u2 < L; ++u2) {
+            double2 q[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            int u2 = 0;
+            for (; u2 + 3 < L; u2 += 4) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const double gv = sg[u1 * L + u2 + r];
+                    const double2 e = sE[(u2 + r) * K + kc];
+                    q[r].x = fma(gv, e.x, q[r].x);
+                    q[r].y = fma(gv, e.y, q[r].y);
+                }
+            }
+            for (; u2 < L; ++u2) {
                 const double gv = sg[u1 * L + u2];
                 const double2 e = sE[u2 * K + kc];
-                acc.x = fma(gv, e.x, acc.x);
-                acc.y = fma(gv, e.y, acc.y);
+                q[0].x = fma(gv, e.x, q[0].x);
+                q[0].y = fma(gv, e.y, q[0].y);
             }
+            acc.x = (q[0].x + q[1].x) + (q[2].x + q[3].x);
+            acc.y = (q[0].y + q[1].y) + (q[2].y + q[3].y);
         }
         sA1[u1 * F12_T2 + j] = acc;
     }
@@ -267,9 +304,15 @@ __global__ void __launch_bounds__(256) f12_kernel(F3Args p) {
     for (int o = threadIdx.x; o < K * F12_T2; o += blockDim.x) {
         const int k1 = o / F12_T2, j = o % F12_T2;
         if (j >= nt) continue;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int u1 = 0; u1 < L; ++u1) acc = cmac(acc, sE[u1 * K + k1], sA1[u1 * F12_T2 + j]);
-        dst[(int64_t)k1 * Kh + k2_0 + j] = acc;
+        double2 q[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        int u1 = 0;
+        for (; u1 + 3 < L; u1 += 4) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) q[r] = cmac(q[r], sE[(u1 + r) * K + k1], sA1[(u1 + r) * F12_T2 + j]);
+        }
+        for (; u1 < L; ++u1) q[0] = cmac(q[0], sE[u1 * K + k1], sA1[u1 * F12_T2 + j]);
+        dst[(int64_t)k1 * Kh + k2_0 + j] = make_double2((q[0].x + q[1].x) + (q[2].x + q[3].x),
+                                                        (q[0].y + q[1].y) + (q[2].y + q[3].y));
     }
 }
 
@@ -280,23 +323,37 @@ __global__ void __launch_bounds__(256) f34_kernel(F3Args p) {
     double2* sE = sm3;               // L*K
     double2* sX = sE + L * K;        // L*T  input columns
     double2* sF = sX + L * F34_T;    // K*T  band columns
+    __shared__ uint64_t bar;
     const int c0 = blockIdx.x * F34_T;
     const int nt = min(F34_T, ncol - c0);
-    load_tw(sE, p.tw, L * K);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < L * F34_T; i += blockDim.x) {
         const int u0 = i / F34_T, t = i % F34_T;
-        sX[i] = (t < nt) ? p.A2[(int64_t)u0 * ncol + c0 + t] : make_double2(0.0, 0.0);
+        if (t < nt) cp_async16(sX + i, p.A2 + (int64_t)u0 * ncol + c0 + t);
+        else sX[i] = make_double2(0.0, 0.0);
     }
+    tma_stage(sE, p.tw, (uint32_t)(L * K * 16), &bar, 0);
+    cp_async_wait_all();
     __syncthreads();
     // sF[k0][t] = F[k0][c] * sum_u0 E[u0][k0] X[u0][t]
     for (int o = threadIdx.x; o < K * F34_T; o += blockDim.x) {
         const int k0 = o / F34_T, t = o % F34_T;
         double2 acc = make_double2(0.0, 0.0);
         if (t < nt) {
-            for (int u0 = 0; u0 < L; ++u0) acc = cmac(acc, sE[u0 * K + k0], sX[u0 * F34_T + t]);
+            double2 q[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            int u0 = 0;
+            for (; u0 + 3 < L; u0 += 4) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) q[r] = cmac(q[r], sE[(u0 + r) * K + k0], sX[(u0 + r) * F34_T + t]);
+            }
+            for (; u0 < L; ++u0) q[0] = cmac(q[0], sE[u0 * K + k0], sX[u0 * F34_T + t]);
             const double f = __ldg(p.fused + (int64_t)k0 * ncol + c0 + t);
-            acc.x *= f;
-            acc.y *= f;
+            acc.x = ((q[0].x + q[1].x) + (q[2].x + q[3].x)) * f;
+            acc.y = ((q[0].y + q[1].y) + (q[2].y + q[3].y)) * f;
         }
         sF[o] = acc;
     }
@@ -305,9 +362,15 @@ __global__ void __launch_bounds__(256) f34_kernel(F3Args p) {
     for (int o = threadIdx.x; o < L * F34_T; o += blockDim.x) {
         const int u0 = o / F34_T, t = o % F34_T;
         if (t >= nt) continue;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int k0 = 0; k0 < K; ++k0) acc = cmac_conj_a(acc, sE[u0 * K + k0], sF[k0 * F34_T + t]);
-        p.Y[(int64_t)u0 * ncol + c0 + t] = acc;
+        double2 q[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        int k0 = 0;
+        for (; k0 + 3 < K; k0 += 4) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) q[r] = cmac_conj_a(q[r], sE[u0 * K + k0 + r], sF[(k0 + r) * F34_T + t]);
+        }
+        for (; k0 < K; ++k0) q[0] = cmac_conj_a(q[0], sE[u0 * K + k0], sF[k0 * F34_T + t]);
+        p.Y[(int64_t)u0 * ncol + c0 + t] = make_double2((q[0].x + q[1].x) + (q[2].x + q[3].x),
+                                                        (q[0].y + q[1].y) + (q[2].y + q[3].y));
     }
 }
 
@@ -317,23 +380,39 @@ __global__ void __launch_bounds__(256) f56_kernel(F3Args p) {
     double2* sE = sm3;               // L*K
     double2* sB = sE + L * K;        // K*Kh slab
     double2* sA = sB + K * Kh;       // T1*Kh
+    __shared__ uint64_t bar;
     const int u0 = blockIdx.y;
     const int u1_0 = blockIdx.x * F56_T1;
     const int nr = min(F56_T1, L - u1_0);
-    load_tw(sE, p.tw, L * K);
-    const double2* slab = p.Y + (int64_t)u0 * K * Kh;
-    for (int i = threadIdx.x; i < K * Kh; i += blockDim.x) sB[i] = slab[i];
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
     __syncthreads();
+    const double2* slab = p.Y + (int64_t)u0 * K * Kh;
+    if (threadIdx.x == 0) {
+        const uint32_t b1 = (uint32_t)(L * K * 16), b2 = (uint32_t)(K * Kh * 16);
+        mbar_arrive_expect_tx(&bar, b1 + b2);
+        tma_load_1d(sE, p.tw, b1, &bar);
+        tma_load_1d(sB, slab, b2, &bar);
+    }
+    mbar_wait(&bar, 0);
     // A5[i][k2] = w(k2) * sum_k1 conj(E[u1][k1]) B[k1][k2]
     for (int o = threadIdx.x; o < F56_T1 * Kh; o += blockDim.x) {
         const int i = o / Kh, k2 = o % Kh;
         double2 acc = make_double2(0.0, 0.0);
         if (i < nr) {
             const int u1 = u1_0 + i;
-            for (int k1 = 0; k1 < K; ++k1) acc = cmac_conj_a(acc, sE[u1 * K + k1], sB[k1 * Kh + k2]);
+            double2 q[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            int k1 = 0;
+            for (; k1 + 3 < K; k1 += 4) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) q[r] = cmac_conj_a(q[r], sE[u1 * K + k1 + r], sB[(k1 + r) * Kh + k2]);
+            }
+            for (; k1 < K; ++k1) q[0] = cmac_conj_a(q[0], sE[u1 * K + k1], sB[k1 * Kh + k2]);
             const double w = (k2 == 0) ? 1.0 : 2.0;
-            acc.x *= w;
-            acc.y *= w;
+            acc.x = ((q[0].x + q[1].x) + (q[2].x + q[3].x)) * w;
+            acc.y = ((q[0].y + q[1].y) + (q[2].y + q[3].y)) * w;
         }
         sA[o] = acc;
     }
@@ -342,13 +421,22 @@ __global__ void __launch_bounds__(256) f56_kernel(F3Args p) {
     for (int o = threadIdx.x; o < F56_T1 * L; o += blockDim.x) {
         const int i = o / L, u2 = o % L;
         if (i >= nr) continue;
-        double s = 0.0;
-        for (int k2 = 0; k2 < Kh; ++k2) {
+        double q[4] = {0, 0, 0, 0};
+        int k2 = 0;
+        for (; k2 + 3 < Kh; k2 += 4) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double2 a = sA[i * Kh + k2 + r];
+                const double2 e = sE[u2 * K + k2 + r + p.half];
+                q[r] = fma(a.x, e.x, fma(a.y, e.y, q[r]));
+            }
+        }
+        for (; k2 < Kh; ++k2) {
             const double2 a = sA[i * Kh + k2];
             const double2 e = sE[u2 * K + k2 + p.half];
-            s = fma(a.x, e.x, fma(a.y, e.y, s));
+            q[0] = fma(a.x, e.x, fma(a.y, e.y, q[0]));
         }
-        p.out[((int64_t)u0 * L + u1_0 + i) * L + u2] = s;
+        p.out[((int64_t)u0 * L + u1_0 + i) * L + u2] = (q[0] + q[1]) + (q[2] + q[3]);
     }
 }
 
@@ -390,7 +478,8 @@ int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_
         return MLB_OK;
     }
     if (b->plan->conv && G.d == 2) {
-        const size_t smem = ((size_t)G.L * G.L + (size_t)(2 * G.L - 1) * (2 * G.L - 1)) * sizeof(double);
+        const size_t smem = ((size_t)((G.L * G.L + 1) & ~1) + (size_t)(2 * G.L - 1) * (2 * G.L - 1) + 2) *
+                            sizeof(double);
         if (smem <= 200 * 1024) {
             MLB_CUDA_TRY(cudaFuncSetAttribute(conv2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)smem));

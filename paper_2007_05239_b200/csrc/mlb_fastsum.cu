@@ -18,6 +18,7 @@
 
 #include "mlb_internal.cuh"
 #include "mlb_window.cuh"
+#include "mlb_tma.cuh"
 
 namespace mlb {
 
@@ -82,6 +83,7 @@ struct FsArgs {
     double* partial;
     int tile_cells;
     int nchunks;
+    int nseg;
 };
 
 // per-point spread inputs, prefetched one 32-point sub-chunk ahead
@@ -108,18 +110,25 @@ __device__ __forceinline__ void load_pt(const FsArgs& a, int p, bool ok, unsigne
 }
 
 // ----------------------------------------------------------------- spread --
-// One CTA per segment.  Each warp owns a private smem copy of the brick tile
-// and a contiguous share of the segment's chunks (sub-chunks of 32 points).
-// Per sub-chunk: each lane computes the d(2m+1) window values of one point
+// Persistent warps.  Each warp owns a private smem tile (one brick's
+// (Tb+2m)^d cells) and repeatedly claims a SEGMENT -- <= a few hundred
+// cell-sorted points of one brick -- from a work counter.  For a segment it
+// zeroes its tile, walks the points in <= 32-point sub-chunks that never
+// straddle a cell: each lane computes the d(2m+1) window values of one point
 // (v*s folded into axis 0) into smem staging; then every lane accumulates its
 // stencil block over the sub-chunk's points in registers (all points of a
-// chunk share one cell, so the block is fixed) and flushes into its warp
-// tile when the cell changes.  The next sub-chunk's inputs are prefetched
-// before the accumulation.  No atomics: warp tiles are summed in a fixed
-// order -> bitwise reproducible.
-template <int D, int M>
-__global__ void __launch_bounds__(256) spread_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v,
-                                                     unsigned flags) {
+// chunk share one cell, so the block is fixed) and flushes into the tile
+// when the cell changes.  The next sub-chunk's inputs are prefetched before
+// the accumulation.  The tile is written as the segment's partial.  No
+// atomics on data and no CTA barriers: every partial is computed by one warp
+// in a fixed order -> bitwise reproducible whatever warp claims it.
+// PERSIST (d <= 2, the whole sub-box is one brick): warps claim segments
+// statically (gw, gw + nwarps, ...), keep accumulating into their tile, and
+// the CTA sums its warp tiles in fixed order into ONE partial per CTA.
+template <int D, int M, bool PERSIST>
+__global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, WinCoef wc,
+                                                                    const double* __restrict__ v, unsigned flags,
+                                                                    int* __restrict__ work) {
     using C = SpreadCfg<D, M>;
     constexpr int S = C::S;
     constexpr int SPAD = StageCfg<D, M>::pad;
@@ -128,241 +137,295 @@ __global__ void __launch_bounds__(256) spread_kernel(FsArgs a, WinCoef wc, const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TL = a.g.TL;
     const int tile = a.tile_cells;
-    double* tiles = smem;                                   // nw * tile
-    double* stage = smem + (size_t)nw * tile;               // nw * 32 * D * SPAD
-    double* my_tile = tiles + (size_t)warp * tile;
-    double* my_stage = stage + (size_t)warp * 32 * D * SPAD;
-
-    for (int i = threadIdx.x; i < nw * tile; i += blockDim.x) tiles[i] = 0.0;
+    double* my_tile = smem + (size_t)warp * tile;
+    double* my_stage = smem + (size_t)nw * tile + (size_t)warp * 32 * D * SPAD;
     for (int i = lane; i < 32 * D * SPAD; i += 32) my_stage[i] = 0.0;
-    __syncthreads();
-
-    const int seg = blockIdx.x;
-    const int c0 = a.seg_chunk[seg], c1 = a.seg_chunk[seg + 1];
-    // balance by points: warp w owns sorted points [wp0, wp1) of the segment,
-    // walked in <= 32-point sub-chunks that never straddle a chunk (cell)
-    const int P0 = a.chunk_start[c0], P1 = a.chunk_start[c1];
-    const int wp0 = P0 + (int)(((long long)(P1 - P0) * warp) / nw);
-    const int wp1 = P0 + (int)(((long long)(P1 - P0) * (warp + 1)) / nw);
-    int chs = c0;
-    {
-        int lo = c0, hi = c1 - 1;  // first chunk with chunk_start[ch+1] > wp0
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (a.chunk_start[mid + 1] > wp0) hi = mid;
-            else lo = mid + 1;
-        }
-        chs = lo;
-    }
 
     const int l0 = lane / (C::P1 * C::P2), l1 = (lane / C::P2) % C::P1, l2 = lane % C::P2;
     const bool active = lane < C::P0 * C::P1 * C::P2;
     const int TL2 = (D == 3) ? TL * TL : 1;
     const int TL1 = (D >= 2) ? TL : 1;
+    const int gwarp = blockIdx.x * nw + warp;
+    const int nwarps = gridDim.x * nw;
+    if (PERSIST)
+        for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
 
-    for (int pass = 0; pass < C::NPASS; ++pass) {
-        const int off2 = pass * C::SP;
-        double acc[C::B0][C::B1][C::B2];
-#pragma unroll
-        for (int i = 0; i < C::B0; ++i)
-#pragma unroll
-            for (int j = 0; j < C::B1; ++j)
-#pragma unroll
-                for (int k = 0; k < C::B2; ++k) acc[i][j][k] = 0.0;
-        int cur = -1;
-
-        auto flush = [&](int cell) {
-            if (!active || cell < 0) return;
-#pragma unroll
-            for (int i = 0; i < C::B0; ++i) {
-                const int o0 = l0 * C::B0 + i;
-#pragma unroll
-                for (int j = 0; j < C::B1; ++j) {
-                    const int o1 = l1 * C::B1 + j;
-#pragma unroll
-                    for (int k = 0; k < C::B2; ++k) {
-                        const int o2 = off2 + l2 * C::B2 + k;
-                        bool ok = (o0 < S);
-                        if (D >= 2) ok = ok && (o1 < S);
-                        if (D == 3) ok = ok && (o2 < S) && (l2 * C::B2 + k < C::SP);
-                        if (ok) {
-                            int t;
-                            if (D == 1) t = cell + o0;
-                            else if (D == 2) t = cell + o0 * TL1 + o1;
-                            else t = cell + o0 * TL2 + o1 * TL1 + o2;
-                            my_tile[t] += acc[i][j][k];
-                        }
-                        acc[i][j][k] = 0.0;
-                    }
-                }
-            }
-        };
-
-        // sub-chunk iterator: (chunk ch, first point sp, end cend <= wp1)
-        int ch = chs;
-        int sp = wp0;
-        int cend = (sp < wp1) ? min(a.chunk_start[ch + 1], wp1) : wp1;
-        PtIn<D> nxt;
-        load_pt<D>(a, sp + lane, sp + lane < cend, flags, nxt);
-        double vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
-        while (sp < wp1) {
-            const int cell = a.chunk_cell[ch];
-            const int np = min(32, cend - sp);
-            const PtIn<D> cin = nxt;
-            const double vcur = vn;
-            // advance the iterator and prefetch the next sub-chunk's inputs
-            int nch2 = ch, nsp = sp + 32, nend = cend;
-            if (nsp >= cend) {
-                nsp = cend;
-                if (cend < wp1) {
-                    ++nch2;
-                    nend = min(a.chunk_start[nch2 + 1], wp1);
-                }
-            }
-            load_pt<D>(a, nsp + lane, nsp + lane < nend, flags, nxt);
-            if (cell != cur) {
-                flush(cur);
-                cur = cell;
-            }
-            __syncwarp();
-            {
-                const double val = (lane < np) ? vcur * cin.s : 0.0;
-                double w[S];
-#pragma unroll
-                for (int ax = 0; ax < D; ++ax) {
-                    kb_windows<M>(cin.f[ax], wc, w);
-                    double* dst = my_stage + (lane * D + ax) * SPAD;
-#pragma unroll
-                    for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * val : w[o];
-                }
-            }
-            vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
-            __syncwarp();
-            if (active) {
-                const int npe = (np + 1) & ~1;  // axis-0 rows past np carry val = 0
-                for (int jp = 0; jp < npe; jp += 2) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const double* ws = my_stage + (jp + h) * D * SPAD;
-                        double w0[C::B0], w1[C::B1], w2[C::B2];
-#pragma unroll
-                        for (int i = 0; i < C::B0; ++i) w0[i] = ws[l0 * C::B0 + i];
-#pragma unroll
-                        for (int j = 0; j < C::B1; ++j) w1[j] = (D >= 2) ? ws[SPAD + l1 * C::B1 + j] : 1.0;
-#pragma unroll
-                        for (int k = 0; k < C::B2; ++k)
-                            w2[k] = (D == 3) ? ws[2 * SPAD + off2 + l2 * C::B2 + k] : 1.0;
-#pragma unroll
-                        for (int i = 0; i < C::B0; ++i)
-#pragma unroll
-                            for (int j = 0; j < C::B1; ++j) {
-                                const double w01 = w0[i] * w1[j];
-#pragma unroll
-                                for (int k = 0; k < C::B2; ++k) acc[i][j][k] = fma(w01, w2[k], acc[i][j][k]);
-                            }
-                    }
-                }
-            }
-            ch = nch2;
-            sp = nsp;
-            cend = nend;
-            if (sp >= cend) break;
+    for (int it = 0;; ++it) {
+        int seg = 0;
+        if (PERSIST) {
+            seg = gwarp + it * nwarps;
+        } else {
+            if (lane == 0) seg = atomicAdd(work, 1);
+            seg = __shfl_sync(0xffffffffu, seg, 0);
         }
-        flush(cur);
+        if (seg >= a.nseg) break;
+        if (!PERSIST)
+            for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
+        const int c0 = a.seg_chunk[seg], c1 = a.seg_chunk[seg + 1];
+        const int wp0 = a.chunk_start[c0], wp1 = a.chunk_start[c1];
         __syncwarp();
+
+        for (int pass = 0; pass < C::NPASS; ++pass) {
+            const int off2 = pass * C::SP;
+            double acc[C::B0][C::B1][C::B2];
+#pragma unroll
+            for (int i = 0; i < C::B0; ++i)
+#pragma unroll
+                for (int j = 0; j < C::B1; ++j)
+#pragma unroll
+                    for (int k = 0; k < C::B2; ++k) acc[i][j][k] = 0.0;
+            int cur = -1;
+
+            auto flush = [&](int cell) {
+                if (!active || cell < 0) return;
+#pragma unroll
+                for (int i = 0; i < C::B0; ++i) {
+                    const int o0 = l0 * C::B0 + i;
+#pragma unroll
+                    for (int j = 0; j < C::B1; ++j) {
+                        const int o1 = l1 * C::B1 + j;
+#pragma unroll
+                        for (int k = 0; k < C::B2; ++k) {
+                            const int o2 = off2 + l2 * C::B2 + k;
+                            bool ok = (o0 < S);
+                            if (D >= 2) ok = ok && (o1 < S);
+                            if (D == 3) ok = ok && (o2 < S) && (l2 * C::B2 + k < C::SP);
+                            if (ok) {
+                                int t;
+                                if (D == 1) t = cell + o0;
+                                else if (D == 2) t = cell + o0 * TL1 + o1;
+                                else t = cell + o0 * TL2 + o1 * TL1 + o2;
+                                my_tile[t] += acc[i][j][k];
+                            }
+                            acc[i][j][k] = 0.0;
+                        }
+                    }
+                }
+            };
+
+            // sub-chunk iterator: (chunk ch, first point sp, end cend)
+            int ch = c0;
+            int sp = wp0;
+            int cend = a.chunk_start[ch + 1];
+            PtIn<D> nxt;
+            load_pt<D>(a, sp + lane, sp + lane < cend, flags, nxt);
+            double vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
+            while (sp < wp1) {
+                const int cell = a.chunk_cell[ch];
+                const int np = min(32, cend - sp);
+                const PtIn<D> cin = nxt;
+                const double vcur = vn;
+                // advance the iterator and prefetch the next sub-chunk's inputs
+                int nch2 = ch, nsp = sp + 32, nend = cend;
+                if (nsp >= cend) {
+                    nsp = cend;
+                    if (cend < wp1) {
+                        ++nch2;
+                        nend = a.chunk_start[nch2 + 1];
+                    }
+                }
+                load_pt<D>(a, nsp + lane, nsp + lane < nend, flags, nxt);
+                if (cell != cur) {
+                    flush(cur);
+                    cur = cell;
+                }
+                __syncwarp();
+                {
+                    const double val = (lane < np) ? vcur * cin.s : 0.0;
+                    double w[S];
+#pragma unroll
+                    for (int ax = 0; ax < D; ++ax) {
+                        kb_windows<M>(cin.f[ax], wc, w);
+                        double* dst = my_stage + (lane * D + ax) * SPAD;
+#pragma unroll
+                        for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * val : w[o];
+                    }
+                }
+                vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
+                __syncwarp();
+                if (active) {
+                    const int npe = (np + 1) & ~1;  // axis-0 rows past np carry val = 0
+                    for (int jp = 0; jp < npe; jp += 2) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const double* ws = my_stage + (jp + h) * D * SPAD;
+                            double w0[C::B0], w1[C::B1], w2[C::B2];
+#pragma unroll
+                            for (int i = 0; i < C::B0; ++i) w0[i] = ws[l0 * C::B0 + i];
+#pragma unroll
+                            for (int j = 0; j < C::B1; ++j) w1[j] = (D >= 2) ? ws[SPAD + l1 * C::B1 + j] : 1.0;
+#pragma unroll
+                            for (int k = 0; k < C::B2; ++k)
+                                w2[k] = (D == 3) ? ws[2 * SPAD + off2 + l2 * C::B2 + k] : 1.0;
+#pragma unroll
+                            for (int i = 0; i < C::B0; ++i)
+#pragma unroll
+                                for (int j = 0; j < C::B1; ++j) {
+                                    const double w01 = w0[i] * w1[j];
+#pragma unroll
+                                    for (int k = 0; k < C::B2; ++k) acc[i][j][k] = fma(w01, w2[k], acc[i][j][k]);
+                                }
+                        }
+                    }
+                }
+                ch = nch2;
+                sp = nsp;
+                cend = nend;
+                if (sp >= cend) break;
+            }
+            flush(cur);
+            __syncwarp();
+        }
+        if (!PERSIST) {
+            double* out = a.partial + (size_t)seg * tile;
+            for (int i = lane; i < tile; i += 32) out[i] = my_tile[i];
+            __syncwarp();
+        }
     }
-    __syncthreads();
-    // fixed-order sum of the warp tiles -> this segment's partial tile
-    double* out = a.partial + (size_t)seg * tile;
-    for (int i = threadIdx.x; i < tile; i += blockDim.x) {
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += tiles[(size_t)w * tile + i];
-        out[i] = s;
-    }
-    if (!a.fuse_brick_sum) return;
-    // Bricks split into several segments: the CTA that finishes last sums the
-    // brick's segment tiles in segment order into the first one (stage R1),
-    // so the result does not depend on which CTA came last.
-    const int brick = a.seg_brick[seg];
-    const int s0 = a.brick_first[brick];
-    const int ns = a.brick_seg[brick + 1] - s0;
-    if (ns < 2) return;
-    __shared__ int last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(a.brick_count + brick, 1);
-        last = (prev == ns - 1);
-        if (last) a.brick_count[brick] = 0;  // ready for the next apply
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    for (int i = threadIdx.x; i < tile; i += blockDim.x) {
-        double t = 0.0;
-        for (int j = 0; j < ns; ++j) t += __ldcg(a.partial + (size_t)(s0 + j) * tile + i);
-        a.partial[(size_t)s0 * tile + i] = t;
+    if (PERSIST) {
+        __syncthreads();
+        double* out = a.partial + (size_t)blockIdx.x * tile;
+        for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += smem[(size_t)w * tile + i];
+            out[i] = t;
+        }
     }
 }
 
 // ------------------------------------------------------------------ reduce --
-// Stage R1: for every brick split into >= 2 segments, sum its segment tiles
-// (fixed order) into the brick's first segment tile.  Block = 8 tile cells x
-// 32 segment groups; group g sums segments g, g+32, ... then the 32 group
-// sums are combined in order through smem -> deterministic.
-__global__ void seg_sum_kernel(double* __restrict__ partial, const int32_t* __restrict__ heavy, int tile,
-                               double* __restrict__ out) {
-    __shared__ double sh[32][9];
-    const int hb = blockIdx.y;
-    const int s0 = heavy[2 * hb], ns = heavy[2 * hb + 1];
-    const int c = threadIdx.x & 7, grp = threadIdx.x >> 3;
-    const int cell = blockIdx.x * 8 + c;
+// Stage R1: bricks split into >= 2 segments get their segment tiles summed
+// (fixed order) in two fully parallel passes: pass 1 sums groups of <= 16
+// consecutive segments per cell, pass 2 sums a brick's group sums in order
+// and writes the brick tile (into its first segment's slot, or straight into
+// the grid when the whole sub-box is one brick).
+constexpr int kSegGroup = 16;
+
+__global__ void seg_group_kernel(const double* __restrict__ partial, const int32_t* __restrict__ groups,
+                                 int ngroups, int tile, double* __restrict__ gsum) {
+    const int e = blockIdx.y;
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= tile) return;
+    const int s0 = groups[2 * e], cnt = groups[2 * e + 1];
+    double v[kSegGroup];
+#pragma unroll
+    for (int k = 0; k < kSegGroup; ++k) v[k] = (k < cnt) ? __ldcg(partial + (size_t)(s0 + k) * tile + cell) : 0.0;
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kSegGroup; ++k) t += v[k];
+    gsum[(size_t)e * tile + cell] = t;
+}
+
+__global__ void seg_final_kernel(double* __restrict__ partial, const int32_t* __restrict__ heavy, int nheavy,
+                                 int tile, const double* __restrict__ gsum, double* __restrict__ out) {
+    const int h = blockIdx.y;
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= tile) return;
+    const int s0 = heavy[3 * h], goff = heavy[3 * h + 1], ng = heavy[3 * h + 2];
+    double t = 0.0;
+    int g = 0;
+    for (; g + 3 < ng; g += 4) {
+        const double a0 = __ldcg(gsum + (size_t)(goff + g) * tile + cell);
+        const double a1 = __ldcg(gsum + (size_t)(goff + g + 1) * tile + cell);
+        const double a2 = __ldcg(gsum + (size_t)(goff + g + 2) * tile + cell);
+        const double a3 = __ldcg(gsum + (size_t)(goff + g + 3) * tile + cell);
+        t += a0;
+        t += a1;
+        t += a2;
+        t += a3;
+    }
+    for (; g < ng; ++g) t += __ldcg(gsum + (size_t)(goff + g) * tile + cell);
+    if (out) out[cell] = t;
+    else partial[(size_t)s0 * tile + cell] = t;
+}
+
+// d <= 2: grid[u] = sum over the spread CTAs' partial grids.  Block = 8
+// cells x 32 slices; slice k sums partials k, k+32, ...; the 32 slice sums
+// combine through a fixed shuffle tree -> deterministic.
+__global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, int cells, double* __restrict__ grid) {
+    const int slice = threadIdx.x & 31;
+    const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
     double s = 0.0;
-    if (cell < tile) {
-        int j = grp;
-        for (; j + 96 < ns; j += 128) {
-            const double a0 = partial[(size_t)(s0 + j) * tile + cell];
-            const double a1 = partial[(size_t)(s0 + j + 32) * tile + cell];
-            const double a2 = partial[(size_t)(s0 + j + 64) * tile + cell];
-            const double a3 = partial[(size_t)(s0 + j + 96) * tile + cell];
+    if (cell < cells) {
+        int j = slice;
+        for (; j + 96 < nparts; j += 128) {
+            const double a0 = __ldcg(partial + (size_t)j * cells + cell);
+            const double a1 = __ldcg(partial + (size_t)(j + 32) * cells + cell);
+            const double a2 = __ldcg(partial + (size_t)(j + 64) * cells + cell);
+            const double a3 = __ldcg(partial + (size_t)(j + 96) * cells + cell);
             s += a0;
             s += a1;
             s += a2;
             s += a3;
         }
-        for (; j < ns; j += 32) s += partial[(size_t)(s0 + j) * tile + cell];
+        for (; j < nparts; j += 32) s += __ldcg(partial + (size_t)j * cells + cell);
     }
-    sh[grp][c] = s;
-    __syncthreads();
-    if (grp == 0 && cell < tile) {
-        double t = 0.0;
-        for (int g2 = 0; g2 < 32; ++g2) t += sh[g2][c];
-        if (out) out[cell] = t;
-        else partial[(size_t)s0 * tile + cell] = t;
-    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (slice == 0 && cell < cells) grid[cell] = s;
 }
 
-// R1 variant for bricks with few segments: one thread per (brick, cell).
-__global__ void seg_sum_small_kernel(double* __restrict__ partial, const int32_t* __restrict__ heavy, int tile,
-                                     int nheavy) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)nheavy * tile) return;
-    const int hb = (int)(idx / tile), cell = (int)(idx % tile);
-    const int s0 = heavy[2 * hb], ns = heavy[2 * hb + 1];
-    double s = 0.0;
-    int j = 0;
-    for (; j + 3 < ns; j += 4) {
-        const double a0 = partial[(size_t)(s0 + j) * tile + cell];
-        const double a1 = partial[(size_t)(s0 + j + 1) * tile + cell];
-        const double a2 = partial[(size_t)(s0 + j + 2) * tile + cell];
-        const double a3 = partial[(size_t)(s0 + j + 3) * tile + cell];
-        s += a0;
-        s += a1;
-        s += a2;
-        s += a3;
+// d = 3, R1 + R2 merged: grid[u] = sum over the covering bricks (fixed
+// order) of the sum over the brick's segments (fixed order) of the segment
+// partial tiles.  A CTA covers 4 grid blocks of 4^3 cells; each grid block's
+// covering bricks are resolved once into smem (base pointer + segment count).
+__global__ void __launch_bounds__(256) reduce3m_kernel(FsArgs a, double* __restrict__ grid) {
+    constexpr int TB = 4, CPB = 64, GB = 4;
+    const Geom g = a.g;
+    const int L = g.L, TL = TB + 2 * g.m, nbr = g.nbr;
+    const int ngb = (L + TB - 1) / TB;
+    const int R = (TL + TB - 1) / TB;
+    const int RRR = R * R * R;
+    __shared__ const double* base[GB][64];
+    __shared__ int nsg[GB][64];
+    const int lb = threadIdx.x / CPB, c = threadIdx.x % CPB;
+    const int gbid = blockIdx.x * GB + lb;
+    const int gb0 = gbid / (ngb * ngb), gb1 = (gbid / ngb) % ngb, gb2 = gbid % ngb;
+    const bool live = gbid < ngb * ngb * ngb;
+    const size_t tile = (size_t)a.tile_cells;
+    for (int q = c; q < RRR; q += CPB) {
+        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
+        const int b0 = gb0 - s0, b1 = gb1 - s1, b2 = gb2 - s2;
+        const double* p = nullptr;
+        int ns = 0;
+        if (live && b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 < nbr && b1 < nbr && b2 < nbr) {
+            const int br = (b0 * nbr + b1) * nbr + b2;
+            const int f = __ldg(a.brick_seg + br);
+            ns = __ldg(a.brick_seg + br + 1) - f;
+            if (ns > 0) p = a.partial + (size_t)f * tile + ((s0 * TB) * TL + s1 * TB) * TL + s2 * TB;
+        }
+        base[lb][q] = p;
+        nsg[lb][q] = ns;
     }
-    for (; j < ns; ++j) s += partial[(size_t)(s0 + j) * tile + cell];
-    partial[(size_t)s0 * tile + cell] = s;
+    __syncthreads();
+    if (!live) return;
+    const int c0 = c / (TB * TB), c1 = (c / TB) % TB, c2 = c % TB;
+    const int u0 = gb0 * TB + c0, u1 = gb1 * TB + c1, u2 = gb2 * TB + c2;
+    if (u0 >= L || u1 >= L || u2 >= L) return;
+    const int local = (c0 * TL + c1) * TL + c2;
+    double sum = 0.0;
+    for (int q = 0; q < RRR; ++q) {
+        const double* p = base[lb][q];
+        const int ns = nsg[lb][q];
+        if (!p) continue;
+        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
+        if (s0 * TB + c0 >= TL || s1 * TB + c1 >= TL || s2 * TB + c2 >= TL) continue;
+        const double* pp = p + local;
+        double bs = 0.0;
+        int j = 0;
+        for (; j + 3 < ns; j += 4) {
+            const double x0 = __ldcg(pp + (size_t)j * tile);
+            const double x1 = __ldcg(pp + (size_t)(j + 1) * tile);
+            const double x2 = __ldcg(pp + (size_t)(j + 2) * tile);
+            const double x3 = __ldcg(pp + (size_t)(j + 3) * tile);
+            bs += x0;
+            bs += x1;
+            bs += x2;
+            bs += x3;
+        }
+        for (; j < ns; ++j) bs += __ldcg(pp + (size_t)j * tile);
+        sum += bs;
+    }
+    grid[((int64_t)u0 * L + u1) * L + u2] = sum;
 }
 
 // Stage R2: grid[u] = sum over the (<= 3^d) bricks whose tile covers u of
@@ -415,45 +478,51 @@ __global__ void reduce_kernel(FsArgs a, double* __restrict__ grid) {
     }
 }
 
-// Stage R2 for d = 3, block-centric: a CTA covers GB = 4 grid blocks of
-// Tb^3 cells; the <= 27 source bricks of each grid block are looked up once
-// (smem), then every cell issues its <= 27 independent tile loads.
-template <int TB>
+// Stage R2 for d = 3, block-centric: a CTA covers GB grid blocks of Tb^3
+// cells; the <= R^3 source brick tiles of each grid block are resolved once
+// into smem base pointers, then every cell issues its independent loads.
+template <int TB, int M>
 __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restrict__ grid) {
     constexpr int CPB = TB * TB * TB;  // cells per grid block
     constexpr int GB = 256 / CPB;      // grid blocks per CTA
+    constexpr int TL = TB + 2 * M;
+    constexpr int R = (TL + TB - 1) / TB;  // source bricks per axis
+    constexpr int RRR = R * R * R;
     const Geom g = a.g;
-    const int L = g.L, TL = TB + 2 * g.m, nbr = g.nbr;
+    const int L = g.L, nbr = g.nbr;
     const int ngb = (L + TB - 1) / TB;  // grid blocks per axis
-    const int R = (TL + TB - 1) / TB;   // source bricks per axis (3 for m=4,Tb=4)
-    __shared__ int src[GB][64];
+    __shared__ const double* base[GB][64];
     const int lb = threadIdx.x / CPB, c = threadIdx.x % CPB;
     const int gbid = blockIdx.x * GB + lb;
     const int gb0 = gbid / (ngb * ngb), gb1 = (gbid / ngb) % ngb, gb2 = gbid % ngb;
     const bool live = gbid < ngb * ngb * ngb;
-    if (c < R * R * R) {
-        const int s0 = c / (R * R), s1 = (c / R) % R, s2 = c % R;
+    for (int q = c; q < RRR; q += CPB) {
+        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
         const int b0 = gb0 - s0, b1 = gb1 - s1, b2 = gb2 - s2;
-        int f = -1;
-        if (live && b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 < nbr && b1 < nbr && b2 < nbr)
-            f = __ldg(a.brick_first + (b0 * nbr + b1) * nbr + b2);
-        src[lb][c] = f;
+        const double* p = nullptr;
+        if (live && b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 < nbr && b1 < nbr && b2 < nbr) {
+            const int f = __ldg(a.brick_first + (b0 * nbr + b1) * nbr + b2);
+            if (f >= 0) p = a.partial + (size_t)f * a.tile_cells + ((s0 * TB) * TL + s1 * TB) * TL + s2 * TB;
+        }
+        base[lb][q] = p;
     }
     __syncthreads();
     if (!live) return;
     const int c0 = c / (TB * TB), c1 = (c / TB) % TB, c2 = c % TB;
     const int u0 = gb0 * TB + c0, u1 = gb1 * TB + c1, u2 = gb2 * TB + c2;
     if (u0 >= L || u1 >= L || u2 >= L) return;
+    const int local = (c0 * TL + c1) * TL + c2;
+    constexpr bool exact = (R * TB == TL);
     double sum = 0.0;
-    const int RRR = R * R * R;
-#pragma unroll 8
+#pragma unroll
     for (int q = 0; q < RRR; ++q) {
-        const int f = src[lb][q];
-        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
-        const int t0 = s0 * TB + c0, t1 = s1 * TB + c1, t2 = s2 * TB + c2;
-        const bool ok = f >= 0 && t0 < TL && t1 < TL && t2 < TL;
-        const double x = ok ? __ldcg(a.partial + (size_t)f * a.tile_cells + (t0 * TL + t1) * TL + t2) : 0.0;
-        sum += x;
+        const double* p = base[lb][q];
+        bool ok = p != nullptr;
+        if (!exact) {
+            const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
+            ok = ok && (s0 * TB + c0 < TL) && (s1 * TB + c1 < TL) && (s2 * TB + c2 < TL);
+        }
+        sum += ok ? __ldcg(p + local) : 0.0;
     }
     grid[((int64_t)u0 * L + u1) * L + u2] = sum;
 }
@@ -466,15 +535,17 @@ __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restri
 // value read (a broadcast LDS: the whole chunk shares one cell) feeds two
 // FMAs.  Epilogue: y = alpha v + s (beta acc + gamma s v).
 template <int D, int M>
-__global__ void __launch_bounds__(256) gather_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
+__global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
                                                      const double* __restrict__ v, double* __restrict__ y,
                                                      double alpha, double beta, double gamma, unsigned flags) {
     constexpr int S = 2 * M + 1;
     constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
+    constexpr int W0S = 2 * S + 1;  // per-lane axis-0 window row (odd stride)
     extern __shared__ double nbs[];
     const int L = a.g.L;
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     double* nb = nbs + wl * NB;
+    double* w0s = nbs + 8 * NB + (wl * 32 + lane) * W0S;  // [0,S): point A, [S,2S): point B
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwt = (gridDim.x * blockDim.x) >> 5;
     const int c_lo = (int)(((long long)a.nchunks * gw) / nwt);
@@ -500,14 +571,22 @@ __global__ void __launch_bounds__(256) gather_kernel(FsArgs a, WinCoef wc, const
                 if (D == 1) off = e;
                 else if (D == 2) off = (e / S) * rs + e % S;
                 else off = (e / (S * S)) * rs + ((e / S) % S) * (int64_t)L + e % S;
-                nb[e] = __ldg(grid + gbase + off);
+                cp_async8(nb + e, grid + gbase + off);
             }
+            cp_async_wait_all();
             __syncwarp();
             cur = gbase;
         }
         double wA0[S], wA1[S], wA2[S], wB0[S], wB1[S], wB2[S];
         kb_windows<M>(fA0, wc, wA0);
         kb_windows<M>(fB0, wc, wB0);
+        if (D == 3) {
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+                w0s[q] = wA0[q];
+                w0s[S + q] = wB0[q];
+            }
+        }
         if (D >= 2) {
             kb_windows<M>(fA1, wc, wA1);
             kb_windows<M>(fB1, wc, wB1);
@@ -554,14 +633,8 @@ __global__ void __launch_bounds__(256) gather_kernel(FsArgs a, WinCoef wc, const
                     rA = fma(wA1[j], qA, rA);
                     rB = fma(wB1[j], qB, rB);
                 }
-                double xA = 0.0, xB = 0.0;
-#pragma unroll
-                for (int q = 0; q < S; ++q) {
-                    xA = (q == i) ? wA0[q] : xA;
-                    xB = (q == i) ? wB0[q] : xB;
-                }
-                accA = fma(xA, rA, accA);
-                accB = fma(xB, rB, accB);
+                accA = fma(w0s[i], rA, accA);
+                accB = fma(w0s[S + i], rB, accB);
             }
         }
 #pragma unroll
@@ -600,6 +673,7 @@ static FsArgs make_args(mlb_binding* b) {
     a.partial = b->partial;
     a.tile_cells = b->tile_cells;
     a.nchunks = b->nchunks;
+    a.nseg = b->nseg;
     return a;
 }
 
@@ -611,12 +685,43 @@ static size_t spread_smem(int nw, int tile_cells) {
 template <int D, int M>
 static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st) {
     FsArgs a = make_args(b);
-    int nw = 8;
-    while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 200 * 1024) --nw;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (D <= 2) {
+        // persistent CTAs of 8 warps, one partial grid per CTA
+        int nw = 8;
+        while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
+        const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
+        if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
+        auto kern = spread_kernel<D, M, true>;
+        MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int blocks = std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);
+        if (blocks < 1) blocks = 1;
+        b->spread_parts = blocks;
+        kern<<<blocks, nw * 32, smem, st>>>(a, b->plan->wc, v, flags, b->work);
+        note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+        return MLB_OK;
+    }
+    const int nw = 2;  // warps per CTA: several CTAs per SM, independent warps
     const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
-    auto kern = spread_kernel<D, M>;
-    MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<b->nseg, nw * 32, smem, st>>>(a, b->plan->wc, v, flags);
+    if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
+    auto kern = spread_kernel<D, M, false>;
+    static int per_sm = 0;
+    static size_t per_sm_smem = 0;
+    if (per_sm == 0 || per_sm_smem != smem) {
+        MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MLB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
+        if (per_sm < 1) per_sm = 1;
+        per_sm_smem = smem;
+    }
+    int blocks = nsm * per_sm;
+    const int need = (b->nseg + nw - 1) / nw;
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    MLB_CUDA_TRY(cudaMemsetAsync(b->work, 0, sizeof(int), st));
+    kern<<<blocks, nw * 32, smem, st>>>(a, b->plan->wc, v, flags, b->work);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
@@ -628,7 +733,7 @@ static int gather_dm(mlb_binding* b, const double* grid, const double* v, double
     constexpr int S = 2 * M + 1;
     constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
     FsArgs a = make_args(b);
-    const size_t smem = (size_t)8 * NB * sizeof(double);
+    const size_t smem = ((size_t)8 * NB + (size_t)256 * (2 * S + 1)) * sizeof(double);
     auto kern = gather_kernel<D, M>;
     static int per_sm = 0;  // resident blocks per SM for this instantiation
     if (per_sm == 0) {
@@ -678,40 +783,51 @@ int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t 
     MLB_DISPATCH_DM(spread_dm, g.d, g.m, b, v, flags, st);
 }
 
+static int launch_seg_sum(mlb_binding* b, double* out, cudaStream_t st) {
+    if (b->nheavy == 0) return MLB_OK;
+    const int tile = b->tile_cells;
+    const unsigned cx = (unsigned)((tile + 255) / 256);
+    seg_group_kernel<<<dim3(cx, b->ngroups), 256, 0, st>>>(b->partial, b->groups, b->ngroups, tile, b->gsum);
+    seg_final_kernel<<<dim3(cx, b->nheavy), 256, 0, st>>>(b->partial, b->heavy, b->nheavy, tile, b->gsum, out);
+    note_launches(2);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
 int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     FsArgs a = make_args(b);
     const Geom& G = b->plan->g;
     if (G.d <= 2) {
-        // one brick covering the whole sub-box: R1 writes the grid directly
-        if (b->nseg == 1) {
-            MLB_CUDA_TRY(cudaMemcpyAsync(grid, b->partial, b->grid_cells * sizeof(double),
-                                         cudaMemcpyDeviceToDevice, st));
-            return MLB_OK;
-        }
-        dim3 g1((b->tile_cells + 7) / 8, 1);
-        seg_sum_kernel<<<g1, 256, 0, st>>>(b->partial, b->heavy, b->tile_cells, grid);
+        // the spread left one partial grid per CTA
+        const int cells = (int)b->grid_cells;
+        grid_sum_kernel<<<(cells + 7) / 8, 256, 0, st>>>(b->partial, b->spread_parts, cells, grid);
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
     }
-    // d = 3: R1 ran inside the spread kernel (last CTA per brick)
     const int Tb = G.Tb;
     const int ngb = (G.L + Tb - 1) / Tb;
     const int64_t nblk = (int64_t)ngb * ngb * ngb;
     const int R = (G.TL + Tb - 1) / Tb;  // source bricks per axis
+    int rc = launch_seg_sum(b, nullptr, st);
+    if (rc != MLB_OK) return rc;
     if (Tb == 4 && R * R * R <= 64) {
-        reduce3_kernel<4><<<(unsigned)((nblk + 3) / 4), 256, 0, st>>>(a, grid);
-    } else if (Tb == 2) {
-        const int64_t total = b->grid_cells;
-        int64_t blocks = (total + 255) / 256;
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        reduce_kernel<3, 2><<<(int)blocks, 256, 0, st>>>(a, grid);
-    } else {
-        const int64_t total = b->grid_cells;
-        int64_t blocks = (total + 255) / 256;
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        reduce_kernel<3, 0><<<(int)blocks, 256, 0, st>>>(a, grid);
+        const unsigned nb = (unsigned)((nblk + 3) / 4);
+        switch (G.m) {
+            case 2: reduce3_kernel<4, 2><<<nb, 256, 0, st>>>(a, grid); break;
+            case 3: reduce3_kernel<4, 3><<<nb, 256, 0, st>>>(a, grid); break;
+            case 4: reduce3_kernel<4, 4><<<nb, 256, 0, st>>>(a, grid); break;
+            default: reduce3_kernel<4, 5><<<nb, 256, 0, st>>>(a, grid); break;
+        }
+        note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+        return MLB_OK;
     }
+    const int64_t total = b->grid_cells;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (Tb == 2) reduce_kernel<3, 2><<<(int)blocks, 256, 0, st>>>(a, grid);
+    else reduce_kernel<3, 0><<<(int)blocks, 256, 0, st>>>(a, grid);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;

@@ -24,6 +24,7 @@ int fail(int code, const std::string& msg);
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
 constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
+constexpr int kSegPoints = 512;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
 // Window polynomial coefficients, passed by value as a kernel parameter
@@ -74,11 +75,17 @@ struct mlb_binding {
     int32_t* seg_chunk = nullptr;    // nseg+1
     int32_t* seg_brick = nullptr;    // nseg
     int32_t* brick_seg = nullptr;    // nbricks+1 (CSR, bricks lexicographic)
-    int32_t* heavy = nullptr;        // nheavy x (first segment, segment count) of bricks with >= 2 segments
+    int32_t* heavy = nullptr;        // nheavy x (first segment, group offset, group count), bricks with >= 2 segments
     int nheavy = 0;
+    int32_t* groups = nullptr;       // ngroups x (first segment, count <= 16) for the R1 pass 1
+    int ngroups = 0;
+    double* gsum = nullptr;          // ngroups x tile group sums
     int max_heavy_segs = 0;
     int32_t* brick_first = nullptr;  // nbricks: first segment of the brick, -1 if empty
-    int32_t* brick_count = nullptr;  // nbricks: completion counters of the spread epilogue (kept at 0)
+    int32_t* brick_count = nullptr;  // nbricks: (unused) completion counters
+    int* work = nullptr;             // spread work counter (reset before every launch)
+    int spread_parts = 0;            // d <= 2: partial grids written by the last spread (one per CTA)
+    int spread_parts_max = 0;        // capacity of `partial` in whole grids (d <= 2)
     double* isd = nullptr;           // sorted order
     // scratch
     double* partial = nullptr;       // nseg x TL^d
