@@ -121,6 +121,12 @@ int mlb_spread(mlb_binding* b, const double* v_dev, double* grid_dev, unsigned f
 int mlb_convolve(mlb_binding* b, const double* grid_in_dev, double* grid_out_dev, void* stream);
 int mlb_gather(mlb_binding* b, const double* grid_dev, double* y_dev, unsigned flags, void* stream);
 
+/* Complex band DFT between the active sub-box (L^d complex cells) and the full
+ * band (K^d complex, k = -N/2..N/2 per axis): forward sum_u in[u] e^{-2 pi i k.u/ng},
+ * inverse sum_k in[k] e^{+2 pi i k.u/ng} (unnormalised).  Building block of the
+ * bare transforms nfft_adjoint / nfft_forward (fastsum.py:418-468). */
+int mlb_band_dft(mlb_binding* b, const double* in_dev, double* out_dev, int inverse, void* stream);
+
 /* Permutations between node order and the binding's sorted order. */
 int mlb_to_sorted(const mlb_binding* b, const double* v_node_dev, double* v_sorted_dev, void* stream);
 int mlb_to_node(const mlb_binding* b, const double* v_sorted_dev, double* v_node_dev, int accumulate,

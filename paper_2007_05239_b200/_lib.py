@@ -54,6 +54,7 @@ SIGNATURES = {
     "mlb_spread": (I, [P, P, P, U, P]),
     "mlb_convolve": (I, [P, P, P, P]),
     "mlb_gather": (I, [P, P, P, U, P]),
+    "mlb_band_dft": (I, [P, P, P, I, P]),
     "mlb_to_sorted": (I, [P, P, P, P]),
     "mlb_to_node": (I, [P, P, P, I, P]),
     "mlb_krylov_work_size": (I64, [I64, I]),

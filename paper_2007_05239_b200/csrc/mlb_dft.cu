@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "mlb_internal.cuh"
 #include "mlb_tma.cuh"
@@ -623,4 +624,76 @@ int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_
     return MLB_OK;
 }
 
+// Complex band DFT between the active sub-box (L^d cells) and the full band
+// (K^d frequencies k = -N/2..N/2): the bare NFFT test hooks of the reference
+// (nfft_adjoint / nfft_forward, fastsum.py:418-468) use it.
+//   forward: out[k] = sum_u in[u] exp(-2 pi i k.u/ng)
+//   inverse: out[u] = sum_k in[k] exp(+2 pi i k.u/ng)   (unnormalised)
+int band_dft(mlb_binding* b, const double* in, double* out, int inverse, cudaStream_t st) {
+    const Geom& G = b->plan->g;
+    const int L = G.L, K = G.K, d = G.d;
+    const int nin = inverse ? K : L, nout = inverse ? L : K;
+    // ping-pong through the stage buffers (grown on demand: max(L,K)^d complex)
+    const int64_t need = 2 * (int64_t)std::llround(std::pow((double)std::max(L, K), d));
+    if (need > b->stage_elems) {
+        cudaFree(b->stage_a);
+        cudaFree(b->stage_b);
+        b->stage_a = b->stage_b = nullptr;
+        MLB_CUDA_TRY(cudaMalloc((void**)&b->stage_a, need * sizeof(double)));
+        MLB_CUDA_TRY(cudaMalloc((void**)&b->stage_b, need * sizeof(double)));
+        b->stage_elems = need;
+    }
+    GemmArgs g;
+    g.tw = b->plan->twid;
+    g.K = K;
+    g.fused = nullptr;
+    const double* cur = in;
+    // row-major [n0]..[n_{d-1}]: transform the last axis first; the data is
+    // viewed as [before][nin][after] -> [before][nout][after]
+    int64_t before = 1, after = 1;
+    for (int i = 1; i < d; ++i) before *= nin;
+    double* bufs[2] = {b->stage_a, b->stage_b};
+    for (int step = 0; step < d; ++step) {
+        double* dst = (step == d - 1) ? out : bufs[step & 1];
+        if (after == 1) {
+            g.A = op(cur, 0, nin);
+            g.B = op(nullptr, 0, 0, 0);
+            g.C = dst;
+            g.c_bstride = 0;
+            g.ldc = nout;
+            g.M = (int)before;
+            g.N = nout;
+            g.Kd = nin;
+            if (inverse) run_gemm<OP_DATA_C, OP_TWC_T, EP_C>(g, 1, st);   // (k,u) = conj(E[u][k])
+            else run_gemm<OP_DATA_C, OP_TW, EP_C>(g, 1, st);              // (u,k) = E[u][k]
+        } else {
+            g.A = op(nullptr, 0, 0, 0);
+            g.B = op(cur, (int64_t)nin * after, (int)after);
+            g.C = dst;
+            g.c_bstride = (int64_t)nout * after;
+            g.ldc = (int)after;
+            g.M = nout;
+            g.N = (int)after;
+            g.Kd = nin;
+            if (inverse) run_gemm<OP_TWC, OP_DATA_C, EP_C>(g, (int)before, st);   // (u,k) = conj(E[u][k])
+            else run_gemm<OP_TW_T, OP_DATA_C, EP_C>(g, (int)before, st);          // (k,u) = E[u][k]
+        }
+        cur = dst;
+        after *= nout;
+        if (step < d - 1) before /= nin;
+    }
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
 }  // namespace mlb
+
+extern "C" int mlb_band_dft(mlb_binding* b, const double* in_dev, double* out_dev, int inverse, void* stream) {
+    if (!b || !in_dev || !out_dev) return mlb::fail(MLB_ERR_ARG, "null argument");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != b->plan->device) cudaSetDevice(b->plan->device);
+    const int rc = mlb::band_dft(b, in_dev, out_dev, inverse, (cudaStream_t)stream);
+    if (dev != b->plan->device) cudaSetDevice(dev);
+    return rc;
+}

@@ -1,0 +1,312 @@
+"""Multi-GPU partitioning of the NFFT Laplacian path.
+
+Two partitionings, one process per GPU, torch.distributed for the plumbing
+(NCCL over NVLink on the B200 box, gloo in the CPU tests):
+
+1. Layer round-robin -- `LayerParallelGraph`.  Layers are independent until
+   the layer sum of apply_Lp_power (powermean.py:80-95) / apply_one_minus_L1
+   (powermean.py:64-77); rank r owns layers t = r, r+W, ...  Each operator
+   apply gathers the per-layer results and every rank sums them in layer
+   order, so all ranks hold bitwise-identical vectors and the outer Lanczos
+   runs replicated with no further communication.
+
+2. Node-range sharding of one large layer -- `ShardedLayer`.  Spreading is
+   additive over point subsets: each rank spreads its node range into a
+   private grid, the grids are summed over the ranks (all-reduce of the
+   active sub-box only), each rank convolves redundantly and gathers its own
+   nodes.  Krylov vectors are sharded by the same ranges; dot products are
+   all-reduced (`sharded_pksm`).
+
+The per-rank compute is an `engine` (spread / convolve / gather on the
+local points): `BindingEngine` runs libmlb on the GPU; the CPU tests plug in
+an engine built from the numpy oracle, which is how the partitioning logic
+is verified with gloo at world_size 2 without GPUs.
+"""
+
+import math
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, NumericalError
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ------------------------------------------------------------------ comm ----
+class Comm:
+    """Thin wrapper over a torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_reduce_sum(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def all_gather(self, t):
+        out = [_torch().empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return out
+
+    def ordered_sum(self, t):
+        """Sum over ranks in rank order (deterministic, unlike a tree all-reduce)."""
+        parts = self.all_gather(t)
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        t.copy_(acc)
+        return t
+
+
+def shard_range(n, rank, world):
+    """Contiguous node range [lo, hi) of `rank` (balanced)."""
+    lo = (n * rank) // world
+    hi = (n * (rank + 1)) // world
+    return lo, hi
+
+
+# ------------------------------------------------ 1. layer round-robin ------
+class LayerParallelGraph:
+    """A MultilayerGraph whose layers are owned round-robin by the ranks.
+
+    `local_layers[t]` is this rank's Layer for global layer t (None if owned
+    elsewhere).  `pksm(layer, p, v)` / `weighted(layer, v)` compute one
+    layer's contribution; by default the GPU ones.
+    """
+
+    def __init__(self, T, n, local_layers, comm, pksm=None, weighted=None):
+        self.T, self.n, self.comm = T, n, comm
+        self.local_layers = local_layers
+        self._pksm = pksm
+        self._weighted = weighted
+
+    def owner(self, t):
+        return t % self.comm.world
+
+    def _layer_sum(self, contrib, v):
+        """(1/T) sum_t contrib(layer_t, v), summed in layer order on every rank."""
+        torch = _torch()
+        mine = [t for t in range(self.T) if self.owner(t) == self.comm.rank]
+        slots = int(math.ceil(self.T / self.comm.world))
+        buf = torch.zeros((slots, self.n), dtype=torch.float64, device=v.device)
+        for i, t in enumerate(mine):
+            buf[i] = contrib(self.local_layers[t], v)
+        gathered = self.comm.all_gather(buf)
+        out = torch.zeros_like(v)
+        for t in range(self.T):                     # fixed layer order
+            out += gathered[self.owner(t)][t // self.comm.world]
+        return out / self.T
+
+    def apply_Lp_power(self, p, v, krylov_dim=50, tol=1e-8):
+        if self._pksm is None:
+            from .krylov import pksm_layer_dev
+
+            def contrib(layer, x):
+                out = _torch().zeros_like(x)
+                return pksm_layer_dev(layer, p, x, out, 1.0, False, krylov_dim, tol)
+        else:
+            def contrib(layer, x):
+                return self._pksm(layer, p, x)
+        return self._layer_sum(contrib, v)
+
+    def apply_one_minus_L1(self, v):
+        if self._weighted is None:
+            from .graphs import KernelWeights
+
+            def contrib(layer, x):
+                out = _torch().zeros_like(x)
+                w = layer.weights
+                if not isinstance(w, KernelWeights):
+                    raise ConfigError("layer-parallel p=1 path needs GPU kernel layers")
+                w.apply_dev(x, out, 0.0, 1.0, -w.kernel.value_at_zero(), _lib.MLB_USE_ISD)
+                return out
+        else:
+            contrib = self._weighted
+        return self._layer_sum(contrib, v)
+
+
+def power_mean_eigs_layer_parallel(lpg, config, k, tol=1e-8, max_subspace=None, max_restarts=60, krylov_dim=50,
+                                   inner_tol=None, seed=0, device=None):
+    """power_mean_eigs (powermean.py:130-189) with the layer sum distributed.
+
+    Every rank runs the same outer Lanczos on identical vectors; only the
+    operator apply communicates.  Returns (values ascending, vectors n x k).
+    """
+    from .krylov import SymmetricOperator, lanczos_largest_eigs
+    p = config.p
+    itol = tol if inner_tol is None else inner_tol
+    if p == 1:
+        apply_dev = lpg.apply_one_minus_L1
+    elif p < 0:
+        apply_dev = lambda v: lpg.apply_Lp_power(p, v, krylov_dim, itol)  # noqa: E731
+    else:
+        raise ConfigError("layer-parallel eigensolver covers p = 1 and p < 0")
+    op = SymmetricOperator(lpg.n, None, "layer-parallel", apply_dev=apply_dev, device=device)
+    res = lanczos_largest_eigs(op, k, tol=tol, max_subspace=max_subspace, max_restarts=max_restarts, seed=seed)
+    if p == 1:
+        values = np.maximum(1.0 - res.values, 0.0)
+    else:
+        if res.values.min() <= 0.0:
+            raise NumericalError("power mean spectrum is not positive; cannot take the 1/p root")
+        values = res.values ** (1.0 / p)
+    return values, res.vectors
+
+
+# ------------------------------------------------ 2. node-range sharding ----
+class BindingEngine:
+    """libmlb spread / convolve / gather on this rank's points (GPU)."""
+
+    def __init__(self, plan, points_local, device=None):
+        from . import fastsum
+        torch = _torch()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.binding = fastsum.bind_points(plan, points_local, device=self.device)
+        self.cells = self.binding.stats()["grid_cells"]
+
+    def new_grid(self):
+        torch = _torch()
+        return torch.zeros(self.cells, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def ones(self, n):
+        torch = _torch()
+        return torch.ones(n, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def spread(self, x):
+        g = self.new_grid()
+        _lib.check(_lib.lib().mlb_spread(self.binding.ptr, _lib.ptr(x), _lib.ptr(g), 0, _lib.stream_ptr()))
+        return g
+
+    def convolve(self, g):
+        out = _torch().empty_like(g)
+        _lib.check(_lib.lib().mlb_convolve(self.binding.ptr, _lib.ptr(g), _lib.ptr(out), _lib.stream_ptr()))
+        return out
+
+    def gather(self, g):
+        y = _torch().empty(self.binding.n, dtype=_torch().float64, device=g.device)
+        _lib.check(_lib.lib().mlb_gather(self.binding.ptr, _lib.ptr(g), _lib.ptr(y), 0, _lib.stream_ptr()))
+        return y
+
+
+class ShardedLayer:
+    """One kernel layer split by node range over the ranks.
+
+    Vectors are this rank's slice [lo, hi).  Every Laplacian apply performs
+    exactly one collective: the sum of the spread grids (active sub-box).
+    """
+
+    def __init__(self, engine, n_global, lo, hi, comm, K0=1.0, shift=0.0, deterministic=True):
+        self.engine, self.n, self.lo, self.hi, self.comm = engine, n_global, lo, hi, comm
+        self.K0, self.shift, self.deterministic = float(K0), float(shift), deterministic
+        self.degrees = None
+        self.isd = None
+
+    @property
+    def n_local(self):
+        return self.hi - self.lo
+
+    def w_tilde(self, x):
+        """(W~ x)_local: spread local charges, sum grids over ranks, convolve, gather."""
+        g = self.engine.spread(x)
+        if self.deterministic:
+            self.comm.ordered_sum(g)
+        else:
+            self.comm.all_reduce_sum(g)
+        return self.engine.gather(self.engine.convolve(g))
+
+    def matvec(self, x):
+        """(W x)_local with zero diagonal (fastsum_apply, fastsum.py:475-497)."""
+        return self.w_tilde(x) - self.K0 * x
+
+    def build(self):
+        """Degrees W 1 and D^-1/2 (graphs.py:168-183); zero degree on any rank raises."""
+        torch = _torch()
+        ones = self._ones()
+        deg = self.matvec(ones)
+        host = deg.cpu().numpy() if isinstance(deg, torch.Tensor) else np.asarray(deg)
+        bad = np.flatnonzero(host <= 1e-300)
+        first = torch.tensor([float(self.lo + bad[0]) if bad.size else float(self.n)], dtype=torch.float64)
+        if isinstance(deg, torch.Tensor) and deg.is_cuda:
+            first = first.to(deg.device)
+        self.comm.dist.all_reduce(first, op=self.comm.dist.ReduceOp.MIN, group=self.comm.group)
+        if int(first.item()) < self.n:
+            raise NumericalError(f"node {int(first.item())} has zero degree; the normalized Laplacian is undefined")
+        self.degrees = deg
+        self.isd = 1.0 / (deg ** 0.5) if isinstance(deg, torch.Tensor) else 1.0 / np.sqrt(deg)
+        return self
+
+    def _ones(self):
+        return self.engine.ones(self.n_local)
+
+    def apply_lsym(self, x):
+        """((1+shift) I - D^-1/2 W D^-1/2) x, local rows (graphs.py:197-201)."""
+        return (1.0 + self.shift) * x - self.isd * self.matvec(self.isd * x)
+
+    def dot(self, a, b):
+        torch = _torch()
+        if isinstance(a, torch.Tensor):
+            t = (a * b).sum().reshape(1).to(torch.float64)
+        else:
+            t = torch.tensor([float(np.dot(a, b))], dtype=torch.float64)
+        parts = self.comm.all_gather(t)
+        return float(sum(float(p.item()) for p in parts))   # rank order: deterministic
+
+
+def sharded_lanczos_fn(layer, v, fn, krylov_dim=50, tol=1e-8):
+    """Lanczos f(A) v (krylov.py:172-216) on node-sharded vectors.
+
+    The basis is sharded with the nodes; every inner product is a global sum
+    over ranks (rank order), so all ranks take identical decisions.
+    """
+    torch = _torch()
+    is_t = isinstance(v, torch.Tensor)
+    nv = math.sqrt(layer.dot(v, v))
+    if nv == 0.0:
+        return v * 0.0
+    dim = int(min(krylov_dim, layer.n))
+    V = [v / nv]
+    alphas, betas = [], []
+    y_prev = None
+    while True:
+        s = len(V) - 1
+        w = layer.apply_lsym(V[s])
+        alphas.append(layer.dot(V[s], w))
+        # CGS2 against V[0..s] with global dot products (krylov.py:65-71)
+        for _ in range(2):
+            h = [layer.dot(Vj, w) for Vj in V]
+            for Vj, hj in zip(V, h):
+                w = w - hj * Vj
+        beta = math.sqrt(layer.dot(w, w))
+        betas.append(beta)
+        m = len(alphas)
+        T = np.diag(alphas)
+        if m > 1:
+            T += np.diag(betas[: m - 1], 1) + np.diag(betas[: m - 1], -1)
+        lam, Q = np.linalg.eigh(T)
+        c = nv * (Q @ (fn(lam) * Q[0, :]))
+        y = c[0] * V[0]
+        for j in range(1, m):
+            y = y + c[j] * V[j]
+        if y_prev is not None:
+            d = y - y_prev
+            if math.sqrt(layer.dot(d, d)) <= tol * max(math.sqrt(layer.dot(y, y)), 1e-300):
+                return y
+        if beta <= 1e-13 * max(1.0, float(np.abs(alphas).max())) or m >= dim:
+            return y
+        y_prev = y
+        V.append(w / beta)
+
+
+def sharded_pksm(layer, p, v, krylov_dim=50, tol=1e-8):
+    """(L_sym + delta)^p v on node-sharded vectors (krylov.py:219-244)."""
+    from .krylov import power_fn
+    if p == 0:
+        raise ConfigError("p must be nonzero")
+    return sharded_lanczos_fn(layer, v, power_fn(p), krylov_dim, tol)

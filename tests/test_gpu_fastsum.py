@@ -164,3 +164,52 @@ def test_large_property_checks():
     op = fo.OraclePlan("gaussian", 0.05, 3, 32, 4, p=8)
     ref = fo.fastsum(op, u[:20000], points=sub)
     assert rel(fastsum_apply(None, u[:20000], plan, binding=b2), ref) < 1e-12
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_bare_nfft_matches_reference_golden(d):
+    """nfft_adjoint / nfft_forward (fastsum.py:418-468) vs reference outputs,
+    plus exact adjointness <forward(c), v> = <c, conj(adjoint(v))>."""
+    from paper_2007_05239_b200 import KernelSpec, build_plan
+    from paper_2007_05239_b200.fastsum import nfft_adjoint, nfft_forward
+    g = load_golden("nfft")
+    plan = build_plan(KernelSpec("gaussian", 0.2), d=d, N=16)
+    pts, v, c = g[f"d{d}/points"], g[f"d{d}/v"], g[f"d{d}/coeffs"]
+    adj = nfft_adjoint(pts, v, plan)
+    ref = g[f"d{d}/adjoint"]
+    assert np.abs(adj - ref).max() <= 1e-12 * np.abs(ref).max()
+    fwd = nfft_forward(c, pts, plan)
+    ref = g[f"d{d}/forward"]
+    assert np.abs(fwd - ref).max() <= 1e-12 * np.abs(ref).max()
+    lhs = np.sum(fwd * v)
+    rhs = np.sum(c * np.conj(adj))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def test_sharded_layer_single_rank_matches_layer():
+    """dist.ShardedLayer + BindingEngine (NCCL, world size 1) == the fused layer."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2007_05239_b200 import KernelSpec, KernelWeights, build_layer, build_plan, with_shift
+    from paper_2007_05239_b200.dist import BindingEngine, Comm, ShardedLayer, sharded_pksm
+    from paper_2007_05239_b200.graphs import apply_sym_laplacian
+    from paper_2007_05239_b200.krylov import pksm_apply
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        rng = np.random.default_rng(5)
+        n = 3000
+        pts = np.clip(rng.normal(0, 0.07, size=(n, 3)), -0.21875, 0.21875)
+        kern = KernelSpec("gaussian", 0.12)
+        plan = build_plan(kern, d=3, N=32, m_nfft=4, p_nfft=8)
+        layer = with_shift(build_layer(KernelWeights(pts, kern, plan=plan)), math.log(2.0))
+        v = rng.standard_normal(n)
+        sl = ShardedLayer(BindingEngine(plan, pts), n, 0, n, Comm(), K0=1.0, shift=math.log(2.0)).build()
+        vd = torch.from_numpy(v).cuda()
+        assert rel(sl.apply_lsym(vd).cpu().numpy(), apply_sym_laplacian(layer, v)) < 1e-12
+        assert rel(sharded_pksm(sl, -1.0, vd).cpu().numpy(), pksm_apply(layer, -1.0, v)) < 1e-9
+    finally:
+        dist.destroy_process_group()
