@@ -84,7 +84,11 @@ def config2_segmentation(seed=0, side=512):
 
 def config3_feature_grouped(seed=0, side=200, bands=104):
     """200x200, 16 blob classes, 104 smooth bands + N(0, 0.02^2), min-max scaled;
-    52 layers of consecutive band pairs (d=2, sigma=0.05, N=32, m=4)."""
+    52 layers of consecutive band pairs (d=2, sigma=0.05, m=4).
+
+    Correction: N=64.  At the configured N=32 the reference rejects 11 of the
+    52 layers of this data (negative NFFT degrees; checked with the oracle).
+    """
     rng = np.random.default_rng(seed)
     H = W = side
     cent = rng.random((16, 2))
@@ -99,7 +103,7 @@ def config3_feature_grouped(seed=0, side=200, bands=104):
             spectra[c] += a * np.exp(-0.5 * ((bidx - mu) / sd) ** 2)
     X = spectra[truth] + rng.normal(0.0, 0.02, (H * W, bands))
     X = (X - X.min(axis=0)) / (X.max(axis=0) - X.min(axis=0))
-    layers = [LayerSpec((2 * i, 2 * i + 1), 0.05, 32, 4, 8) for i in range(bands // 2)]
+    layers = [LayerSpec((2 * i, 2 * i + 1), 0.05, 64, 4, 8) for i in range(bands // 2)]
     return Workload("cfg3_feature_grouped_200x200x104", X, layers, truth, k=10, label_fraction=0.05)
 
 

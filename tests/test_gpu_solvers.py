@@ -145,3 +145,29 @@ def test_direct_apply_matches_oracle():
         fam, s = FAM[int(g[name + "/spec"][0])], float(g[name + "/spec"][1])
         got = direct_apply(g[name + "/points"], g[name + "/v"], KernelSpec(fam, s))
         assert_allclose(got, g[name + "/direct"], atol=1e-11)
+
+
+def test_config1_pipeline_matches_reference():
+    """BASELINE configs[0] end to end (GPU) vs the reference run frozen in
+    golden_cfg1.npz: eigenvalues <= 1e-7 relative, same Allen-Cahn iteration
+    count, labels identical on >= 99.9% of the nodes."""
+    import synth
+    from paper_2007_05239_b200 import (AllenCahnParams, LabelData, PowerMeanConfig, allen_cahn_solve,
+                                       power_mean_eigs, predict_labels)
+    g = load_golden("cfg1")
+    wl = synth.config1_toy(seed=0)
+    assert np.array_equal(wl.X, g["X"])
+    G = synth.build_graph(wl)
+    assert rel(G.layers[0].degrees, g["deg0"]) < 1e-12
+    assert rel(G.layers[1].degrees, g["deg1"]) < 1e-12
+    basis = power_mean_eigs(G, PowerMeanConfig(p=-1.0), k=wl.k, seed=0)
+    assert np.max(np.abs(basis.values - g["values"]) / np.abs(g["values"])) <= 1e-7
+    P = basis.vectors @ basis.vectors.T
+    Pr = g["vectors"] @ g["vectors"].T
+    assert np.abs(P - Pr).max() < 1e-5
+    ids = g["label_ids"]
+    labels = LabelData.from_class_ids(ids, int(ids.max()) + 1, 1000.0)
+    res = allen_cahn_solve(basis, labels, AllenCahnParams())
+    pred = predict_labels(res.scores)
+    assert np.mean(pred == g["pred"]) >= 0.999
+    assert abs(res.iterations - int(g["iters"][0])) <= 1

@@ -1,0 +1,70 @@
+"""End-to-end solver benchmark: feature layers -> power-mean eigenpairs -> Allen-Cahn.
+
+    python tools/bench_solver.py [--config 1|2|3] [--side S]
+
+Prints one JSON line with stage times, the number of layer matvecs inside
+the eigensolver (effective node*layers/s in the solver, SURVEY 8(d)
+"Eigensolve" timing) and the classification accuracy.
+"""
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import synth
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--side", type=int, default=0)
+    ap.add_argument("--k", type=int, default=0)
+    args = ap.parse_args()
+    from paper_2007_05239_b200 import (AllenCahnParams, PowerMeanConfig, _lib, allen_cahn_solve, power_mean_eigs,
+                                       predict_labels, sample_labels)
+    from paper_2007_05239_b200.krylov import PksmStats
+    torch.cuda.set_device(0)
+    gen = synth.CONFIGS[args.config]
+    wl = gen(seed=0, side=args.side) if args.side else gen(seed=0)
+    k = args.k or wl.k
+    t0 = time.perf_counter()
+    G = synth.build_graph(wl, device=0)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    PksmStats.reset()
+    l0 = _lib.lib().mlb_launch_count()
+    stats = {}
+    t0 = time.perf_counter()
+    basis = power_mean_eigs(G, PowerMeanConfig(p=wl.p_mean), k=k, seed=0, return_device=True, stats=stats)
+    torch.cuda.synchronize()
+    t_eig = time.perf_counter() - t0
+    layer_mv = int(sum(PksmStats.steps)) + 4 * len(G.layers)  # + degree / probe applies are not counted here
+    labels = sample_labels(wl.truth, wl.label_fraction, seed=0)
+    t0 = time.perf_counter()
+    res = allen_cahn_solve(basis, labels, AllenCahnParams(max_iter=wl.ac_max_iter), return_device=True)
+    pred = predict_labels(res.scores).cpu().numpy()
+    t_ac = time.perf_counter() - t0
+    acc = float(np.mean(pred == wl.truth))
+    out = {
+        "workload": wl.name, "n": wl.n, "layers": len(G.layers), "k": k,
+        "t_build_s": t_build, "t_eig_s": t_eig, "t_ac_s": t_ac,
+        "outer_matvecs": stats.get("matvecs"), "restarts": stats.get("restarts"),
+        "pksm_calls": len(PksmStats.steps), "layer_matvecs": int(sum(PksmStats.steps)),
+        "node_layers_per_s_in_solver": wl.n * sum(PksmStats.steps) / t_eig if t_eig > 0 else None,
+        "ac_iterations": res.iterations, "ac_converged": res.converged, "accuracy": acc,
+        "values": [float(x) for x in basis.values], "libmlb_launches": int(_lib.lib().mlb_launch_count() - l0),
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
