@@ -56,7 +56,11 @@ typedef struct mlb_binding mlb_binding;
  *                of fastsum.py:158-167 as an exact-to-1e-14 polynomial).
  *   conv_kernel: d <= 2 only (NULL for d = 3): (2L-1)^d real spatial kernel
  *                Kc[D] = sum_{|k|<=N/2} F(k) cos(2 pi k.D / ng), D = -(L-1)..L-1,
- *                so the convolution stage is a direct sub-box convolution. */
+ *                so the convolution stage is a direct sub-box convolution.
+ *   sep_kernel : nullable, 2L-1 reals: when the band weights are a rank-1
+ *                tensor F(k) = prod_a f(k_a) (checked on the host to 1e-13),
+ *                c[D] = sum_k f(k) cos(2 pi k D / ng) and the convolution runs
+ *                as d one-dimensional passes. */
 typedef struct mlb_plan_desc {
     int d, N, m, ng;
     int bin_lo, bin_hi;       /* admissible floor(ng*x) range per axis */
@@ -66,6 +70,7 @@ typedef struct mlb_plan_desc {
     const double* twiddle;    /* host */
     const double* win_coef;   /* host */
     const double* conv_kernel;/* host, d <= 2 (nullable for d = 3) */
+    const double* sep_kernel; /* host, nullable: separable 1-D kernel */
 } mlb_plan_desc;
 
 int mlb_abi_version(void);

@@ -30,7 +30,7 @@ U = C.c_uint
 class PlanDesc(C.Structure):
     _fields_ = [("d", I), ("N", I), ("m", I), ("ng", I), ("bin_lo", I), ("bin_hi", I),
                 ("win_deg", I), ("K0", D), ("fused_band", P), ("twiddle", P), ("win_coef", P),
-                ("conv_kernel", P)]
+                ("conv_kernel", P), ("sep_kernel", P)]
 
 
 # name -> (restype, argtypes); mirrors include/multilap_b200.h

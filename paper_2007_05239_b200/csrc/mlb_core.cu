@@ -140,6 +140,7 @@ int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
         for (size_t i = 0; i < tw.size(); ++i) tw[i] = make_double2(desc->twiddle[2 * i], desc->twiddle[2 * i + 1]);
         rc = dev_upload(&p->twid, tw.data(), tw.size());
     }
+    if (rc == MLB_OK && desc->sep_kernel) rc = dev_upload(&p->sep, desc->sep_kernel, (size_t)(2 * g.L - 1));
     if (rc == MLB_OK && d <= 2 && desc->conv_kernel) {
         const size_t nk = (d == 1) ? (size_t)(2 * g.L - 1) : (size_t)(2 * g.L - 1) * (2 * g.L - 1);
         // +2 doubles: TMA bulk copies round sizes up to 16 bytes
@@ -151,6 +152,7 @@ int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
         dev_free(p->fused);
         dev_free(p->twid);
         dev_free(p->conv);
+        dev_free(p->sep);
         delete p;
         return rc;
     }
@@ -164,6 +166,7 @@ int mlb_plan_destroy(mlb_plan* p) {
     dev_free(p->fused);
     dev_free(p->twid);
     dev_free(p->conv);
+    dev_free(p->sep);
     delete p;
     return MLB_OK;
 }
@@ -317,7 +320,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         st = std::max((int64_t)g.L * g.L * g.Kh, (int64_t)g.L * g.K * g.Kh);
         st = std::max(st, (int64_t)g.K * g.K * g.Kh);
     }
-    b->stage_elems = 2 * st;
+    b->stage_elems = std::max<int64_t>(2 * st, b->grid_cells);  // >= one real grid (separable passes)
     int rc = MLB_OK;
     if (rc == MLB_OK) rc = dev_upload(&b->perm, perm_node.data(), (size_t)n);
     if (rc == MLB_OK) rc = dev_upload(&b->frac, fs.data(), (size_t)n * d);

@@ -59,6 +59,7 @@ struct mlb_plan {
     double* fused = nullptr;     // band weights (K^(d-1) x Kh)
     double2* twid = nullptr;     // L x K
     double* conv = nullptr;      // d <= 2: (2L-1)^d spatial kernel (nullptr: use the DFT stages)
+    double* sep = nullptr;       // separable 1-D kernel (2L-1), nullptr if F is not rank-1
     std::vector<double> win_coef_host;
 };
 

@@ -56,9 +56,12 @@ def test_two_point_hand_sum():
     assert_allclose(got, math.exp(-4.0) * np.array([2.0, 1.0]), rtol=1e-6)
 
 
-@pytest.mark.parametrize("d,N,m", [(1, 32, 4), (2, 32, 4), (2, 64, 5), (3, 16, 4), (3, 32, 5), (2, 16, 6), (3, 16, 6), (3, 64, 4)])
-def test_stages_match_oracle(d, N, m):
-    """spread grid, convolved grid and gather, each against the oracle."""
+@pytest.mark.parametrize("d,N,m,sigma", [(1, 32, 4, 0.15), (2, 32, 4, 0.15), (2, 64, 5, 0.15), (3, 16, 4, 0.15),
+                                         (3, 32, 5, 0.15), (2, 16, 6, 0.15), (3, 16, 6, 0.15), (3, 64, 4, 0.15),
+                                         (2, 32, 4, 0.05), (3, 32, 4, 0.05), (3, 64, 4, 0.08), (3, 16, 6, 0.05)])
+def test_stages_match_oracle(d, N, m, sigma):
+    """spread grid, convolved grid and gather, each against the oracle
+    (sigma <= 0.1 exercises the separable convolution path)."""
     import torch
     from paper_2007_05239_b200 import KernelSpec, bind_points, build_plan
     from paper_2007_05239_b200 import _lib
@@ -67,7 +70,7 @@ def test_stages_match_oracle(d, N, m):
     hw = 0.25 - 0.5 / 16
     pts = rng.uniform(-hw, hw, size=(n, d))
     v = rng.standard_normal(n)
-    plan = build_plan(KernelSpec("gaussian", 0.15), d=d, N=N, m_nfft=m, p_nfft=8)
+    plan = build_plan(KernelSpec("gaussian", sigma), d=d, N=N, m_nfft=m, p_nfft=8)
     b = bind_points(plan, pts)
     L, ulo = b._plan_handle.L, b._plan_handle.ulo
     lib = _lib.lib()
@@ -75,7 +78,7 @@ def test_stages_match_oracle(d, N, m):
     grid = torch.zeros(L ** d, dtype=torch.float64, device="cuda")
     _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(vd), _lib.ptr(grid), 0, _lib.stream_ptr()))
     # oracle spread on the full ng^d torus, folded onto the sub-box indices
-    op = fo.OraclePlan("gaussian", 0.15, d, N, m, p=8)
+    op = fo.OraclePlan("gaussian", sigma, d, N, m, p=8)
     ob = fo.bind(op, pts)
     full = fo.spread(ob, v).reshape((op.ng,) * d)
     idx = np.mod(np.arange(ulo, ulo + L), op.ng)
