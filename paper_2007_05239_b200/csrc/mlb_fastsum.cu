@@ -43,14 +43,18 @@ struct SpreadCfg<2, M> {
     static constexpr int B0 = 1, B1 = (S + P1 - 1) / P1, B2 = 1;
     static constexpr int NPASS = 1, SP = S;
 };
+// d = 3: lane (i, j-block) owns one axis-0 offset, B1 axis-1 offsets and a
+// whole axis-2 row, so each product w0[i] w1[j] is formed by exactly one lane
+// (no redundant DMULs) and w2 is a broadcast read; NPASS splits axis 2 so the
+// B1 x SP accumulator block stays <= 36 doubles.
 template <int M>
 struct SpreadCfg<3, M> {
     static constexpr int S = 2 * M + 1;
-    static constexpr bool small = (M <= 4);
-    static constexpr int P0 = small ? 3 : 4, P1 = small ? 3 : 4, P2 = small ? 3 : 2;
-    static constexpr int NPASS = (M >= 6) ? 2 : 1;
+    static constexpr int P0 = S, P1 = 32 / S, P2 = 1;
+    static constexpr int B0 = 1, B1 = (S + P1 - 1) / P1;
+    static constexpr int NPASS = (B1 * S <= 36) ? 1 : ((B1 * ((S + 1) / 2) <= 36) ? 2 : 3);
     static constexpr int SP = (S + NPASS - 1) / NPASS;  // cells of axis 2 per pass
-    static constexpr int B0 = (S + P0 - 1) / P0, B1 = (S + P1 - 1) / P1, B2 = (SP + P2 - 1) / P2;
+    static constexpr int B2 = SP;
 };
 
 // staged window row stride: covers every lane's reach (entries >= S stay 0)
@@ -62,7 +66,7 @@ struct StageCfg {
     static constexpr int r1 = C::P1 * C::B1;
     static constexpr int r2 = (C::NPASS - 1) * C::SP + C::P2 * C::B2;
     static constexpr int reach = (r0 > r1 ? (r0 > r2 ? r0 : r2) : (r1 > r2 ? r1 : r2));
-    static constexpr int pad = (reach % 2) ? reach : reach + 1;
+    static constexpr int pad = (reach % 2) ? reach : reach + 1;  // odd: conflict-free staging writes
 };
 
 struct FsArgs {
@@ -539,7 +543,8 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
                                                      const double* __restrict__ v, double* __restrict__ y,
                                                      double alpha, double beta, double gamma, unsigned flags) {
     constexpr int S = 2 * M + 1;
-    constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
+    constexpr int SR = S;  // staged row length
+    constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * SR);
     constexpr int W0S = 2 * S + 1;  // per-lane axis-0 window row (odd stride)
     extern __shared__ double nbs[];
     const int L = a.g.L;
@@ -566,12 +571,14 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         const double fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
         if (gbase != cur) {
             __syncwarp();
-            for (int e = lane; e < NB; e += 32) {
+            constexpr int NSRC = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
+            for (int e = lane; e < NSRC; e += 32) {
                 int64_t off;
                 if (D == 1) off = e;
                 else if (D == 2) off = (e / S) * rs + e % S;
                 else off = (e / (S * S)) * rs + ((e / S) % S) * (int64_t)L + e % S;
-                cp_async8(nb + e, grid + gbase + off);
+                const int dst = (D == 3) ? (e / S) * SR + e % S : e;
+                cp_async8(nb + dst, grid + gbase + off);
             }
             cp_async_wait_all();
             __syncwarp();
@@ -619,14 +626,14 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         } else {
 #pragma unroll 1
             for (int i = 0; i < S; ++i) {
-                const double* gi = nb + i * S * S;
+                const double* gi = nb + i * S * SR;
                 double rA = 0.0, rB = 0.0;
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
                     double qA = 0.0, qB = 0.0;
 #pragma unroll
                     for (int k = 0; k < S; ++k) {
-                        const double gv = gi[j * S + k];
+                        const double gv = gi[j * SR + k];
                         qA = fma(wA2[k], gv, qA);
                         qB = fma(wB2[k], gv, qB);
                     }

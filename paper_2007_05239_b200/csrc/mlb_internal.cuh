@@ -24,7 +24,7 @@ int fail(int code, const std::string& msg);
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
 constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
-constexpr int kSegPoints = 512;   // points per spread work unit (one warp)
+constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
 // Window polynomial coefficients, passed by value as a kernel parameter
