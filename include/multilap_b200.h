@@ -40,6 +40,7 @@ extern "C" {
 #define MLB_USE_ISD 1u        /* s = D^-1/2 (set by mlb_binding_set_isd), else s = 1 */
 #define MLB_ACCUMULATE 2u     /* y += result instead of y = result */
 #define MLB_SORTED 4u         /* v and y are in the binding's sorted (cell) order */
+#define MLB_SPREAD_ONLY 8u    /* mlb_spread: run the spread kernel only (partials, no reduction) */
 
 typedef struct mlb_plan mlb_plan;
 typedef struct mlb_binding mlb_binding;
@@ -123,6 +124,8 @@ int mlb_apply(mlb_binding* b, const double* v_dev, double* y_dev, double alpha, 
  * (fastsum.py:492-495), gather (fastsum.py:400-406). */
 int mlb_grid_cells(const mlb_binding* b, int64_t* cells, int* L, int* u_lo);
 int mlb_spread(mlb_binding* b, const double* v_dev, double* grid_dev, unsigned flags, void* stream);
+/* the deterministic partial-tile reduction of the last spread into grid_dev */
+int mlb_reduce(mlb_binding* b, double* grid_dev, void* stream);
 int mlb_convolve(mlb_binding* b, const double* grid_in_dev, double* grid_out_dev, void* stream);
 int mlb_gather(mlb_binding* b, const double* grid_dev, double* y_dev, unsigned flags, void* stream);
 

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmlb.so")
 
 MLB_OK, MLB_ERR_CONFIG, MLB_ERR_NUMERICAL, MLB_ERR_CUDA, MLB_ERR_ARG = 0, 1, 2, 3, 4
-MLB_USE_ISD, MLB_ACCUMULATE, MLB_SORTED = 1, 2, 4
+MLB_USE_ISD, MLB_ACCUMULATE, MLB_SORTED, MLB_SPREAD_ONLY = 1, 2, 4, 8
 
 _lock = threading.Lock()
 _lib = None
@@ -52,6 +52,7 @@ SIGNATURES = {
     "mlb_apply": (I, [P, P, P, D, D, D, U, P]),
     "mlb_grid_cells": (I, [P, P, P, P]),
     "mlb_spread": (I, [P, P, P, U, P]),
+    "mlb_reduce": (I, [P, P, P]),
     "mlb_convolve": (I, [P, P, P, P]),
     "mlb_gather": (I, [P, P, P, U, P]),
     "mlb_band_dft": (I, [P, P, P, I, P]),

@@ -444,13 +444,24 @@ int mlb_spread(mlb_binding* b, const double* v, double* grid, unsigned flags, vo
     if (!b || !grid) return fail(MLB_ERR_ARG, "null argument");
     DeviceGuard guard(b->plan->device);
     cudaStream_t st = (cudaStream_t)stream;
-    int rc = launch_spread(b, v, flags, st);
+    int rc = launch_spread(b, v, flags & ~MLB_SPREAD_ONLY, st);
     if (rc != MLB_OK) return rc;
+    if (flags & MLB_SPREAD_ONLY) return MLB_OK;
     if (b->nseg == 0) {
         MLB_CUDA_TRY(cudaMemsetAsync(grid, 0, b->grid_cells * sizeof(double), st));
         return MLB_OK;
     }
     return launch_reduce(b, grid, st);
+}
+
+int mlb_reduce(mlb_binding* b, double* grid, void* stream) {
+    if (!b || !grid) return fail(MLB_ERR_ARG, "null argument");
+    DeviceGuard guard(b->plan->device);
+    if (b->nseg == 0) {
+        MLB_CUDA_TRY(cudaMemsetAsync(grid, 0, b->grid_cells * sizeof(double), (cudaStream_t)stream));
+        return MLB_OK;
+    }
+    return launch_reduce(b, grid, (cudaStream_t)stream);
 }
 
 int mlb_convolve(mlb_binding* b, const double* gin, double* gout, void* stream) {
