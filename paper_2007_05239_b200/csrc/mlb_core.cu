@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -180,6 +181,8 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->chunk_cell);
     dev_free(b->chunk_gcell);
     dev_free(b->seg_chunk);
+    dev_free(b->sub_desc);
+    dev_free(b->seg_sub);
     dev_free(b->seg_brick);
     dev_free(b->brick_seg);
     dev_free(b->heavy);
@@ -264,6 +267,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     // (large n: grow segments so the partial tiles stay ~ 148 x 16 of them)
     int seg_points = (int)std::max<int64_t>(kSegPoints, n / (148 * 16));
     while (seg_points > 64 && (n / seg_points) < 148 * 8) seg_points /= 2;
+    if (const char* env = std::getenv("MLB_SEG_POINTS")) seg_points = std::max(32, std::atoi(env));  // tuning
     std::vector<int32_t> seg_chunk, seg_brick, brick_seg(nbricks + 1, 0);
     for (int c = 0; c < nch;) {
         const int br = chunk_brick[c];
@@ -276,6 +280,18 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     }
     const int nseg = (int)seg_brick.size();
     seg_chunk.push_back(nch);
+    // sub-chunk descriptors (<= 32 points of one cell), in segment order
+    std::vector<int32_t> sub_desc, seg_sub(nseg + 1, 0);
+    for (int sg = 0; sg < nseg; ++sg) {
+        seg_sub[sg] = (int)(sub_desc.size() / 2);
+        for (int c = seg_chunk[sg]; c < seg_chunk[sg + 1]; ++c)
+            for (int32_t p = chunk_start[c]; p < chunk_start[c + 1]; p += 32) {
+                const int cnt = std::min<int32_t>(32, chunk_start[c + 1] - p);
+                sub_desc.push_back(p);
+                sub_desc.push_back((cnt << 24) | chunk_cell[c]);
+            }
+    }
+    seg_sub[nseg] = (int)(sub_desc.size() / 2);
     for (int br = 0; br < nbricks; ++br) brick_seg[br + 1] += brick_seg[br];
     std::vector<int32_t> heavy, groups, brick_first(nbricks, -1);
     int max_heavy = 0;
@@ -328,6 +344,8 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_cell, chunk_cell.data(), chunk_cell.size());
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_gcell, chunk_gcell.data(), chunk_gcell.size());
     if (rc == MLB_OK) rc = dev_upload(&b->seg_chunk, seg_chunk.data(), seg_chunk.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->sub_desc, sub_desc.data(), sub_desc.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->seg_sub, seg_sub.data(), seg_sub.size());
     if (rc == MLB_OK) rc = dev_upload(&b->seg_brick, seg_brick.data(), seg_brick.size());
     if (rc == MLB_OK) rc = dev_upload(&b->brick_seg, brick_seg.data(), brick_seg.size());
     if (rc == MLB_OK) rc = dev_upload(&b->heavy, heavy.data(), heavy.size());
@@ -473,7 +491,7 @@ int mlb_convolve(mlb_binding* b, const double* gin, double* gout, void* stream) 
 int mlb_gather(mlb_binding* b, const double* grid, double* y, unsigned flags, void* stream) {
     if (!b || !grid || !y) return fail(MLB_ERR_ARG, "null argument");
     DeviceGuard guard(b->plan->device);
-    return launch_gather(b, grid, nullptr, y, 0.0, 1.0, 0.0, flags & (MLB_SORTED | MLB_ACCUMULATE),
+    return launch_gather(b, grid, nullptr, y, 0.0, 1.0, 0.0, flags & (MLB_SORTED | MLB_ACCUMULATE | 0x30000u),
                          (cudaStream_t)stream);
 }
 

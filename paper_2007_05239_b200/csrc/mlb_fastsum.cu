@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "mlb_internal.cuh"
 #include "mlb_window.cuh"
@@ -66,7 +67,9 @@ struct StageCfg {
     static constexpr int r1 = C::P1 * C::B1;
     static constexpr int r2 = (C::NPASS - 1) * C::SP + C::P2 * C::B2;
     static constexpr int reach = (r0 > r1 ? (r0 > r2 ? r0 : r2) : (r1 > r2 ? r1 : r2));
-    static constexpr int pad = (reach % 2) ? reach : reach + 1;  // odd: conflict-free staging writes
+    // d = 3: even stride so the broadcast axis-2 row is read as 16-byte pairs
+    static constexpr bool vec2 = (D == 3) && (C::NPASS == 1 || C::SP % 2 == 0);
+    static constexpr int pad = vec2 ? (reach + (reach & 1)) : ((reach % 2) ? reach : reach + 1);
 };
 
 struct FsArgs {
@@ -77,6 +80,8 @@ struct FsArgs {
     const int32_t* chunk_start;
     const int32_t* chunk_cell;
     const int32_t* chunk_gcell;
+    const int2* sub_desc;     // sub-chunks in segment order: {first point, (count << 24) | tile cell}
+    const int32_t* seg_sub;   // nseg + 1: CSR of sub-chunks per segment
     const int32_t* seg_chunk;
     const int32_t* seg_brick;
     const int32_t* brick_seg;
@@ -114,21 +119,47 @@ __device__ __forceinline__ void load_pt(const FsArgs& a, int p, bool ok, unsigne
 }
 
 // ----------------------------------------------------------------- spread --
-// Persistent warps.  Each warp owns a private smem tile (one brick's
-// (Tb+2m)^d cells) and repeatedly claims a SEGMENT -- <= a few hundred
-// cell-sorted points of one brick -- from a work counter.  For a segment it
-// zeroes its tile, walks the points in <= 32-point sub-chunks that never
-// straddle a cell: each lane computes the d(2m+1) window values of one point
-// (v*s folded into axis 0) into smem staging; then every lane accumulates its
-// stencil block over the sub-chunk's points in registers (all points of a
-// chunk share one cell, so the block is fixed) and flushes into the tile
-// when the cell changes.  The next sub-chunk's inputs are prefetched before
-// the accumulation.  The tile is written as the segment's partial.  No
-// atomics on data and no CTA barriers: every partial is computed by one warp
-// in a fixed order -> bitwise reproducible whatever warp claims it.
-// PERSIST (d <= 2, the whole sub-box is one brick): warps claim segments
-// statically (gw, gw + nwarps, ...), keep accumulating into their tile, and
-// the CTA sums its warp tiles in fixed order into ONE partial per CTA.
+// Warps own segments statically (gw, gw + W, ...).  A segment is a list of
+// sub-chunks (<= 32 cell-sorted points of ONE cell; descriptor table built at
+// bind time), walked through a 3-deep software pipeline so that no load waits
+// on another in the steady state: descriptors 3 sub-chunks ahead, point
+// indices (perm) 2 ahead, coordinates / D^-1/2 / v 1 ahead.
+// Per sub-chunk each lane evaluates one point's d(2m+1) windows (v s folded
+// into axis 0) into smem staging; then the lanes, which own disjoint blocks
+// of the (2m+1)^d stencil, accumulate the sub-chunk's points in registers and
+// flush into the warp's smem brick tile when the cell changes.  PERSIST
+// (d <= 2: one brick = the whole sub-box) keeps the tile across segments and
+// the CTA sums its warp tiles into one partial grid; otherwise every segment
+// writes its own partial tile.  No atomics -> bitwise reproducible.
+struct SubPos {
+    int sub;   // global sub-chunk index, -1 = no more work
+    int seg;   // its segment
+    int end;   // one past the segment's last sub-chunk
+};
+
+__device__ __forceinline__ SubPos sub_first(const FsArgs& a, int seg) {
+    SubPos p;
+    if (seg >= a.nseg) {
+        p.sub = -1;
+        p.seg = seg;
+        p.end = 0;
+        return p;
+    }
+    p.sub = __ldg(a.seg_sub + seg);
+    p.end = __ldg(a.seg_sub + seg + 1);
+    p.seg = seg;
+    return p;
+}
+
+__device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps) {
+    if (p.sub < 0) return p;
+    if (p.sub + 1 < p.end) {
+        p.sub += 1;
+        return p;
+    }
+    return sub_first(a, p.seg + nwarps);
+}
+
 template <int D, int M, bool PERSIST>
 __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, WinCoef wc,
                                                                     const double* __restrict__ v, unsigned flags,
@@ -144,6 +175,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     double* my_tile = smem + (size_t)warp * tile;
     double* my_stage = smem + (size_t)nw * tile + (size_t)warp * 32 * D * SPAD;
     for (int i = lane; i < 32 * D * SPAD; i += 32) my_stage[i] = 0.0;
+    for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
 
     const int l0 = lane / (C::P1 * C::P2), l1 = (lane / C::P2) % C::P1, l2 = lane % C::P2;
     const bool active = lane < C::P0 * C::P1 * C::P2;
@@ -151,138 +183,191 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     const int TL1 = (D >= 2) ? TL : 1;
     const int gwarp = blockIdx.x * nw + warp;
     const int nwarps = gridDim.x * nw;
-    if (PERSIST)
-        for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
+    const bool sorted = (flags & MLB_SORTED) != 0;
+    const bool use_isd = (flags & MLB_USE_ISD) != 0;
 
-    for (int it = 0;; ++it) {
-        int seg = 0;
-        if (PERSIST) {
-            seg = gwarp + it * nwarps;
-        } else {
-            if (lane == 0) seg = atomicAdd(work, 1);
-            seg = __shfl_sync(0xffffffffu, seg, 0);
-        }
-        if (seg >= a.nseg) break;
-        if (!PERSIST)
-            for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
-        const int c0 = a.seg_chunk[seg], c1 = a.seg_chunk[seg + 1];
-        const int wp0 = a.chunk_start[c0], wp1 = a.chunk_start[c1];
-        __syncwarp();
+    for (int pass = 0; pass < C::NPASS; ++pass) {
+        const int off2 = pass * C::SP;
+        double acc[C::B0][C::B1][C::B2];
+#pragma unroll
+        for (int i = 0; i < C::B0; ++i)
+#pragma unroll
+            for (int j = 0; j < C::B1; ++j)
+#pragma unroll
+                for (int k = 0; k < C::B2; ++k) acc[i][j][k] = 0.0;
+        int cur = -1;
 
-        for (int pass = 0; pass < C::NPASS; ++pass) {
-            const int off2 = pass * C::SP;
-            double acc[C::B0][C::B1][C::B2];
+        auto flush = [&](int cell) {
+            if (!active || cell < 0) return;
+            if (flags & (1u << 18)) return;  // ablation (profiling only)
 #pragma unroll
-            for (int i = 0; i < C::B0; ++i)
+            for (int i = 0; i < C::B0; ++i) {
+                const int o0 = l0 * C::B0 + i;
 #pragma unroll
-                for (int j = 0; j < C::B1; ++j)
+                for (int j = 0; j < C::B1; ++j) {
+                    const int o1 = l1 * C::B1 + j;
 #pragma unroll
-                    for (int k = 0; k < C::B2; ++k) acc[i][j][k] = 0.0;
-            int cur = -1;
-
-            auto flush = [&](int cell) {
-                if (!active || cell < 0) return;
-#pragma unroll
-                for (int i = 0; i < C::B0; ++i) {
-                    const int o0 = l0 * C::B0 + i;
-#pragma unroll
-                    for (int j = 0; j < C::B1; ++j) {
-                        const int o1 = l1 * C::B1 + j;
-#pragma unroll
-                        for (int k = 0; k < C::B2; ++k) {
-                            const int o2 = off2 + l2 * C::B2 + k;
-                            bool ok = (o0 < S);
-                            if (D >= 2) ok = ok && (o1 < S);
-                            if (D == 3) ok = ok && (o2 < S) && (l2 * C::B2 + k < C::SP);
-                            if (ok) {
-                                int t;
-                                if (D == 1) t = cell + o0;
-                                else if (D == 2) t = cell + o0 * TL1 + o1;
-                                else t = cell + o0 * TL2 + o1 * TL1 + o2;
-                                my_tile[t] += acc[i][j][k];
-                            }
-                            acc[i][j][k] = 0.0;
+                    for (int k = 0; k < C::B2; ++k) {
+                        const int o2 = off2 + l2 * C::B2 + k;
+                        bool ok = (o0 < S);
+                        if (D >= 2) ok = ok && (o1 < S);
+                        if (D == 3) ok = ok && (o2 < S) && (l2 * C::B2 + k < C::SP);
+                        if (ok) {
+                            int t;
+                            if (D == 1) t = cell + o0;
+                            else if (D == 2) t = cell + o0 * TL1 + o1;
+                            else t = cell + o0 * TL2 + o1 * TL1 + o2;
+                            my_tile[t] += acc[i][j][k];
                         }
+                        acc[i][j][k] = 0.0;
                     }
                 }
-            };
-
-            // sub-chunk iterator: (chunk ch, first point sp, end cend)
-            int ch = c0;
-            int sp = wp0;
-            int cend = a.chunk_start[ch + 1];
-            PtIn<D> nxt;
-            load_pt<D>(a, sp + lane, sp + lane < cend, flags, nxt);
-            double vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
-            while (sp < wp1) {
-                const int cell = a.chunk_cell[ch];
-                const int np = min(32, cend - sp);
-                const PtIn<D> cin = nxt;
-                const double vcur = vn;
-                // advance the iterator and prefetch the next sub-chunk's inputs
-                int nch2 = ch, nsp = sp + 32, nend = cend;
-                if (nsp >= cend) {
-                    nsp = cend;
-                    if (cend < wp1) {
-                        ++nch2;
-                        nend = a.chunk_start[nch2 + 1];
-                    }
-                }
-                load_pt<D>(a, nsp + lane, nsp + lane < nend, flags, nxt);
-                if (cell != cur) {
-                    flush(cur);
-                    cur = cell;
-                }
-                __syncwarp();
-                {
-                    const double val = (lane < np) ? vcur * cin.s : 0.0;
-                    double w[S];
-#pragma unroll
-                    for (int ax = 0; ax < D; ++ax) {
-                        kb_windows<M>(cin.f[ax], wc, w);
-                        double* dst = my_stage + (lane * D + ax) * SPAD;
-#pragma unroll
-                        for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * val : w[o];
-                    }
-                }
-                vn = (nxt.node >= 0) ? __ldg(v + nxt.node) : 0.0;
-                __syncwarp();
-                if (active) {
-                    const int npe = (np + 1) & ~1;  // axis-0 rows past np carry val = 0
-                    for (int jp = 0; jp < npe; jp += 2) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const double* ws = my_stage + (jp + h) * D * SPAD;
-                            double w0[C::B0], w1[C::B1], w2[C::B2];
-#pragma unroll
-                            for (int i = 0; i < C::B0; ++i) w0[i] = ws[l0 * C::B0 + i];
-#pragma unroll
-                            for (int j = 0; j < C::B1; ++j) w1[j] = (D >= 2) ? ws[SPAD + l1 * C::B1 + j] : 1.0;
-#pragma unroll
-                            for (int k = 0; k < C::B2; ++k)
-                                w2[k] = (D == 3) ? ws[2 * SPAD + off2 + l2 * C::B2 + k] : 1.0;
-#pragma unroll
-                            for (int i = 0; i < C::B0; ++i)
-#pragma unroll
-                                for (int j = 0; j < C::B1; ++j) {
-                                    const double w01 = w0[i] * w1[j];
-#pragma unroll
-                                    for (int k = 0; k < C::B2; ++k) acc[i][j][k] = fma(w01, w2[k], acc[i][j][k]);
-                                }
-                        }
-                    }
-                }
-                ch = nch2;
-                sp = nsp;
-                cend = nend;
-                if (sp >= cend) break;
             }
-            flush(cur);
+        };
+
+        // pipeline: p0 (compute), p1 (data in flight), p2 (perm in flight), p3 (descriptor in flight)
+        SubPos p0 = sub_first(a, gwarp);
+        SubPos p1 = sub_next(a, p0, nwarps);
+        SubPos p2 = sub_next(a, p1, nwarps);
+        SubPos p3 = sub_next(a, p2, nwarps);
+        int2 d0 = (p0.sub >= 0) ? __ldg(a.sub_desc + p0.sub) : make_int2(0, 0);
+        int2 d1 = (p1.sub >= 0) ? __ldg(a.sub_desc + p1.sub) : make_int2(0, 0);
+        int2 d2 = (p2.sub >= 0) ? __ldg(a.sub_desc + p2.sub) : make_int2(0, 0);
+        int2 d3 = (p3.sub >= 0) ? __ldg(a.sub_desc + p3.sub) : make_int2(0, 0);
+        auto np_of = [](int2 d) { return d.y >> 24; };
+        // branch-free loads: lanes past the sub-chunk's count re-read its last
+        // point (always a valid index) and are masked with v = 0 when consumed
+        auto pidx = [&](int2 d) { return d.x + min(lane, max(np_of(d) - 1, 0)); };
+        auto node_of = [&](int2 d) -> int {
+            const int p = pidx(d);
+            return sorted ? p : __ldg(a.perm + p);
+        };
+        auto load_data = [&](int2 d, int node, double* f, double& s, double& vv) {
+            const int p = pidx(d);
+#pragma unroll
+            for (int ax = 0; ax < D; ++ax) f[ax] = __ldg(a.frac + (int64_t)ax * a.n + p);
+            s = use_isd ? __ldg(a.isd + p) : 1.0;
+            vv = __ldg(v + node);
+        };
+        int n1 = node_of(d1);
+        int n2 = node_of(d2);
+        double f0[D], s0, v0;
+        load_data(d0, node_of(d0), f0, s0, v0);
+        double f1[D], s1, v1;
+        load_data(d1, n1, f1, s1, v1);
+        int seg_cur = p0.seg;
+
+        while (p0.sub >= 0) {
+            const int np = np_of(d0);
+            const int cell = d0.y & 0xffffff;
+            if (!PERSIST && p0.seg != seg_cur) {
+                // segment boundary: finish the previous segment's partial tile
+                flush(cur);
+                cur = -1;
+                __syncwarp();
+                if (!(flags & (1u << 19))) {
+                    double* out = a.partial + (size_t)seg_cur * tile;
+                    for (int i = lane; i < tile; i += 32) {
+                        out[i] = (pass ? out[i] : 0.0) + my_tile[i];  // same warp owns the segment in every pass
+                        my_tile[i] = 0.0;
+                    }
+                }
+                __syncwarp();
+                seg_cur = p0.seg;
+            }
+            if (cell != cur) {
+                flush(cur);
+                cur = cell;
+            }
             __syncwarp();
+            if (!(flags & (1u << 17))) {  // bit 17: ablation (profiling only)
+                const double sv0 = (lane < np && p0.sub >= 0) ? s0 * v0 : 0.0;
+                double w[S];
+#pragma unroll
+                for (int ax = 0; ax < D; ++ax) {
+                    kb_windows<M>(f0[ax], wc, w);
+                    double* dst = my_stage + (lane * D + ax) * SPAD;
+#pragma unroll
+                    for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * sv0 : w[o];
+                }
+            }
+            // advance the pipeline (loads of later sub-chunks overlap the accumulation)
+            SubPos p4 = sub_next(a, p3, nwarps);
+            const int2 d4 = (p4.sub >= 0) ? __ldg(a.sub_desc + p4.sub) : make_int2(0, 0);
+            const int n3 = node_of(d3);
+            double f2[D], s2, v2;
+            load_data(d2, n2, f2, s2, v2);
+            __syncwarp();
+            if (active && !(flags & (1u << 16))) {  // bit 16: ablation (profiling only)
+                // rows past np carry v = 0, so the loop may run to an even count;
+                // the next point's windows are loaded while this one accumulates
+                auto ldw = [&](int j, double* w0, double* w1, double* w2) {
+                    const double* ws = my_stage + j * D * SPAD;
+#pragma unroll
+                    for (int i = 0; i < C::B0; ++i) w0[i] = ws[l0 * C::B0 + i];
+#pragma unroll
+                    for (int jj = 0; jj < C::B1; ++jj) w1[jj] = (D >= 2) ? ws[SPAD + l1 * C::B1 + jj] : 1.0;
+                    if constexpr (StageCfg<D, M>::vec2) {
+                        const double* w2p = ws + 2 * SPAD + off2;  // 16-byte aligned (P2 = 1)
+#pragma unroll
+                        for (int k = 0; k + 1 < C::B2; k += 2) {
+                            const double2 t = *reinterpret_cast<const double2*>(w2p + k);
+                            w2[k] = t.x;
+                            w2[k + 1] = t.y;
+                        }
+                        if (C::B2 & 1) w2[C::B2 - 1] = w2p[C::B2 - 1];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < C::B2; ++k) w2[k] = (D == 3) ? ws[2 * SPAD + off2 + l2 * C::B2 + k] : 1.0;
+                    }
+                };
+                auto acc_pt = [&](const double* w0, const double* w1, const double* w2) {
+#pragma unroll
+                    for (int i = 0; i < C::B0; ++i)
+#pragma unroll
+                        for (int jj = 0; jj < C::B1; ++jj) {
+                            const double w01 = w0[i] * w1[jj];
+#pragma unroll
+                            for (int k = 0; k < C::B2; ++k) acc[i][jj][k] = fma(w01, w2[k], acc[i][jj][k]);
+                        }
+                };
+                double a0[C::B0], a1[C::B1], a2[C::B2], b0[C::B0], b1[C::B1], b2[C::B2];
+                ldw(0, a0, a1, a2);
+                for (int j = 0; j < np; j += 2) {
+                    ldw(j + 1, b0, b1, b2);
+                    acc_pt(a0, a1, a2);
+                    ldw(min(j + 2, 31), a0, a1, a2);
+                    acc_pt(b0, b1, b2);
+                }
+            }
+            // rotate
+            p0 = p1;
+            p1 = p2;
+            p2 = p3;
+            p3 = p4;
+            d0 = d1;
+            d1 = d2;
+            d2 = d3;
+            d3 = d4;
+            n2 = n3;
+#pragma unroll
+            for (int ax = 0; ax < D; ++ax) {
+                f0[ax] = f1[ax];
+                f1[ax] = f2[ax];
+            }
+            s0 = s1;
+            s1 = s2;
+            v0 = v1;
+            v1 = v2;
         }
-        if (!PERSIST) {
-            double* out = a.partial + (size_t)seg * tile;
-            for (int i = lane; i < tile; i += 32) out[i] = my_tile[i];
+        flush(cur);
+        __syncwarp();
+        if (!PERSIST && seg_cur < a.nseg && !(flags & (1u << 19))) {
+            double* out = a.partial + (size_t)seg_cur * tile;
+            for (int i = lane; i < tile; i += 32) {
+                out[i] = (pass ? out[i] : 0.0) + my_tile[i];
+                my_tile[i] = 0.0;
+            }
             __syncwarp();
         }
     }
@@ -585,8 +670,21 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             cur = gbase;
         }
         double wA0[S], wA1[S], wA2[S], wB0[S], wB1[S], wB2[S];
-        kb_windows<M>(fA0, wc, wA0);
-        kb_windows<M>(fB0, wc, wB0);
+        if (flags & (1u << 17)) {  // ablation (profiling only): constant windows
+#pragma unroll
+            for (int q = 0; q < S; ++q) wA0[q] = wB0[q] = wA1[q] = wB1[q] = wA2[q] = wB2[q] = fA0 + fB1 + fA2;
+        } else {
+            kb_windows<M>(fA0, wc, wA0);
+            kb_windows<M>(fB0, wc, wB0);
+            if (D >= 2) {
+                kb_windows<M>(fA1, wc, wA1);
+                kb_windows<M>(fB1, wc, wB1);
+            }
+            if (D == 3) {
+                kb_windows<M>(fA2, wc, wA2);
+                kb_windows<M>(fB2, wc, wB2);
+            }
+        }
         if (D == 3) {
 #pragma unroll
             for (int q = 0; q < S; ++q) {
@@ -594,16 +692,11 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
                 w0s[S + q] = wB0[q];
             }
         }
-        if (D >= 2) {
-            kb_windows<M>(fA1, wc, wA1);
-            kb_windows<M>(fB1, wc, wB1);
-        }
-        if (D == 3) {
-            kb_windows<M>(fA2, wc, wA2);
-            kb_windows<M>(fB2, wc, wB2);
-        }
         double accA = 0.0, accB = 0.0;
-        if (D == 1) {
+        if (flags & (1u << 16)) {  // ablation (profiling only): skip the contraction
+            accA = wA0[0] + wA1[S - 1] + wA2[1];
+            accB = wB0[0] + wB1[S - 1] + wB2[1] + nb[lane];
+        } else if (D == 1) {
 #pragma unroll
             for (int i = 0; i < S; ++i) {
                 const double gv = nb[i];
@@ -670,6 +763,8 @@ static FsArgs make_args(mlb_binding* b) {
     a.chunk_start = b->chunk_start;
     a.chunk_cell = b->chunk_cell;
     a.chunk_gcell = b->chunk_gcell;
+    a.sub_desc = reinterpret_cast<const int2*>(b->sub_desc);
+    a.seg_sub = b->seg_sub;
     a.seg_chunk = b->seg_chunk;
     a.seg_brick = b->seg_brick;
     a.brick_seg = b->brick_seg;
@@ -724,10 +819,10 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         per_sm_smem = smem;
     }
     int blocks = nsm * per_sm;
+    if (const char* e = getenv("MLB_SPREAD_PER_SM")) blocks = nsm * std::max(1, std::min(per_sm, atoi(e)));  // tuning aid
     const int need = (b->nseg + nw - 1) / nw;
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    MLB_CUDA_TRY(cudaMemsetAsync(b->work, 0, sizeof(int), st));
     kern<<<blocks, nw * 32, smem, st>>>(a, b->plan->wc, v, flags, b->work);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());

@@ -74,6 +74,8 @@ struct mlb_binding {
     int32_t* chunk_cell = nullptr;   // nchunks: flat tile index of the chunk's bin base cell
     int32_t* chunk_gcell = nullptr;  // nchunks: flat sub-box (L^d) index of the bin base cell
     int32_t* seg_chunk = nullptr;    // nseg+1
+    int32_t* sub_desc = nullptr;     // 2 x nsub: {first point, (count << 24) | tile cell}, segment order
+    int32_t* seg_sub = nullptr;      // nseg+1: CSR of sub-chunks per segment
     int32_t* seg_brick = nullptr;    // nseg
     int32_t* brick_seg = nullptr;    // nbricks+1 (CSR, bricks lexicographic)
     int32_t* heavy = nullptr;        // nheavy x (first segment, group offset, group count), bricks with >= 2 segments

@@ -1,0 +1,42 @@
+"""Time the d=3 spread kernel of config 2 with parts switched off (profiling aid)."""
+import math, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np, torch
+import synth
+from paper_2007_05239_b200 import _lib, with_shift
+torch.cuda.set_device(0)
+wl = synth.config2_segmentation(seed=0)
+G = synth.build_graph(wl, device=0, layer_ids=[0])
+lay = with_shift(G.layers[0], math.log(2.0))
+b = lay.weights._bindings[0]
+lib = _lib.lib()
+v = torch.from_numpy(np.random.default_rng(1).standard_normal(wl.n)).cuda()
+grid = torch.empty(b.stats()["grid_cells"], dtype=torch.float64, device="cuda")
+for name, bits in [("full", 0), ("no-accumulate", 1 << 16), ("no-windows", 1 << 17), ("no-flush", 1 << 18),
+                   ("none", (1 << 16) | (1 << 17) | (1 << 18)), ("no-tile-io", 1 << 19),
+                   ("none+no-tile-io", (1 << 16) | (1 << 17) | (1 << 18) | (1 << 19))]:
+    f = _lib.MLB_USE_ISD | _lib.MLB_SPREAD_ONLY | bits
+    for _ in range(3):
+        lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), f, _lib.stream_ptr())
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(20):
+        lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), f, _lib.stream_ptr())
+    e.record(); e.synchronize()
+    print(f"{name:15s} {s.elapsed_time(e) / 20 * 1e3:8.1f} us")
+print(b.stats())
+grid2 = torch.empty_like(grid)
+lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD, _lib.stream_ptr())
+lib.mlb_convolve(b.ptr, _lib.ptr(grid), _lib.ptr(grid2), _lib.stream_ptr())
+y = torch.empty_like(v)
+for name, bits in [("gather full", 0), ("gather no-contraction", 1 << 16), ("gather no-windows", 1 << 17),
+                   ("gather none", (1 << 16) | (1 << 17))]:
+    for _ in range(3):
+        lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), bits, _lib.stream_ptr())
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(20):
+        lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), bits, _lib.stream_ptr())
+    e.record(); e.synchronize()
+    print(f"{name:22s} {s.elapsed_time(e) / 20 * 1e3:8.1f} us")
