@@ -14,6 +14,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <queue>
+#include <cstdio>
 #include <vector>
 
 #include "mlb_internal.cuh"
@@ -182,6 +184,16 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->chunk_gcell);
     dev_free(b->seg_chunk);
     dev_free(b->sub_desc);
+    dev_free(b->cblk);
+    dev_free(b->wstream);
+    dev_free(b->wstream_off);
+    dev_free(b->citem);
+    dev_free(b->citem_off);
+    dev_free(b->brick_blk);
+    dev_free(b->active_brick);
+    dev_free(b->merge_off);
+    dev_free(b->merge_pairs);
+    dev_free(b->blocks);
     dev_free(b->seg_sub);
     dev_free(b->seg_brick);
     dev_free(b->brick_seg);
@@ -311,6 +323,153 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
             max_heavy = std::max(max_heavy, ns);
         }
     }
+    // d = 3: cell blocks, CTA items and per-warp sub-chunk streams
+    std::vector<int32_t> cblk, wstream, wstream_off, citem, citem_off, brick_blk, active_brick, merge_off, merge_pairs;
+    int ncta_cells = 0;
+    if (d == 3 && n > 0) {
+        int cap = 1024;
+        if (const char* env = std::getenv("MLB_CELL_CAP")) cap = std::max(32, std::atoi(env) / 32 * 32);  // tuning
+        brick_blk.assign(nbricks + 1, 0);
+        for (int64_t k = 0; k < nkeys; ++k) {
+            const int64_t lo = cnt[k], hi = cnt[k + 1];
+            if (hi == lo) continue;
+            const int64_t np = hi - lo;
+            const int64_t parts = (np + cap - 1) / cap;
+            const int64_t per = ((np + parts - 1) / parts + 31) / 32 * 32;
+            for (int64_t s0 = lo; s0 < hi; s0 += per) {
+                cblk.push_back((int32_t)s0);
+                cblk.push_back((int32_t)std::min<int64_t>(per, hi - s0));
+                cblk.push_back(cell_local[perm[s0]]);
+                cblk.push_back((int32_t)(k / nloc));
+                brick_blk[k / nloc + 1]++;
+            }
+        }
+        for (int br = 0; br < nbricks; ++br) brick_blk[br + 1] += brick_blk[br];
+        const int nb = (int)(cblk.size() / 4);
+        // items: best-fit decreasing packing of blocks (w_b = min(8, sub-chunks) warps) into 8-warp CTAs
+        std::vector<int> ord(nb), wb(nb), nsub(nb);
+        for (int i = 0; i < nb; ++i) {
+            ord[i] = i;
+            nsub[i] = (cblk[4 * i + 1] + 31) / 32;
+            wb[i] = std::min(kCellWarps, nsub[i]);
+        }
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cblk[4 * x + 1] > cblk[4 * y + 1]; });
+        struct Item { int used = 0, cost = 0; std::vector<int> blk; };
+        std::vector<Item> items;
+        std::vector<std::vector<int>> open(kCellWarps);  // open[r]: items with r free warps
+        for (int i : ord) {
+            const int w = wb[i];
+            int it = -1;
+            for (int r = w; r < kCellWarps && it < 0; ++r)
+                while (!open[r].empty() && it < 0) {
+                    const int c = open[r].back();
+                    open[r].pop_back();
+                    if (kCellWarps - items[c].used == r) it = c;  // stale entries are skipped
+                }
+            if (it < 0) {
+                it = (int)items.size();
+                items.emplace_back();
+            }
+            Item& I = items[it];
+            I.blk.push_back(i);
+            I.used += w;
+            I.cost = std::max(I.cost, (nsub[i] + w - 1) / w);
+            if (I.used < kCellWarps) open[kCellWarps - I.used].push_back(it);
+        }
+        std::vector<int> iord(items.size());
+        for (size_t i = 0; i < items.size(); ++i) iord[i] = (int)i;
+        std::stable_sort(iord.begin(), iord.end(), [&](int x, int y) { return items[x].cost > items[y].cost; });
+        ncta_cells = std::min<int>((int)items.size(), 148 * 2);
+        // longest-processing-time-first: each item goes to the least loaded CTA
+        std::vector<std::vector<int>> cta_items(ncta_cells);
+        {
+            using LC = std::pair<int64_t, int>;
+            std::priority_queue<LC, std::vector<LC>, std::greater<LC>> pq;
+            for (int c = 0; c < ncta_cells; ++c) pq.push({0, c});
+            for (int k : iord) {
+                LC t = pq.top();
+                pq.pop();
+                cta_items[t.second].push_back(k);
+                pq.push({t.first + items[k].cost + 1, t.second});
+            }
+        }
+        wstream_off.assign((size_t)ncta_cells * kCellWarps + 1, 0);
+        citem_off.assign(ncta_cells + 1, 0);
+        std::vector<std::vector<int32_t>> ws((size_t)ncta_cells * kCellWarps);
+        for (int c = 0; c < ncta_cells; ++c) {
+            citem_off[c] = (int)(citem.size() / kItemInts);
+            for (int k : cta_items[c]) {
+                const Item& I = items[k];
+                std::vector<int32_t> row(kItemInts, 0);
+                row[0] = (int)I.blk.size();
+                int wlo = 0;
+                for (size_t e = 0; e < I.blk.size(); ++e) {
+                    const int bi = I.blk[e], w = wb[bi];
+                    row[1 + 3 * e] = bi;
+                    row[2 + 3 * e] = wlo;
+                    row[3 + 3 * e] = w;
+                    for (int r = 0; r < w; ++r) {
+                        auto& st = ws[(size_t)c * kCellWarps + wlo + r];
+                        for (int sc = r; sc < nsub[bi]; sc += w) {
+                            const int32_t p0 = cblk[4 * bi] + 32 * sc;
+                            const int32_t cntp = std::min(32, cblk[4 * bi + 1] - 32 * sc);
+                            st.push_back(p0);
+                            st.push_back(cntp << 24);
+                        }
+                    }
+                    wlo += w;
+                }
+                for (int w = 0; w < kCellWarps; ++w) {  // end-of-item marker (an empty entry for idle warps)
+                    auto& st = ws[(size_t)c * kCellWarps + w];
+                    if (w >= wlo || st.empty() || (st.back() & 1)) {
+                        st.push_back(0);
+                        st.push_back(1);
+                    } else {
+                        st.back() |= 1;
+                    }
+                }
+                citem.insert(citem.end(), row.begin(), row.end());
+            }
+        }
+        citem_off[ncta_cells] = (int)(citem.size() / kItemInts);
+        for (size_t i = 0; i < ws.size(); ++i) {
+            wstream_off[i] = (int)(wstream.size() / 2);
+            wstream.insert(wstream.end(), ws[i].begin(), ws[i].end());
+        }
+        wstream_off[ws.size()] = (int)(wstream.size() / 2);
+        for (int br = 0; br < nbricks; ++br)
+            if (brick_blk[br + 1] > brick_blk[br]) {
+                brick_first[br] = (int)active_brick.size();
+                active_brick.push_back(br);
+            } else {
+                brick_first[br] = -1;
+            }
+        // merge lists: for every (active brick, tile slab s0) the block rows
+        // o0 = s0 - c0 that land in the slab, in block order
+        const int S = 2 * g.m + 1;
+        merge_off.assign(active_brick.size() * TL + 1, 0);
+        for (size_t sl = 0; sl < active_brick.size(); ++sl) {
+            const int br = active_brick[sl];
+            for (int s0 = 0; s0 < TL; ++s0) {
+                merge_off[sl * TL + s0] = (int)(merge_pairs.size() / 2);
+                for (int bb = brick_blk[br]; bb < brick_blk[br + 1]; ++bb) {
+                    const int tc = cblk[4 * bb + 2];
+                    const int c2 = tc % TL, c1 = (tc / TL) % TL, c0 = tc / (TL * TL);
+                    const int o0 = s0 - c0;
+                    if (o0 < 0 || o0 >= S) continue;
+                    merge_pairs.push_back(bb * S + o0);  // block row index: element offset (bb*S + o0) * S^2
+                    merge_pairs.push_back((c1 << 8) | c2);
+                }
+            }
+        }
+        merge_off[active_brick.size() * TL] = (int)(merge_pairs.size() / 2);
+        if (std::getenv("MLB_DEBUG")) {
+            int mx = 0;
+            for (size_t i = 0; i + 1 < merge_off.size(); ++i) mx = std::max(mx, merge_off[i + 1] - merge_off[i]);
+            fprintf(stderr, "[mlb] d3 blocks %d items %zu ctas %d active bricks %zu merge rows %zu max/slab %d\n",
+                    (int)(cblk.size() / 4), items.size(), ncta_cells, active_brick.size(), merge_pairs.size() / 2, mx);
+        }
+    }
     // frac in sorted order, SoA
     std::vector<double> fs((size_t)n * d);
     for (int64_t j = 0; j < n; ++j)
@@ -328,6 +487,9 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     b->ngroups = (int)(groups.size() / 2);
     b->max_heavy_segs = max_heavy;
     b->tile_cells = ipow_h(TL, d);
+    b->nblk = (int)(cblk.size() / 4);
+    b->ncta_cells = ncta_cells;
+    b->nactive = (int)active_brick.size();
     b->grid_cells = 1;
     for (int a = 0; a < d; ++a) b->grid_cells *= g.L;
     int64_t st = (int64_t)g.Kh;
@@ -352,6 +514,19 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->groups, groups.data(), groups.size());
     if (rc == MLB_OK) rc = dev_upload<double>(&b->gsum, nullptr, (size_t)b->ngroups * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload(&b->brick_first, brick_first.data(), brick_first.size());
+    if (d == 3 && n > 0) {
+        if (rc == MLB_OK) rc = dev_upload(&b->cblk, cblk.data(), cblk.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->wstream, wstream.data(), wstream.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->wstream_off, wstream_off.data(), wstream_off.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->citem, citem.data(), citem.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->citem_off, citem_off.data(), citem_off.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->brick_blk, brick_blk.data(), brick_blk.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->active_brick, active_brick.data(), active_brick.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->merge_off, merge_off.data(), merge_off.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->merge_pairs, merge_pairs.data(), std::max<size_t>(2, merge_pairs.size()));
+        const int S = 2 * g.m + 1;
+        if (rc == MLB_OK) rc = dev_upload<double>(&b->blocks, nullptr, (size_t)b->nblk * S * S * S);
+    }
     if (rc == MLB_OK) {
         std::vector<int32_t> zeros(nbricks, 0);
         rc = dev_upload(&b->brick_count, zeros.data(), zeros.size());
@@ -360,7 +535,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
     // d <= 2: one partial grid per spread CTA (<= 2 per SM); d = 3: one per segment
     b->spread_parts_max = 148 * 2;
-    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)nseg;
+    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)std::max(nseg, b->nactive);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, nparts * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells + 2);

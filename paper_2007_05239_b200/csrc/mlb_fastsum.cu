@@ -90,6 +90,17 @@ struct FsArgs {
     int fuse_brick_sum;       // 1: the last CTA of a multi-segment brick sums its tiles
     const double* isd;
     double* partial;
+    // d = 3 cell blocks
+    const int4* cblk;
+    const int2* wstream;
+    const int32_t* wstream_off;
+    const int32_t* citem;
+    const int32_t* citem_off;
+    const int32_t* brick_blk;
+    const int32_t* active_brick;
+    const int32_t* merge_off;
+    const int32_t* merge_pairs;
+    double* blocks;
     int tile_cells;
     int nchunks;
     int nseg;
@@ -380,6 +391,225 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
             out[i] = t;
         }
     }
+}
+
+// ------------------------------------------------------ spread d=3: cells --
+// The d = 3 spread works per CELL: all points of a cell (or of a part of at
+// most cell_cap points of a heavy cell) share one (2m+1)^3 stencil position,
+// so their contributions sum in registers into one block -- no per-warp
+// brick tile in shared memory (which capped residency at ~10 warps/SM), no
+// flushes.  A CTA of 8 warps walks a static list of items (bind time: blocks
+// packed onto warps, largest first); within an item every warp walks its own
+// precomputed stream of 32-point sub-chunks (one cell each): it evaluates
+// the 32 points' windows (v s folded into axis 0) into its staging rows,
+// then accumulates them with the SpreadCfg lane blocks (lane (i, j-block)
+// owns one axis-0 offset, B1 axis-1 offsets and an axis-2 row).  At the end
+// of an item the warps' sums meet in shared memory and each block is the
+// fixed-order sum over its warps -> bitwise reproducible.  Global loads run
+// two sub-chunks ahead (stream entries, point indices) and one ahead
+// (coordinates, D^-1/2, v) across item boundaries.
+template <int M>
+__global__ void __launch_bounds__(256, 2) spread_cells_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v,
+                                                              unsigned flags) {
+    using C = SpreadCfg<3, M>;
+    constexpr int S = C::S;
+    constexpr int SPAD = StageCfg<3, M>::pad;
+    constexpr int STG = 32 * 3 * SPAD;        // staging doubles per warp
+    constexpr int NRED = S * S * C::SP;       // one pass slice of a block
+    extern __shared__ __align__(16) double smem[];
+    double* red = smem + kCellWarps * STG;     // kCellWarps x NRED
+    __shared__ int irow[kItemInts];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* stage = smem + warp * STG;
+    const int l0 = lane / C::P1, l1 = lane % C::P1;
+    const bool active = lane < C::P0 * C::P1;
+    const bool sorted = (flags & MLB_SORTED) != 0;
+    const bool use_isd = (flags & MLB_USE_ISD) != 0;
+    for (int i = lane; i < STG; i += 32) stage[i] = 0.0;
+    const int e0 = __ldg(a.wstream_off + blockIdx.x * kCellWarps + warp);
+    const int e1 = __ldg(a.wstream_off + blockIdx.x * kCellWarps + warp + 1);
+    const int it0 = __ldg(a.citem_off + blockIdx.x);
+
+    for (int pass = 0; pass < C::NPASS; ++pass) {
+        const int off2 = pass * C::SP;
+        double acc[C::B1][C::SP];
+#pragma unroll
+        for (int j = 0; j < C::B1; ++j)
+#pragma unroll
+            for (int k = 0; k < C::SP; ++k) acc[j][k] = 0.0;
+        // pipeline: q0 compute, q1 data in flight, q2 point index in flight
+        auto ent = [&](int e) { return (e < e1) ? __ldg(a.wstream + e) : make_int2(0, 0); };
+        auto cnt_of = [](int2 q) { return (q.y >> 24) & 63; };
+        auto pidx = [&](int2 q) { return q.x + min(lane, max(cnt_of(q) - 1, 0)); };
+        auto node_of = [&](int2 q) -> int {
+            const int p = pidx(q);
+            return (sorted || cnt_of(q) == 0) ? p : __ldg(a.perm + p);
+        };
+        int e = e0;
+        int2 q0 = ent(e), q1 = ent(e + 1), q2 = ent(e + 2);
+        double f0[3], f1[3], s0 = 1.0, s1 = 1.0, v0 = 0.0, v1 = 0.0;
+        auto load_data = [&](int2 q, int node, double* f, double& sv, double& vv) {
+            const int p = pidx(q);
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) f[ax] = __ldg(a.frac + (int64_t)ax * a.n + p);
+            sv = use_isd ? __ldg(a.isd + p) : 1.0;
+            vv = __ldg(v + node);
+        };
+        load_data(q0, node_of(q0), f0, s0, v0);
+        load_data(q1, node_of(q1), f1, s1, v1);
+        int n2 = node_of(q2);
+        int item = it0;
+        for (; e < e1; ++e) {
+            const int np = cnt_of(q0);
+            if (np > 0 && !(flags & (1u << 17))) {  // bit 17: ablation (profiling only)
+                const double sv = (lane < np) ? s0 * v0 : 0.0;
+                double w[S];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    kb_windows<M>(f0[ax], wc, w);
+                    double* dst = stage + (lane * 3 + ax) * SPAD;
+#pragma unroll
+                    for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * sv : w[o];
+                }
+            }
+            // advance the loads (they overlap the accumulation below)
+            const int2 q3 = ent(e + 3);
+            const int n3 = node_of(q3);
+            double f2[3], s2, v2;
+            load_data(q2, n2, f2, s2, v2);
+            __syncwarp();
+            if (np > 0 && active && !(flags & (1u << 16))) {  // bit 16: ablation (profiling only)
+                auto ldw = [&](int j, double& w0, double* w1, double* w2) {
+                    const double* ws = stage + j * 3 * SPAD;
+                    w0 = ws[l0];
+#pragma unroll
+                    for (int jj = 0; jj < C::B1; ++jj) w1[jj] = ws[SPAD + l1 * C::B1 + jj];
+                    if constexpr (StageCfg<3, M>::vec2) {
+                        const double* w2p = ws + 2 * SPAD + off2;
+#pragma unroll
+                        for (int k = 0; k + 1 < C::SP; k += 2) {
+                            const double2 t = *reinterpret_cast<const double2*>(w2p + k);
+                            w2[k] = t.x;
+                            w2[k + 1] = t.y;
+                        }
+                        if (C::SP & 1) w2[C::SP - 1] = w2p[C::SP - 1];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < C::SP; ++k) w2[k] = ws[2 * SPAD + off2 + k];
+                    }
+                };
+                auto acc_pt = [&](double w0, const double* w1, const double* w2) {
+#pragma unroll
+                    for (int jj = 0; jj < C::B1; ++jj) {
+                        const double w01 = w0 * w1[jj];
+#pragma unroll
+                        for (int k = 0; k < C::SP; ++k) acc[jj][k] = fma(w01, w2[k], acc[jj][k]);
+                    }
+                };
+                double a0, a1[C::B1], a2[C::SP], b0, b1[C::B1], b2[C::SP];
+                ldw(0, a0, a1, a2);
+                for (int j = 0; j < np; j += 2) {  // rows past np carry v = 0
+                    ldw(j + 1, b0, b1, b2);
+                    acc_pt(a0, a1, a2);
+                    ldw(min(j + 2, 31), a0, a1, a2);
+                    acc_pt(b0, b1, b2);
+                }
+            }
+            __syncwarp();
+            if (q0.y & 1) {  // end of item: every warp of the CTA is here
+                __syncthreads();  // previous item's reduction reads of `red` are done
+                if (active) {
+                    double* r = red + warp * NRED + l0 * S * C::SP;
+#pragma unroll
+                    for (int jj = 0; jj < C::B1; ++jj)
+#pragma unroll
+                        for (int k = 0; k < C::SP; ++k)
+                            if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                }
+#pragma unroll
+                for (int jj = 0; jj < C::B1; ++jj)
+#pragma unroll
+                    for (int k = 0; k < C::SP; ++k) acc[jj][k] = 0.0;
+                if (threadIdx.x < kItemInts) irow[threadIdx.x] = __ldg(a.citem + (size_t)item * kItemInts + threadIdx.x);
+                __syncthreads();
+                const int nb = irow[0];
+                for (int eb = 0; eb < nb; ++eb) {
+                    const int blk = irow[1 + 3 * eb], wlo = irow[2 + 3 * eb], nwb = irow[3 + 3 * eb];
+                    double* out = a.blocks + (size_t)blk * (S * S * S);
+                    for (int t = threadIdx.x; t < NRED; t += blockDim.x) {
+                        double sum = 0.0;
+                        for (int r = 0; r < nwb; ++r) sum += red[(wlo + r) * NRED + t];
+                        const int o01 = t / C::SP, k = t % C::SP;
+                        if (off2 + k < S) out[o01 * S + off2 + k] = sum;
+                    }
+                }
+                ++item;
+            }
+            q0 = q1;
+            q1 = q2;
+            q2 = q3;
+            n2 = n3;
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                f0[ax] = f1[ax];
+                f1[ax] = f2[ax];
+            }
+            s0 = s1;
+            s1 = s2;
+            v0 = v1;
+            v1 = v2;
+        }
+        __syncthreads();  // `red` reads of the last item done before the next pass
+    }
+}
+
+// d = 3 stage R1: brick tile = fixed-order sum of the brick's cell blocks,
+// each placed at its cell.  CTA = (tile slab s0 along axis 0, active brick).
+template <int M>
+struct MergeCfg {
+    static constexpr int TL = 4 + 2 * M;  // largest tile: d = 3 bricks are <= 4^3 cells
+    static constexpr int MT = (TL * TL + 31) / 32 * 32;
+};
+
+template <int M>
+__global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick_merge_kernel(FsArgs a, int abl) {
+    constexpr int S = 2 * M + 1;
+    constexpr int SS = S * S;
+    if (abl == 2) return;
+    const int TL = a.g.TL;
+    const int s0 = blockIdx.x, slot = blockIdx.y;
+    const int q0 = __ldg(a.merge_off + slot * TL + s0), q1 = __ldg(a.merge_off + slot * TL + s0 + 1);
+    double* out = a.partial + (size_t)slot * a.tile_cells + (size_t)s0 * TL * TL;
+    // The block rows landing in this slab were listed at bind time (block
+    // order) and are staged in shared memory with one cooperative load; the
+    // thread of slab position t then sums them in list order, 8 independent
+    // (branch-free) loads in flight.  One small CTA per (brick, slab): the
+    // whole grid is resident at once, so the latency chain is paid once.
+    __shared__ int2 pr[256];
+    const int t = threadIdx.x;
+    const bool live = t < TL * TL;
+    const int i1 = live ? t / TL : 0, i2 = live ? t % TL : 0;
+    double sum = 0.0;
+    for (int base = q0; base < q1; base += 256) {
+        const int nq = min(256, q1 - base);
+        __syncthreads();
+        for (int i = t; i < nq; i += blockDim.x) pr[i] = __ldg(reinterpret_cast<const int2*>(a.merge_pairs) + base + i);
+        __syncthreads();
+        for (int q = 0; q < nq; q += 8) {
+            double vals[8];
+            bool ok[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int2 p = pr[min(q + u, nq - 1)];
+                const int o1 = i1 - (p.y >> 8), o2 = i2 - (p.y & 255);
+                ok[u] = (q + u < nq) && (unsigned)o1 < (unsigned)S && (unsigned)o2 < (unsigned)S;
+                vals[u] = abl ? 1.0 : __ldcg(a.blocks + (size_t)p.x * SS + (ok[u] ? o1 * S + o2 : 0));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += ok[u] ? vals[u] : 0.0;
+        }
+    }
+    if (live) out[t] = sum;
 }
 
 // ------------------------------------------------------------------ reduce --
@@ -764,6 +994,16 @@ static FsArgs make_args(mlb_binding* b) {
     a.chunk_cell = b->chunk_cell;
     a.chunk_gcell = b->chunk_gcell;
     a.sub_desc = reinterpret_cast<const int2*>(b->sub_desc);
+    a.cblk = reinterpret_cast<const int4*>(b->cblk);
+    a.wstream = reinterpret_cast<const int2*>(b->wstream);
+    a.wstream_off = b->wstream_off;
+    a.citem = b->citem;
+    a.citem_off = b->citem_off;
+    a.brick_blk = b->brick_blk;
+    a.active_brick = b->active_brick;
+    a.merge_off = b->merge_off;
+    a.merge_pairs = b->merge_pairs;
+    a.blocks = b->blocks;
     a.seg_sub = b->seg_sub;
     a.seg_chunk = b->seg_chunk;
     a.seg_brick = b->seg_brick;
@@ -802,6 +1042,23 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         if (blocks < 1) blocks = 1;
         b->spread_parts = blocks;
         kern<<<blocks, nw * 32, smem, st>>>(a, b->plan->wc, v, flags, b->work);
+        note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+        return MLB_OK;
+    }
+    if constexpr (D == 3) {
+        using C3 = SpreadCfg<3, M>;
+        const size_t smem = (size_t)kCellWarps *
+                            (32 * 3 * StageCfg<3, M>::pad + (size_t)C3::S * C3::S * C3::SP) * sizeof(double);
+        if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread staging too large for shared memory");
+        auto kern3 = spread_cells_kernel<M>;
+        static bool attr = false;
+        if (!attr) {
+            MLB_CUDA_TRY(cudaFuncSetAttribute(kern3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        if (b->ncta_cells == 0) return MLB_OK;
+        kern3<<<b->ncta_cells, kCellWarps * 32, smem, st>>>(a, b->plan->wc, v, flags);
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
@@ -911,8 +1168,21 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     const int ngb = (G.L + Tb - 1) / Tb;
     const int64_t nblk = (int64_t)ngb * ngb * ngb;
     const int R = (G.TL + Tb - 1) / Tb;  // source bricks per axis
-    int rc = launch_seg_sum(b, nullptr, st);
-    if (rc != MLB_OK) return rc;
+    if (b->nactive > 0) {
+        const dim3 mg(G.TL, b->nactive);
+        const char* ab = getenv("MLB_MERGE_ABL");  // profiling aid: 1 skip the block loads, 2 skip all
+        const int abl = ab ? atoi(ab) : 0;
+        switch (G.m) {
+            case 1: brick_merge_kernel<1><<<mg, MergeCfg<1>::MT, 0, st>>>(a, abl); break;
+            case 2: brick_merge_kernel<2><<<mg, MergeCfg<2>::MT, 0, st>>>(a, abl); break;
+            case 3: brick_merge_kernel<3><<<mg, MergeCfg<3>::MT, 0, st>>>(a, abl); break;
+            case 4: brick_merge_kernel<4><<<mg, MergeCfg<4>::MT, 0, st>>>(a, abl); break;
+            case 5: brick_merge_kernel<5><<<mg, MergeCfg<5>::MT, 0, st>>>(a, abl); break;
+            default: brick_merge_kernel<6><<<mg, MergeCfg<6>::MT, 0, st>>>(a, abl); break;
+        }
+        note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+    }
     if (Tb == 4 && R * R * R <= 64) {
         const unsigned nb = (unsigned)((nblk + 3) / 4);
         switch (G.m) {

@@ -23,7 +23,9 @@ int fail(int code, const std::string& msg);
     } while (0)
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
-constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
+constexpr int kChunk = 64;
+constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
+constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA        // points per chunk (<= 2 per warp lane)
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
@@ -84,7 +86,22 @@ struct mlb_binding {
     int ngroups = 0;
     double* gsum = nullptr;          // ngroups x tile group sums
     int max_heavy_segs = 0;
-    int32_t* brick_first = nullptr;  // nbricks: first segment of the brick, -1 if empty
+    int32_t* brick_first = nullptr;  // nbricks: first segment of the brick (d = 3: brick tile slot), -1 if empty
+    // d = 3 cell blocks: every cell's points (split into parts of <= cell_cap)
+    // spread into one (2m+1)^3 block; CTAs of 8 warps own static item lists
+    int32_t* cblk = nullptr;         // nblk x {first point, count, tile cell, brick}
+    int nblk = 0;
+    int32_t* wstream = nullptr;      // per-warp sub-chunk streams: {first point, (count << 24) | end-of-item}
+    int32_t* wstream_off = nullptr;  // ncta*8 + 1
+    int32_t* citem = nullptr;        // items in CTA order, kItemInts ints each: nb, (block, warp lo, warps) x nb
+    int32_t* citem_off = nullptr;    // ncta + 1
+    int ncta_cells = 0;              // spread CTAs the streams were built for
+    int32_t* brick_blk = nullptr;    // nbricks + 1: CSR of blocks per brick (merge)
+    int32_t* active_brick = nullptr; // nactive: bricks with points, slot order
+    int32_t* merge_off = nullptr;    // nactive*TL + 1: CSR of block rows per (brick slot, tile slab)
+    int32_t* merge_pairs = nullptr;  // {block * S + row o0, (c1 << 8) | c2}
+    int nactive = 0;
+    double* blocks = nullptr;        // nblk x (2m+1)^3
     int32_t* brick_count = nullptr;  // nbricks: (unused) completion counters
     int* work = nullptr;             // spread work counter (reset before every launch)
     int spread_parts = 0;            // d <= 2: partial grids written by the last spread (one per CTA)

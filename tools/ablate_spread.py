@@ -40,3 +40,12 @@ for name, bits in [("gather full", 0), ("gather no-contraction", 1 << 16), ("gat
         lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), bits, _lib.stream_ptr())
     e.record(); e.synchronize()
     print(f"{name:22s} {s.elapsed_time(e) / 20 * 1e3:8.1f} us")
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD | _lib.MLB_SPREAD_ONLY, _lib.stream_ptr())
+for _ in range(3):
+    lib.mlb_reduce(b.ptr, _lib.ptr(grid), _lib.stream_ptr())
+s.record()
+for _ in range(20):
+    lib.mlb_reduce(b.ptr, _lib.ptr(grid), _lib.stream_ptr())
+e.record(); e.synchronize()
+print(f"reduce (merge + R2)     {s.elapsed_time(e) / 20 * 1e3:8.1f} us")
