@@ -263,7 +263,7 @@ def run_ours(args):
     device = local
     torch.cuda.set_device(device)
     import synth
-    from paper_2007_05239_b200 import _lib, apply_sym_laplacian
+    from paper_2007_05239_b200 import LaplacianBatch, MultilayerGraph, _lib
     from paper_2007_05239_b200.graphs import apply_sym_laplacian_dev
     lib = _lib.lib()
     wl = synth.config2_segmentation(seed=rank)   # rank r owns the layers of image r
@@ -276,21 +276,18 @@ def run_ours(args):
     ys = [torch.empty_like(v) for _ in layers]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
 
-    # the layers are independent: one CUDA stream per layer, joined per step
+    # the layers are independent: one CUDA stream per layer, joined per step,
+    # the whole step replayed from one captured CUDA graph (LaplacianBatch)
     main = torch.cuda.current_stream()
     lstreams = [torch.cuda.Stream() for _ in layers]
     fork = torch.cuda.Event()
     joins = [torch.cuda.Event() for _ in layers]
+    graph = MultilayerGraph(tuple(layers))
+    batch = LaplacianBatch(graph, use_graph=not args.no_cuda_graph)
+    batch._v.copy_(v)
 
     def step():
-        fork.record(main)
-        for lay, y, s, j in zip(layers, ys, lstreams, joins):
-            s.wait_event(fork)
-            with torch.cuda.stream(s):
-                apply_sym_laplacian_dev(lay, v, y)
-            j.record(s)
-        for j in joins:
-            main.wait_event(j)
+        batch._run()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -329,17 +326,18 @@ def run_ours(args):
     value = n * T * args.steps * ws / (total_ms * 1e-3)
 
     # ---- end-to-end through the public API: pinned host in, host out ----------
+    # (one call = every layer's L_sym of one host vector: pinned H2D of v,
+    # per-layer D2H of the results as each layer finishes, host sync)
     v_pin = torch.from_numpy(v_host).pin_memory()
+    y_pin = torch.empty((T, n), dtype=torch.float64, pin_memory=True)
     for _ in range(2):
-        for lay in layers:
-            apply_sym_laplacian(lay, v_pin)
+        batch.apply(v_pin, out=y_pin)
     torch.cuda.synchronize()
     e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(3, min(args.steps, 10))
     e_s.record()
     for _ in range(e2e_steps):
-        for lay in layers:
-            out = apply_sym_laplacian(lay, v_pin)
+        batch.apply(v_pin, out=y_pin)
     e_e.record()
     e_e.synchronize()
     e2e_ms = e_s.elapsed_time(e_e)
@@ -417,10 +415,12 @@ def run_ours(args):
         "data": "synthetic (seeded BASELINE configs[1] image; no dataset exists for it)",
         "config": {"workload": wl.name, "nodes_per_rank": n, "layers": [vars(l) for l in wl.layers],
                    "delta": delta, "vector_order": "node", "l2": "256 MB flush between steps (outside events)",
-                   "streams": "one CUDA stream per layer (independent layers), joined every step",
+                   "streams": "one CUDA stream per layer (independent layers), joined every step; the step is "
+                              "one captured CUDA graph replay" + (" (disabled)" if args.no_cuda_graph else ""),
                    "parallelism": f"layer-parallel x{ws} (independent layers per rank, no collective)"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * T, "d2h_bytes_per_step": 8 * n * T,
-                "path": "paper_2007_05239_b200.apply_sym_laplacian(layer, pinned host tensor) per layer"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * T,
+                "path": "paper_2007_05239_b200.LaplacianBatch(graph).apply(pinned host v, out=pinned host (T, n)) "
+                        "(one H2D of v, per-layer D2H as each layer finishes, host sync per step)"},
         "gpu_launches": int(launches),
         "clocks": clk,
         "roofline": roof,
@@ -452,6 +452,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cuda-graph", action="store_true", help="launch the step kernel by kernel")
     ap.add_argument("--cpu-sample", type=int, default=32768)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-sample", type=int, default=16384)

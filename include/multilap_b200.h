@@ -79,6 +79,9 @@ const char* mlb_last_error(void);
 int mlb_device_count(void);
 /* number of kernels libmlb has launched in this process (bench evidence) */
 int64_t mlb_launch_count(void);
+/* add k launches to that count: kernels replayed from a captured CUDA graph
+   (the graph's launches were counted once, at capture) */
+void mlb_note_launches(int64_t k);
 /* FP64 FMA throughput probe: `blocks` x 256 threads x iters x 8 DFMA (roofline
  * denominator; MEASURED_PEAKS.json carries no FP64 figure) */
 int mlb_probe_fp64(int64_t iters, int blocks, double* out_dev, void* stream);

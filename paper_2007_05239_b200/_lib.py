@@ -39,6 +39,7 @@ SIGNATURES = {
     "mlb_last_error": (C.c_char_p, []),
     "mlb_device_count": (I, []),
     "mlb_launch_count": (I64, []),
+    "mlb_note_launches": (None, [I64]),
     "mlb_probe_fp64": (I, [I64, I, P, P]),
     "mlb_probe_dmma": (I, [I64, I, P, P]),
     "mlb_plan_create": (I, [C.POINTER(PlanDesc), I, C.POINTER(P)]),
@@ -91,7 +92,10 @@ def load(path=LIB_PATH):
     with _lock:
         if _lib is not None:
             return _lib
-        if path == LIB_PATH:
+        if path == LIB_PATH and os.environ.get("MLB_LIB_VARIANT"):
+            # A/B experiments: an alternative in-tree build of the same ABI
+            path = os.path.join(_HERE, os.environ["MLB_LIB_VARIANT"])
+        elif path == LIB_PATH:
             _maybe_rebuild()
         if not os.path.exists(path):
             raise RuntimeError(

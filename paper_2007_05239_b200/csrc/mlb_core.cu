@@ -79,6 +79,9 @@ int mlb_abi_version(void) { return MLB_ABI_VERSION; }
 const char* mlb_last_error(void) { return g_err.c_str(); }
 
 int64_t mlb_launch_count(void) { return g_launches.load(); }
+void mlb_note_launches(int64_t k) {
+    if (k > 0) g_launches += k;
+}
 
 int mlb_device_count(void) {
     int n = 0;

@@ -877,6 +877,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         const int np = a.chunk_start[ch + 1] - p0;
         const int gbase = a.chunk_gcell[ch];
         const bool okA = lane < np, okB = lane + 32 < np;
+        const bool two = np > 32;  // warp-uniform: chunks of <= 32 points skip the second point
         const int pA = p0 + lane, pB = p0 + 32 + lane;
         // issue the point loads before (possibly) restaging the neighbourhood
         const double fA0 = okA ? __ldg(a.frac + pA) : 0.5, fB0 = okB ? __ldg(a.frac + pB) : 0.5;
@@ -905,14 +906,15 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             for (int q = 0; q < S; ++q) wA0[q] = wB0[q] = wA1[q] = wB1[q] = wA2[q] = wB2[q] = fA0 + fB1 + fA2;
         } else {
             kb_windows<M>(fA0, wc, wA0);
-            kb_windows<M>(fB0, wc, wB0);
-            if (D >= 2) {
-                kb_windows<M>(fA1, wc, wA1);
-                kb_windows<M>(fB1, wc, wB1);
-            }
-            if (D == 3) {
-                kb_windows<M>(fA2, wc, wA2);
-                kb_windows<M>(fB2, wc, wB2);
+            if (D >= 2) kb_windows<M>(fA1, wc, wA1);
+            if (D == 3) kb_windows<M>(fA2, wc, wA2);
+            if (two) {
+                kb_windows<M>(fB0, wc, wB0);
+                if (D >= 2) kb_windows<M>(fB1, wc, wB1);
+                if (D == 3) kb_windows<M>(fB2, wc, wB2);
+            } else {
+#pragma unroll
+                for (int q = 0; q < S; ++q) wB0[q] = wB1[q] = wB2[q] = 0.0;
             }
         }
         if (D == 3) {
@@ -945,6 +947,23 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
                 }
                 accA = fma(wA0[i], rA, accA);
                 accB = fma(wB0[i], rB, accB);
+            }
+        } else if (!two) {
+#pragma unroll 1
+            for (int i = 0; i < S; ++i) {
+                const double* gi = nb + i * S * SR;
+                double rA = 0.0;
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    double qA = 0.0, qA2 = 0.0;  // two chains
+#pragma unroll
+                    for (int k = 0; k < S; ++k) {
+                        if (k & 1) qA2 = fma(wA2[k], gi[j * SR + k], qA2);
+                        else qA = fma(wA2[k], gi[j * SR + k], qA);
+                    }
+                    rA = fma(wA1[j], qA + qA2, rA);
+                }
+                accA = fma(w0s[i], rA, accA);
             }
         } else {
 #pragma unroll 1

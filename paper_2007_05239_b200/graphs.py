@@ -352,6 +352,158 @@ class MultilayerGraph:
         return MultilayerGraph(tuple(self.layers[i] for i in layer_indices))
 
 
+class LaplacianBatch:
+    """Every layer's normalized Laplacian applied to one vector: the
+    independent layers run on their own CUDA streams (fork / join on the
+    caller's stream), each replayed from its own captured CUDA graph (one
+    launch per layer instead of ~8).  Host input: one pinned host->device
+    copy of v; each layer's result is copied to pinned host memory on its own
+    stream as soon as that layer finishes.
+
+        batch = LaplacianBatch(graph)
+        Y = batch.apply(v)            # (T, n) host results; v host or device
+    """
+
+    def __init__(self, graph, use_graph=True):
+        torch = _torch()
+        if not all(layer.on_device for layer in graph.layers):
+            raise ConfigError("LaplacianBatch needs device-resident layers")
+        self.graph = graph
+        self.device = graph.layers[0].weights.device
+        self.n, self.T = graph.n, graph.T
+        dev = torch.device("cuda", self.device)
+        with torch.cuda.device(dev):
+            self._v = torch.empty(self.n, dtype=torch.float64, device=dev)
+            self._y = torch.empty((self.T, self.n), dtype=torch.float64, device=dev)
+            self._streams = [torch.cuda.Stream(device=dev) for _ in graph.layers]
+            self._fork = torch.cuda.Event()
+            self._joins = [torch.cuda.Event() for _ in graph.layers]
+        self._pin_in = None
+        self._use_graph = use_graph
+        self._graphs = None
+        self._graph_launches = []
+        self._full = {}   # (host src, host out) pointers -> whole-step graph
+        self._seen = {}
+
+    def _capture(self):
+        torch = _torch()
+        for t, layer in enumerate(self.graph.layers):  # warm-up: kernel attributes, D^-1/2
+            apply_sym_laplacian_dev(layer, self._v, self._y[t])
+        torch.cuda.synchronize(self.device)
+        graphs, counts = [], []
+        for t, layer in enumerate(self.graph.layers):
+            l0 = _lib.lib().mlb_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self._streams[t]):
+                apply_sym_laplacian_dev(layer, self._v, self._y[t])
+            counts.append(int(_lib.lib().mlb_launch_count() - l0))
+            graphs.append(g)
+        torch.cuda.synchronize(self.device)
+        self._graphs, self._graph_launches = graphs, counts
+
+    def _layer(self, t):
+        if self._use_graph:
+            self._graphs[t].replay()
+            _lib.lib().mlb_note_launches(self._graph_launches[t])
+        else:
+            apply_sym_laplacian_dev(self.graph.layers[t], self._v, self._y[t])
+
+    def _run(self, out=None):
+        """Y = L_t v for every layer on the caller's stream (device buffers);
+        with `out` (pinned (T, n)) each layer's row is copied out on its stream."""
+        torch = _torch()
+        if self._use_graph and self._graphs is None:
+            self._capture()
+        main = torch.cuda.current_stream(self.device)
+        self._fork.record(main)
+        for t, (s, j) in enumerate(zip(self._streams, self._joins)):
+            s.wait_event(self._fork)
+            with torch.cuda.stream(s):
+                self._layer(t)
+                if out is not None:
+                    out[t].copy_(self._y[t], non_blocking=True)
+            j.record(s)
+        for j in self._joins:
+            main.wait_event(j)
+
+    def apply_dev(self, v):
+        """(T, n) device tensor of L_t v (a view of the batch's buffer)."""
+        self._v.copy_(v)
+        self._run()
+        return self._y
+
+    def apply(self, v, out=None):
+        """(T, n) results for a host (numpy / pinned tensor) or device vector v;
+        `out`: optional pinned (T, n) float64 tensor to receive them (no allocation)."""
+        torch = _torch()
+        if _is_tensor(v) and v.is_cuda:
+            return self.apply_dev(v).clone()
+        if _is_tensor(v) and v.is_pinned() and v.dtype == torch.float64 and v.is_contiguous():
+            src = v
+        else:
+            if self._pin_in is None:
+                self._pin_in = torch.empty(self.n, dtype=torch.float64, pin_memory=True)
+            self._pin_in.copy_(torch.as_tensor(np.asarray(v, dtype=float)) if not _is_tensor(v) else v)
+            src = self._pin_in
+        if tuple(src.shape) != (self.n,):
+            raise ConfigError("v must match the graph size")
+        if out is None:
+            out = torch.empty((self.T, self.n), dtype=torch.float64, pin_memory=True)
+        elif not (_is_tensor(out) and out.is_pinned() and out.dtype == torch.float64
+                  and tuple(out.shape) == (self.T, self.n) and out.is_contiguous()):
+            raise ConfigError("out must be a contiguous pinned float64 tensor of shape (T, n)")
+        main = torch.cuda.current_stream(self.device)
+        key = (src.data_ptr(), out.data_ptr())
+        if self._use_graph and key in self._full:
+            # persistent host buffers: the whole step (H2D, every layer, D2H)
+            # is one captured graph
+            g, cnt = self._full[key]
+            g.replay()
+            _lib.lib().mlb_note_launches(cnt)
+        elif self._use_graph and self._seen.get(key, 0) >= 1 and len(self._full) < 4:
+            self._run(out)  # (graphs of the layers exist after the first call)
+            torch.cuda.synchronize(self.device)
+            l0 = _lib.lib().mlb_launch_count()
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(device=self.device)
+            with torch.cuda.graph(g, stream=cap):
+                self._v.copy_(src, non_blocking=True)
+                self._step_direct(cap, out)
+            self._full[key] = (g, int(_lib.lib().mlb_launch_count() - l0))
+            g.replay()
+            _lib.lib().mlb_note_launches(self._full[key][1])
+        else:
+            self._seen[key] = self._seen.get(key, 0) + 1
+            self._v.copy_(src, non_blocking=True)
+            self._run(out)
+        main.synchronize()
+        return out.numpy() if not _is_tensor(v) else out
+
+    def _step_direct(self, main, out):
+        """Kernel-by-kernel step with per-layer D2H (for whole-step capture)."""
+        torch = _torch()
+        self._fork.record(main)
+        for t, (layer, s, j) in enumerate(zip(self.graph.layers, self._streams, self._joins)):
+            s.wait_event(self._fork)
+            with torch.cuda.stream(s):
+                apply_sym_laplacian_dev(layer, self._v, self._y[t])
+                out[t].copy_(self._y[t], non_blocking=True)
+            j.record(s)
+        for j in self._joins:
+            main.wait_event(j)
+
+
+def apply_sym_laplacians(graph, v, use_graph=True):
+    """(T, n): every layer's L_{sym} applied to v (host or device vector)."""
+    if not all(layer.on_device for layer in graph.layers):
+        return np.stack([apply_sym_laplacian(layer, v) for layer in graph.layers])
+    cache = graph.__dict__.setdefault("_batch_cache", {})
+    key = bool(use_graph)
+    if key not in cache:
+        cache[key] = LaplacianBatch(graph, use_graph=use_graph)
+    return cache[key].apply(v)
+
+
 def load_edge_list(path, n=None):
     """`i j w` edge list -> SparseWeights (graphs.py:241-279)."""
     import scipy.sparse as sp

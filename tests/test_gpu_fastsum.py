@@ -116,6 +116,37 @@ def test_laplacian_matches_reference_golden():
     assert np.linalg.norm(r) < 1e-10 * np.linalg.norm(np.sqrt(L2.degrees))
 
 
+def test_laplacian_batch_matches_per_layer():
+    """LaplacianBatch / apply_sym_laplacians (streams + CUDA graphs, host and
+    device inputs, persistent host buffers) == the per-layer operator, bitwise."""
+    import torch
+    from paper_2007_05239_b200 import KernelSpec, LaplacianBatch, MultilayerGraph, apply_sym_laplacians
+    from paper_2007_05239_b200.graphs import KernelWeights, apply_sym_laplacian, build_layer, with_shift
+    g = load_golden("solvers")
+    layers = []
+    for key in ("3", "2"):
+        plan = _plan(g["spec" + key])
+        fam, s = FAM[int(g["spec" + key][0])], float(g["spec" + key][1])
+        layers.append(with_shift(build_layer(KernelWeights(g["pts" + key], KernelSpec(fam, s), plan=plan)), 0.3))
+    G = MultilayerGraph(tuple(layers))
+    v = g["v"]
+    ref = np.stack([apply_sym_laplacian(layer, v) for layer in layers])
+    assert np.array_equal(apply_sym_laplacians(G, v), ref)
+    assert np.array_equal(apply_sym_laplacians(G, v, use_graph=False), ref)
+    batch = LaplacianBatch(G)
+    vp = torch.from_numpy(v).pin_memory()
+    out = torch.empty((G.T, G.n), dtype=torch.float64, pin_memory=True)
+    for _ in range(4):  # first calls per-layer graphs, then the whole-step graph
+        out.zero_()
+        batch.apply(vp, out=out)
+        assert np.array_equal(out.numpy(), ref)
+    assert np.array_equal(batch.apply(torch.from_numpy(v).cuda()).cpu().numpy(), ref)
+    w = np.random.default_rng(5).standard_normal(G.n)
+    ref_w = np.stack([apply_sym_laplacian(layer, w) for layer in layers])
+    vp.copy_(torch.from_numpy(w))  # same host buffers, new contents: the graph re-reads them
+    assert np.array_equal(batch.apply(vp, out=out).numpy(), ref_w)
+
+
 def test_per_component_blocks_match_oracle():
     from paper_2007_05239_b200 import KernelSpec, build_plan
     from paper_2007_05239_b200.graphs import KernelWeights
