@@ -573,6 +573,111 @@ __global__ void sep_cols_kernel(const double* __restrict__ gin, double* __restri
     }
 }
 
+// d = 3 in two launches: (a) one CTA per axis-0 slab: the L x L plane is
+// convolved along axis 2 then axis 1 in shared memory; (b) one CTA per
+// axis-1 index: the (axis 0, axis 2) plane is convolved along axis 0.
+__device__ __forceinline__ double sep_line(const double* __restrict__ cc, const double* __restrict__ x, int L,
+                                           int stride) {
+    // sum_v cc[-v] x[v * stride], two chains
+    double q0 = 0.0, q1 = 0.0;
+    int v = 0;
+    for (; v + 1 < L; v += 2) {
+        q0 = fma(cc[-v], x[v * stride], q0);
+        q1 = fma(cc[-v - 1], x[(v + 1) * stride], q1);
+    }
+    if (v < L) q0 = fma(cc[-v], x[v * stride], q0);
+    return q0 + q1;
+}
+
+// 4 consecutive outputs u0..u0+3 of one line: out[u] = sum_v c[u - v] x[v];
+// the kernel taps slide through registers (2 shared loads per 4 FMAs)
+__device__ __forceinline__ void sep_line4(const double* __restrict__ sc, int u0, const double* __restrict__ x,
+                                          int L, int stride, double* o) {
+    const double* cc = sc + L - 1 + u0;  // cc[j - v] = c[u0 + j - v]
+    double w0 = cc[0], w1 = cc[1], w2 = cc[2], w3 = cc[3];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int v = 0; v < L; ++v) {
+        const double xv = x[v * stride];
+        s0 = fma(w0, xv, s0);
+        s1 = fma(w1, xv, s1);
+        s2 = fma(w2, xv, s2);
+        s3 = fma(w3, xv, s3);
+        w3 = w2;
+        w2 = w1;
+        w1 = w0;
+        w0 = cc[-v - 1];
+    }
+    o[0] = s0;
+    o[1] = s1;
+    o[2] = s2;
+    o[3] = s3;
+}
+
+__global__ void __launch_bounds__(512) sep3_p21_kernel(const double* __restrict__ gin, double* __restrict__ gout,
+                                                       const double* __restrict__ c, int L) {
+    extern __shared__ double sm[];
+    const int LL = L * L;
+    const int LQ = (L + 3) / 4;  // 4-output groups per line
+    double* a = sm;                  // plane [u1][u2]
+    double* b = sm + LL + 4 * L;     // after the axis-2 pass (padded rows)
+    double* sc = b + LL + 4 * L;     // 2L-1 taps, padded by 4 on both sides with zeros
+    const int64_t base = (int64_t)blockIdx.x * LL;
+    for (int i = threadIdx.x; i < LL; i += blockDim.x) cp_async8(a + i, gin + base + i);
+    for (int i = threadIdx.x; i < 2 * L + 7; i += blockDim.x) {
+        const int k = i - 4;  // tap index
+        sc[i] = (k >= 0 && k < 2 * L - 1) ? __ldg(c + k) : 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double* scp = sc + 4;
+    for (int w = threadIdx.x; w < L * LQ; w += blockDim.x) {  // axis 2: line u1, outputs 4q..4q+3
+        const int u1 = w / LQ, q = w % LQ;
+        double o[4];
+        sep_line4(scp, 4 * q, a + u1 * L, L, 1, o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (4 * q + j < L) b[u1 * L + 4 * q + j] = o[j];
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < L * LQ; w += blockDim.x) {  // axis 1: column u2, outputs 4q..4q+3
+        const int u2 = w % L, q = w / L;
+        double o[4];
+        sep_line4(scp, 4 * q, b + u2, L, L, o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (4 * q + j < L) gout[base + (4 * q + j) * L + u2] = o[j];
+    }
+}
+
+__global__ void __launch_bounds__(512) sep3_p0_kernel(const double* __restrict__ gin, double* __restrict__ gout,
+                                                      const double* __restrict__ c, int L) {
+    extern __shared__ double sm[];
+    const int LL = L * L;
+    const int LQ = (L + 3) / 4;
+    double* a = sm;              // plane [u0][u2] at fixed u1
+    double* sc = sm + LL + 4 * L;
+    const int u1 = blockIdx.x;
+    for (int i = threadIdx.x; i < LL; i += blockDim.x) {
+        const int u0 = i / L, u2 = i % L;
+        cp_async8(a + i, gin + ((int64_t)u0 * L + u1) * L + u2);
+    }
+    for (int i = threadIdx.x; i < 2 * L + 7; i += blockDim.x) {
+        const int k = i - 4;
+        sc[i] = (k >= 0 && k < 2 * L - 1) ? __ldg(c + k) : 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double* scp = sc + 4;
+    for (int w = threadIdx.x; w < L * LQ; w += blockDim.x) {  // axis 0: column u2, outputs 4q..4q+3
+        const int u2 = w % L, q = w / L;
+        double o[4];
+        sep_line4(scp, 4 * q, a + u2, L, L, o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (4 * q + j < L) gout[((int64_t)(4 * q + j) * L + u1) * L + u2] = o[j];
+    }
+}
+
 static int convolve_separable(mlb_binding* b, const double* gin, double* gout, cudaStream_t st) {
     const Geom& G = b->plan->g;
     const int L = G.L, d = G.d;
@@ -584,6 +689,24 @@ static int convolve_separable(mlb_binding* b, const double* gin, double* gout, c
                                           (int)smem));
         sep_small_kernel<<<1, 512, smem, st>>>(gin, gout, c, L, d);
         note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+        return MLB_OK;
+    }
+    if (d == 3 && (2 * (size_t)L * L + 16 * L) * 8 <= 200 * 1024) {
+        const size_t s21 = (2 * (size_t)L * L + 8 * L + 2 * L + 8) * sizeof(double);
+        const size_t s0 = ((size_t)L * L + 4 * L + 2 * L + 8) * sizeof(double);
+        static size_t attr21 = 0, attr0 = 0;  // the largest sizes requested so far (L varies per plan)
+        if (s21 > attr21) {
+            MLB_CUDA_TRY(cudaFuncSetAttribute(sep3_p21_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s21));
+            attr21 = s21;
+        }
+        if (s0 > attr0) {
+            MLB_CUDA_TRY(cudaFuncSetAttribute(sep3_p0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0));
+            attr0 = s0;
+        }
+        sep3_p21_kernel<<<L, 512, s21, st>>>(gin, b->stage_a, c, L);
+        sep3_p0_kernel<<<L, 512, s0, st>>>(b->stage_a, gout, c, L);
+        note_launches(2);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
     }
