@@ -188,6 +188,7 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->seg_chunk);
     dev_free(b->sub_desc);
     dev_free(b->cblk);
+    dev_free(b->gwarp_off);
     dev_free(b->wstream);
     dev_free(b->wstream_off);
     dev_free(b->citem);
@@ -351,10 +352,12 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         const int nb = (int)(cblk.size() / 4);
         // items: best-fit decreasing packing of blocks (w_b = min(8, sub-chunks) warps) into 8-warp CTAs
         std::vector<int> ord(nb), wb(nb), nsub(nb);
+        int spw = 3;  // sub-chunks per warp before a block gets another warp (tuned on config 2)
+        if (const char* env = std::getenv("MLB_WARP_SUBS")) spw = std::max(1, std::atoi(env));  // tuning
         for (int i = 0; i < nb; ++i) {
             ord[i] = i;
             nsub[i] = (cblk[4 * i + 1] + 31) / 32;
-            wb[i] = std::min(kCellWarps, nsub[i]);
+            wb[i] = std::min(kCellWarps, (nsub[i] + spw - 1) / spw);
         }
         std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cblk[4 * x + 1] > cblk[4 * y + 1]; });
         struct Item { int used = 0, cost = 0; std::vector<int> blk; };
@@ -473,6 +476,23 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
                     (int)(cblk.size() / 4), items.size(), ncta_cells, active_brick.size(), merge_pairs.size() / 2, mx);
         }
     }
+    // gather: chunk ranges per warp balanced by work (lane-slots of the
+    // chunk's points + a fixed per-chunk cost), for kGatherWarps warps
+    std::vector<int32_t> gwarp_off(kGatherWarps + 1, 0);
+    {
+        std::vector<int64_t> pre(nch + 1, 0);
+        for (int c = 0; c < nch; ++c) {
+            const int np = chunk_start[c + 1] - chunk_start[c];
+            pre[c + 1] = pre[c] + (np > 32 ? 2 : 1) * 4 + 1;
+        }
+        int c = 0;
+        for (int w = 0; w <= kGatherWarps; ++w) {
+            const int64_t target = pre[nch] * w / kGatherWarps;
+            while (c < nch && pre[c] < target) ++c;
+            gwarp_off[w] = c;
+        }
+        gwarp_off[kGatherWarps] = nch;
+    }
     // frac in sorted order, SoA
     std::vector<double> fs((size_t)n * d);
     for (int64_t j = 0; j < n; ++j)
@@ -517,6 +537,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->groups, groups.data(), groups.size());
     if (rc == MLB_OK) rc = dev_upload<double>(&b->gsum, nullptr, (size_t)b->ngroups * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload(&b->brick_first, brick_first.data(), brick_first.size());
+    if (rc == MLB_OK) rc = dev_upload(&b->gwarp_off, gwarp_off.data(), gwarp_off.size());
     if (d == 3 && n > 0) {
         if (rc == MLB_OK) rc = dev_upload(&b->cblk, cblk.data(), cblk.size());
         if (rc == MLB_OK) rc = dev_upload(&b->wstream, wstream.data(), wstream.size());

@@ -418,7 +418,6 @@ __global__ void __launch_bounds__(256, 2) spread_cells_kernel(FsArgs a, WinCoef 
     constexpr int NRED = S * S * C::SP;       // one pass slice of a block
     extern __shared__ __align__(16) double smem[];
     double* red = smem + kCellWarps * STG;     // kCellWarps x NRED
-    __shared__ int irow[kItemInts];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* stage = smem + warp * STG;
     const int l0 = lane / C::P1, l1 = lane % C::P1;
@@ -517,32 +516,65 @@ __global__ void __launch_bounds__(256, 2) spread_cells_kernel(FsArgs a, WinCoef 
             }
             __syncwarp();
             if (q0.y & 1) {  // end of item: every warp of the CTA is here
-                __syncthreads();  // previous item's reduction reads of `red` are done
-                if (active) {
-                    double* r = red + warp * NRED + l0 * S * C::SP;
+                // the item row (L1-cached, read by every warp): this warp's block
+                const int* ir = a.citem + (size_t)item * kItemInts;
+                const int nb = __ldg(ir);
+                int blk = -1, nwb = 0;
+                bool multi = false;
+                for (int eb = 0; eb < nb; ++eb) {
+                    const int wlo = __ldg(ir + 2 + 3 * eb), nw = __ldg(ir + 3 + 3 * eb);
+                    multi |= nw > 1;
+                    if (warp >= wlo && warp < wlo + nw) {
+                        blk = __ldg(ir + 1 + 3 * eb);
+                        nwb = nw;
+                    }
+                }
+                if (blk >= 0 && nwb == 1) {  // a one-warp block: transposed through the warp's staging, coalesced out
+                    static_assert(NRED <= STG, "block slice must fit the warp's staging");
+                    __syncwarp();
+                    if (active) {
+                        double* r = stage + l0 * S * C::SP;
 #pragma unroll
-                    for (int jj = 0; jj < C::B1; ++jj)
+                        for (int jj = 0; jj < C::B1; ++jj)
 #pragma unroll
-                        for (int k = 0; k < C::SP; ++k)
-                            if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                            for (int k = 0; k < C::SP; ++k)
+                                if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                    }
+                    __syncwarp();
+                    double* out = a.blocks + (size_t)blk * (S * S * S);
+                    for (int t = lane; t < NRED; t += 32) {
+                        const int o01 = t / C::SP, k = t % C::SP;
+                        if (off2 + k < S) out[o01 * S + off2 + k] = stage[t];
+                    }
+                    __syncwarp();
+                }
+                if (multi) {  // uniform over the CTA: multi-warp blocks meet in shared memory
+                    __syncthreads();  // previous item's reduction reads of `red` are done
+                    if (active && nwb > 1) {
+                        double* r = red + warp * NRED + l0 * S * C::SP;
+#pragma unroll
+                        for (int jj = 0; jj < C::B1; ++jj)
+#pragma unroll
+                            for (int k = 0; k < C::SP; ++k)
+                                if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                    }
+                    __syncthreads();
+                    for (int eb = 0; eb < nb; ++eb) {
+                        const int bk = __ldg(ir + 1 + 3 * eb), wlo = __ldg(ir + 2 + 3 * eb), nw = __ldg(ir + 3 + 3 * eb);
+                        if (nw == 1) continue;
+                        double* out = a.blocks + (size_t)bk * (S * S * S);
+                        for (int t = threadIdx.x; t < NRED; t += blockDim.x) {
+                            double sum = 0.0;
+                            for (int r = 0; r < nw; ++r) sum += red[(wlo + r) * NRED + t];
+                            const int o01 = t / C::SP, k = t % C::SP;
+                            if (off2 + k < S) out[o01 * S + off2 + k] = sum;
+                        }
+                    }
                 }
 #pragma unroll
                 for (int jj = 0; jj < C::B1; ++jj)
 #pragma unroll
                     for (int k = 0; k < C::SP; ++k) acc[jj][k] = 0.0;
-                if (threadIdx.x < kItemInts) irow[threadIdx.x] = __ldg(a.citem + (size_t)item * kItemInts + threadIdx.x);
-                __syncthreads();
-                const int nb = irow[0];
-                for (int eb = 0; eb < nb; ++eb) {
-                    const int blk = irow[1 + 3 * eb], wlo = irow[2 + 3 * eb], nwb = irow[3 + 3 * eb];
-                    double* out = a.blocks + (size_t)blk * (S * S * S);
-                    for (int t = threadIdx.x; t < NRED; t += blockDim.x) {
-                        double sum = 0.0;
-                        for (int r = 0; r < nwb; ++r) sum += red[(wlo + r) * NRED + t];
-                        const int o01 = t / C::SP, k = t % C::SP;
-                        if (off2 + k < S) out[o01 * S + off2 + k] = sum;
-                    }
-                }
                 ++item;
             }
             q0 = q1;

@@ -24,6 +24,7 @@ int fail(int code, const std::string& msg);
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
 constexpr int kChunk = 64;
+constexpr int kGatherWarps = 148 * 2 * 8;  // gather launch: 2 CTAs of 8 warps per SM
 constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
 constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA        // points per chunk (<= 2 per warp lane)
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
@@ -86,6 +87,7 @@ struct mlb_binding {
     int ngroups = 0;
     double* gsum = nullptr;          // ngroups x tile group sums
     int max_heavy_segs = 0;
+    int32_t* gwarp_off = nullptr;    // kGatherWarps + 1: work-balanced chunk ranges of the gather warps
     int32_t* brick_first = nullptr;  // nbricks: first segment of the brick (d = 3: brick tile slot), -1 if empty
     // d = 3 cell blocks: every cell's points (split into parts of <= cell_cap)
     // spread into one (2m+1)^3 block; CTAs of 8 warps own static item lists
