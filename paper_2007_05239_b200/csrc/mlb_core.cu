@@ -201,11 +201,7 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->seg_sub);
     dev_free(b->seg_brick);
     dev_free(b->brick_seg);
-    dev_free(b->heavy);
-    dev_free(b->groups);
-    dev_free(b->gsum);
     dev_free(b->brick_first);
-    dev_free(b->brick_count);
     dev_free(b->work);
     dev_free(b->isd);
     dev_free(b->partial);
@@ -309,24 +305,8 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     }
     seg_sub[nseg] = (int)(sub_desc.size() / 2);
     for (int br = 0; br < nbricks; ++br) brick_seg[br + 1] += brick_seg[br];
-    std::vector<int32_t> heavy, groups, brick_first(nbricks, -1);
-    int max_heavy = 0;
-    for (int br = 0; br < nbricks; ++br) {
-        const int ns = brick_seg[br + 1] - brick_seg[br];
-        if (ns >= 1) brick_first[br] = brick_seg[br];
-        if (ns >= 2) {
-            const int goff = (int)(groups.size() / 2);
-            int ng = 0;
-            for (int s0 = 0; s0 < ns; s0 += 16, ++ng) {
-                groups.push_back(brick_seg[br] + s0);
-                groups.push_back(std::min(16, ns - s0));
-            }
-            heavy.push_back(brick_seg[br]);
-            heavy.push_back(goff);
-            heavy.push_back(ng);
-            max_heavy = std::max(max_heavy, ns);
-        }
-    }
+    // d = 3: brick tile slot per brick (set with the cell blocks below), -1 if empty
+    std::vector<int32_t> brick_first(nbricks, -1);
     // d = 3: cell blocks, CTA items and per-warp sub-chunk streams
     std::vector<int32_t> cblk, wstream, wstream_off, citem, citem_off, brick_blk, active_brick, merge_off, merge_pairs;
     int ncta_cells = 0;
@@ -506,9 +486,6 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     b->nseg = nseg;
     b->nbricks = nbricks;
     b->max_seg_chunks = seg_points;
-    b->nheavy = (int)(heavy.size() / 3);
-    b->ngroups = (int)(groups.size() / 2);
-    b->max_heavy_segs = max_heavy;
     b->tile_cells = ipow_h(TL, d);
     b->nblk = (int)(cblk.size() / 4);
     b->ncta_cells = ncta_cells;
@@ -533,9 +510,6 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->seg_sub, seg_sub.data(), seg_sub.size());
     if (rc == MLB_OK) rc = dev_upload(&b->seg_brick, seg_brick.data(), seg_brick.size());
     if (rc == MLB_OK) rc = dev_upload(&b->brick_seg, brick_seg.data(), brick_seg.size());
-    if (rc == MLB_OK) rc = dev_upload(&b->heavy, heavy.data(), heavy.size());
-    if (rc == MLB_OK) rc = dev_upload(&b->groups, groups.data(), groups.size());
-    if (rc == MLB_OK) rc = dev_upload<double>(&b->gsum, nullptr, (size_t)b->ngroups * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload(&b->brick_first, brick_first.data(), brick_first.size());
     if (rc == MLB_OK) rc = dev_upload(&b->gwarp_off, gwarp_off.data(), gwarp_off.size());
     if (d == 3 && n > 0) {
@@ -551,15 +525,11 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         const int S = 2 * g.m + 1;
         if (rc == MLB_OK) rc = dev_upload<double>(&b->blocks, nullptr, (size_t)b->nblk * S * S * S);
     }
-    if (rc == MLB_OK) {
-        std::vector<int32_t> zeros(nbricks, 0);
-        rc = dev_upload(&b->brick_count, zeros.data(), zeros.size());
-    }
     if (rc == MLB_OK) rc = dev_upload<int>(&b->work, nullptr, 1);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
     // d <= 2: one partial grid per spread CTA (<= 2 per SM); d = 3: one per segment
     b->spread_parts_max = 148 * 2;
-    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)std::max(nseg, b->nactive);
+    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)std::max(1, b->nactive);  // d = 3: brick tiles
     if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, nparts * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells + 2);

@@ -86,8 +86,6 @@ struct FsArgs {
     const int32_t* seg_brick;
     const int32_t* brick_seg;
     const int32_t* brick_first;
-    int32_t* brick_count;     // per-brick completion counters (spread epilogue), left at 0
-    int fuse_brick_sum;       // 1: the last CTA of a multi-segment brick sums its tiles
     const double* isd;
     double* partial;
     // d = 3 cell blocks
@@ -105,29 +103,6 @@ struct FsArgs {
     int nchunks;
     int nseg;
 };
-
-// per-point spread inputs, prefetched one 32-point sub-chunk ahead
-template <int D>
-struct PtIn {
-    double f[D];
-    double s;
-    int node;
-};
-
-template <int D>
-__device__ __forceinline__ void load_pt(const FsArgs& a, int p, bool ok, unsigned flags, PtIn<D>& r) {
-    if (ok) {
-        r.node = (flags & MLB_SORTED) ? p : __ldg(a.perm + p);
-        r.s = (flags & MLB_USE_ISD) ? __ldg(a.isd + p) : 1.0;
-#pragma unroll
-        for (int ax = 0; ax < D; ++ax) r.f[ax] = __ldg(a.frac + (int64_t)ax * a.n + p);
-    } else {
-        r.node = -1;
-        r.s = 0.0;
-#pragma unroll
-        for (int ax = 0; ax < D; ++ax) r.f[ax] = 0.5;
-    }
-}
 
 // ----------------------------------------------------------------- spread --
 // Warps own segments statically (gw, gw + W, ...).  A segment is a list of
@@ -645,51 +620,6 @@ __global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick
 }
 
 // ------------------------------------------------------------------ reduce --
-// Stage R1: bricks split into >= 2 segments get their segment tiles summed
-// (fixed order) in two fully parallel passes: pass 1 sums groups of <= 16
-// consecutive segments per cell, pass 2 sums a brick's group sums in order
-// and writes the brick tile (into its first segment's slot, or straight into
-// the grid when the whole sub-box is one brick).
-constexpr int kSegGroup = 16;
-
-__global__ void seg_group_kernel(const double* __restrict__ partial, const int32_t* __restrict__ groups,
-                                 int ngroups, int tile, double* __restrict__ gsum) {
-    const int e = blockIdx.y;
-    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= tile) return;
-    const int s0 = groups[2 * e], cnt = groups[2 * e + 1];
-    double v[kSegGroup];
-#pragma unroll
-    for (int k = 0; k < kSegGroup; ++k) v[k] = (k < cnt) ? __ldcg(partial + (size_t)(s0 + k) * tile + cell) : 0.0;
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < kSegGroup; ++k) t += v[k];
-    gsum[(size_t)e * tile + cell] = t;
-}
-
-__global__ void seg_final_kernel(double* __restrict__ partial, const int32_t* __restrict__ heavy, int nheavy,
-                                 int tile, const double* __restrict__ gsum, double* __restrict__ out) {
-    const int h = blockIdx.y;
-    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= tile) return;
-    const int s0 = heavy[3 * h], goff = heavy[3 * h + 1], ng = heavy[3 * h + 2];
-    double t = 0.0;
-    int g = 0;
-    for (; g + 3 < ng; g += 4) {
-        const double a0 = __ldcg(gsum + (size_t)(goff + g) * tile + cell);
-        const double a1 = __ldcg(gsum + (size_t)(goff + g + 1) * tile + cell);
-        const double a2 = __ldcg(gsum + (size_t)(goff + g + 2) * tile + cell);
-        const double a3 = __ldcg(gsum + (size_t)(goff + g + 3) * tile + cell);
-        t += a0;
-        t += a1;
-        t += a2;
-        t += a3;
-    }
-    for (; g < ng; ++g) t += __ldcg(gsum + (size_t)(goff + g) * tile + cell);
-    if (out) out[cell] = t;
-    else partial[(size_t)s0 * tile + cell] = t;
-}
-
 // d <= 2: grid[u] = sum over the spread CTAs' partial grids.  Block = 8
 // cells x 32 slices; slice k sums partials k, k+32, ...; the 32 slice sums
 // combine through a fixed shuffle tree -> deterministic.
@@ -1060,8 +990,6 @@ static FsArgs make_args(mlb_binding* b) {
     a.seg_brick = b->seg_brick;
     a.brick_seg = b->brick_seg;
     a.brick_first = b->brick_first;
-    a.brick_count = b->brick_count;
-    a.fuse_brick_sum = (b->plan->g.d == 3) ? 1 : 0;
     a.isd = b->isd;
     a.partial = b->partial;
     a.tile_cells = b->tile_cells;
@@ -1081,7 +1009,8 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (D <= 2) {
+    (void)nsm;
+    if constexpr (D <= 2) {
         // persistent CTAs of 8 warps, one partial grid per CTA
         int nw = 8;
         while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
@@ -1096,8 +1025,7 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
-    }
-    if constexpr (D == 3) {
+    } else {
         using C3 = SpreadCfg<3, M>;
         const size_t smem = (size_t)kCellWarps *
                             (32 * 3 * StageCfg<3, M>::pad + (size_t)C3::S * C3::S * C3::SP) * sizeof(double);
@@ -1114,27 +1042,6 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
     }
-    const int nw = 2;  // warps per CTA: several CTAs per SM, independent warps
-    const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
-    if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
-    auto kern = spread_kernel<D, M, false>;
-    static int per_sm = 0;
-    static size_t per_sm_smem = 0;
-    if (per_sm == 0 || per_sm_smem != smem) {
-        MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MLB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
-        if (per_sm < 1) per_sm = 1;
-        per_sm_smem = smem;
-    }
-    int blocks = nsm * per_sm;
-    if (const char* e = getenv("MLB_SPREAD_PER_SM")) blocks = nsm * std::max(1, std::min(per_sm, atoi(e)));  // tuning aid
-    const int need = (b->nseg + nw - 1) / nw;
-    if (blocks > need) blocks = need;
-    if (blocks < 1) blocks = 1;
-    kern<<<blocks, nw * 32, smem, st>>>(a, b->plan->wc, v, flags, b->work);
-    note_launches(1);
-    MLB_CUDA_TRY(cudaGetLastError());
-    return MLB_OK;
 }
 
 template <int D, int M>
@@ -1191,17 +1098,6 @@ int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t 
     if (b->nseg == 0) return MLB_OK;
     const Geom& g = b->plan->g;
     MLB_DISPATCH_DM(spread_dm, g.d, g.m, b, v, flags, st);
-}
-
-static int launch_seg_sum(mlb_binding* b, double* out, cudaStream_t st) {
-    if (b->nheavy == 0) return MLB_OK;
-    const int tile = b->tile_cells;
-    const unsigned cx = (unsigned)((tile + 255) / 256);
-    seg_group_kernel<<<dim3(cx, b->ngroups), 256, 0, st>>>(b->partial, b->groups, b->ngroups, tile, b->gsum);
-    seg_final_kernel<<<dim3(cx, b->nheavy), 256, 0, st>>>(b->partial, b->heavy, b->nheavy, tile, b->gsum, out);
-    note_launches(2);
-    MLB_CUDA_TRY(cudaGetLastError());
-    return MLB_OK;
 }
 
 int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {

@@ -81,12 +81,6 @@ struct mlb_binding {
     int32_t* seg_sub = nullptr;      // nseg+1: CSR of sub-chunks per segment
     int32_t* seg_brick = nullptr;    // nseg
     int32_t* brick_seg = nullptr;    // nbricks+1 (CSR, bricks lexicographic)
-    int32_t* heavy = nullptr;        // nheavy x (first segment, group offset, group count), bricks with >= 2 segments
-    int nheavy = 0;
-    int32_t* groups = nullptr;       // ngroups x (first segment, count <= 16) for the R1 pass 1
-    int ngroups = 0;
-    double* gsum = nullptr;          // ngroups x tile group sums
-    int max_heavy_segs = 0;
     int32_t* gwarp_off = nullptr;    // kGatherWarps + 1: work-balanced chunk ranges of the gather warps
     int32_t* brick_first = nullptr;  // nbricks: first segment of the brick (d = 3: brick tile slot), -1 if empty
     // d = 3 cell blocks: every cell's points (split into parts of <= cell_cap)
@@ -104,7 +98,6 @@ struct mlb_binding {
     int32_t* merge_pairs = nullptr;  // {block * S + row o0, (c1 << 8) | c2}
     int nactive = 0;
     double* blocks = nullptr;        // nblk x (2m+1)^3
-    int32_t* brick_count = nullptr;  // nbricks: (unused) completion counters
     int* work = nullptr;             // spread work counter (reset before every launch)
     int spread_parts = 0;            // d <= 2: partial grids written by the last spread (one per CTA)
     int spread_parts_max = 0;        // capacity of `partial` in whole grids (d <= 2)

@@ -32,3 +32,17 @@ t0 = time.perf_counter()
 for _ in range(20):
     b.apply(vp, out=yp)
 print("apply wall     %.1f us" % ((time.perf_counter() - t0) / 20 * 1e6))
+# host-side split of one apply (whole-step graph path)
+import time as _t
+key = (vp.data_ptr(), yp.data_ptr())
+print("whole-step graph cached:", key in b._full)
+g, cnt = b._full[key]
+main = torch.cuda.current_stream()
+ts = []
+for _ in range(20):
+    t0 = _t.perf_counter(); g.replay(); t1 = _t.perf_counter(); main.synchronize(); t2 = _t.perf_counter()
+    ts.append((t1 - t0, t2 - t1))
+ts = np.array(ts) * 1e6
+print("replay launch %.1f us, wait %.1f us (median)" % tuple(np.median(ts, axis=0)))
+ev[0].record(); g.replay(); ev[1].record(); ev[1].synchronize()
+print("whole-step graph device time %.1f us" % (ev[0].elapsed_time(ev[1]) * 1e3))
