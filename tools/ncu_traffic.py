@@ -19,10 +19,13 @@ def main(rep, out=os.path.join(ROOT, "profiles", "ncu_traffic.json")):
     res = {}
     for r in rows[2:]:
         name = r[col["Kernel Name"]]
-        for kern in ("spread", "gather"):
+        for kern in ("spread", "gather", "spread_cells"):
             if name.startswith(f"void mlb::{kern}_kernel") or f"{kern}_kernel<" in name:
-                d = name.split("<")[1].split(",")[0].replace("(int)", "").strip()
-                key = f"{kern}_d{d}"
+                if kern == "spread_cells":  # the d = 3 spread
+                    key = "spread_d3"
+                else:
+                    d = name.split("<")[1].split(",")[0].replace("(int)", "").strip()
+                    key = f"{kern}_d{d}"
 
                 def val(metric):
                     i = col[metric]
