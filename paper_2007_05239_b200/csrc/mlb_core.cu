@@ -27,6 +27,14 @@ static std::atomic<long long> g_launches{0};
 
 void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MLB_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 void set_error(const std::string& msg) { g_err = msg; }
 
 int fail(int code, const std::string& msg) {

@@ -485,8 +485,9 @@ __global__ void sep_small_kernel(const double* __restrict__ gin, double* __restr
     double* a = sm;
     double* b = sm + cells;
     double* sc = sm + 2 * cells;
-    for (int i = threadIdx.x; i < cells; i += blockDim.x) a[i] = __ldg(gin + i);
     for (int i = threadIdx.x; i < 2 * L - 1; i += blockDim.x) sc[i] = __ldg(c + i);
+    pdl_wait();  // the grid comes from the reduction
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) a[i] = __ldg(gin + i);
     __syncthreads();
     // last axis
     for (int o = threadIdx.x; o < cells; o += blockDim.x) {
@@ -622,11 +623,12 @@ __global__ void __launch_bounds__(512) sep3_p21_kernel(const double* __restrict_
     double* b = sm + LL + 4 * L;     // after the axis-2 pass (padded rows)
     double* sc = b + LL + 4 * L;     // 2L-1 taps, padded by 4 on both sides with zeros
     const int64_t base = (int64_t)blockIdx.x * LL;
-    for (int i = threadIdx.x; i < LL; i += blockDim.x) cp_async8(a + i, gin + base + i);
     for (int i = threadIdx.x; i < 2 * L + 7; i += blockDim.x) {
         const int k = i - 4;  // tap index
         sc[i] = (k >= 0 && k < 2 * L - 1) ? __ldg(c + k) : 0.0;
     }
+    pdl_wait();  // the grid comes from the reduction
+    for (int i = threadIdx.x; i < LL; i += blockDim.x) cp_async8(a + i, gin + base + i);
     cp_async_wait_all();
     __syncthreads();
     const double* scp = sc + 4;
@@ -647,6 +649,7 @@ __global__ void __launch_bounds__(512) sep3_p21_kernel(const double* __restrict_
         for (int j = 0; j < 4; ++j)
             if (4 * q + j < L) gout[base + (4 * q + j) * L + u2] = o[j];
     }
+    pdl_launch();
 }
 
 __global__ void __launch_bounds__(512) sep3_p0_kernel(const double* __restrict__ gin, double* __restrict__ gout,
@@ -657,13 +660,14 @@ __global__ void __launch_bounds__(512) sep3_p0_kernel(const double* __restrict__
     double* a = sm;              // plane [u0][u2] at fixed u1
     double* sc = sm + LL + 4 * L;
     const int u1 = blockIdx.x;
-    for (int i = threadIdx.x; i < LL; i += blockDim.x) {
-        const int u0 = i / L, u2 = i % L;
-        cp_async8(a + i, gin + ((int64_t)u0 * L + u1) * L + u2);
-    }
     for (int i = threadIdx.x; i < 2 * L + 7; i += blockDim.x) {
         const int k = i - 4;
         sc[i] = (k >= 0 && k < 2 * L - 1) ? __ldg(c + k) : 0.0;
+    }
+    pdl_wait();  // the first pass
+    for (int i = threadIdx.x; i < LL; i += blockDim.x) {
+        const int u0 = i / L, u2 = i % L;
+        cp_async8(a + i, gin + ((int64_t)u0 * L + u1) * L + u2);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -676,6 +680,7 @@ __global__ void __launch_bounds__(512) sep3_p0_kernel(const double* __restrict__
         for (int j = 0; j < 4; ++j)
             if (4 * q + j < L) gout[((int64_t)(4 * q + j) * L + u1) * L + u2] = o[j];
     }
+    pdl_launch();
 }
 
 static int convolve_separable(mlb_binding* b, const double* gin, double* gout, cudaStream_t st) {
@@ -687,7 +692,7 @@ static int convolve_separable(mlb_binding* b, const double* gin, double* gout, c
         const size_t smem = (size_t)(2 * cells + 2 * L) * sizeof(double);
         MLB_CUDA_TRY(cudaFuncSetAttribute(sep_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-        sep_small_kernel<<<1, 512, smem, st>>>(gin, gout, c, L, d);
+        MLB_CUDA_TRY(launch_k(sep_small_kernel, dim3(1), dim3(512), smem, st, gin, gout, c, L, d));
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
@@ -704,8 +709,8 @@ static int convolve_separable(mlb_binding* b, const double* gin, double* gout, c
             MLB_CUDA_TRY(cudaFuncSetAttribute(sep3_p0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0));
             attr0 = s0;
         }
-        sep3_p21_kernel<<<L, 512, s21, st>>>(gin, b->stage_a, c, L);
-        sep3_p0_kernel<<<L, 512, s0, st>>>(b->stage_a, gout, c, L);
+        MLB_CUDA_TRY(launch_k(sep3_p21_kernel, dim3(L), dim3(512), s21, st, gin, b->stage_a, c, L));
+        MLB_CUDA_TRY(launch_k(sep3_p0_kernel, dim3(L), dim3(512), s0, st, (const double*)b->stage_a, gout, c, L));
         note_launches(2);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;

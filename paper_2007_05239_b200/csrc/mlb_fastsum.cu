@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     double* my_stage = smem + (size_t)nw * tile + (size_t)warp * 32 * D * SPAD;
     for (int i = lane; i < 32 * D * SPAD; i += 32) my_stage[i] = 0.0;
     for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
+    pdl_wait();  // v (and the partial grids' previous readers) are stream predecessors
 
     const int l0 = lane / (C::P1 * C::P2), l1 = (lane / C::P2) % C::P1, l2 = lane % C::P2;
     const bool active = lane < C::P0 * C::P1 * C::P2;
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
             __syncwarp();
         }
     }
+    pdl_launch();
     if (PERSIST) {
         __syncthreads();
         double* out = a.partial + (size_t)blockIdx.x * tile;
@@ -429,6 +431,7 @@ __global__ void __launch_bounds__(256, 2) spread_cells_kernel(FsArgs a, WinCoef 
             sv = use_isd ? __ldg(a.isd + p) : 1.0;
             vv = __ldg(v + node);
         };
+        pdl_wait();  // v (and D^-1/2) may come from the stream predecessor
         load_data(q0, node_of(q0), f0, s0, v0);
         load_data(q1, node_of(q1), f1, s1, v1);
         int n2 = node_of(q2);
@@ -568,6 +571,7 @@ __global__ void __launch_bounds__(256, 2) spread_cells_kernel(FsArgs a, WinCoef 
         }
         __syncthreads();  // `red` reads of the last item done before the next pass
     }
+    pdl_launch();
 }
 
 // d = 3 stage R1: brick tile = fixed-order sum of the brick's cell blocks,
@@ -602,6 +606,7 @@ __global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick
         __syncthreads();
         for (int i = t; i < nq; i += blockDim.x) pr[i] = __ldg(reinterpret_cast<const int2*>(a.merge_pairs) + base + i);
         __syncthreads();
+        pdl_wait();  // the cell blocks come from the spread
         for (int q = 0; q < nq; q += 8) {
             double vals[8];
             bool ok[8];
@@ -616,6 +621,8 @@ __global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick
             for (int u = 0; u < 8; ++u) sum += ok[u] ? vals[u] : 0.0;
         }
     }
+    pdl_wait();  // (a slab without rows still orders its write after the predecessor)
+    pdl_launch();
     if (live) out[t] = sum;
 }
 
@@ -627,6 +634,7 @@ __global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, 
     const int slice = threadIdx.x & 31;
     const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
     double s = 0.0;
+    pdl_wait();  // the partial grids come from the spread
     if (cell < cells) {
         int j = slice;
         for (; j + 96 < nparts; j += 128) {
@@ -642,6 +650,7 @@ __global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, 
         for (; j < nparts; j += 32) s += __ldcg(partial + (size_t)j * cells + cell);
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    pdl_launch();
     if (slice == 0 && cell < cells) grid[cell] = s;
 }
 
@@ -788,6 +797,7 @@ __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restri
         base[lb][q] = p;
     }
     __syncthreads();
+    pdl_wait();  // the brick tiles come from the merge
     if (!live) return;
     const int c0 = c / (TB * TB), c1 = (c / TB) % TB, c2 = c % TB;
     const int u0 = gb0 * TB + c0, u1 = gb1 * TB + c1, u2 = gb2 * TB + c2;
@@ -805,6 +815,7 @@ __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restri
         }
         sum += ok ? __ldcg(p + local) : 0.0;
     }
+    pdl_launch();
     grid[((int64_t)u0 * L + u1) * L + u2] = sum;
 }
 
@@ -834,6 +845,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     const int c_hi = (int)(((long long)a.nchunks * (gw + 1)) / nwt);
     const int64_t rs = (D == 3) ? (int64_t)L * L : (int64_t)L;  // stride of axis 0
     int cur = -1;
+    pdl_wait();  // the grid (convolution) and v come from stream predecessors
     for (int ch = c_lo; ch < c_hi; ++ch) {
         const int p0 = a.chunk_start[ch];
         const int np = a.chunk_start[ch + 1] - p0;
@@ -962,6 +974,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             y[node] = res;
         }
     }
+    pdl_launch();
 }
 
 // --------------------------------------------------------------- launchers --
@@ -1021,7 +1034,7 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         int blocks = std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);
         if (blocks < 1) blocks = 1;
         b->spread_parts = blocks;
-        kern<<<blocks, nw * 32, smem, st>>>(a, b->plan->wc, v, flags, b->work);
+        MLB_CUDA_TRY(launch_k(kern, dim3(blocks), dim3(nw * 32), smem, st, a, b->plan->wc, v, flags, b->work));
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
@@ -1037,7 +1050,7 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
             attr = true;
         }
         if (b->ncta_cells == 0) return MLB_OK;
-        kern3<<<b->ncta_cells, kCellWarps * 32, smem, st>>>(a, b->plan->wc, v, flags);
+        MLB_CUDA_TRY(launch_k(kern3, dim3(b->ncta_cells), dim3(kCellWarps * 32), smem, st, a, b->plan->wc, v, flags));
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
@@ -1068,7 +1081,7 @@ static int gather_dm(mlb_binding* b, const double* grid, const double* v, double
     const int need = (b->nchunks + 7) / 8;  // at least one chunk per warp
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    kern<<<blocks, 256, smem, st>>>(a, b->plan->wc, grid, v, y, alpha, beta, gamma, flags);
+    MLB_CUDA_TRY(launch_k(kern, dim3(blocks), dim3(256), smem, st, a, b->plan->wc, grid, v, y, alpha, beta, gamma, flags));
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
@@ -1106,7 +1119,8 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     if (G.d <= 2) {
         // the spread left one partial grid per CTA
         const int cells = (int)b->grid_cells;
-        grid_sum_kernel<<<(cells + 7) / 8, 256, 0, st>>>(b->partial, b->spread_parts, cells, grid);
+        MLB_CUDA_TRY(launch_k(grid_sum_kernel, dim3((cells + 7) / 8), dim3(256), 0, st, (const double*)b->partial,
+                              b->spread_parts, cells, grid));
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
         return MLB_OK;
@@ -1120,12 +1134,12 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
         const char* ab = getenv("MLB_MERGE_ABL");  // profiling aid: 1 skip the block loads, 2 skip all
         const int abl = ab ? atoi(ab) : 0;
         switch (G.m) {
-            case 1: brick_merge_kernel<1><<<mg, MergeCfg<1>::MT, 0, st>>>(a, abl); break;
-            case 2: brick_merge_kernel<2><<<mg, MergeCfg<2>::MT, 0, st>>>(a, abl); break;
-            case 3: brick_merge_kernel<3><<<mg, MergeCfg<3>::MT, 0, st>>>(a, abl); break;
-            case 4: brick_merge_kernel<4><<<mg, MergeCfg<4>::MT, 0, st>>>(a, abl); break;
-            case 5: brick_merge_kernel<5><<<mg, MergeCfg<5>::MT, 0, st>>>(a, abl); break;
-            default: brick_merge_kernel<6><<<mg, MergeCfg<6>::MT, 0, st>>>(a, abl); break;
+            case 1: MLB_CUDA_TRY(launch_k(brick_merge_kernel<1>, mg, dim3(MergeCfg<1>::MT), 0, st, a, abl)); break;
+            case 2: MLB_CUDA_TRY(launch_k(brick_merge_kernel<2>, mg, dim3(MergeCfg<2>::MT), 0, st, a, abl)); break;
+            case 3: MLB_CUDA_TRY(launch_k(brick_merge_kernel<3>, mg, dim3(MergeCfg<3>::MT), 0, st, a, abl)); break;
+            case 4: MLB_CUDA_TRY(launch_k(brick_merge_kernel<4>, mg, dim3(MergeCfg<4>::MT), 0, st, a, abl)); break;
+            case 5: MLB_CUDA_TRY(launch_k(brick_merge_kernel<5>, mg, dim3(MergeCfg<5>::MT), 0, st, a, abl)); break;
+            default: MLB_CUDA_TRY(launch_k(brick_merge_kernel<6>, mg, dim3(MergeCfg<6>::MT), 0, st, a, abl)); break;
         }
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());
@@ -1133,10 +1147,10 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     if (Tb == 4 && R * R * R <= 64) {
         const unsigned nb = (unsigned)((nblk + 3) / 4);
         switch (G.m) {
-            case 2: reduce3_kernel<4, 2><<<nb, 256, 0, st>>>(a, grid); break;
-            case 3: reduce3_kernel<4, 3><<<nb, 256, 0, st>>>(a, grid); break;
-            case 4: reduce3_kernel<4, 4><<<nb, 256, 0, st>>>(a, grid); break;
-            default: reduce3_kernel<4, 5><<<nb, 256, 0, st>>>(a, grid); break;
+            case 2: MLB_CUDA_TRY(launch_k(reduce3_kernel<4, 2>, dim3(nb), dim3(256), 0, st, a, grid)); break;
+            case 3: MLB_CUDA_TRY(launch_k(reduce3_kernel<4, 3>, dim3(nb), dim3(256), 0, st, a, grid)); break;
+            case 4: MLB_CUDA_TRY(launch_k(reduce3_kernel<4, 4>, dim3(nb), dim3(256), 0, st, a, grid)); break;
+            default: MLB_CUDA_TRY(launch_k(reduce3_kernel<4, 5>, dim3(nb), dim3(256), 0, st, a, grid)); break;
         }
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());

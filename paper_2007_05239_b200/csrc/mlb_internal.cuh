@@ -15,6 +15,29 @@ void set_error(const std::string& msg);
 void note_launches(int k);  // libmlb kernel-launch counter (bench evidence)
 int fail(int code, const std::string& msg);
 
+// Programmatic dependent launch: a kernel launched with launch_k may start
+// (prologue: static tables, shared memory) while its stream predecessor is
+// finishing; it must call pdl_wait() before touching anything a predecessor
+// writes or reads, and calls pdl_launch() once its own main work is done.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // MLB_NO_PDL=1 disables (A/B)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 #define MLB_CUDA_TRY(expr)                                                              \
     do {                                                                                \
         cudaError_t _e = (expr);                                                        \
@@ -23,10 +46,10 @@ int fail(int code, const std::string& msg);
     } while (0)
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
-constexpr int kChunk = 64;
+constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
 constexpr int kGatherWarps = 148 * 2 * 8;  // gather launch: 2 CTAs of 8 warps per SM
 constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
-constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA        // points per chunk (<= 2 per warp lane)
+constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
