@@ -355,6 +355,139 @@ def lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None,
         axpby(1.0 / beta, w, 0.0, V[s])
 
 
+class _LayerPksm:
+    """One layer's state inside the batched PKSM (same arithmetic, in the same
+    order, as lanczos_fn_apply_dev on that layer alone)."""
+
+    def __init__(self, layer, v_node, dim, hrow):
+        torch = _torch()
+        from .graphs import KernelWeights  # noqa: F401  (eligibility checked by the caller)
+        w = layer.weights
+        self.b = w._bindings[0]
+        if w._isd_dev is None:
+            w.set_isd(layer.isd_device(w.device))
+        self.n = layer.n
+        self.K0 = w.kernel.value_at_zero()
+        self.a = 1.0 + layer.shift
+        self.vs = torch.empty_like(v_node)
+        lib = _lib.lib()
+        _lib.check(lib.mlb_to_sorted(self.b.ptr, _lib.ptr(v_node), _lib.ptr(self.vs), _sp()))
+        self.dim = dim
+        self.V = None
+        self.h = hrow  # device row: h (dim) | h1 (dim) | nrm2 ...
+        self.alphas = np.empty(dim)
+        self.betas = np.empty(dim)
+        self.c_prev = None
+        self.nv = None
+        self.w = None
+        self.ys = None
+        self.done = False
+
+    def apply(self, x):
+        y = _torch().empty_like(x)
+        _lib.check(_lib.lib().mlb_apply(self.b.ptr, _lib.ptr(x), _lib.ptr(y), self.a, -1.0, self.K0,
+                                        _lib.MLB_USE_ISD | _lib.MLB_SORTED, _sp()))
+        return y
+
+
+def pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1e-8):
+    """out += out_scale * (L_t + delta)^p v for every layer t, summed into out in
+    ascending layer order.  The layers' Krylov steps advance in lockstep so
+    each step costs ONE device->host read for all layers (alpha, beta) and
+    one batched host eigh; per layer the arithmetic and its order are those
+    of pksm_layer_dev, so the result is bitwise identical to the sequential
+    loop.  Layers must be single-binding fused kernel layers."""
+    torch = _torch()
+    fn = power_fn(p)
+    n = v_node.numel()
+    dim = int(min(krylov_dim, n))
+    if dim < 1:
+        raise ConfigError(f"krylov_dim must be >= 1, got {krylov_dim}")
+    T = len(layers)
+    H = torch.empty((T, 2 * dim + 3), dtype=torch.float64, device=v_node.device)
+    st = [_LayerPksm(layer, v_node, dim, H[t]) for t, layer in enumerate(layers)]
+    for t, x in enumerate(st):
+        dot(x.vs, x.vs, H[t, 0:1])
+    nv2 = H[:, 0].cpu().numpy()
+    for t, x in enumerate(st):
+        x.nv = float(np.sqrt(nv2[t]))
+        if x.nv == 0.0:
+            x.done = True
+            x.ys = None
+        else:
+            x.V = torch.empty((dim, n), dtype=torch.float64, device=v_node.device)
+            axpby(1.0 / x.nv, x.vs, 0.0, x.V[0])
+    s = 0
+    while True:
+        act = [x for x in st if not x.done]
+        if not act:
+            break
+        for x in act:
+            x.w = x.apply(x.V[s])
+            cgs2(x.V, s + 1, x.w, x.h[: s + 1], x.h[dim:dim + s + 1], x.h[dim + s + 1:dim + s + 2])
+        hb = H[:, dim + s:dim + s + 2].cpu().numpy()  # alpha, ||w||^2 of every layer: one read
+        for x in act:
+            t = st.index(x)
+            x.alphas[s] = hb[t, 0]
+            x.betas[s] = float(np.sqrt(max(hb[t, 1], 0.0)))
+        ss = s + 1
+        Ts = np.zeros((len(act), ss, ss))
+        for i, x in enumerate(act):
+            Ts[i] = np.diag(x.alphas[:ss])
+            if ss > 1:
+                off = x.betas[: ss - 1]
+                Ts[i] += np.diag(off, 1) + np.diag(off, -1)
+        for i, x in enumerate(act):
+            lam, Q = np.linalg.eigh(Ts[i])
+            c = x.nv * (Q @ (fn(lam) * Q[0, :]))
+            stop = False
+            if x.c_prev is not None:
+                diff = c.copy()
+                diff[: ss - 1] -= x.c_prev
+                lhs = np.linalg.norm(diff)
+                rhs = tol * max(np.linalg.norm(c), 1e-300)
+                if rhs > 0 and abs(lhs / rhs - 1.0) < 1e-3:
+                    y = torch.zeros(n, dtype=torch.float64, device=v_node.device)
+                    yp = torch.zeros(n, dtype=torch.float64, device=v_node.device)
+                    gemv_n(x.V, n, ss, _to_dev(c, v_node.device.index), y)
+                    gemv_n(x.V, n, ss - 1, _to_dev(x.c_prev, v_node.device.index), yp)
+                    nb = torch.empty(2, dtype=torch.float64, device=v_node.device)
+                    d = axpby(1.0, y, -1.0, yp)
+                    dot(d, d, nb[0:1])
+                    dot(y, y, nb[1:2])
+                    a2, b2 = nb.cpu().numpy()
+                    lhs, rhs = np.sqrt(a2), tol * max(np.sqrt(b2), 1e-300)
+                stop = lhs <= rhs
+            beta = x.betas[s]
+            happy = beta <= 1e-13 * max(1.0, np.abs(x.alphas[:ss]).max())
+            if stop or happy or ss >= dim:
+                PksmStats.steps.append(ss)
+                x.ys = torch.empty(n, dtype=torch.float64, device=v_node.device)
+                gemv_n(x.V, n, ss, _to_dev(c, v_node.device.index), x.ys)
+                x.done = True
+                x.V = None
+            else:
+                x.c_prev = c
+                axpby(1.0 / beta, x.w, 0.0, x.V[ss])
+        s += 1
+    lib = _lib.lib()
+    for x in st:  # ascending layer order, exactly as the sequential loop
+        if x.ys is None:
+            continue
+        if out_scale != 1.0:
+            x.ys.mul_(out_scale)
+        _lib.check(lib.mlb_to_node(x.b.ptr, _lib.ptr(x.ys), _lib.ptr(out), 1, _sp()))
+    return out
+
+
+def batchable_layers(layers):
+    """True when every layer is a single-binding fused GPU kernel layer."""
+    from .graphs import KernelWeights
+    return all(isinstance(layer.weights, KernelWeights) and layer.weights.fused
+               and layer.weights._bindings is not None and len(layer.weights._bindings) == 1
+               for layer in layers)
+
+
 def lanczos_fn_apply(op, v, fn, krylov_dim=50, tol=1e-8):
     """y ~= f(A) v via the Lanczos relation (krylov.py:172-216)."""
     torch = _torch()

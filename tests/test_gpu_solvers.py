@@ -48,6 +48,26 @@ def test_pksm_and_power_operators_match_golden():
     assert rel(apply_one_minus_L1(G, v), g["one_minus_L1"]) < 1e-12
 
 
+def test_batched_pksm_is_bitwise_sequential():
+    """The lockstep multi-layer PKSM (one host read per step for all layers)
+    reproduces the per-layer loop bit for bit, including the layer-order sum."""
+    import torch
+    from paper_2007_05239_b200 import with_shift
+    from paper_2007_05239_b200.krylov import pksm_layer_dev, pksm_layers_dev
+    g = load_golden("solvers")
+    L3, L2 = _layers(g)
+    dl = math.log(2.0)
+    layers = [with_shift(L3, dl), with_shift(L2, dl), with_shift(L3, dl)]
+    v = torch.from_numpy(g["v"]).cuda()
+    for p in (-1.0, -3.0):
+        seq = torch.zeros_like(v)
+        for layer in layers:
+            pksm_layer_dev(layer, p, v, seq, 1.0, True)
+        bat = torch.zeros_like(v)
+        pksm_layers_dev(layers, p, v, bat, 1.0)
+        assert torch.equal(seq, bat)
+
+
 def test_power_mean_eigs_match_golden():
     from paper_2007_05239_b200 import MultilayerGraph, PowerMeanConfig, power_mean_eigs
     g = load_golden("solvers")
