@@ -196,7 +196,6 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->seg_chunk);
     dev_free(b->sub_desc);
     dev_free(b->cblk);
-    dev_free(b->gwarp_off);
     dev_free(b->wstream);
     dev_free(b->wstream_off);
     dev_free(b->citem);
@@ -464,23 +463,6 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
                     (int)(cblk.size() / 4), items.size(), ncta_cells, active_brick.size(), merge_pairs.size() / 2, mx);
         }
     }
-    // gather: chunk ranges per warp balanced by work (lane-slots of the
-    // chunk's points + a fixed per-chunk cost), for kGatherWarps warps
-    std::vector<int32_t> gwarp_off(kGatherWarps + 1, 0);
-    {
-        std::vector<int64_t> pre(nch + 1, 0);
-        for (int c = 0; c < nch; ++c) {
-            const int np = chunk_start[c + 1] - chunk_start[c];
-            pre[c + 1] = pre[c] + (np > 32 ? 2 : 1) * 4 + 1;
-        }
-        int c = 0;
-        for (int w = 0; w <= kGatherWarps; ++w) {
-            const int64_t target = pre[nch] * w / kGatherWarps;
-            while (c < nch && pre[c] < target) ++c;
-            gwarp_off[w] = c;
-        }
-        gwarp_off[kGatherWarps] = nch;
-    }
     // frac in sorted order, SoA
     std::vector<double> fs((size_t)n * d);
     for (int64_t j = 0; j < n; ++j)
@@ -519,7 +501,6 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload(&b->seg_brick, seg_brick.data(), seg_brick.size());
     if (rc == MLB_OK) rc = dev_upload(&b->brick_seg, brick_seg.data(), brick_seg.size());
     if (rc == MLB_OK) rc = dev_upload(&b->brick_first, brick_first.data(), brick_first.size());
-    if (rc == MLB_OK) rc = dev_upload(&b->gwarp_off, gwarp_off.data(), gwarp_off.size());
     if (d == 3 && n > 0) {
         if (rc == MLB_OK) rc = dev_upload(&b->cblk, cblk.data(), cblk.size());
         if (rc == MLB_OK) rc = dev_upload(&b->wstream, wstream.data(), wstream.size());

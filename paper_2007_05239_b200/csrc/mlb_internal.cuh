@@ -47,7 +47,6 @@ cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 
 constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
 constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
-constexpr int kGatherWarps = 148 * 2 * 8;  // gather launch: 2 CTAs of 8 warps per SM
 constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
 constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
@@ -104,7 +103,6 @@ struct mlb_binding {
     int32_t* seg_sub = nullptr;      // nseg+1: CSR of sub-chunks per segment
     int32_t* seg_brick = nullptr;    // nseg
     int32_t* brick_seg = nullptr;    // nbricks+1 (CSR, bricks lexicographic)
-    int32_t* gwarp_off = nullptr;    // kGatherWarps + 1: work-balanced chunk ranges of the gather warps
     int32_t* brick_first = nullptr;  // nbricks: first segment of the brick (d = 3: brick tile slot), -1 if empty
     // d = 3 cell blocks: every cell's points (split into parts of <= cell_cap)
     // spread into one (2m+1)^3 block; CTAs of 8 warps own static item lists
