@@ -187,6 +187,18 @@ int64_t mlb_ac_work_size(int64_t n, int k, int m);
 int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, const double* F,
                 const double* fid, const double* denom, double c_dt, double dt_2eps, double dt,
                 double* U_next, double* stats, double* work, void* stream);
+/* one binary Allen-Cahn step (allencahn.py:261-309): v_next = (lead v - dt/eps Phi^T u^3
+   - dt Phi^T (fid (u - f))) / denom, u_next = Phi v_next; stats = (max (u_next-u)^2, max u_next^2);
+   work: mlb_ac_work_size(n, k, 1) doubles */
+int mlb_bac_step(const double* Phi, int64_t n, int k, const double* u, const double* f, const double* fid,
+                 const double* v, const double* denom, double lead, double dt_eps, double dt, double* v_next,
+                 double* u_next, double* stats, double* work, void* stream);
+/* Ginzburg-Landau energy terms (allencahn.py:232-252): per block (fixed partition)
+   [Phi^T U (k x m, only if Phi) | sum_i prod_q A_iq^2/4 | sum_i fid_i |F_i - U_i|^2];
+   the caller sums the *nblocks rows in order.  partial: mlb_gl_energy_work_size doubles */
+int64_t mlb_gl_energy_work_size(int k, int m);
+int mlb_gl_energy_partials(const double* Phi, int64_t n, int k, int m, const double* U, const double* F,
+                           const double* fid, double* partial, int* nblocks, void* stream);
 /* argmax per row, ties to the lowest class (allencahn.py:226-229) */
 int mlb_argmax_rows(const double* U, int64_t n, int m, int32_t* labels, void* stream);
 

@@ -223,10 +223,42 @@ def gen_featuregroup():
     return out
 
 
+def gen_binary():
+    """Binary Allen-Cahn and the Ginzburg-Landau energy (allencahn.py:232-314)
+    on the eigenbasis frozen in golden_solvers.npz."""
+    g = np.load(os.path.join(OUT, "golden_solvers.npz"))
+    out = {}
+    basis = powermean.SpectralBasis(values=g["eig_m1_values"], vectors=g["eig_m1_vectors"])
+    truth = g["truth"]
+    rng = np.random.default_rng(70)
+    f = np.where(truth == 0, 1.0, -1.0)
+    f[rng.random(f.shape[0]) > 0.1] = 0.0  # ~10 % labeled, +1 / -1
+    out["f"] = f
+    res = allencahn.binary_allen_cahn_solve(basis, f, allencahn.AllenCahnParams())
+    out["bac_scores"] = res.scores
+    out["bac_iters"] = np.array([res.iterations, int(res.converged)])
+    out["bac_pred"] = allencahn.predict_binary(res.scores)
+    ids = g["label_ids"]
+    labels = allencahn.LabelData.from_class_ids(ids, int(ids.max()) + 1, 1000.0)
+    U = g["ac_scores"]
+    out["energy_basis"] = np.array([allencahn.ginzburg_landau_energy(U, basis, labels, 5e-3)])
+    # dense-operator branch on a 64-node slice (the reference accepts any dense Laplacian)
+    L2 = kernel_layer(g["pts2"], "gaussian", 0.2, 32, 4, 8)
+    Ld = graphs.materialize_sym_laplacian(L2)[:64, :64]
+    lab64 = allencahn.LabelData.from_class_ids(ids[:64], int(ids.max()) + 1, 1000.0)
+    out["energy_dense64"] = np.array([allencahn.ginzburg_landau_energy(U[:64], Ld, lab64, 5e-3)])
+    out["L_dense64"] = Ld
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    only = sys.argv[1:]  # e.g. `python oracle/gen_golden.py binary`
     for name, fn in [("window", gen_window), ("plans", gen_plans), ("fastsum", gen_fastsum),
-                     ("nfft", gen_nfft), ("solvers", gen_solvers), ("featuregroup", gen_featuregroup)]:
+                     ("nfft", gen_nfft), ("solvers", gen_solvers), ("featuregroup", gen_featuregroup),
+                     ("binary", gen_binary)]:
+        if only and name not in only:
+            continue
         data = fn()
         path = os.path.join(OUT, f"golden_{name}.npz")
         np.savez_compressed(path, **data)

@@ -299,3 +299,67 @@ def allen_cahn(values, vectors, F, fidelity, epsilon=5e-3, omega0=1000.0, c=None
 
 def predict(scores):
     return np.argmax(np.asarray(scores), axis=1)             # allencahn.py:226-229
+
+
+def corner_distances(U):
+    """A_iq = sum_l |U_il| - |U_iq| + |U_iq - 1| (allencahn.py:127-130)."""
+    U = np.asarray(U, dtype=float)
+    aU = np.abs(U)
+    return aU.sum(axis=1, keepdims=True) - aU + np.abs(U - 1.0)
+
+
+def gl_energy(U, values, vectors, F, fidelity, epsilon, L_dense=None):
+    """Ginzburg-Landau diagnostic energy (allencahn.py:232-252): Dirichlet term in
+    the eigenbasis (0.5 eps sum lambda C^2, C = Phi^T U) or with a dense
+    Laplacian (0.5 eps sum U * (L U)), double-well sum prod_q A^2/4 / (2 eps),
+    fidelity 0.5 sum_i fid_i |F_i - U_i|^2."""
+    U = np.asarray(U, dtype=float)
+    if L_dense is None:
+        C = vectors.T @ U
+        dirichlet = 0.5 * epsilon * float(np.sum(np.asarray(values)[:, None] * C * C))
+    else:
+        dirichlet = 0.5 * epsilon * float(np.sum(U * (np.asarray(L_dense) @ U)))
+    A = corner_distances(U)
+    well = float(np.sum(np.prod(0.25 * A * A, axis=1))) / (2.0 * epsilon)
+    diff = F - U
+    fid = 0.5 * float(fidelity @ np.einsum("ij,ij->i", diff, diff))
+    return dirichlet + well + fid
+
+
+def binary_allen_cahn(values, vectors, f, epsilon=5e-3, omega0=1000.0, c=None, dt=0.01, tolerance=1e-6,
+                      max_iter=300):
+    """Two-class spectral scheme with the (u^2-1)^2/4 well (allencahn.py:261-309).
+
+    Returns (scores, iterations, converged)."""
+    f = np.asarray(f, dtype=float)
+    cv = omega0 + 3.0 / epsilon if c is None else c
+    fid = np.where(f != 0, omega0, 0.0)
+    denom = 1.0 + cv * dt + epsilon * dt * np.asarray(values)
+    lead = 1.0 + cv * dt + dt / epsilon
+    v = vectors.T @ f
+    u = vectors @ v
+    conv = False
+    it_done = 0
+    for it in range(1, max_iter + 1):
+        rhs = lead * v
+        rhs -= (dt / epsilon) * (vectors.T @ (u ** 3))
+        rhs -= dt * (vectors.T @ (fid * (u - f)))
+        v = rhs / denom
+        un = vectors @ v
+        num = np.max((un - u) ** 2)
+        den = np.max(un ** 2)
+        u = un
+        it_done = it
+        if den <= 0:
+            conv = True
+            break
+        if not np.isfinite(num):
+            raise OracleNumericalError("binary iterate degenerated")
+        if num / den <= tolerance:
+            conv = True
+            break
+    return u, it_done, conv
+
+
+def predict_binary(scores):
+    return np.where(np.asarray(scores) >= 0, 1, -1)          # allencahn.py:312-314

@@ -194,3 +194,133 @@ def nonlinearity_T(U):
     np.cumprod(B[:, :0:-1], axis=1, out=right[:, -2::-1])
     wt = A * (left * right)
     return 0.5 * wt.sum(axis=1, keepdims=True) - wt
+
+
+# ------------------------------------------------------- binary scheme ----
+@dataclass
+class BinaryAllenCahnResult:
+    scores: np.ndarray
+    iterations: int
+    converged: bool
+
+
+def binary_allen_cahn_solve(basis, f, params, callback=None, device=None, return_device=False):
+    """Two-class spectral scheme with the (u^2 - 1)^2 / 4 well (allencahn.py:261-309):
+
+        v+ = [(1 + c dt + dt/eps) v - dt/eps Phi^T u^3 - dt Phi^T (omega (u - f))]
+             / (1 + c dt + eps dt lambda),   u = Phi v,
+
+    one mlb_bac_step per iteration (two fixed-order Phi^T reductions, the
+    coefficient update, Phi v and the stopping maxima on the device)."""
+    torch = _torch()
+    phi = basis.vectors
+    lam = np.asarray(basis.values, dtype=float)
+    f_host = f.cpu().numpy() if isinstance(f, torch.Tensor) else np.asarray(f, dtype=float)
+    if f_host.shape != (phi.shape[0],):
+        raise ConfigError("labels f must be one value per node")
+    if np.any(np.abs(f_host[f_host != 0]) != 1.0):
+        raise ConfigError("binary labels must be -1, 0 or +1")
+    if device is None:
+        device = phi.device.index if isinstance(phi, torch.Tensor) else torch.cuda.current_device()
+    n, k = int(phi.shape[0]), int(phi.shape[1])
+    eps, dt, c = params.epsilon, params.dt, params.c_value
+    Phi = _dev(phi, device)
+    fd = _dev(f_host, device)
+    fid = _dev(np.where(f_host != 0, params.omega0, 0.0), device)
+    denom = _dev(1.0 + c * dt + eps * dt * lam, device)
+    lead = 1.0 + c * dt + dt / eps
+    lib = _lib.lib()
+    from .krylov import gemv_n, gemv_t
+    # v = Phi^T f, u = Phi v (Phi row-major n x k == column-major k x n)
+    PhiT = Phi.t().contiguous()          # k x n row-major == column-major n x k
+    v = torch.empty(k, dtype=torch.float64, device=Phi.device)
+    gemv_t(PhiT, n, k, fd, v)
+    u = torch.empty(n, dtype=torch.float64, device=Phi.device)
+    gemv_n(PhiT, n, k, v, u)
+    vn, un = torch.empty_like(v), torch.empty_like(u)
+    work = torch.empty(int(lib.mlb_ac_work_size(n, k, 1)), dtype=torch.float64, device=Phi.device)
+    stats = torch.empty(2, dtype=torch.float64, device=Phi.device)
+    converged = False
+    iterations = 0
+    for it in range(1, params.max_iter + 1):
+        _lib.check(lib.mlb_bac_step(_lib.ptr(Phi), n, k, _lib.ptr(u), _lib.ptr(fd), _lib.ptr(fid), _lib.ptr(v),
+                                    _lib.ptr(denom), lead, dt / eps, dt, _lib.ptr(vn), _lib.ptr(un),
+                                    _lib.ptr(stats), _lib.ptr(work), _lib.stream_ptr()))
+        num, den = stats.cpu().numpy()
+        u, un = un, u
+        v, vn = vn, v
+        iterations = it
+        if callback is not None:
+            callback(it, u.cpu().numpy())
+        if den <= 0:
+            converged = True  # the all-zero state is a fixed point
+            break
+        if not np.isfinite(num):
+            raise NumericalError("binary Allen-Cahn iterate degenerated")
+        if num / den <= params.tolerance:
+            converged = True
+            break
+    scores = u if return_device else u.cpu().numpy()
+    return BinaryAllenCahnResult(scores=scores, iterations=iterations, converged=converged)
+
+
+def predict_binary(scores):
+    """+1 / -1 by sign, an exact zero counts as +1 (allencahn.py:312-314)."""
+    torch = _torch()
+    if isinstance(scores, torch.Tensor):
+        return torch.where(scores >= 0, 1, -1).to(torch.int32)
+    return np.where(np.asarray(scores) >= 0, 1, -1)
+
+
+def ginzburg_landau_energy(scores, operator, labels, epsilon):
+    """Diagnostic energy (allencahn.py:232-252): Dirichlet term in the eigenbasis
+    (0.5 eps sum_a lambda_a |Phi^T U|_a^2) or with a dense Laplacian
+    (0.5 eps sum U * (L U)), the multi-well term and the fidelity term.  The
+    row sums run on the device (mlb_gl_energy_partials, fixed partition); the
+    host adds the per-block partials in order."""
+    torch = _torch()
+    U_host = scores.cpu().numpy() if isinstance(scores, torch.Tensor) else np.asarray(scores, dtype=float)
+    n, m = U_host.shape
+    if labels.F.shape != (n, m):
+        raise ConfigError("scores and labels disagree in shape")
+    spectral = isinstance(operator, SpectralBasis)
+    if spectral:
+        phi = operator.vectors
+        device = phi.device.index if isinstance(phi, torch.Tensor) else torch.cuda.current_device()
+        Phi = _dev(phi, device)
+        k = int(Phi.shape[1])
+    else:
+        device = torch.cuda.current_device()
+        Phi, k = None, 0
+    U = _dev(U_host, device)
+    F = _dev(labels.F, device)
+    fid = _dev(labels.fidelity, device)
+    lib = _lib.lib()
+    part = torch.empty(int(lib.mlb_gl_energy_work_size(max(k, 1), m)), dtype=torch.float64, device=U.device)
+    nb = C.c_int(0)
+    _lib.check(lib.mlb_gl_energy_partials(_lib.ptr(Phi) if Phi is not None else None, n, k, m, _lib.ptr(U),
+                                          _lib.ptr(F), _lib.ptr(fid), _lib.ptr(part), C.byref(nb),
+                                          _lib.stream_ptr()))
+    width = k * m + 2
+    rows = part[: nb.value * width].view(nb.value, width).cpu().numpy()
+    tot = np.zeros(width)
+    for r in rows:  # fixed block order
+        tot += r
+    well = tot[k * m] / (2.0 * epsilon)
+    fidelity = 0.5 * tot[k * m + 1]
+    if spectral:
+        Cm = tot[: k * m].reshape(k, m)
+        dirichlet = 0.5 * epsilon * float(np.sum(np.asarray(operator.values, dtype=float)[:, None] * Cm * Cm))
+    else:
+        from .krylov import dot, gemv_n
+        L = _dev(np.asarray(operator, dtype=float), device)  # symmetric: row-major == column-major
+        LU = torch.empty(n, dtype=torch.float64, device=U.device)
+        acc = torch.empty(1, dtype=torch.float64, device=U.device)
+        Ut = U.t().contiguous()
+        dirichlet = 0.0
+        for cidx in range(m):
+            gemv_n(L, n, n, Ut[cidx], LU)
+            dot(Ut[cidx], LU, acc)
+            dirichlet += float(acc.item())
+        dirichlet *= 0.5 * epsilon
+    return dirichlet + well + fidelity

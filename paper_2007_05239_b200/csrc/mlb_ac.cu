@@ -186,6 +186,167 @@ __global__ void ac_max_finish(const double* __restrict__ mx_partial, int nb, dou
     stats[1] = mu;
 }
 
+// ---- binary scheme (allencahn.py:261-309): scalar scores u = Phi v ------
+// partial[b][a] = sum_i Phi[i][a] u_i^3, partial[b][k + a] = sum_i Phi[i][a] fid_i (u_i - f_i)
+__global__ void bac_rhs_kernel(const double* __restrict__ Phi, int64_t n, int k, const double* __restrict__ u,
+                               const double* __restrict__ f, const double* __restrict__ fid,
+                               double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    double* X = sm;                  // kAcRows x 2
+    double* Pt = sm + 2 * kAcRows;   // kAcRows x k
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    const int o = threadIdx.x;  // output: a = o % k, which = o / k
+    const bool live = o < 2 * k;
+    const int a = o % k, which = o / k;
+    double acc = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += kAcRows) {
+        const int rows = (int)min((int64_t)kAcRows, r1 - t0);
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+            const double ui = u[t0 + r];
+            X[2 * r] = ui * ui * ui;
+            X[2 * r + 1] = fid[t0 + r] * (ui - f[t0 + r]);
+        }
+        for (int e = threadIdx.x; e < rows * k; e += blockDim.x) Pt[e] = Phi[t0 * k + e];
+        __syncthreads();
+        if (live)
+            for (int r = 0; r < rows; ++r) acc = fma(Pt[r * k + a], X[2 * r + which], acc);
+        __syncthreads();
+    }
+    if (live) partial[(int64_t)blockIdx.x * 2 * k + o] = acc;
+}
+
+__global__ void bac_finish_kernel(const double* __restrict__ partial, int nb, int k, const double* __restrict__ v,
+                                  const double* __restrict__ denom, double lead, double dt_eps, double dt,
+                                  double* __restrict__ v_next) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= k) return;
+    double g1 = 0.0, g2 = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        g1 += partial[(int64_t)b * 2 * k + a];
+        g2 += partial[(int64_t)b * 2 * k + k + a];
+    }
+    double rhs = lead * v[a];
+    rhs -= dt_eps * g1;
+    rhs -= dt * g2;
+    v_next[a] = rhs / denom[a];
+}
+
+__global__ void bac_update_kernel(const double* __restrict__ Phi, int64_t n, int k, const double* __restrict__ v,
+                                  const double* __restrict__ u, double* __restrict__ un,
+                                  double* __restrict__ mx_partial) {
+    extern __shared__ double vsh[];
+    __shared__ double sh_d[32], sh_u[32];
+    for (int e = threadIdx.x; e < k; e += blockDim.x) vsh[e] = v[e];
+    __syncthreads();
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    double md = 0.0, mu = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        double y = 0.0;
+        for (int a = 0; a < k; ++a) y = fma(Phi[i * k + a], vsh[a], y);
+        const double df = y - u[i];
+        md = fmax(md, df * df);
+        mu = fmax(mu, y * y);
+        un[i] = y;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        md = fmax(md, __shfl_down_sync(0xffffffffu, md, o));
+        mu = fmax(mu, __shfl_down_sync(0xffffffffu, mu, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh_d[w] = md;
+        sh_u[w] = mu;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            md = fmax(md, sh_d[i]);
+            mu = fmax(mu, sh_u[i]);
+        }
+        mx_partial[2 * blockIdx.x] = md;
+        mx_partial[2 * blockIdx.x + 1] = mu;
+    }
+}
+
+// ---- Ginzburg-Landau energy partials (allencahn.py:232-252) -------------
+// partial[b] = [ C_b (k x m: sum_i Phi[i][a] U[i][c]) | well_b | fid_b ] with
+// well = sum_i prod_q (0.25 A_iq^2), fid = sum_i fid_i |F_i - U_i|^2
+__global__ void gl_energy_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
+                                 const double* __restrict__ U, const double* __restrict__ F,
+                                 const double* __restrict__ fid, double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    double* Ut = sm;                 // kAcRows x m
+    double* Pt = sm + kAcRows * m;   // kAcRows x k
+    __shared__ double red[2][256];
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    const int nout = k * m;
+    constexpr int kMaxOut = 16;
+    double acc[kMaxOut];
+#pragma unroll
+    for (int j = 0; j < kMaxOut; ++j) acc[j] = 0.0;
+    double well = 0.0, fsum = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += kAcRows) {
+        const int rows = (int)min((int64_t)kAcRows, r1 - t0);
+        for (int e = threadIdx.x; e < rows * m; e += blockDim.x) Ut[e] = U[t0 * m + e];
+        if (Phi)
+            for (int e = threadIdx.x; e < rows * k; e += blockDim.x) Pt[e] = Phi[t0 * k + e];
+        __syncthreads();
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+            const int64_t i = t0 + r;
+            double asum = 0.0;
+            for (int q = 0; q < m; ++q) asum += fabs(Ut[r * m + q]);
+            double prod = 1.0, dd = 0.0;
+            for (int q = 0; q < m; ++q) {
+                const double uq = Ut[r * m + q];
+                const double A = asum - fabs(uq) + fabs(uq - 1.0);
+                prod *= 0.25 * A * A;
+                const double df = F[i * m + q] - uq;
+                dd = fma(df, df, dd);
+            }
+            well += prod;
+            fsum += fid[i] * dd;
+        }
+        if (Phi) {
+#pragma unroll
+            for (int j = 0; j < kMaxOut; ++j) {
+                const int o = threadIdx.x + j * blockDim.x;
+                if (o < nout) {
+                    const int a = o / m, c = o % m;
+                    double s = acc[j];
+                    for (int r = 0; r < rows; ++r) s = fma(Pt[r * k + a], Ut[r * m + c], s);
+                    acc[j] = s;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double* out = partial + (int64_t)blockIdx.x * (nout + 2);
+#pragma unroll
+    for (int j = 0; j < kMaxOut; ++j) {
+        const int o = threadIdx.x + j * blockDim.x;
+        if (o < nout) out[o] = acc[j];
+    }
+    // fixed-order block sums of the per-thread well / fidelity terms
+    red[0][threadIdx.x] = well;
+    red[1][threadIdx.x] = fsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double w = 0.0, fs = 0.0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            w += red[0][t];
+            fs += red[1][t];
+        }
+        out[nout] = w;
+        out[nout + 1] = fs;
+    }
+}
+
 __global__ void argmax_kernel(const double* __restrict__ U, int64_t n, int m, int32_t* __restrict__ lab) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int best = 0;
@@ -251,8 +412,8 @@ using namespace mlb;
 extern "C" {
 
 int64_t mlb_ac_work_size(int64_t n, int k, int m) {
-    (void)n;
-    return (int64_t)kAcBlocks * k * m + 2 * kAcBlocks + (int64_t)k * m;
+    (void)n;  // (m = 1: the binary scheme's 2k partials + maxima fit as well)
+    return (int64_t)kAcBlocks * k * std::max(m, 2) + 2 * kAcBlocks + (int64_t)k * std::max(m, 2);
 }
 
 int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, const double* F, const double* fid,
@@ -274,6 +435,41 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
     ac_update_kernel<<<nb, 256, (size_t)k * m * sizeof(double), st>>>(Phi, n, k, m, Vc, U, U_next, mx);
     note_launches(1);
     ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
+    note_launches(1);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_bac_step(const double* Phi, int64_t n, int k, const double* u, const double* f, const double* fid,
+                 const double* v, const double* denom, double lead, double dt_eps, double dt, double* v_next,
+                 double* u_next, double* stats, double* work, void* stream) {
+    if (k < 1 || 2 * k > 256) return fail(MLB_ERR_CONFIG, "binary Allen-Cahn kernels need 1 <= k <= 128");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kAcBlocks, (n + kAcRows - 1) / kAcRows));
+    double* partial = work;                       // nb x 2k
+    double* mx = work + (int64_t)kAcBlocks * 2 * k;  // 2 x nb
+    const size_t sm1 = (size_t)kAcRows * (2 + k) * sizeof(double);
+    MLB_CUDA_TRY(cudaFuncSetAttribute(bac_rhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    bac_rhs_kernel<<<nb, 256, sm1, st>>>(Phi, n, k, u, f, fid, partial);
+    bac_finish_kernel<<<(k + 127) / 128, 128, 0, st>>>(partial, nb, k, v, denom, lead, dt_eps, dt, v_next);
+    bac_update_kernel<<<nb, 256, (size_t)k * sizeof(double), st>>>(Phi, n, k, v_next, u, u_next, mx);
+    ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
+    note_launches(4);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int64_t mlb_gl_energy_work_size(int k, int m) { return (int64_t)kAcBlocks * ((int64_t)k * m + 2); }
+
+int mlb_gl_energy_partials(const double* Phi, int64_t n, int k, int m, const double* U, const double* F,
+                           const double* fid, double* partial, int* nblocks, void* stream) {
+    if (m < 1 || m > kAcMaxM) return fail(MLB_ERR_CONFIG, "energy kernels support m <= 32 classes");
+    if (Phi && (k < 1 || k * m > 16 * 256)) return fail(MLB_ERR_CONFIG, "energy kernels need k*m <= 4096");
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kAcBlocks, (n + kAcRows - 1) / kAcRows));
+    if (nblocks) *nblocks = nb;
+    const size_t sm1 = (size_t)kAcRows * (m + (Phi ? k : 0)) * sizeof(double);
+    MLB_CUDA_TRY(cudaFuncSetAttribute(gl_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    gl_energy_kernel<<<nb, 256, sm1, (cudaStream_t)stream>>>(Phi, n, Phi ? k : 0, m, U, F, fid, partial);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;

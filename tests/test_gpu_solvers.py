@@ -191,3 +191,29 @@ def test_config1_pipeline_matches_reference():
     pred = predict_labels(res.scores)
     assert np.mean(pred == g["pred"]) >= 0.999
     assert abs(res.iterations - int(g["iters"][0])) <= 1
+
+
+def test_binary_allen_cahn_and_energy_match_golden():
+    """GPU binary scheme (mlb_bac_step) and the energy diagnostic vs the
+    reference run frozen in golden_binary.npz."""
+    import torch
+    from paper_2007_05239_b200 import (AllenCahnParams, LabelData, SpectralBasis, binary_allen_cahn_solve,
+                                       ginzburg_landau_energy, predict_binary)
+    gs = load_golden("solvers")
+    gb = load_golden("binary")
+    basis = SpectralBasis(values=gs["eig_m1_values"], vectors=gs["eig_m1_vectors"])
+    res = binary_allen_cahn_solve(basis, gb["f"], AllenCahnParams())
+    assert [res.iterations, int(res.converged)] == list(gb["bac_iters"])
+    assert np.abs(res.scores - gb["bac_scores"]).max() < 1e-9
+    assert np.array_equal(predict_binary(res.scores), gb["bac_pred"])
+    d = binary_allen_cahn_solve(basis, torch.from_numpy(gb["f"]).cuda(), AllenCahnParams(), return_device=True)
+    assert np.array_equal(predict_binary(d.scores).cpu().numpy(), gb["bac_pred"])
+    with pytest.raises(Exception, match="binary labels"):
+        binary_allen_cahn_solve(basis, 2.0 * gb["f"], AllenCahnParams())
+    ids = gs["label_ids"]
+    labels = LabelData.from_class_ids(ids, int(ids.max()) + 1, 1000.0)
+    e = ginzburg_landau_energy(gs["ac_scores"], basis, labels, 5e-3)
+    assert abs(e - gb["energy_basis"][0]) <= 1e-10 * abs(gb["energy_basis"][0])
+    lab64 = LabelData.from_class_ids(ids[:64], int(ids.max()) + 1, 1000.0)
+    e64 = ginzburg_landau_energy(gs["ac_scores"][:64], gb["L_dense64"], lab64, 5e-3)
+    assert abs(e64 - gb["energy_dense64"][0]) <= 1e-10 * abs(gb["energy_dense64"][0])

@@ -140,3 +140,23 @@ def test_allen_cahn_pieces_match_reference():
     assert_allclose(so.well_force(np.array([[0.75, 0.25]])), g["T_hand"], atol=1e-15)
     assert_allclose(so.simplex_project(g["proj_in"]), g["proj_out"], atol=1e-15)
     assert_allclose(so.well_force(g["T_in"]), g["T_out"], rtol=1e-13, atol=1e-13)
+
+
+def test_binary_allen_cahn_and_energy_match_reference():
+    """Oracle binary scheme and Ginzburg-Landau energy vs the reference run
+    frozen in golden_binary.npz (allencahn.py:232-314)."""
+    gs = load_golden("solvers")
+    gb = load_golden("binary")
+    u, it, conv = so.binary_allen_cahn(gs["eig_m1_values"], gs["eig_m1_vectors"], gb["f"])
+    assert [it, int(conv)] == list(gb["bac_iters"])
+    assert np.abs(u - gb["bac_scores"]).max() < 1e-12
+    assert np.array_equal(so.predict_binary(u), gb["bac_pred"])
+    ids = gs["label_ids"]
+    m = int(ids.max()) + 1
+    F = np.zeros((ids.size, m))
+    F[ids >= 0, ids[ids >= 0]] = 1.0
+    fid = np.where(ids >= 0, 1000.0, 0.0)
+    e = so.gl_energy(gs["ac_scores"], gs["eig_m1_values"], gs["eig_m1_vectors"], F, fid, 5e-3)
+    assert abs(e - gb["energy_basis"][0]) <= 1e-12 * abs(gb["energy_basis"][0])
+    e64 = so.gl_energy(gs["ac_scores"][:64], None, None, F[:64], fid[:64], 5e-3, L_dense=gb["L_dense64"])
+    assert abs(e64 - gb["energy_dense64"][0]) <= 1e-12 * abs(gb["energy_dense64"][0])
