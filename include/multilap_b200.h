@@ -41,6 +41,9 @@ extern "C" {
 #define MLB_ACCUMULATE 2u     /* y += result instead of y = result */
 #define MLB_SORTED 4u         /* v and y are in the binding's sorted (cell) order */
 #define MLB_SPREAD_ONLY 8u    /* mlb_spread: run the spread kernel only (partials, no reduction) */
+/* bits 16-19 of the mlb_spread / mlb_gather stage hooks switch parts of those
+   kernels off for profiling ablations (tools/ablate_spread.py); mlb_apply
+   ignores every bit but MLB_USE_ISD | MLB_ACCUMULATE | MLB_SORTED */
 
 typedef struct mlb_plan mlb_plan;
 typedef struct mlb_binding mlb_binding;

@@ -659,6 +659,7 @@ int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double b
     if (!b->n) return MLB_OK;
     DeviceGuard guard(b->plan->device);
     cudaStream_t st = (cudaStream_t)stream;
+    flags &= (MLB_USE_ISD | MLB_ACCUMULATE | MLB_SORTED);  // the public bits only
     int rc = launch_spread(b, v, flags, st);
     if (rc == MLB_OK) rc = launch_reduce(b, b->grid, st);
     if (rc == MLB_OK) rc = launch_convolve(b, b->grid, b->grid2, st);

@@ -583,10 +583,9 @@ struct MergeCfg {
 };
 
 template <int M>
-__global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick_merge_kernel(FsArgs a, int abl) {
+__global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick_merge_kernel(FsArgs a) {
     constexpr int S = 2 * M + 1;
     constexpr int SS = S * S;
-    if (abl == 2) return;
     const int TL = a.g.TL;
     const int s0 = blockIdx.x, slot = blockIdx.y;
     const int q0 = __ldg(a.merge_off + slot * TL + s0), q1 = __ldg(a.merge_off + slot * TL + s0 + 1);
@@ -615,7 +614,7 @@ __global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick
                 const int2 p = pr[min(q + u, nq - 1)];
                 const int o1 = i1 - (p.y >> 8), o2 = i2 - (p.y & 255);
                 ok[u] = (q + u < nq) && (unsigned)o1 < (unsigned)S && (unsigned)o2 < (unsigned)S;
-                vals[u] = abl ? 1.0 : __ldcg(a.blocks + (size_t)p.x * SS + (ok[u] ? o1 * S + o2 : 0));
+                vals[u] = __ldcg(a.blocks + (size_t)p.x * SS + (ok[u] ? o1 * S + o2 : 0));
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) sum += ok[u] ? vals[u] : 0.0;
@@ -1131,15 +1130,13 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     const int R = (G.TL + Tb - 1) / Tb;  // source bricks per axis
     if (b->nactive > 0) {
         const dim3 mg(G.TL, b->nactive);
-        const char* ab = getenv("MLB_MERGE_ABL");  // profiling aid: 1 skip the block loads, 2 skip all
-        const int abl = ab ? atoi(ab) : 0;
         switch (G.m) {
-            case 1: MLB_CUDA_TRY(launch_k(brick_merge_kernel<1>, mg, dim3(MergeCfg<1>::MT), 0, st, a, abl)); break;
-            case 2: MLB_CUDA_TRY(launch_k(brick_merge_kernel<2>, mg, dim3(MergeCfg<2>::MT), 0, st, a, abl)); break;
-            case 3: MLB_CUDA_TRY(launch_k(brick_merge_kernel<3>, mg, dim3(MergeCfg<3>::MT), 0, st, a, abl)); break;
-            case 4: MLB_CUDA_TRY(launch_k(brick_merge_kernel<4>, mg, dim3(MergeCfg<4>::MT), 0, st, a, abl)); break;
-            case 5: MLB_CUDA_TRY(launch_k(brick_merge_kernel<5>, mg, dim3(MergeCfg<5>::MT), 0, st, a, abl)); break;
-            default: MLB_CUDA_TRY(launch_k(brick_merge_kernel<6>, mg, dim3(MergeCfg<6>::MT), 0, st, a, abl)); break;
+            case 1: MLB_CUDA_TRY(launch_k(brick_merge_kernel<1>, mg, dim3(MergeCfg<1>::MT), 0, st, a)); break;
+            case 2: MLB_CUDA_TRY(launch_k(brick_merge_kernel<2>, mg, dim3(MergeCfg<2>::MT), 0, st, a)); break;
+            case 3: MLB_CUDA_TRY(launch_k(brick_merge_kernel<3>, mg, dim3(MergeCfg<3>::MT), 0, st, a)); break;
+            case 4: MLB_CUDA_TRY(launch_k(brick_merge_kernel<4>, mg, dim3(MergeCfg<4>::MT), 0, st, a)); break;
+            case 5: MLB_CUDA_TRY(launch_k(brick_merge_kernel<5>, mg, dim3(MergeCfg<5>::MT), 0, st, a)); break;
+            default: MLB_CUDA_TRY(launch_k(brick_merge_kernel<6>, mg, dim3(MergeCfg<6>::MT), 0, st, a)); break;
         }
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());

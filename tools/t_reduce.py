@@ -10,10 +10,10 @@ lib = _lib.lib()
 v = torch.from_numpy(np.random.default_rng(1).standard_normal(wl.n)).cuda()
 grid = torch.empty(b.stats()["grid_cells"], dtype=torch.float64, device="cuda")
 lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD | _lib.MLB_SPREAD_ONLY, _lib.stream_ptr())
-if len(sys.argv) > 1: os.environ["MLB_MERGE_ABL"] = sys.argv[1]
+
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for _ in range(3): lib.mlb_reduce(b.ptr, _lib.ptr(grid), _lib.stream_ptr())
 s.record()
 for _ in range(20): lib.mlb_reduce(b.ptr, _lib.ptr(grid), _lib.stream_ptr())
 e.record(); e.synchronize()
-print("reduce", os.environ.get("MLB_MERGE_ABL"), s.elapsed_time(e) / 20 * 1e3, "us")
+print("reduce", s.elapsed_time(e) / 20 * 1e3, "us")
