@@ -477,39 +477,73 @@ static int convolve3_fused(mlb_binding* b, const double* gin, double* gout, cuda
 // convolution is d one-dimensional passes out[..u..] = sum_v c[u-v] in[..v..]
 // with the real kernel c[D] = sum_k f(k) cos(2 pi k D / ng).
 
+// 4 consecutive outputs u0..u0+3 of one line: out[u] = sum_v c[u - v] x[v];
+// the kernel taps slide through registers (2 shared loads per 4 FMAs)
+__device__ __forceinline__ void sep_line4(const double* __restrict__ sc, int u0, const double* __restrict__ x,
+                                          int L, int stride, double* o) {
+    const double* cc = sc + L - 1 + u0;  // cc[j - v] = c[u0 + j - v]
+    double w0 = cc[0], w1 = cc[1], w2 = cc[2], w3 = cc[3];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int v = 0; v < L; ++v) {
+        const double xv = x[v * stride];
+        s0 = fma(w0, xv, s0);
+        s1 = fma(w1, xv, s1);
+        s2 = fma(w2, xv, s2);
+        s3 = fma(w3, xv, s3);
+        w3 = w2;
+        w2 = w1;
+        w1 = w0;
+        w0 = cc[-v - 1];
+    }
+    o[0] = s0;
+    o[1] = s1;
+    o[2] = s2;
+    o[3] = s3;
+}
+
 // whole sub-box in smem, one CTA, all passes (d <= 2 and small grids)
 __global__ void sep_small_kernel(const double* __restrict__ gin, double* __restrict__ gout,
                                  const double* __restrict__ c, int L, int d) {
     extern __shared__ double sm[];
     const int cells = (d == 1) ? L : L * L;
+    const int rows = cells / L;
+    const int LQ = (L + 3) / 4;  // 4-output groups per line
     double* a = sm;
     double* b = sm + cells;
-    double* sc = sm + 2 * cells;
-    for (int i = threadIdx.x; i < 2 * L - 1; i += blockDim.x) sc[i] = __ldg(c + i);
+    double* sc = sm + 2 * cells;  // 2L-1 taps padded by 4 zeros on both sides
+    for (int i = threadIdx.x; i < 2 * L + 7; i += blockDim.x) {
+        const int k = i - 4;
+        sc[i] = (k >= 0 && k < 2 * L - 1) ? __ldg(c + k) : 0.0;
+    }
     pdl_wait();  // the grid comes from the reduction
     for (int i = threadIdx.x; i < cells; i += blockDim.x) a[i] = __ldg(gin + i);
     __syncthreads();
+    const double* scp = sc + 4;
     // last axis
-    for (int o = threadIdx.x; o < cells; o += blockDim.x) {
-        const int u = o % L, row = o - u;
-        const double* cc = sc + u + L - 1;
-        double s = 0.0;
-        for (int v = 0; v < L; ++v) s = fma(cc[-v], a[row + v], s);
-        b[o] = s;
+    for (int w = threadIdx.x; w < rows * LQ; w += blockDim.x) {
+        const int r = w / LQ, q = w % LQ;
+        double o[4];
+        sep_line4(scp, 4 * q, a + r * L, L, 1, o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (4 * q + j < L) b[r * L + 4 * q + j] = o[j];
     }
     __syncthreads();
     if (d == 1) {
         for (int o = threadIdx.x; o < cells; o += blockDim.x) gout[o] = b[o];
+        pdl_launch();
         return;
     }
     // first axis (d = 2)
-    for (int o = threadIdx.x; o < cells; o += blockDim.x) {
-        const int u = o / L, col = o % L;
-        const double* cc = sc + u + L - 1;
-        double s = 0.0;
-        for (int v = 0; v < L; ++v) s = fma(cc[-v], b[v * L + col], s);
-        gout[o] = s;
+    for (int w = threadIdx.x; w < L * LQ; w += blockDim.x) {
+        const int col = w % L, q = w / L;
+        double o[4];
+        sep_line4(scp, 4 * q, b + col, L, L, o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (4 * q + j < L) gout[(4 * q + j) * L + col] = o[j];
     }
+    pdl_launch();
 }
 
 // one pass over a contiguous axis (rows of length L): CTA = 8 rows
@@ -590,30 +624,6 @@ __device__ __forceinline__ double sep_line(const double* __restrict__ cc, const 
     return q0 + q1;
 }
 
-// 4 consecutive outputs u0..u0+3 of one line: out[u] = sum_v c[u - v] x[v];
-// the kernel taps slide through registers (2 shared loads per 4 FMAs)
-__device__ __forceinline__ void sep_line4(const double* __restrict__ sc, int u0, const double* __restrict__ x,
-                                          int L, int stride, double* o) {
-    const double* cc = sc + L - 1 + u0;  // cc[j - v] = c[u0 + j - v]
-    double w0 = cc[0], w1 = cc[1], w2 = cc[2], w3 = cc[3];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    for (int v = 0; v < L; ++v) {
-        const double xv = x[v * stride];
-        s0 = fma(w0, xv, s0);
-        s1 = fma(w1, xv, s1);
-        s2 = fma(w2, xv, s2);
-        s3 = fma(w3, xv, s3);
-        w3 = w2;
-        w2 = w1;
-        w1 = w0;
-        w0 = cc[-v - 1];
-    }
-    o[0] = s0;
-    o[1] = s1;
-    o[2] = s2;
-    o[3] = s3;
-}
-
 __global__ void __launch_bounds__(512) sep3_p21_kernel(const double* __restrict__ gin, double* __restrict__ gout,
                                                        const double* __restrict__ c, int L) {
     extern __shared__ double sm[];
@@ -688,8 +698,8 @@ static int convolve_separable(mlb_binding* b, const double* gin, double* gout, c
     const int L = G.L, d = G.d;
     const double* c = b->plan->sep;
     const int64_t cells = b->grid_cells;
-    if (d <= 2 && (2 * cells + 2 * L) * 8 <= 96 * 1024) {
-        const size_t smem = (size_t)(2 * cells + 2 * L) * sizeof(double);
+    if (d <= 2 && (2 * cells + 2 * L + 8) * 8 <= 96 * 1024) {
+        const size_t smem = (size_t)(2 * cells + 2 * L + 8) * sizeof(double);
         MLB_CUDA_TRY(cudaFuncSetAttribute(sep_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         MLB_CUDA_TRY(launch_k(sep_small_kernel, dim3(1), dim3(512), smem, st, gin, gout, c, L, d));
