@@ -18,7 +18,7 @@ namespace mlb {
 
 constexpr int kAcMaxM = 32;     // classes
 constexpr int kAcRows = 128;    // rows per tile
-constexpr int kAcBlocks = 296;  // fixed partition (2 x SMs)
+constexpr int kAcBlocks = 148 * 6;  // fixed partition (6 CTAs per SM)
 
 // well force for one row (m <= kAcMaxM), leave-one-out products as the reference
 __device__ void well_force_row(const double* u, int m, double* t) {
@@ -95,13 +95,314 @@ __global__ void ac_rhs_kernel(const double* __restrict__ Phi, int64_t n, int k, 
     }
 }
 
+// ---- register-resident row kernels (m <= MM, MM in {4, 8, 16, 32}) -------
+template <int MM>
+__device__ __forceinline__ void well_force_t(const double* u, int m, double* t) {
+    double asum = 0.0;
+#pragma unroll
+    for (int q = 0; q < MM; ++q)
+        if (q < m) asum += fabs(u[q]);
+    double A[MM], B[MM];
+#pragma unroll
+    for (int q = 0; q < MM; ++q) {
+        A[q] = (q < m) ? asum - fabs(u[q]) + fabs(u[q] - 1.0) : 0.0;
+        B[q] = (q < m) ? 0.25 * A[q] * A[q] : 1.0;
+    }
+    double left[MM];
+    double acc = 1.0;
+#pragma unroll
+    for (int q = 0; q < MM; ++q) {
+        left[q] = acc;
+        if (q < m) acc *= B[q];
+    }
+    double wt[MM];
+    double right = 1.0;
+#pragma unroll
+    for (int q = MM - 1; q >= 0; --q) {
+        if (q < m) {
+            wt[q] = A[q] * (left[q] * right);
+            right *= B[q];
+        } else {
+            wt[q] = 0.0;
+        }
+    }
+    double wsum = 0.0;
+#pragma unroll
+    for (int q = 0; q < MM; ++q)
+        if (q < m) wsum += wt[q];
+#pragma unroll
+    for (int q = 0; q < MM; ++q) t[q] = 0.5 * wsum - wt[q];
+}
+
+// descending bitonic sort of MM register values (padding = -inf sorts last)
+template <int MM>
+__device__ __forceinline__ void sort_desc(double* s) {
+#pragma unroll
+    for (int size = 2; size <= MM; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+            for (int i = 0; i < MM; ++i) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool desc = ((i & size) == 0);
+                    const double x = s[i], y = s[j];
+                    const bool sw = desc ? (x < y) : (x > y);
+                    s[i] = sw ? y : x;
+                    s[j] = sw ? x : y;
+                }
+            }
+}
+
+// rhs: R rows from staged U / F tiles, then Phi^T R with every thread busy
+// (4 x 8 output tiles x row groups, fixed-order group reduction)
+template <int MM>
+__global__ void __launch_bounds__(256, 2) ac_rhs3_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
+                                                      const double* __restrict__ U, const double* __restrict__ F,
+                                                      const double* __restrict__ fid, double c_dt, double dt_2eps,
+                                                      double dt, double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    constexpr int T = 256;
+    double* Pt = sm;              // T x k
+    double* Ut = Pt + T * k;      // T x m (U, then R in place)
+    double* Ft = Ut + T * m;      // T x m
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    constexpr int TC = MM < 8 ? MM : 8;  // output tile: 4 rows of Phi^T x TC classes
+    const int ta = (k + 3) / 4, tc = (m + TC - 1) / TC;
+    const int NO = ta * tc, NG = blockDim.x / NO;
+    const int o = threadIdx.x % NO, g = threadIdx.x / NO;
+    const bool live = g < NG;
+    const int a0 = (o / tc) * 4, c0 = (o % tc) * TC;
+    double acc[4][TC];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += T) {
+        const int rows = (int)min((int64_t)T, r1 - t0);
+        for (int e = threadIdx.x; e < rows * k; e += blockDim.x) Pt[e] = __ldg(Phi + t0 * k + e);
+        for (int e = threadIdx.x; e < rows * m; e += blockDim.x) {
+            Ut[e] = __ldg(U + t0 * m + e);
+            Ft[e] = __ldg(F + t0 * m + e);
+        }
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const int r = threadIdx.x;
+            double u[MM], t[MM];
+#pragma unroll
+            for (int q = 0; q < MM; ++q) u[q] = (q < m) ? Ut[r * m + q] : 0.0;
+            well_force_t<MM>(u, m, t);
+            const double fi = __ldg(fid + t0 + r);
+#pragma unroll
+            for (int q = 0; q < MM; ++q)
+                if (q < m) Ut[r * m + q] = c_dt * u[q] - dt_2eps * t[q] - dt * fi * (u[q] - Ft[r * m + q]);
+        }
+        __syncthreads();
+        if (live) {
+            for (int r = g; r < rows; r += NG) {
+                double pa[4], rc[TC];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pa[i] = (a0 + i < k) ? Pt[r * k + a0 + i] : 0.0;
+#pragma unroll
+                for (int j = 0; j < TC; ++j) rc[j] = (c0 + j < m) ? Ut[r * m + c0 + j] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < TC; ++j) acc[i][j] = fma(pa[i], rc[j], acc[i][j]);
+            }
+        }
+        __syncthreads();
+    }
+    double* red = sm;  // NG * NO * 4 * TC <= 256 * 32 doubles
+    if (live)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < TC; ++j) red[((size_t)g * NO + o) * (4 * TC) + i * TC + j] = acc[i][j];
+    __syncthreads();
+    const int nout = k * m;
+    for (int e = threadIdx.x; e < nout; e += blockDim.x) {
+        const int a = e / m, c = e % m;
+        const int oo = (a / 4) * tc + c / TC, slot = (a % 4) * TC + (c % TC);
+        double sum = 0.0;
+        for (int gg = 0; gg < NG; ++gg) sum += red[((size_t)gg * NO + oo) * (4 * TC) + slot];
+        partial[(int64_t)blockIdx.x * nout + e] = sum;
+    }
+}
+
+// update: U_next = proj_simplex(Phi Vc) per row from staged Phi / U tiles,
+// written back through shared memory (coalesced), plus the stopping maxima
+template <int MM>
+__global__ void __launch_bounds__(256) ac_update3_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
+                                                         const double* __restrict__ Vc,
+                                                         const double* __restrict__ U, double* __restrict__ Un,
+                                                         double* __restrict__ mx_partial) {
+    extern __shared__ double sm[];
+    constexpr int T = 256;
+    double* vsh = sm;                 // k x m
+    double* Pt = vsh + ((k * m + 1) & ~1);  // T x k
+    double* Ut = Pt + T * k;          // T x m (U, then U_next in place)
+    __shared__ double sh_d[8], sh_u[8];
+    for (int e = threadIdx.x; e < k * m; e += blockDim.x) vsh[e] = Vc[e];
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    double md = 0.0, mu = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += T) {
+        const int rows = (int)min((int64_t)T, r1 - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < rows * k; e += blockDim.x) Pt[e] = __ldg(Phi + t0 * k + e);
+        for (int e = threadIdx.x; e < rows * m; e += blockDim.x) Ut[e] = __ldg(U + t0 * m + e);
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const int r = threadIdx.x;
+            double y[MM];
+#pragma unroll
+            for (int c = 0; c < MM; ++c) y[c] = 0.0;
+            for (int a = 0; a < k; ++a) {
+                const double p = Pt[r * k + a];
+#pragma unroll
+                for (int c = 0; c < MM; ++c)
+                    if (c < m) y[c] = fma(p, vsh[a * m + c], y[c]);
+            }
+            double s[MM];
+#pragma unroll
+            for (int c = 0; c < MM; ++c) s[c] = (c < m) ? y[c] : -INFINITY;
+            sort_desc<MM>(s);
+            double cs = 0.0, cs_rho = 0.0;
+            int rho = 0;
+#pragma unroll
+            for (int j = 0; j < MM; ++j) {
+                if (j < m) {
+                    cs += s[j];
+                    if (s[j] + (1.0 - cs) / (j + 1) > 0) {
+                        rho = j;
+                        cs_rho = cs;
+                    }
+                }
+            }
+            const double tau = (1.0 - cs_rho) / (rho + 1);
+            double dd = 0.0, uu = 0.0;
+#pragma unroll
+            for (int c = 0; c < MM; ++c) {
+                if (c < m) {
+                    const double v = fmax(y[c] + tau, 0.0);
+                    const double df = v - Ut[r * m + c];
+                    dd = fma(df, df, dd);
+                    uu = fma(v, v, uu);
+                    Ut[r * m + c] = v;
+                }
+            }
+            md = fmax(md, dd);
+            mu = fmax(mu, uu);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < rows * m; e += blockDim.x) Un[t0 * m + e] = Ut[e];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        md = fmax(md, __shfl_down_sync(0xffffffffu, md, o));
+        mu = fmax(mu, __shfl_down_sync(0xffffffffu, mu, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh_d[w] = md;
+        sh_u[w] = mu;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            md = fmax(md, sh_d[i]);
+            mu = fmax(mu, sh_u[i]);
+        }
+        mx_partial[2 * blockIdx.x] = md;
+        mx_partial[2 * blockIdx.x + 1] = mu;
+    }
+}
+
+// Phi^T R with every thread busy: per tile of kTile rows the CTA stages Phi
+// (a linear, coalesced copy: Phi is row-major) and R (one row per thread) in
+// shared memory; thread t then owns a 4 x 8 output tile o = t % NO and a row
+// group g = t / NO, accumulating its rows in registers; the NG group partials
+// of each output meet in a fixed order at the end (deterministic).
+constexpr int kTile = 256;
+__global__ void __launch_bounds__(256) ac_rhs2_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
+                                                      const double* __restrict__ U, const double* __restrict__ F,
+                                                      const double* __restrict__ fid, double c_dt, double dt_2eps,
+                                                      double dt, double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    double* Pt = sm;                  // kTile x k
+    double* Rt = sm + kTile * k;      // kTile x m (reused for the group reduction)
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    const int ta = (k + 3) / 4, tc = (m + 7) / 8;
+    const int NO = ta * tc, NG = blockDim.x / NO;
+    const int o = threadIdx.x % NO, g = threadIdx.x / NO;
+    const bool live = g < NG;
+    const int a0 = (o / tc) * 4, c0 = (o % tc) * 8;
+    double acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += kTile) {
+        const int rows = (int)min((int64_t)kTile, r1 - t0);
+        for (int e = threadIdx.x; e < rows * k; e += blockDim.x) Pt[e] = __ldg(Phi + t0 * k + e);
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+            const int64_t i = t0 + r;
+            double u[kAcMaxM], t[kAcMaxM];
+            for (int q = 0; q < m; ++q) u[q] = U[i * m + q];
+            well_force_row(u, m, t);
+            const double fi = fid[i];
+            for (int q = 0; q < m; ++q) Rt[r * m + q] = c_dt * u[q] - dt_2eps * t[q] - dt * fi * (u[q] - F[i * m + q]);
+        }
+        __syncthreads();
+        if (live) {
+            for (int r = g; r < rows; r += NG) {
+                double pa[4], rc[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pa[i] = (a0 + i < k) ? Pt[r * k + a0 + i] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) rc[j] = (c0 + j < m) ? Rt[r * m + c0 + j] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fma(pa[i], rc[j], acc[i][j]);
+            }
+        }
+        __syncthreads();
+    }
+    // group reduction in fixed order: red[g][o][32]
+    double* red = sm;  // NG * NO * 32 <= 256 * 32 doubles
+    if (live)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) red[((size_t)g * NO + o) * 32 + i * 8 + j] = acc[i][j];
+    __syncthreads();
+    const int nout = k * m;
+    for (int e = threadIdx.x; e < nout; e += blockDim.x) {
+        const int a = e / m, c = e % m;
+        const int oo = (a / 4) * tc + c / 8, slot = (a % 4) * 8 + (c % 8);
+        double sum = 0.0;
+        for (int gg = 0; gg < NG; ++gg) sum += red[((size_t)gg * NO + oo) * 32 + slot];
+        partial[(int64_t)blockIdx.x * nout + e] = sum;
+    }
+}
+
+// one warp per output: lanes sum strided block partials, then a fixed
+// shuffle tree (deterministic; no serial 296-long chain)
 __global__ void ac_finish_kernel(const double* __restrict__ partial, int nb, int k, int m,
                                  const double* __restrict__ denom, double* __restrict__ Vc) {
-    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    const int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (o >= k * m) return;
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * k * m + o];
-    Vc[o] = s / denom[o / m];
+    for (int b = lane; b < nb; b += 32) s += partial[(int64_t)b * k * m + o];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) Vc[o] = s / denom[o / m];
 }
 
 __global__ void ac_update_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
@@ -176,14 +477,23 @@ __global__ void ac_update_kernel(const double* __restrict__ Phi, int64_t n, int 
 }
 
 __global__ void ac_max_finish(const double* __restrict__ mx_partial, int nb, double* __restrict__ stats) {
-    if (threadIdx.x != 0) return;
+    // one warp: strided maxima then a shuffle tree (max is order-independent)
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32) return;
     double md = 0.0, mu = 0.0;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = lane; b < nb; b += 32) {
         md = fmax(md, mx_partial[2 * b]);
         mu = fmax(mu, mx_partial[2 * b + 1]);
     }
-    stats[0] = md;
-    stats[1] = mu;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        md = fmax(md, __shfl_down_sync(0xffffffffu, md, off));
+        mu = fmax(mu, __shfl_down_sync(0xffffffffu, mu, off));
+    }
+    if (lane == 0) {
+        stats[0] = md;
+        stats[1] = mu;
+    }
 }
 
 // ---- binary scheme (allencahn.py:261-309): scalar scores u = Phi v ------
@@ -220,17 +530,25 @@ __global__ void bac_rhs_kernel(const double* __restrict__ Phi, int64_t n, int k,
 __global__ void bac_finish_kernel(const double* __restrict__ partial, int nb, int k, const double* __restrict__ v,
                                   const double* __restrict__ denom, double lead, double dt_eps, double dt,
                                   double* __restrict__ v_next) {
-    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per coefficient: strided block partials + a fixed shuffle tree
+    const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (a >= k) return;
     double g1 = 0.0, g2 = 0.0;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = lane; b < nb; b += 32) {
         g1 += partial[(int64_t)b * 2 * k + a];
         g2 += partial[(int64_t)b * 2 * k + k + a];
     }
-    double rhs = lead * v[a];
-    rhs -= dt_eps * g1;
-    rhs -= dt * g2;
-    v_next[a] = rhs / denom[a];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        g1 += __shfl_down_sync(0xffffffffu, g1, off);
+        g2 += __shfl_down_sync(0xffffffffu, g2, off);
+    }
+    if (lane == 0) {
+        double rhs = lead * v[a];
+        rhs -= dt_eps * g1;
+        rhs -= dt * g2;
+        v_next[a] = rhs / denom[a];
+    }
 }
 
 __global__ void bac_update_kernel(const double* __restrict__ Phi, int64_t n, int k, const double* __restrict__ v,
@@ -422,18 +740,39 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
     if (m < 2 || m > kAcMaxM) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels support 2 <= m <= 32 classes");
     if (k < 1 || k * m > 16 * 256) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels need k*m <= 4096");
     cudaStream_t st = (cudaStream_t)stream;
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kAcBlocks, (n + kAcRows - 1) / kAcRows));
+    // row partition: ~1k rows per CTA, between one and six CTAs per SM
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(
+        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(148, n / 1024))));
     double* partial = work;
     double* mx = work + (int64_t)kAcBlocks * k * m;
     double* Vc = mx + 2 * kAcBlocks;
-    const size_t sm1 = (size_t)kAcRows * (m + k) * sizeof(double);
-    MLB_CUDA_TRY(cudaFuncSetAttribute(ac_rhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-    ac_rhs_kernel<<<nb, 256, sm1, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
-    note_launches(1);
-    ac_finish_kernel<<<(k * m + 127) / 128, 128, 0, st>>>(partial, nb, k, m, denom, Vc);
-    note_launches(1);
-    ac_update_kernel<<<nb, 256, (size_t)k * m * sizeof(double), st>>>(Phi, n, k, m, Vc, U, U_next, mx);
-    note_launches(1);
+    const size_t sm1 = std::max((size_t)256 * (k + 2 * m), (size_t)256 * 32) * sizeof(double);
+    const size_t sm3 = ((size_t)((k * m + 1) & ~1) + (size_t)256 * (k + m)) * sizeof(double);
+    if (std::max(sm1, sm3) > 200 * 1024) return fail(MLB_ERR_CONFIG, "Allen-Cahn tiles too large (k, m)");
+    auto run = [&](auto rhs, auto upd) -> int {
+        MLB_CUDA_TRY(cudaFuncSetAttribute(rhs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+        MLB_CUDA_TRY(cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
+        rhs<<<nb, 256, sm1, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
+        ac_finish_kernel<<<(k * m * 32 + 255) / 256, 256, 0, st>>>(partial, nb, k, m, denom, Vc);
+        upd<<<nb, 256, sm3, st>>>(Phi, n, k, m, Vc, U, U_next, mx);
+        return MLB_OK;
+    };
+    int rc;
+    if (m <= 4) {
+        rc = run(ac_rhs3_kernel<4>, ac_update3_kernel<4>);
+    } else if (m <= 8) {
+        rc = run(ac_rhs3_kernel<8>, ac_update3_kernel<8>);
+    } else {
+        // many classes: the register-resident row kernels would spill; generic kernels
+        const size_t sm2 = std::max((size_t)kTile * (m + k), (size_t)256 * 32) * sizeof(double);
+        MLB_CUDA_TRY(cudaFuncSetAttribute(ac_rhs2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+        ac_rhs2_kernel<<<nb, 256, sm2, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
+        ac_finish_kernel<<<(k * m * 32 + 255) / 256, 256, 0, st>>>(partial, nb, k, m, denom, Vc);
+        ac_update_kernel<<<nb, 256, (size_t)k * m * sizeof(double), st>>>(Phi, n, k, m, Vc, U, U_next, mx);
+        rc = MLB_OK;
+    }
+    if (rc != MLB_OK) return rc;
+    note_launches(3);
     ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
@@ -451,7 +790,7 @@ int mlb_bac_step(const double* Phi, int64_t n, int k, const double* u, const dou
     const size_t sm1 = (size_t)kAcRows * (2 + k) * sizeof(double);
     MLB_CUDA_TRY(cudaFuncSetAttribute(bac_rhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     bac_rhs_kernel<<<nb, 256, sm1, st>>>(Phi, n, k, u, f, fid, partial);
-    bac_finish_kernel<<<(k + 127) / 128, 128, 0, st>>>(partial, nb, k, v, denom, lead, dt_eps, dt, v_next);
+    bac_finish_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(partial, nb, k, v, denom, lead, dt_eps, dt, v_next);
     bac_update_kernel<<<nb, 256, (size_t)k * sizeof(double), st>>>(Phi, n, k, v_next, u, u_next, mx);
     ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
     note_launches(4);

@@ -1,0 +1,57 @@
+"""Allen-Cahn iteration throughput vs the HBM roofline.
+
+    python tools/bench_ac.py [--n 262144] [--k 20] [--m 5] [--iters 50]
+
+Per iteration the algorithmic traffic is the two passes over Phi (n k 8 B
+each) plus U, F (read), fid (read) and U_next (write): 8 n (2k + 3m + 1) B.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=262144)
+    ap.add_argument("--k", type=int, default=20)
+    ap.add_argument("--m", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=50)
+    args = ap.parse_args()
+    from paper_2007_05239_b200 import AllenCahnParams, LabelData, SpectralBasis, allen_cahn_solve
+    rng = np.random.default_rng(0)
+    n, k, m = args.n, args.k, args.m
+    phi = torch.from_numpy(np.linalg.qr(rng.standard_normal((n, k)))[0]).cuda()
+    vals = np.sort(rng.uniform(0.5, 1.5, k))
+    ids = rng.integers(0, m, n)
+    ids[rng.random(n) > 0.05] = -1
+    labels = LabelData.from_class_ids(ids, m, 1000.0)
+    basis = SpectralBasis(values=vals, vectors=phi)
+    # per-iteration time = difference of two runs (the setup -- initial scores,
+    # host->device copies of F and the fidelity -- cancels)
+    allen_cahn_solve(basis, labels, AllenCahnParams(tolerance=0.0, max_iter=3), return_device=True)
+    times = []
+    for iters in (args.iters, 2 * args.iters):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = allen_cahn_solve(basis, labels, AllenCahnParams(tolerance=0.0, max_iter=iters), return_device=True)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    dt = (times[1] - times[0]) / args.iters
+    nbytes = 8 * n * (2 * k + 3 * m + 1)
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6548.5) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6548.5
+    print(json.dumps({"n": n, "k": k, "m": m, "iterations": res.iterations, "ms_per_iter": dt * 1e3,
+                      "algorithmic_GB_per_iter": nbytes / 1e9, "achieved_GBps": nbytes / dt / 1e9,
+                      "hbm_frac": nbytes / dt / 1e9 / hbm}))
+
+
+if __name__ == "__main__":
+    main()
