@@ -190,6 +190,13 @@ int64_t mlb_ac_work_size(int64_t n, int k, int m);
 int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, const double* F,
                 const double* fid, const double* denom, double c_dt, double dt_2eps, double dt,
                 double* U_next, double* stats, double* work, void* stream);
+/* the same step with one pass over Phi (m <= 8): the update of iteration t and
+   the right-hand side of iteration t+1 share the staged Phi tile; first = 1 on
+   the first call of a solve (it also forms R(U_0)); the right-hand side stays
+   in `work` between calls (m > 8: the two-pass mlb_ac_step) */
+int mlb_ac_step2(const double* Phi, int64_t n, int k, int m, const double* U, const double* F, const double* fid,
+                 const double* denom, double c_dt, double dt_2eps, double dt, int first, double* U_next,
+                 double* stats, double* work, void* stream);
 /* one binary Allen-Cahn step (allencahn.py:261-309): v_next = (lead v - dt/eps Phi^T u^3
    - dt Phi^T (fid (u - f))) / denom, u_next = Phi v_next; stats = (max (u_next-u)^2, max u_next^2);
    work: mlb_ac_work_size(n, k, 1) doubles */

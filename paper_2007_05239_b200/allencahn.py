@@ -4,9 +4,10 @@ One convexity-splitting iteration (allencahn.py:172-223):
     R  = (1 + c dt) U - dt/(2 eps) T(U) - dt omega (U - F)
     Vc = Phi^T R / (1 + c dt + eps dt lambda)
     U+ = proj_simplex(Phi Vc)
-runs as the libmlb kernel sequence mlb_ac_step (rows of U, F, Phi streamed
-once per pass; fixed-order Phi^T R reduction); the host only reads the two
-maxima of the stopping rule each iteration.
+runs as the libmlb kernel sequence mlb_ac_step2: one pass over Phi per
+iteration (the projection of iteration t and the right-hand side of t+1
+share the staged, double-buffered Phi tile; fixed-order Phi^T R reduction);
+the host only reads the two maxima of the stopping rule each iteration.
 """
 
 import ctypes as C
@@ -136,9 +137,9 @@ def allen_cahn_solve(basis, labels, params, callback=None, device=None, return_d
     converged = False
     iterations = 0
     for it in range(1, params.max_iter + 1):
-        _lib.check(lib.mlb_ac_step(_lib.ptr(Phi), n, k, m, _lib.ptr(U), _lib.ptr(F), _lib.ptr(fid),
-                                   _lib.ptr(denom), 1.0 + c * dt, dt / (2.0 * eps), dt, _lib.ptr(Un),
-                                   _lib.ptr(stats), _lib.ptr(work), _lib.stream_ptr()))
+        _lib.check(lib.mlb_ac_step2(_lib.ptr(Phi), n, k, m, _lib.ptr(U), _lib.ptr(F), _lib.ptr(fid),
+                                    _lib.ptr(denom), 1.0 + c * dt, dt / (2.0 * eps), dt, int(it == 1), _lib.ptr(Un),
+                                    _lib.ptr(stats), _lib.ptr(work), _lib.stream_ptr()))
         num, den = stats.cpu().numpy()
         if den <= 0 or not np.isfinite(num):
             raise NumericalError("Allen-Cahn iterate degenerated")

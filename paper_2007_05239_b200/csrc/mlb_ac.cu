@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include "mlb_internal.cuh"
+#include "mlb_tma.cuh"
 
 namespace mlb {
 
@@ -311,6 +312,170 @@ __global__ void __launch_bounds__(256) ac_update3_kernel(const double* __restric
         sh_u[w] = mu;
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            md = fmax(md, sh_d[i]);
+            mu = fmax(mu, sh_u[i]);
+        }
+        mx_partial[2 * blockIdx.x] = md;
+        mx_partial[2 * blockIdx.x + 1] = mu;
+    }
+}
+
+// One pass over Phi per iteration: the update of iteration t (U -> U_next)
+// and the right-hand side of iteration t+1 (R(U_next), Phi^T R) share the
+// staged Phi tile.  Per tile: stage Phi, U, F; per row: y = Phi_i Vc,
+// simplex projection, the stopping maxima, then R(U_next); write U_next;
+// accumulate Phi^T R in register tiles (the same partition and order as
+// ac_rhs3, so the iterates are those of the two-pass step).
+template <int MM>
+__global__ void __launch_bounds__(256, 2) ac_fused_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
+                                                          const double* __restrict__ Vc,
+                                                          const double* __restrict__ U,
+                                                          const double* __restrict__ F,
+                                                          const double* __restrict__ fid, double c_dt,
+                                                          double dt_2eps, double dt, double* __restrict__ Un,
+                                                          double* __restrict__ mx_partial,
+                                                          double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    constexpr int T = 256;
+    constexpr int TC = MM < 8 ? MM : 8;
+    // two stage buffers (tile t computes while tile t+1 loads by cp.async)
+    double* vsh = sm;                               // k x m
+    double* Rt = vsh + ((k * m + 1) & ~1);          // T x m
+    double* buf0 = Rt + T * m;                      // [Pt T x k | Ut T x m | Ft T x m]
+    const int bstride = T * (k + 2 * m);
+    __shared__ double sh_d[8], sh_u[8];
+    for (int e = threadIdx.x; e < k * m; e += blockDim.x) vsh[e] = Vc[e];
+    const int nb = gridDim.x;
+    const int64_t per = (n + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    const int ta = (k + 3) / 4, tc = (m + TC - 1) / TC;
+    const int NO = ta * tc, NG = blockDim.x / NO;
+    const int o = threadIdx.x % NO, g = threadIdx.x / NO;
+    const bool live = g < NG;
+    const int a0 = (o / tc) * 4, c0 = (o % tc) * TC;
+    double acc[4][TC];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
+    double md = 0.0, mu = 0.0;
+    auto stage = [&](int64_t ts, double* bf) {
+        const int rows = (int)min((int64_t)T, r1 - ts);
+        double* P = bf;
+        double* Uu = bf + T * k;
+        double* Ff = Uu + T * m;
+        for (int e = threadIdx.x; e < rows * k; e += blockDim.x) cp_async8(P + e, Phi + ts * k + e);
+        for (int e = threadIdx.x; e < rows * m; e += blockDim.x) {
+            cp_async8(Uu + e, U + ts * m + e);
+            cp_async8(Ff + e, F + ts * m + e);
+        }
+        cp_async_commit();
+    };
+    if (r0 < r1) stage(r0, buf0);
+    int bsel = 0;
+    for (int64_t t0 = r0; t0 < r1; t0 += T) {
+        const int rows = (int)min((int64_t)T, r1 - t0);
+        double* Pt = buf0 + bsel * bstride;
+        double* Ut = Pt + T * k;
+        double* Ft = Ut + T * m;
+        cp_async_wait_all();
+        __syncthreads();  // tile t landed; the previous tile's readers are done
+        if (t0 + T < r1) stage(t0 + T, buf0 + (bsel ^ 1) * bstride);
+        if (threadIdx.x < rows) {
+            const int r = threadIdx.x;
+            double y[MM];
+#pragma unroll
+            for (int c = 0; c < MM; ++c) y[c] = 0.0;
+            for (int a = 0; a < k; ++a) {
+                const double p = Pt[r * k + a];
+#pragma unroll
+                for (int c = 0; c < MM; ++c)
+                    if (c < m) y[c] = fma(p, vsh[a * m + c], y[c]);
+            }
+            double s[MM];
+#pragma unroll
+            for (int c = 0; c < MM; ++c) s[c] = (c < m) ? y[c] : -INFINITY;
+            sort_desc<MM>(s);
+            double cs = 0.0, cs_rho = 0.0;
+            int rho = 0;
+#pragma unroll
+            for (int j = 0; j < MM; ++j) {
+                if (j < m) {
+                    cs += s[j];
+                    if (s[j] + (1.0 - cs) / (j + 1) > 0) {
+                        rho = j;
+                        cs_rho = cs;
+                    }
+                }
+            }
+            const double tau = (1.0 - cs_rho) / (rho + 1);
+            double un[MM];
+            double dd = 0.0, uu = 0.0;
+#pragma unroll
+            for (int c = 0; c < MM; ++c) {
+                un[c] = (c < m) ? fmax(y[c] + tau, 0.0) : 0.0;
+                if (c < m) {
+                    const double df = un[c] - Ut[r * m + c];
+                    dd = fma(df, df, dd);
+                    uu = fma(un[c], un[c], uu);
+                    Ut[r * m + c] = un[c];
+                }
+            }
+            md = fmax(md, dd);
+            mu = fmax(mu, uu);
+            // next iteration's right-hand side row
+            double t[MM];
+            well_force_t<MM>(un, m, t);
+            const double fi = __ldg(fid + t0 + r);
+#pragma unroll
+            for (int q = 0; q < MM; ++q)
+                if (q < m) Rt[r * m + q] = c_dt * un[q] - dt_2eps * t[q] - dt * fi * (un[q] - Ft[r * m + q]);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < rows * m; e += blockDim.x) Un[t0 * m + e] = Ut[e];
+        if (live) {
+            for (int r = g; r < rows; r += NG) {
+                double pa[4], rc[TC];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pa[i] = (a0 + i < k) ? Pt[r * k + a0 + i] : 0.0;
+#pragma unroll
+                for (int j = 0; j < TC; ++j) rc[j] = (c0 + j < m) ? Rt[r * m + c0 + j] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < TC; ++j) acc[i][j] = fma(pa[i], rc[j], acc[i][j]);
+            }
+        }
+        bsel ^= 1;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double* red = sm;
+    if (live)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < TC; ++j) red[((size_t)g * NO + o) * (4 * TC) + i * TC + j] = acc[i][j];
+    for (int off = 16; off > 0; off >>= 1) {
+        md = fmax(md, __shfl_down_sync(0xffffffffu, md, off));
+        mu = fmax(mu, __shfl_down_sync(0xffffffffu, mu, off));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh_d[w] = md;
+        sh_u[w] = mu;
+    }
+    __syncthreads();
+    const int nout = k * m;
+    for (int e = threadIdx.x; e < nout; e += blockDim.x) {
+        const int a = e / m, c = e % m;
+        const int oo = (a / 4) * tc + c / TC, slot = (a % 4) * TC + (c % TC);
+        double sum = 0.0;
+        for (int gg = 0; gg < NG; ++gg) sum += red[((size_t)gg * NO + oo) * (4 * TC) + slot];
+        partial[(int64_t)blockIdx.x * nout + e] = sum;
+    }
     if (threadIdx.x == 0) {
         for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
             md = fmax(md, sh_d[i]);
@@ -775,6 +940,43 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
     note_launches(3);
     ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
     note_launches(1);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_ac_step2(const double* Phi, int64_t n, int k, int m, const double* U, const double* F, const double* fid,
+                 const double* denom, double c_dt, double dt_2eps, double dt, int first, double* U_next,
+                 double* stats, double* work, void* stream) {
+    if (m > 8) {  // many classes: the two-pass step
+        return mlb_ac_step(Phi, n, k, m, U, F, fid, denom, c_dt, dt_2eps, dt, U_next, stats, work, stream);
+    }
+    if (m < 2) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels support 2 <= m <= 32 classes");
+    if (k < 1 || k * m > 16 * 256) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels need k*m <= 4096");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(
+        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(148, n / 1024))));
+    double* partial = work;
+    double* mx = work + (int64_t)kAcBlocks * k * m;
+    double* Vc = mx + 2 * kAcBlocks;
+    const size_t sm1 = std::max((size_t)256 * (k + 2 * m), (size_t)256 * 32) * sizeof(double);
+    const size_t smf = std::max((size_t)((k * m + 1) & ~1) + (size_t)256 * (2 * k + 5 * m), (size_t)256 * 32) *
+                       sizeof(double);
+    if (std::max(sm1, smf) > 200 * 1024) return fail(MLB_ERR_CONFIG, "Allen-Cahn tiles too large (k, m)");
+    auto run = [&](auto rhs, auto fused) -> int {
+        if (first) {  // R(U_0) and Phi^T R once; afterwards the fused kernel provides them
+            MLB_CUDA_TRY(cudaFuncSetAttribute(rhs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+            rhs<<<nb, 256, sm1, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
+            note_launches(1);
+        }
+        MLB_CUDA_TRY(cudaFuncSetAttribute(fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
+        ac_finish_kernel<<<(k * m * 32 + 255) / 256, 256, 0, st>>>(partial, nb, k, m, denom, Vc);
+        fused<<<nb, 256, smf, st>>>(Phi, n, k, m, Vc, U, F, fid, c_dt, dt_2eps, dt, U_next, mx, partial);
+        ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
+        note_launches(3);
+        return MLB_OK;
+    };
+    const int rc = (m <= 4) ? run(ac_rhs3_kernel<4>, ac_fused_kernel<4>) : run(ac_rhs3_kernel<8>, ac_fused_kernel<8>);
+    if (rc != MLB_OK) return rc;
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
