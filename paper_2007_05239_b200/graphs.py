@@ -11,6 +11,7 @@ Vectors may be numpy arrays (copied to / from the device -- the reference's
 calling convention) or float64 CUDA tensors (stay on the device).
 """
 
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -352,6 +353,15 @@ class MultilayerGraph:
         return MultilayerGraph(tuple(self.layers[i] for i in layer_indices))
 
 
+def _layer_cost(layer):
+    """Relative cost of one L_sym apply of a layer: n (2m+1)^d for NFFT layers."""
+    w = layer.weights
+    plan = getattr(w, "plan", None)
+    if plan is not None:
+        return layer.n * (2 * plan.m_nfft + 1) ** plan.d
+    return layer.n
+
+
 class LaplacianBatch:
     """Every layer's normalized Laplacian applied to one vector: the
     independent layers run on their own CUDA streams (fork / join on the
@@ -375,7 +385,13 @@ class LaplacianBatch:
         with torch.cuda.device(dev):
             self._v = torch.empty(self.n, dtype=torch.float64, device=dev)
             self._y = torch.empty((self.T, self.n), dtype=torch.float64, device=dev)
-            self._streams = [torch.cuda.Stream(device=dev) for _ in graph.layers]
+            # the costliest layer (the step's critical path) gets the highest
+            # stream priority; cheaper layers fill the SMs it leaves idle
+            cost = [_layer_cost(layer) for layer in graph.layers]
+            top = max(range(len(cost)), key=lambda i: cost[i])
+            prio = os.environ.get("MLB_NO_STREAM_PRIORITY") is None
+            self._streams = [torch.cuda.Stream(device=dev, priority=(-1 if (prio and i == top) else 0))
+                             for i in range(len(graph.layers))]
             self._fork = torch.cuda.Event()
             self._joins = [torch.cuda.Event() for _ in graph.layers]
         self._pin_in = None
