@@ -649,7 +649,7 @@ int mlb_convolve(mlb_binding* b, const double* gin, double* gout, void* stream) 
 int mlb_gather(mlb_binding* b, const double* grid, double* y, unsigned flags, void* stream) {
     if (!b || !grid || !y) return fail(MLB_ERR_ARG, "null argument");
     DeviceGuard guard(b->plan->device);
-    return launch_gather(b, grid, nullptr, y, 0.0, 1.0, 0.0, flags & (MLB_SORTED | MLB_ACCUMULATE | 0x30000u),
+    return launch_gather(b, grid, nullptr, y, 0.0, 1.0, 0.0, flags & (MLB_SORTED | MLB_ACCUMULATE | 0x70000u),
                          (cudaStream_t)stream);
 }
 

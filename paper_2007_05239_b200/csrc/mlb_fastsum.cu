@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         const double fB1 = (D >= 2 && okB) ? __ldg(a.frac + a.n + pB) : 0.5;
         const double fA2 = (D == 3 && okA) ? __ldg(a.frac + 2 * a.n + pA) : 0.5;
         const double fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
-        if (gbase != cur) {
+        if (gbase != cur && !(flags & (1u << 18))) {  // bit 18: ablation (profiling only): no restaging
             __syncwarp();
             constexpr int NSRC = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
             for (int e = lane; e < NSRC; e += 32) {

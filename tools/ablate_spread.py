@@ -31,7 +31,8 @@ lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD, _lib.stream
 lib.mlb_convolve(b.ptr, _lib.ptr(grid), _lib.ptr(grid2), _lib.stream_ptr())
 y = torch.empty_like(v)
 for name, bits in [("gather full", 0), ("gather no-contraction", 1 << 16), ("gather no-windows", 1 << 17),
-                   ("gather none", (1 << 16) | (1 << 17))]:
+                   ("gather none", (1 << 16) | (1 << 17)), ("gather none+no-staging", (1 << 16) | (1 << 17) | (1 << 18)),
+                   ("gather no-staging", 1 << 18)]:
     for _ in range(3):
         lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), bits, _lib.stream_ptr())
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
