@@ -53,7 +53,10 @@ struct SpreadCfg<3, M> {
     static constexpr int S = 2 * M + 1;
     static constexpr int P0 = S, P1 = 32 / S, P2 = 1;
     static constexpr int B0 = 1, B1 = (S + P1 - 1) / P1;
-    static constexpr int NPASS = (B1 * S <= 36) ? 1 : ((B1 * ((S + 1) / 2) <= 36) ? 2 : 3);
+    // m >= 5 runs one 8-warp CTA per SM (shared memory), so it can hold 72
+    // accumulators per lane: fewer passes = fewer window evaluations
+    static constexpr int ACC = (M >= 5) ? 72 : 36;
+    static constexpr int NPASS = (B1 * S <= ACC) ? 1 : ((B1 * ((S + 1) / 2) <= ACC) ? 2 : 3);
     static constexpr int SP = (S + NPASS - 1) / NPASS;  // cells of axis 2 per pass
     static constexpr int B2 = SP;
 };
@@ -386,13 +389,14 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
 // two sub-chunks ahead (stream entries, point indices) and one ahead
 // (coordinates, D^-1/2, v) across item boundaries.
 template <int M>
-__global__ void __launch_bounds__(256, 2) spread_cells_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v,
+__global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v,
                                                               unsigned flags) {
     using C = SpreadCfg<3, M>;
     constexpr int S = C::S;
     constexpr int SPAD = StageCfg<3, M>::pad;
-    constexpr int STG = 32 * 3 * SPAD;        // staging doubles per warp
     constexpr int NRED = S * S * C::SP;       // one pass slice of a block
+    // staging doubles per warp: >= one block slice, even (16-byte aligned rows)
+    constexpr int STG = (((32 * 3 * SPAD > NRED) ? 32 * 3 * SPAD : NRED) + 1) & ~1;
     extern __shared__ __align__(16) double smem[];
     double* red = smem + kCellWarps * STG;     // kCellWarps x NRED
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1039,8 +1043,9 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         return MLB_OK;
     } else {
         using C3 = SpreadCfg<3, M>;
-        const size_t smem = (size_t)kCellWarps *
-                            (32 * 3 * StageCfg<3, M>::pad + (size_t)C3::S * C3::S * C3::SP) * sizeof(double);
+        const size_t nred = (size_t)C3::S * C3::S * C3::SP;
+        const size_t stg = (std::max<size_t>(32 * 3 * StageCfg<3, M>::pad, nred) + 1) & ~(size_t)1;
+        const size_t smem = (size_t)kCellWarps * (stg + nred) * sizeof(double);
         if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread staging too large for shared memory");
         auto kern3 = spread_cells_kernel<M>;
         static bool attr = false;
