@@ -318,7 +318,9 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     std::vector<int32_t> cblk, wstream, wstream_off, citem, citem_off, brick_blk, active_brick, merge_off, merge_pairs;
     int ncta_cells = 0;
     if (d == 3 && n > 0) {
-        int cap = 1024;
+        // points per block: >= 1024, and at large n about one CTA's share, so
+        // a heavy cell splits into few parts (every part is a merge row set)
+        int cap = (int)std::max<int64_t>(1024, ((n / (148 * 2)) + 31) / 32 * 32);
         if (const char* env = std::getenv("MLB_CELL_CAP")) cap = std::max(32, std::atoi(env) / 32 * 32);  // tuning
         brick_blk.assign(nbricks + 1, 0);
         for (int64_t k = 0; k < nkeys; ++k) {
