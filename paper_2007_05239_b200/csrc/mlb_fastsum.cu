@@ -402,7 +402,11 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* stage = smem + warp * STG;
     const int l0 = lane / C::P1, l1 = lane % C::P1;
-    const bool active = lane < C::P0 * C::P1;
+    // m = 5: lanes own PPL consecutive (o0, o1) pairs (one pass, 31 of 32
+    // lanes busy) instead of the (o0, o1-block) split (22 lanes)
+    constexpr bool PAIRS = (M == 5);
+    constexpr int PPL = (S * S + 31) / 32;
+    const bool active = PAIRS ? (lane * PPL < S * S) : (lane < C::P0 * C::P1);
     const bool sorted = (flags & MLB_SORTED) != 0;
     const bool use_isd = (flags & MLB_USE_ISD) != 0;
     for (int i = lane; i < STG; i += 32) stage[i] = 0.0;
@@ -487,13 +491,35 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
                         for (int k = 0; k < C::SP; ++k) acc[jj][k] = fma(w01, w2[k], acc[jj][k]);
                     }
                 };
-                double a0, a1[C::B1], a2[C::SP], b0, b1[C::B1], b2[C::SP];
-                ldw(0, a0, a1, a2);
-                for (int j = 0; j < np; j += 2) {  // rows past np carry v = 0
-                    ldw(j + 1, b0, b1, b2);
-                    acc_pt(a0, a1, a2);
-                    ldw(min(j + 2, 31), a0, a1, a2);
-                    acc_pt(b0, b1, b2);
+                if constexpr (PAIRS) {
+                    static_assert(C::NPASS == 1 && C::B1 >= PPL, "pair path: one pass, acc rows >= pairs");
+                    for (int j = 0; j < np; ++j) {  // rows past np carry v = 0
+                        const double* ws = stage + j * 3 * SPAD;
+                        double w2[S];
+#pragma unroll
+                        for (int k = 0; k + 1 < S; k += 2) {
+                            const double2 t = *reinterpret_cast<const double2*>(ws + 2 * SPAD + k);
+                            w2[k] = t.x;
+                            w2[k + 1] = t.y;
+                        }
+                        w2[S - 1] = ws[2 * SPAD + S - 1];
+#pragma unroll
+                        for (int i = 0; i < PPL; ++i) {
+                            const int q = min(lane * PPL + i, S * S - 1);
+                            const double w01 = ws[q / S] * ws[SPAD + q % S];
+#pragma unroll
+                            for (int k = 0; k < S; ++k) acc[i][k] = fma(w01, w2[k], acc[i][k]);
+                        }
+                    }
+                } else {
+                    double a0, a1[C::B1], a2[C::SP], b0, b1[C::B1], b2[C::SP];
+                    ldw(0, a0, a1, a2);
+                    for (int j = 0; j < np; j += 2) {  // rows past np carry v = 0
+                        ldw(j + 1, b0, b1, b2);
+                        acc_pt(a0, a1, a2);
+                        ldw(min(j + 2, 31), a0, a1, a2);
+                        acc_pt(b0, b1, b2);
+                    }
                 }
             }
             __syncwarp();
@@ -515,12 +541,20 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
                     static_assert(NRED <= STG, "block slice must fit the warp's staging");
                     __syncwarp();
                     if (active) {
-                        double* r = stage + l0 * S * C::SP;
+                        if constexpr (PAIRS) {
 #pragma unroll
-                        for (int jj = 0; jj < C::B1; ++jj)
+                            for (int i = 0; i < PPL; ++i)
+                                if (lane * PPL + i < S * S)
 #pragma unroll
-                            for (int k = 0; k < C::SP; ++k)
-                                if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                                    for (int k = 0; k < S; ++k) stage[(lane * PPL + i) * S + k] = acc[i][k];
+                        } else {
+                            double* r = stage + l0 * S * C::SP;
+#pragma unroll
+                            for (int jj = 0; jj < C::B1; ++jj)
+#pragma unroll
+                                for (int k = 0; k < C::SP; ++k)
+                                    if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                        }
                     }
                     __syncwarp();
                     double* out = a.blocks + (size_t)blk * (S * S * S);
@@ -533,12 +567,20 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
                 if (multi) {  // uniform over the CTA: multi-warp blocks meet in shared memory
                     __syncthreads();  // previous item's reduction reads of `red` are done
                     if (active && nwb > 1) {
-                        double* r = red + warp * NRED + l0 * S * C::SP;
+                        if constexpr (PAIRS) {
 #pragma unroll
-                        for (int jj = 0; jj < C::B1; ++jj)
+                            for (int i = 0; i < PPL; ++i)
+                                if (lane * PPL + i < S * S)
 #pragma unroll
-                            for (int k = 0; k < C::SP; ++k)
-                                if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                                    for (int k = 0; k < S; ++k) red[warp * NRED + (lane * PPL + i) * S + k] = acc[i][k];
+                        } else {
+                            double* r = red + warp * NRED + l0 * S * C::SP;
+#pragma unroll
+                            for (int jj = 0; jj < C::B1; ++jj)
+#pragma unroll
+                                for (int k = 0; k < C::SP; ++k)
+                                    if (l1 * C::B1 + jj < S) r[(l1 * C::B1 + jj) * C::SP + k] = acc[jj][k];
+                        }
                     }
                     __syncthreads();
                     for (int eb = 0; eb < nb; ++eb) {
