@@ -160,3 +160,16 @@ def test_binary_allen_cahn_and_energy_match_reference():
     assert abs(e - gb["energy_basis"][0]) <= 1e-12 * abs(gb["energy_basis"][0])
     e64 = so.gl_energy(gs["ac_scores"][:64], None, None, F[:64], fid[:64], 5e-3, L_dense=gb["L_dense64"])
     assert abs(e64 - gb["energy_dense64"][0]) <= 1e-12 * abs(gb["energy_dense64"][0])
+
+
+def test_parallel_reference_arm_matches_serial_oracle():
+    """bench.py's multi-process reference arm (oracle/parallel_ref.py) computes
+    the same shifted normalized-Laplacian matvecs as the serial oracle."""
+    from oracle.parallel_ref import check_against_serial
+    rng = np.random.default_rng(5)
+    hw = fo.box_halfwidth(1.0 / 16)
+    specs = []
+    for d, N in ((3, 16), (2, 32)):
+        pts = np.clip(0.05 * rng.standard_normal((700, d)), -hw, hw)
+        specs.append((fo.OraclePlan("gaussian", 0.12, d, N, 4, p=8), pts))
+    assert check_against_serial(specs, math.log(2.0), rng.standard_normal(700), procs=3) < 1e-13
