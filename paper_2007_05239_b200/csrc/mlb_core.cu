@@ -193,6 +193,8 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->chunk_start);
     dev_free(b->chunk_cell);
     dev_free(b->chunk_gcell);
+    dev_free(b->ggrp);
+    dev_free(b->gslot);
     dev_free(b->seg_chunk);
     dev_free(b->sub_desc);
     dev_free(b->cblk);
@@ -280,6 +282,66 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     }
     const int nch = (int)chunk_cell.size();
     chunk_start.push_back((int32_t)n);
+    // d = 3 gather groups: the points of one brick "pencil" (same brick and
+    // axis-0/1 cell, <= Tb consecutive axis-2 cells) packed into 32 lanes.
+    // Two-point groups pair points of the SAME cell in a lane (one staged
+    // value read feeds both); a pencil's last group holding <= 32 points is a
+    // one-point group.  Slot = sorted point | (axis-2 offset from the group's
+    // first staged cell) << 29, -1 = empty.  Packing across the pencil's cells
+    // fills the lanes that one-cell chunks leave idle on light cells.
+    std::vector<int32_t> ggrp, gslot;
+    if (d == 3 && n > 0) {
+        if (n >= ((int64_t)1 << 29)) return fail(MLB_ERR_CONFIG, "d = 3 bindings hold fewer than 2^29 points");
+        struct Lane { int32_t a, b; int dc; };
+        std::vector<Lane> lanes;
+        int lo = 0, hi = 0;  // the pencil's occupied axis-2 range: one staging serves all its groups
+        auto emit = [&](const std::vector<Lane>& ls, bool two) {
+            // grid index of the first staged cell: any member's cell minus its offset
+            const int32_t gb = cell_glob[perm[ls[0].a]] - (ls[0].dc - lo);
+            ggrp.push_back(gb);
+            ggrp.push_back((hi - lo + 1) | (two ? 256 : 0));
+            const size_t base = gslot.size();
+            gslot.resize(base + 64, -1);
+            for (size_t i = 0; i < ls.size(); ++i) {
+                gslot[base + i] = ls[i].a | ((ls[i].dc - lo) << 29);
+                if (ls[i].b >= 0) gslot[base + 32 + i] = ls[i].b | ((ls[i].dc - lo) << 29);
+            }
+        };
+        int64_t k = 0;
+        while (k < nkeys) {
+            const int64_t pen = k / Tb, kend = std::min<int64_t>(nkeys, (pen + 1) * Tb);
+            lanes.clear();
+            lo = 1 << 30;
+            hi = -1;
+            for (int64_t kk = k; kk < kend; ++kk) {
+                const int dc = (int)(kk % Tb);
+                if (cnt[kk + 1] > cnt[kk]) {
+                    lo = std::min(lo, dc);
+                    hi = std::max(hi, dc);
+                }
+                for (int64_t s = cnt[kk]; s < cnt[kk + 1]; s += 2)
+                    lanes.push_back({(int32_t)s, s + 1 < cnt[kk + 1] ? (int32_t)(s + 1) : -1, dc});
+            }
+            for (size_t g0 = 0; g0 < lanes.size(); g0 += 32) {
+                const size_t g1 = std::min(lanes.size(), g0 + 32);
+                std::vector<Lane> ls(lanes.begin() + g0, lanes.begin() + g1);
+                int pts = 0;
+                for (const Lane& l : ls) pts += 1 + (l.b >= 0);
+                if (g1 == lanes.size() && pts <= 32) {  // tail: one point per lane
+                    std::vector<Lane> one;
+                    for (const Lane& l : ls) {
+                        one.push_back({l.a, -1, l.dc});
+                        if (l.b >= 0) one.push_back({l.b, -1, l.dc});
+                    }
+                    emit(one, false);
+                } else {
+                    emit(ls, true);
+                }
+            }
+            k = kend;
+        }
+    }
+    const int ngrp = (int)(ggrp.size() / 2);
     // segments (one warp's work unit): <= kSegPoints points of one brick,
     // never splitting a chunk; a bit smaller when n is small so every SM
     // gets work
@@ -475,6 +537,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     b->plan = plan;
     b->n = n;
     b->nchunks = nch;
+    b->ngrp = ngrp;
     b->nseg = nseg;
     b->nbricks = nbricks;
     b->max_seg_chunks = seg_points;
@@ -513,6 +576,8 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         if (rc == MLB_OK) rc = dev_upload(&b->active_brick, active_brick.data(), active_brick.size());
         if (rc == MLB_OK) rc = dev_upload(&b->merge_off, merge_off.data(), merge_off.size());
         if (rc == MLB_OK) rc = dev_upload(&b->merge_pairs, merge_pairs.data(), std::max<size_t>(2, merge_pairs.size()));
+        if (rc == MLB_OK) rc = dev_upload(&b->ggrp, ggrp.data(), ggrp.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->gslot, gslot.data(), gslot.size());
         const int S = 2 * g.m + 1;
         if (rc == MLB_OK) rc = dev_upload<double>(&b->blocks, nullptr, (size_t)b->nblk * S * S * S);
     }

@@ -102,6 +102,9 @@ struct FsArgs {
     const int32_t* merge_off;
     const int32_t* merge_pairs;
     double* blocks;
+    const int2* ggrp;
+    const int32_t* gslot;
+    int ngrp;
     int tile_cells;
     int nchunks;
     int nseg;
@@ -312,6 +315,13 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
                     }
                 };
                 auto acc_pt = [&](const double* w0, const double* w1, const double* w2) {
+                    if constexpr (D == 2) {  // one FMA per stencil entry: acc += (s v w0) w1
+#pragma unroll
+                        for (int i = 0; i < C::B0; ++i)
+#pragma unroll
+                            for (int jj = 0; jj < C::B1; ++jj) acc[i][jj][0] = fma(w0[i], w1[jj], acc[i][jj][0]);
+                        return;
+                    }
 #pragma unroll
                     for (int i = 0; i < C::B0; ++i)
 #pragma unroll
@@ -872,12 +882,21 @@ __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restri
 // value read (a broadcast LDS: the whole chunk shares one cell) feeds two
 // FMAs.  Epilogue: y = alpha v + s (beta acc + gamma s v).
 template <int D, int M>
+struct GatherCfg {
+    static constexpr int S = 2 * M + 1;
+    // d = 3 stages a pencil: the neighbourhoods of <= Tb consecutive axis-2
+    // cells (Tb = 4, or 2 for m >= 6) share one (2m+1)^2 x (2m+Tb) block
+    static constexpr int SR = (D == 3) ? S + (M >= 6 ? 1 : 3) : S;
+    static constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * SR);
+};
+
+template <int D, int M>
 __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
                                                      const double* __restrict__ v, double* __restrict__ y,
                                                      double alpha, double beta, double gamma, unsigned flags) {
     constexpr int S = 2 * M + 1;
-    constexpr int SR = S;  // staged row length
-    constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * SR);
+    constexpr int SR = GatherCfg<D, M>::SR;  // staged row length (d = 3: a pencil of <= Tb cells)
+    constexpr int NB = GatherCfg<D, M>::NB;
     constexpr int W0S = 2 * S + 1;  // per-lane axis-0 window row (odd stride)
     extern __shared__ double nbs[];
     const int L = a.g.L;
@@ -886,38 +905,62 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     double* w0s = nbs + 8 * NB + (wl * 32 + lane) * W0S;  // [0,S): point A, [S,2S): point B
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwt = (gridDim.x * blockDim.x) >> 5;
-    const int c_lo = (int)(((long long)a.nchunks * gw) / nwt);
-    const int c_hi = (int)(((long long)a.nchunks * (gw + 1)) / nwt);
+    const int nunits = (D == 3) ? a.ngrp : a.nchunks;  // d = 3: pencil groups, else one-cell chunks
+    const int c_lo = (int)(((long long)nunits * gw) / nwt);
+    const int c_hi = (int)(((long long)nunits * (gw + 1)) / nwt);
     const int64_t rs = (D == 3) ? (int64_t)L * L : (int64_t)L;  // stride of axis 0
-    int cur = -1;
+    long long cur = -1;
     pdl_wait();  // the grid (convolution) and v come from stream predecessors
     for (int ch = c_lo; ch < c_hi; ++ch) {
-        const int p0 = a.chunk_start[ch];
-        const int np = a.chunk_start[ch + 1] - p0;
-        const int gbase = a.chunk_gcell[ch];
-        const bool okA = lane < np, okB = lane + 32 < np;
-        const bool two = np > 32;  // warp-uniform: chunks of <= 32 points skip the second point
-        const int pA = p0 + lane, pB = p0 + 32 + lane;
+        int gbase, wst = S, dcA = 0, pA, pB;
+        bool okA, okB, two;
+        if (D == 3) {
+            const int2 gg = __ldg(a.ggrp + ch);
+            const int sA = __ldg(a.gslot + (int64_t)ch * 64 + lane);
+            const int sB = __ldg(a.gslot + (int64_t)ch * 64 + 32 + lane);
+            gbase = gg.x;
+            wst = S - 1 + (gg.y & 255);  // staged cells along axis 2
+            two = (gg.y >> 8) != 0;      // warp-uniform: one-point groups skip the second point
+            okA = sA >= 0;
+            okB = sB >= 0;
+            pA = okA ? (sA & 0x1fffffff) : 0;
+            pB = okB ? (sB & 0x1fffffff) : 0;
+            dcA = okA ? (sA >> 29) : 0;  // a lane's two points share one cell
+        } else {
+            const int p0 = a.chunk_start[ch];
+            const int np = a.chunk_start[ch + 1] - p0;
+            gbase = a.chunk_gcell[ch];
+            okA = lane < np;
+            okB = lane + 32 < np;
+            two = np > 32;  // warp-uniform: chunks of <= 32 points skip the second point
+            pA = p0 + lane;
+            pB = p0 + 32 + lane;
+        }
+        const long long key = (long long)gbase * 16 + wst;
         // issue the point loads before (possibly) restaging the neighbourhood
         const double fA0 = okA ? __ldg(a.frac + pA) : 0.5, fB0 = okB ? __ldg(a.frac + pB) : 0.5;
         const double fA1 = (D >= 2 && okA) ? __ldg(a.frac + a.n + pA) : 0.5;
         const double fB1 = (D >= 2 && okB) ? __ldg(a.frac + a.n + pB) : 0.5;
         const double fA2 = (D == 3 && okA) ? __ldg(a.frac + 2 * a.n + pA) : 0.5;
         const double fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
-        if (gbase != cur && !(flags & (1u << 18))) {  // bit 18: ablation (profiling only): no restaging
+        if (key != cur && !(flags & (1u << 18))) {  // bit 18: ablation (profiling only): no restaging
             __syncwarp();
-            constexpr int NSRC = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
-            for (int e = lane; e < NSRC; e += 32) {
-                int64_t off;
-                if (D == 1) off = e;
-                else if (D == 2) off = (e / S) * rs + e % S;
-                else off = (e / (S * S)) * rs + ((e / S) % S) * (int64_t)L + e % S;
-                const int dst = (D == 3) ? (e / S) * SR + e % S : e;
-                cp_async8(nb + dst, grid + gbase + off);
+            if (D == 3) {
+                // rows (i, j) of the pencil block; columns past the group's width are not read
+                for (int e = lane; e < S * S * SR; e += 32) {
+                    const int row = e / SR, col = e % SR;
+                    if (col < wst) cp_async8(nb + e, grid + gbase + (row / S) * rs + (row % S) * (int64_t)L + col);
+                }
+            } else {
+                constexpr int NSRC = (D == 1) ? S : S * S;
+                for (int e = lane; e < NSRC; e += 32) {
+                    const int64_t off = (D == 1) ? e : (e / S) * rs + e % S;
+                    cp_async8(nb + e, grid + gbase + off);
+                }
             }
             cp_async_wait_all();
             __syncwarp();
-            cur = gbase;
+            cur = key;
         }
         double wA0[S], wA1[S], wA2[S], wB0[S], wB1[S], wB2[S];
         if (flags & (1u << 17)) {  // ablation (profiling only): constant windows
@@ -970,7 +1013,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         } else if (!two) {
 #pragma unroll 1
             for (int i = 0; i < S; ++i) {
-                const double* gi = nb + i * S * SR;
+                const double* gi = nb + dcA + i * S * SR;
                 double rA = 0.0;
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
@@ -987,7 +1030,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         } else {
 #pragma unroll 1
             for (int i = 0; i < S; ++i) {
-                const double* gi = nb + i * S * SR;
+                const double* gi = nb + dcA + i * S * SR;
                 double rA = 0.0, rB = 0.0;
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
@@ -1043,6 +1086,9 @@ static FsArgs make_args(mlb_binding* b) {
     a.merge_off = b->merge_off;
     a.merge_pairs = b->merge_pairs;
     a.blocks = b->blocks;
+    a.ggrp = reinterpret_cast<const int2*>(b->ggrp);
+    a.gslot = b->gslot;
+    a.ngrp = b->ngrp;
     a.seg_sub = b->seg_sub;
     a.seg_chunk = b->seg_chunk;
     a.seg_brick = b->seg_brick;
@@ -1107,7 +1153,7 @@ template <int D, int M>
 static int gather_dm(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                      double beta, double gamma, unsigned flags, cudaStream_t st) {
     constexpr int S = 2 * M + 1;
-    constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
+    constexpr int NB = GatherCfg<D, M>::NB;
     FsArgs a = make_args(b);
     const size_t smem = ((size_t)8 * NB + (size_t)256 * (2 * S + 1)) * sizeof(double);
     auto kern = gather_kernel<D, M>;
@@ -1124,7 +1170,7 @@ static int gather_dm(mlb_binding* b, const double* grid, const double* v, double
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     int blocks = nsm * per_sm;
-    const int need = (b->nchunks + 7) / 8;  // at least one chunk per warp
+    const int need = ((D == 3 ? b->ngrp : b->nchunks) + 7) / 8;  // at least one unit per warp
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
     MLB_CUDA_TRY(launch_k(kern, dim3(blocks), dim3(256), smem, st, a, b->plan->wc, grid, v, y, alpha, beta, gamma, flags));
