@@ -290,7 +290,19 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     // first staged cell) << 29, -1 = empty.  Packing across the pencil's cells
     // fills the lanes that one-cell chunks leave idle on light cells.
     std::vector<int32_t> ggrp, gslot;
+    // pack only where one-cell chunks leave lanes idle: lane fill of the
+    // chunk path (64-point chunks; a tail of <= 32 points takes 32 lanes)
+    bool packed = false;
     if (d == 3 && n > 0) {
+        int64_t slots = 0;
+        for (int64_t k = 0; k < nkeys; ++k) {
+            const int64_t c = cnt[k + 1] - cnt[k], r = c % 64;
+            slots += 64 * (c / 64) + (r == 0 ? 0 : (r <= 32 ? 32 : 64));
+        }
+        packed = (double)n / (double)slots < 0.9;
+        if (const char* env = std::getenv("MLB_GATHER_PACKED")) packed = env[0] == '1';  // tuning
+    }
+    if (packed) {
         if (n >= ((int64_t)1 << 29)) return fail(MLB_ERR_CONFIG, "d = 3 bindings hold fewer than 2^29 points");
         struct Lane { int32_t a, b; int dc; };
         std::vector<Lane> lanes;
@@ -538,6 +550,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     b->n = n;
     b->nchunks = nch;
     b->ngrp = ngrp;
+    b->gather_packed = packed ? 1 : 0;
     b->nseg = nseg;
     b->nbricks = nbricks;
     b->max_seg_chunks = seg_points;
@@ -576,8 +589,8 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         if (rc == MLB_OK) rc = dev_upload(&b->active_brick, active_brick.data(), active_brick.size());
         if (rc == MLB_OK) rc = dev_upload(&b->merge_off, merge_off.data(), merge_off.size());
         if (rc == MLB_OK) rc = dev_upload(&b->merge_pairs, merge_pairs.data(), std::max<size_t>(2, merge_pairs.size()));
-        if (rc == MLB_OK) rc = dev_upload(&b->ggrp, ggrp.data(), ggrp.size());
-        if (rc == MLB_OK) rc = dev_upload(&b->gslot, gslot.data(), gslot.size());
+        if (packed && rc == MLB_OK) rc = dev_upload(&b->ggrp, ggrp.data(), ggrp.size());
+        if (packed && rc == MLB_OK) rc = dev_upload(&b->gslot, gslot.data(), gslot.size());
         const int S = 2 * g.m + 1;
         if (rc == MLB_OK) rc = dev_upload<double>(&b->blocks, nullptr, (size_t)b->nblk * S * S * S);
     }

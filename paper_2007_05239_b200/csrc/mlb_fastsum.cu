@@ -881,22 +881,23 @@ __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restri
 // lane owns TWO points of the chunk (p0+lane, p0+32+lane), so every staged
 // value read (a broadcast LDS: the whole chunk shares one cell) feeds two
 // FMAs.  Epilogue: y = alpha v + s (beta acc + gamma s v).
-template <int D, int M>
+template <int D, int M, bool PK>
 struct GatherCfg {
     static constexpr int S = 2 * M + 1;
-    // d = 3 stages a pencil: the neighbourhoods of <= Tb consecutive axis-2
-    // cells (Tb = 4, or 2 for m >= 6) share one (2m+1)^2 x (2m+Tb) block
-    static constexpr int SR = (D == 3) ? S + (M >= 6 ? 1 : 3) : S;
+    // d = 3 packed (PK) stages a pencil: the neighbourhoods of <= Tb
+    // consecutive axis-2 cells (Tb = 4, or 2 for m >= 6) share one
+    // (2m+1)^2 x (2m+Tb) block
+    static constexpr int SR = (D == 3 && PK) ? S + (M >= 6 ? 1 : 3) : S;
     static constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * SR);
 };
 
-template <int D, int M>
+template <int D, int M, bool PK>
 __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
                                                      const double* __restrict__ v, double* __restrict__ y,
                                                      double alpha, double beta, double gamma, unsigned flags) {
     constexpr int S = 2 * M + 1;
-    constexpr int SR = GatherCfg<D, M>::SR;  // staged row length (d = 3: a pencil of <= Tb cells)
-    constexpr int NB = GatherCfg<D, M>::NB;
+    constexpr int SR = GatherCfg<D, M, PK>::SR;  // staged row length (d = 3 packed: a pencil of <= Tb cells)
+    constexpr int NB = GatherCfg<D, M, PK>::NB;
     constexpr int W0S = 2 * S + 1;  // per-lane axis-0 window row (odd stride)
     extern __shared__ double nbs[];
     const int L = a.g.L;
@@ -905,7 +906,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     double* w0s = nbs + 8 * NB + (wl * 32 + lane) * W0S;  // [0,S): point A, [S,2S): point B
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwt = (gridDim.x * blockDim.x) >> 5;
-    const int nunits = (D == 3) ? a.ngrp : a.nchunks;  // d = 3: pencil groups, else one-cell chunks
+    const int nunits = (D == 3 && PK) ? a.ngrp : a.nchunks;  // pencil groups, or one-cell chunks
     const int c_lo = (int)(((long long)nunits * gw) / nwt);
     const int c_hi = (int)(((long long)nunits * (gw + 1)) / nwt);
     const int64_t rs = (D == 3) ? (int64_t)L * L : (int64_t)L;  // stride of axis 0
@@ -914,7 +915,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     for (int ch = c_lo; ch < c_hi; ++ch) {
         int gbase, wst = S, dcA = 0, pA, pB;
         bool okA, okB, two;
-        if (D == 3) {
+        if (D == 3 && PK) {
             const int2 gg = __ldg(a.ggrp + ch);
             const int sA = __ldg(a.gslot + (int64_t)ch * 64 + lane);
             const int sB = __ldg(a.gslot + (int64_t)ch * 64 + 32 + lane);
@@ -945,16 +946,19 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         const double fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
         if (key != cur && !(flags & (1u << 18))) {  // bit 18: ablation (profiling only): no restaging
             __syncwarp();
-            if (D == 3) {
+            if (D == 3 && PK) {
                 // rows (i, j) of the pencil block; columns past the group's width are not read
                 for (int e = lane; e < S * S * SR; e += 32) {
                     const int row = e / SR, col = e % SR;
                     if (col < wst) cp_async8(nb + e, grid + gbase + (row / S) * rs + (row % S) * (int64_t)L + col);
                 }
             } else {
-                constexpr int NSRC = (D == 1) ? S : S * S;
+                constexpr int NSRC = (D == 1) ? S : (D == 2 ? S * S : S * S * S);
                 for (int e = lane; e < NSRC; e += 32) {
-                    const int64_t off = (D == 1) ? e : (e / S) * rs + e % S;
+                    int64_t off;
+                    if (D == 1) off = e;
+                    else if (D == 2) off = (e / S) * rs + e % S;
+                    else off = (e / (S * S)) * rs + ((e / S) % S) * (int64_t)L + e % S;
                     cp_async8(nb + e, grid + gbase + off);
                 }
             }
@@ -1149,14 +1153,14 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
     }
 }
 
-template <int D, int M>
-static int gather_dm(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
-                     double beta, double gamma, unsigned flags, cudaStream_t st) {
+template <int D, int M, bool PK>
+static int gather_dmp(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
+                      double beta, double gamma, unsigned flags, cudaStream_t st) {
     constexpr int S = 2 * M + 1;
-    constexpr int NB = GatherCfg<D, M>::NB;
+    constexpr int NB = GatherCfg<D, M, PK>::NB;
     FsArgs a = make_args(b);
     const size_t smem = ((size_t)8 * NB + (size_t)256 * (2 * S + 1)) * sizeof(double);
-    auto kern = gather_kernel<D, M>;
+    auto kern = gather_kernel<D, M, PK>;
     static int per_sm = 0;  // resident blocks per SM for this instantiation
     if (per_sm == 0) {
         MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1170,13 +1174,20 @@ static int gather_dm(mlb_binding* b, const double* grid, const double* v, double
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     int blocks = nsm * per_sm;
-    const int need = ((D == 3 ? b->ngrp : b->nchunks) + 7) / 8;  // at least one unit per warp
+    const int need = ((D == 3 && PK ? b->ngrp : b->nchunks) + 7) / 8;  // at least one unit per warp
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
     MLB_CUDA_TRY(launch_k(kern, dim3(blocks), dim3(256), smem, st, a, b->plan->wc, grid, v, y, alpha, beta, gamma, flags));
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
+}
+
+template <int D, int M>
+static int gather_dm(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
+                     double beta, double gamma, unsigned flags, cudaStream_t st) {
+    if (D == 3 && b->gather_packed) return gather_dmp<D, M, true>(b, grid, v, y, alpha, beta, gamma, flags, st);
+    return gather_dmp<D, M, false>(b, grid, v, y, alpha, beta, gamma, flags, st);
 }
 
 #define MLB_DISPATCH_DM(FN, D, M, ...)                                   \

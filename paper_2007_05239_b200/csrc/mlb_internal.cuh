@@ -102,6 +102,7 @@ struct mlb_binding {
     int32_t* ggrp = nullptr;         // ngrp x {grid index of the first staged cell, width | two << 8}
     int32_t* gslot = nullptr;        // ngrp x 64: sorted point | axis-2 offset << 29, -1 = empty
     int ngrp = 0;
+    int gather_packed = 0;           // d = 3: gather on pencil groups (light cells) instead of one-cell chunks
     int32_t* seg_chunk = nullptr;    // nseg+1
     int32_t* sub_desc = nullptr;     // 2 x nsub: {first point, (count << 24) | tile cell}, segment order
     int32_t* seg_sub = nullptr;      // nseg+1: CSR of sub-chunks per segment
