@@ -291,6 +291,9 @@ def run_ours(args):
     # settled), and a user that streams many vectors keeps its buffers
     v_pin = torch.from_numpy(v_host).pin_memory()
     y_pin = torch.empty((T, n), dtype=torch.float64, pin_memory=True)
+    e2e_k = max(3, args.steps)  # one distinct host vector per e2e step
+    V_pin = torch.from_numpy(rng.standard_normal((e2e_k, n))).pin_memory()
+    Y_pin = torch.empty((e2e_k, T, n), dtype=torch.float64, pin_memory=True)
 
     def step():
         batch._run()
@@ -344,8 +347,20 @@ def run_ours(args):
         batch.apply(v_pin, out=y_pin)
     e_e.record()
     e_e.synchronize()
+    e2e_sync_ms = e_s.elapsed_time(e_e)
+    e2e_sync_value = n * T * e2e_steps * ws / (e2e_sync_ms * 1e-3)
+    # streamed: the K steps' distinct host vectors through apply_many (vector
+    # i+1's H2D and vector i-1's D2H overlap vector i's compute); the call
+    # returns once every result is in host memory
+    for _ in range(2):
+        batch.apply_many(V_pin[:3], out=Y_pin[:3])
+    torch.cuda.synchronize()
+    e_s.record()
+    batch.apply_many(V_pin, out=Y_pin)
+    e_e.record()
+    e_e.synchronize()
     e2e_ms = e_s.elapsed_time(e_e)
-    e2e_value = n * T * e2e_steps * ws / (e2e_ms * 1e-3)
+    e2e_value = n * T * e2e_k * ws / (e2e_ms * 1e-3)
 
     # ---- sorted-order variant (what the PKSM inner loop runs) -----------------
     sorted_value = None
@@ -423,8 +438,14 @@ def run_ours(args):
                               "one captured CUDA graph replay" + (" (disabled)" if args.no_cuda_graph else ""),
                    "parallelism": f"layer-parallel x{ws} (independent layers per rank, no collective)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * T,
-                "path": "paper_2007_05239_b200.LaplacianBatch(graph).apply(pinned host v, out=pinned host (T, n)) "
-                        "(one H2D of v, per-layer D2H as each layer finishes, host sync per step)"},
+                "steps": e2e_k,
+                "path": "paper_2007_05239_b200.LaplacianBatch(graph).apply_many(pinned host (K, n), out=pinned host "
+                        "(K, T, n)): K distinct host vectors, each one H2D of v and T D2H of its results, copies "
+                        "on their own streams overlapping the neighbouring vectors' compute; timed until the last "
+                        "result is in host memory",
+                "synchronous": {"value": e2e_sync_value, "unit": UNIT,
+                                "path": "LaplacianBatch(graph).apply(pinned host v, out=pinned host (T, n)) per step: "
+                                        "H2D, compute, D2H and a host sync every step (no overlap between steps)"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "roofline": roof,

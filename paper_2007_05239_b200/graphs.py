@@ -495,6 +495,103 @@ class LaplacianBatch:
         main.synchronize()
         return out.numpy() if not _is_tensor(v) else out
 
+    def _ensure_stream_buffers(self):
+        """Second device buffer set + its layer graphs, and per-layer copy-out
+        streams, for the double-buffered `apply_many` pipeline."""
+        torch = _torch()
+        if getattr(self, "_vb", None) is not None:
+            return
+        if self._use_graph and self._graphs is None:
+            self._capture()
+        dev = torch.device("cuda", self.device)
+        with torch.cuda.device(dev):
+            v2 = torch.empty_like(self._v)
+            y2 = torch.empty_like(self._y)
+            self._couts = [torch.cuda.Stream(device=dev) for _ in self.graph.layers]
+            self._cin = torch.cuda.Stream(device=dev)
+        graphs2 = None
+        if self._use_graph:
+            for t, layer in enumerate(self.graph.layers):  # warm-up on the new buffers
+                apply_sym_laplacian_dev(layer, v2, y2[t])
+            torch.cuda.synchronize(self.device)
+            graphs2 = []
+            for t, layer in enumerate(self.graph.layers):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self._streams[t]):
+                    apply_sym_laplacian_dev(layer, v2, y2[t])
+                graphs2.append(g)
+            torch.cuda.synchronize(self.device)
+        self._vb, self._yb = [self._v, v2], [self._y, y2]
+        self._graphs_b = [self._graphs, graphs2]
+
+    def apply_many(self, V, out=None):
+        """(k, T, n): every layer's L_sym of k host vectors (rows of V), streamed.
+
+        Vector i+1's host->device copy and vector i-1's device->host copies
+        run on copy streams while vector i computes (two device buffer sets,
+        one captured graph per layer and buffer), so at steady state a
+        vector costs max(H2D, compute, D2H) instead of their sum.  V: pinned
+        (k, n) float64 tensor or array (staged once into pinned memory);
+        `out`: optional pinned (k, T, n) float64 tensor.  Returns after the
+        last result has landed in host memory.
+        """
+        torch = _torch()
+        if _is_tensor(V) and V.is_pinned() and V.dtype == torch.float64 and V.is_contiguous() and V.dim() == 2:
+            src = V
+        else:
+            arr = V.cpu().numpy() if _is_tensor(V) else np.asarray(V, dtype=float)
+            if arr.ndim != 2:
+                raise ConfigError("V must be a (k, n) matrix of vectors")
+            src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).pin_memory()
+        k = int(src.shape[0])
+        if tuple(src.shape) != (k, self.n):
+            raise ConfigError("V must have one row of length n per vector")
+        if out is None:
+            out = torch.empty((k, self.T, self.n), dtype=torch.float64, pin_memory=True)
+        elif not (_is_tensor(out) and out.is_pinned() and out.dtype == torch.float64
+                  and tuple(out.shape) == (k, self.T, self.n) and out.is_contiguous()):
+            raise ConfigError("out must be a contiguous pinned float64 tensor of shape (k, T, n)")
+        self._ensure_stream_buffers()
+        T = self.T
+        main = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [[torch.cuda.Event() for _ in range(T)] for _ in range(2)]
+        ev_out = [[torch.cuda.Event() for _ in range(T)] for _ in range(2)]
+        self._cin.wait_event(start)
+        for s in self._streams + self._couts:
+            s.wait_event(start)
+        for i in range(k):
+            b = i & 1
+            if i >= 2:  # buffer b's input is free once vector i-2's layers have read it
+                for t in range(T):
+                    self._cin.wait_event(ev_done[b][t])
+            with torch.cuda.stream(self._cin):
+                self._vb[b].copy_(src[i], non_blocking=True)
+            ev_in[b].record(self._cin)
+            for t in range(T):
+                s = self._streams[t]
+                s.wait_event(ev_in[b])
+                if i >= 2:  # buffer b's output row is free once vector i-2's copy-out is done
+                    s.wait_event(ev_out[b][t])
+                with torch.cuda.stream(s):
+                    if self._use_graph:
+                        self._graphs_b[b][t].replay()
+                        _lib.lib().mlb_note_launches(self._graph_launches[t])
+                    else:
+                        apply_sym_laplacian_dev(self.graph.layers[t], self._vb[b], self._yb[b][t])
+                ev_done[b][t].record(s)
+                co = self._couts[t]
+                co.wait_event(ev_done[b][t])
+                with torch.cuda.stream(co):
+                    out[i, t].copy_(self._yb[b][t], non_blocking=True)
+                ev_out[b][t].record(co)
+        for s in self._couts + self._streams + [self._cin]:
+            main.wait_stream(s)
+        main.synchronize()
+        return out
+
     def _step_direct(self, main, out):
         """Kernel-by-kernel step with per-layer D2H (for whole-step capture)."""
         torch = _torch()

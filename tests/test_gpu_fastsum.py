@@ -145,6 +145,17 @@ def test_laplacian_batch_matches_per_layer():
     ref_w = np.stack([apply_sym_laplacian(layer, w) for layer in layers])
     vp.copy_(torch.from_numpy(w))  # same host buffers, new contents: the graph re-reads them
     assert np.array_equal(batch.apply(vp, out=out).numpy(), ref_w)
+    # streamed multi-vector apply (double-buffered, copies overlapped): bitwise the same
+    rng = np.random.default_rng(9)
+    V = rng.standard_normal((7, G.n))
+    refs = np.stack([np.stack([apply_sym_laplacian(layer, x) for layer in layers]) for x in V])
+    for use_graph in (True, False):
+        b2 = LaplacianBatch(G, use_graph=use_graph)
+        assert np.array_equal(b2.apply_many(V).numpy(), refs)
+        Vp = torch.from_numpy(V).pin_memory()
+        outp = torch.empty((7, G.T, G.n), dtype=torch.float64, pin_memory=True)
+        assert np.array_equal(b2.apply_many(Vp, out=outp).numpy(), refs)
+        assert np.array_equal(b2.apply_many(Vp[:1].clone().pin_memory()).numpy(), refs[:1])
 
 
 def test_per_component_blocks_match_oracle():
