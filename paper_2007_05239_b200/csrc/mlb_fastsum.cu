@@ -709,70 +709,6 @@ __global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, 
     if (slice == 0 && cell < cells) grid[cell] = s;
 }
 
-// d = 3, R1 + R2 merged: grid[u] = sum over the covering bricks (fixed
-// order) of the sum over the brick's segments (fixed order) of the segment
-// partial tiles.  A CTA covers 4 grid blocks of 4^3 cells; each grid block's
-// covering bricks are resolved once into smem (base pointer + segment count).
-__global__ void __launch_bounds__(256) reduce3m_kernel(FsArgs a, double* __restrict__ grid) {
-    constexpr int TB = 4, CPB = 64, GB = 4;
-    const Geom g = a.g;
-    const int L = g.L, TL = TB + 2 * g.m, nbr = g.nbr;
-    const int ngb = (L + TB - 1) / TB;
-    const int R = (TL + TB - 1) / TB;
-    const int RRR = R * R * R;
-    __shared__ const double* base[GB][64];
-    __shared__ int nsg[GB][64];
-    const int lb = threadIdx.x / CPB, c = threadIdx.x % CPB;
-    const int gbid = blockIdx.x * GB + lb;
-    const int gb0 = gbid / (ngb * ngb), gb1 = (gbid / ngb) % ngb, gb2 = gbid % ngb;
-    const bool live = gbid < ngb * ngb * ngb;
-    const size_t tile = (size_t)a.tile_cells;
-    for (int q = c; q < RRR; q += CPB) {
-        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
-        const int b0 = gb0 - s0, b1 = gb1 - s1, b2 = gb2 - s2;
-        const double* p = nullptr;
-        int ns = 0;
-        if (live && b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 < nbr && b1 < nbr && b2 < nbr) {
-            const int br = (b0 * nbr + b1) * nbr + b2;
-            const int f = __ldg(a.brick_seg + br);
-            ns = __ldg(a.brick_seg + br + 1) - f;
-            if (ns > 0) p = a.partial + (size_t)f * tile + ((s0 * TB) * TL + s1 * TB) * TL + s2 * TB;
-        }
-        base[lb][q] = p;
-        nsg[lb][q] = ns;
-    }
-    __syncthreads();
-    if (!live) return;
-    const int c0 = c / (TB * TB), c1 = (c / TB) % TB, c2 = c % TB;
-    const int u0 = gb0 * TB + c0, u1 = gb1 * TB + c1, u2 = gb2 * TB + c2;
-    if (u0 >= L || u1 >= L || u2 >= L) return;
-    const int local = (c0 * TL + c1) * TL + c2;
-    double sum = 0.0;
-    for (int q = 0; q < RRR; ++q) {
-        const double* p = base[lb][q];
-        const int ns = nsg[lb][q];
-        if (!p) continue;
-        const int s0 = q / (R * R), s1 = (q / R) % R, s2 = q % R;
-        if (s0 * TB + c0 >= TL || s1 * TB + c1 >= TL || s2 * TB + c2 >= TL) continue;
-        const double* pp = p + local;
-        double bs = 0.0;
-        int j = 0;
-        for (; j + 3 < ns; j += 4) {
-            const double x0 = __ldcg(pp + (size_t)j * tile);
-            const double x1 = __ldcg(pp + (size_t)(j + 1) * tile);
-            const double x2 = __ldcg(pp + (size_t)(j + 2) * tile);
-            const double x3 = __ldcg(pp + (size_t)(j + 3) * tile);
-            bs += x0;
-            bs += x1;
-            bs += x2;
-            bs += x3;
-        }
-        for (; j < ns; ++j) bs += __ldcg(pp + (size_t)j * tile);
-        sum += bs;
-    }
-    grid[((int64_t)u0 * L + u1) * L + u2] = sum;
-}
-
 // Stage R2: grid[u] = sum over the (<= 3^d) bricks whose tile covers u of
 // that brick's (first-segment) tile value.  One thread per active cell.
 template <int D, int TBC>

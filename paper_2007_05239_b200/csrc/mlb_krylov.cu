@@ -16,6 +16,7 @@ namespace mlb {
 
 constexpr int kRedThreads = 256;
 constexpr int kMaxRowBlocks = 256;
+constexpr int kFusedBlocks = 296;  // fused CGS2 row blocks (2 per SM)
 
 static int row_blocks(int64_t n) {
     int64_t b = (n + 2047) / 2048;
@@ -154,6 +155,167 @@ __global__ void gemm_vs_kernel(const double* __restrict__ V, int64_t ld, int64_t
         }
 }
 
+// ---- CGS2 for cols <= 64: 4 bandwidth passes, 4 launches -----------------
+// Row blocks are a FIXED partition of the rows (nb blocks of contiguous
+// rows, multiples of 4); a thread owns 4 consecutive rows of a 1024-row tile
+// and reads them as two 16-byte loads per column, a warp covering 1 KB of a
+// column per load pair; 4 columns are in flight per step.  Every sum has a
+// fixed order (4 rows, fixed shuffle tree, tiles in order, warps in order,
+// blocks in order by warp-per-column finishes that every block repeats
+// identically): bitwise reproducible.  Needs an even leading dimension and
+// 16-byte aligned V / w (checked by the launcher).
+constexpr int kTileRows = 1024;
+
+__device__ __forceinline__ void ld4(const double* p, bool ok, double* v) {
+    if (ok) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+        v[0] = v[1] = v[2] = v[3] = 0.0;
+    }
+}
+
+// part[j * nb + b] = sum over block b's rows of V[j][i] w[i]
+__global__ void __launch_bounds__(256) cgs_dot_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                                                      const double* __restrict__ w, double* __restrict__ part) {
+    __shared__ double acc[8][64];  // per warp, per column (tiles accumulate in order)
+    const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t per = ((n + nb - 1) / nb + 3) & ~(int64_t)3;
+    const int64_t r0 = min(n, blockIdx.x * per), r1 = min(n, r0 + per);
+    for (int j = threadIdx.x; j < 8 * 64; j += blockDim.x) (&acc[0][0])[j] = 0.0;
+    __syncthreads();
+    for (int64_t t0 = r0; t0 < r1; t0 += kTileRows) {
+        const int64_t i0 = t0 + 4 * threadIdx.x;
+        const bool full = i0 + 3 < r1;
+        double wr[4];
+        if (full) {
+            ld4(w + i0, true, wr);
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) wr[r] = (i0 + r < r1) ? w[i0 + r] : 0.0;
+        }
+        for (int j0 = 0; j0 < cols; j0 += 4) {
+            double vr[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double* col = V + (int64_t)min(j0 + q, cols - 1) * ld + i0;
+                if (full) {
+                    ld4(col, true, vr[q]);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) vr[q][r] = (i0 + r < r1) ? __ldg(col + r) : 0.0;
+                }
+            }
+            double s[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                s[q] = 0.0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) s[q] = fma(vr[q][r], wr[r], s[q]);
+            }
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s[q] += __shfl_down_sync(0xffffffffu, s[q], o);
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j0 + q < cols) acc[warp][j0 + q] += s[q];
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < 8; ++k) s += acc[k][j];
+        part[(int64_t)j * nb + blockIdx.x] = s;
+    }
+}
+
+// h[j] = sum_b part_in[j * nb + b] (warp per column, same in every block);
+// w -= V h on the block's rows; npart[b] = the block's partial of ||w||^2.
+// Block 0 stores h into h_save and h_prev + h into h_sum.
+__global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                                                         const double* __restrict__ part_in, double* __restrict__ w,
+                                                         double* __restrict__ npart, double* __restrict__ h_save,
+                                                         const double* __restrict__ h_prev, double* __restrict__ h_sum) {
+    __shared__ double h[64];
+    __shared__ double sh[8];
+    const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < cols; j += 8) {
+        double s = 0.0;
+        for (int b = lane; b < nb; b += 32) s += __ldcg(part_in + (int64_t)j * nb + b);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            h[j] = s;
+            if (blockIdx.x == 0) {
+                if (h_save) h_save[j] = s;
+                if (h_sum) h_sum[j] = h_prev[j] + s;
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t per = ((n + nb - 1) / nb + 3) & ~(int64_t)3;
+    const int64_t r0 = min(n, blockIdx.x * per), r1 = min(n, r0 + per);
+    double ss = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += kTileRows) {
+        const int64_t i0 = t0 + 4 * threadIdx.x;
+        const bool full = i0 + 3 < r1;
+        double x[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int j = 0; j < cols; ++j) {
+            const double* col = V + (int64_t)j * ld + i0;
+            const double hj = h[j];
+            double v[4];
+            if (full) {
+                ld4(col, true, v);
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[r] = (i0 + r < r1) ? __ldg(col + r) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) x[r] = fma(v[r], hj, x[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i = i0 + r;
+            if (i >= r1) continue;
+            const double wn = w[i] - x[r];
+            w[i] = wn;
+            ss = fma(wn, wn, ss);
+        }
+    }
+    if (npart) {
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
+        if (lane == 0) sh[warp] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+            npart[blockIdx.x] = t;
+        }
+    }
+}
+
+static int cgs2_fused(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out, double* h1_out,
+                      double* nrm2_out, double* work, cudaStream_t st) {
+    const int nb = std::max(1, std::min(kFusedBlocks, (int)((n + kTileRows - 1) / kTileRows)));
+    double* part = work;                              // nb x cols
+    double* npart = part + (int64_t)kFusedBlocks * 64;  // nb
+    double* h1 = npart + kFusedBlocks;                 // cols
+    cgs_dot_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, w, part);
+    cgs_update_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, part, w, nullptr, h1, nullptr, nullptr);
+    cgs_dot_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, w, part);
+    cgs_update_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, part, w, npart, nullptr, h1, h_out);
+    note_launches(4);
+    if (nrm2_out) {
+        finish_partial<<<1, 64, 0, st>>>(npart, nb, 1, nrm2_out, nullptr);
+        note_launches(1);
+    }
+    if (h1_out) MLB_CUDA_TRY(cudaMemcpyAsync(h1_out, h1, cols * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
 static int ew_grid(int64_t n) {
     int64_t b = (n + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
@@ -168,7 +330,9 @@ extern "C" {
 
 int64_t mlb_krylov_work_size(int64_t n, int maxcols) {
     (void)n;
-    return (int64_t)kMaxRowBlocks * (maxcols + 2) + 2 * (maxcols + 2);
+    const int64_t unfused = (int64_t)kMaxRowBlocks * (maxcols + 2) + 2 * (maxcols + 2);
+    const int64_t fused = (int64_t)kFusedBlocks * (64 + 1) + 64;
+    return std::max(unfused, fused);
 }
 
 int mlb_gemv_t(const double* V, int64_t ld, int64_t n, int cols, const double* w, double* h, double* work,
@@ -197,6 +361,9 @@ int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c
 int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out, double* h1_out,
              double* nrm2_out, double* work, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (cols <= 0 || n <= 0) return MLB_OK;
+    const bool aligned = !(ld & 1) && !(reinterpret_cast<uintptr_t>(V) & 15) && !(reinterpret_cast<uintptr_t>(w) & 15);
+    if (cols <= 64 && aligned) return cgs2_fused(V, ld, n, cols, w, h_out, h1_out, nrm2_out, work, st);
     const int nb = row_blocks(n);
     double* part = work;                                     // kMaxRowBlocks * cols
     double* h1 = work + (int64_t)kMaxRowBlocks * (cols + 2);  // cols
