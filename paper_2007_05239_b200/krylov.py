@@ -19,6 +19,7 @@ formed once at the end.  Borderline steps (ratio within
 """
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -279,11 +280,147 @@ class PksmStats:
         cls.steps = []
 
 
+_PINNED = {}
+
+
+def _pinned_snapshots(shape):
+    """Reused pinned host buffer for the per-step alpha / beta snapshots (a
+    fresh pinned allocation per solve costs far more than the solve's reads;
+    reuse is safe: every read waits for its own step's event, which follows
+    any earlier copy into the buffer on the stream)."""
+    torch = _torch()
+    buf = _PINNED.get(shape)
+    if buf is None:
+        buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        _PINNED[shape] = buf
+    return buf
+
+
+_VPOOL = {}
+_VPOOL_DEPTH = [0]  # nesting level of running solves (an operator may itself run a solve)
+
+
+def _krylov_basis(device, slot, dim, n):
+    """Reused (dim, n) Krylov basis buffer number `slot` on `device`: PKSM
+    solves run back to back on one stream, so a solve may overwrite the
+    previous solve's basis (stream order); allocating ~100 MB per solve made
+    the caching allocator release and re-allocate (device syncs)."""
+    torch = _torch()
+    key = (int(device.index if hasattr(device, "index") else device), _VPOOL_DEPTH[0], slot)
+    buf = _VPOOL.get(key)
+    if buf is None or buf.numel() < dim * n:
+        _VPOOL[key] = buf = torch.empty(dim * n, dtype=torch.float64, device=device)
+    return buf[: dim * n].view(dim, n)
+
+
+def _run_ahead():
+    """Krylov steps the device may run ahead of the host's convergence test
+    (MLB_PKSM_DEPTH; 1 = lockstep with the host)."""
+    try:
+        return max(1, int(os.environ.get("MLB_PKSM_DEPTH", "2")))
+    except ValueError:
+        return 2
+
+
+def _converged(c, c_prev, tol, exact):
+    """The PKSM stopping test on coefficient vectors (krylov.py:205-211),
+    re-run on the exact device vectors when within 1e-3 of the threshold."""
+    s = c.shape[0]
+    diff = c.copy()
+    diff[: s - 1] -= c_prev
+    lhs = np.linalg.norm(diff)
+    rhs = tol * max(np.linalg.norm(c), 1e-300)
+    if rhs > 0 and abs(lhs / rhs - 1.0) < 1e-3:
+        lhs, rhs = exact()
+    return lhs <= rhs
+
+
+def _exact_test(V, n, c, c_prev, tol, device):
+    torch = _torch()
+    s = c.shape[0]
+    y = torch.zeros(n, dtype=torch.float64, device=device)
+    yp = torch.zeros(n, dtype=torch.float64, device=device)
+    gemv_n(V, n, s, _to_dev(c, device.index), y)
+    gemv_n(V, n, s - 1, _to_dev(c_prev, device.index), yp)
+    nb = torch.empty(2, dtype=torch.float64, device=device)
+    d = axpby(1.0, y, -1.0, yp)
+    dot(d, d, nb[0:1])
+    dot(y, y, nb[1:2])
+    a2, b2 = nb.cpu().numpy()
+    return np.sqrt(a2), tol * max(np.sqrt(b2), 1e-300)
+
+
+def _tridiag(alphas, betas, s):
+    T = np.diag(alphas[:s])
+    if s > 1:
+        off = betas[: s - 1]
+        T += np.diag(off, 1) + np.diag(off, -1)
+    return T
+
+
+class _Chain:
+    """Device side of one Lanczos chain: step j = matvec of V[j], CGS2 against
+    V[:j+1] (alpha_j = first-pass coefficient, ||w||^2 into AB), and
+    V[j+1] = w / sqrt(||w||^2) computed ON THE DEVICE, so steps can be queued
+    ahead of the host's convergence test without changing any value (the
+    host's 1 / sqrt is the same correctly rounded operation).
+
+    `fused` = (binding, alpha, beta, gamma, flags): the matvec is one mlb_apply
+    into a persistent w; a step is then three C-ABI calls on pointers and a
+    stream resolved once per solve (per-call torch stream / pointer lookups
+    cost more host time than the device spends on a step).  Otherwise
+    `apply_dev(V[j])` is called."""
+
+    def __init__(self, V, ab_row, stream, apply_dev=None, fused=None):
+        torch = _torch()
+        self.V, self.ab, self.apply_dev, self.fused = V, ab_row, apply_dev, fused
+        self.dim, self.n = V.shape
+        dev = V.device
+        self.h = torch.empty(self.dim + 1, dtype=torch.float64, device=dev)
+        self.w = torch.empty(self.n, dtype=torch.float64, device=dev) if fused is not None else None
+        self.work = _Work.get(dev.index, self.dim)
+        self.sp = C.c_void_p(stream.cuda_stream)
+        self.v0 = V.data_ptr()
+        self.ab0 = ab_row.data_ptr()
+        self.lib = _lib.lib()
+
+    def issue(self, j):
+        lib, n, dim, sp = self.lib, self.n, self.dim, self.sp
+        row = lambda k: C.c_void_p(self.v0 + 8 * n * k)  # noqa: E731
+        if self.fused is not None:
+            b, a, bt, g, fl = self.fused
+            _lib.check(lib.mlb_apply(b, row(j), C.c_void_p(self.w.data_ptr()), a, bt, g, fl, sp))
+            w = self.w
+        else:
+            w = self.apply_dev(self.V[j])
+        wp = C.c_void_p(w.data_ptr())
+        nrm = C.c_void_p(self.ab0 + 8 * (dim + j))
+        # h1 of this pass lands in ab[0, :j+1]: entry j is alpha_j (earlier
+        # entries are stale, the host reads each step's snapshot at column j)
+        _lib.check(lib.mlb_cgs2(C.c_void_p(self.v0), n, n, j + 1, wp, C.c_void_p(self.h.data_ptr()),
+                                C.c_void_p(self.ab0), nrm, C.c_void_p(self.work.data_ptr()), sp))
+        if j + 1 < dim:
+            _lib.check(lib.mlb_scale_by(wp, row(j + 1), n, nrm, -0.5, sp))
+
+
 def lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None, out_scale=1.0,
-                         accumulate=False):
+                         accumulate=False, fused=None):
+    """Device Lanczos f(A) v (see _lanczos_fn_apply_dev)."""
+    _VPOOL_DEPTH[0] += 1
+    try:
+        return _lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim, tol, out, out_scale, accumulate, fused)
+    finally:
+        _VPOOL_DEPTH[0] -= 1
+
+
+def _lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None, out_scale=1.0,
+                          accumulate=False, fused=None):
     """Device Lanczos f(A) v; v is a CUDA tensor (not modified).
 
-    Returns y (or writes out (=|+=) out_scale * y).
+    Returns y (or writes out (=|+=) out_scale * y).  The device runs up to
+    MLB_PKSM_DEPTH steps ahead of the host's convergence test (steps past
+    the stopping point are computed and discarded; the result only uses
+    V[:, :s] and T_s, so it is independent of the depth).
     """
     torch = _torch()
     if tuple(v.shape) != (n,):
@@ -300,47 +437,40 @@ def lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None,
         if not accumulate:
             out.zero_()
         return out
-    V = torch.empty((dim, n), dtype=torch.float64, device=v.device)
+    V = _krylov_basis(v.device, 0, dim, n)
     axpby(1.0 / nv, v, 0.0, V[0])
+    AB = torch.zeros((2, dim), dtype=torch.float64, device=v.device)
+    ABh = _pinned_snapshots((dim, 2, dim))
+    stream = torch.cuda.current_stream(v.device)
+    chain = _Chain(V, AB, stream, apply_dev=apply_dev, fused=fused)
+    events = [None] * dim
+
+    def issue(j):
+        chain.issue(j)
+        ABh[j].copy_(AB, non_blocking=True)
+        events[j] = torch.cuda.Event()
+        events[j].record(stream)
+
     alphas = np.empty(dim)
     betas = np.empty(dim)
-    hbuf = torch.empty(2 * dim + 3, dtype=torch.float64, device=v.device)
+    depth = _run_ahead()
+    issued = 0
+    while issued < min(depth, dim):
+        issue(issued)
+        issued += 1
     c_prev = None
     s = 0
     while True:
-        w = apply_dev(V[s])
-        cgs2(V, s + 1, w, hbuf[: s + 1], hbuf[dim:dim + s + 1], hbuf[dim + s + 1:dim + s + 2])
-        # alpha = V[:, s] . w before orthogonalisation (krylov.py:198) and ||w||^2 after
-        pair = hbuf[dim + s:dim + s + 2].cpu().numpy()
-        alphas[s] = pair[0]
-        beta = float(np.sqrt(max(pair[1], 0.0)))
+        events[s].synchronize()
+        alphas[s] = ABh[s, 0, s].item()
+        beta = float(np.sqrt(max(ABh[s, 1, s].item(), 0.0)))
         betas[s] = beta
         s += 1
-        T = np.diag(alphas[:s])
-        if s > 1:
-            off = betas[: s - 1]
-            T += np.diag(off, 1) + np.diag(off, -1)
-        lam, Q = np.linalg.eigh(T)
+        lam, Q = np.linalg.eigh(_tridiag(alphas, betas, s))
         c = nv * (Q @ (fn(lam) * Q[0, :]))
         stop = False
         if c_prev is not None:
-            diff = c.copy()
-            diff[: s - 1] -= c_prev
-            lhs = np.linalg.norm(diff)
-            rhs = tol * max(np.linalg.norm(c), 1e-300)
-            if rhs > 0 and abs(lhs / rhs - 1.0) < 1e-3:
-                # borderline: exact test on the device vectors (krylov.py:208-211)
-                y = torch.zeros(n, dtype=torch.float64, device=v.device)
-                yp = torch.zeros(n, dtype=torch.float64, device=v.device)
-                gemv_n(V, n, s, _to_dev(c, v.device.index), y)
-                gemv_n(V, n, s - 1, _to_dev(c_prev, v.device.index), yp)
-                nb = torch.empty(2, dtype=torch.float64, device=v.device)
-                d = axpby(1.0, y, -1.0, yp)
-                dot(d, d, nb[0:1])
-                dot(y, y, nb[1:2])
-                a2, b2 = nb.cpu().numpy()
-                lhs, rhs = np.sqrt(a2), tol * max(np.sqrt(b2), 1e-300)
-            stop = lhs <= rhs
+            stop = _converged(c, c_prev, tol, lambda: _exact_test(V, n, c, c_prev, tol, v.device))
         happy = beta <= 1e-13 * max(1.0, np.abs(alphas[:s]).max())
         if stop or happy or s >= dim:
             PksmStats.steps.append(s)
@@ -352,7 +482,9 @@ def lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None,
             gemv_n(V, n, s, cd, out, out_scale, accumulate)
             return out
         c_prev = c
-        axpby(1.0 / beta, w, 0.0, V[s])
+        if issued < dim:
+            issue(issued)
+            issued += 1
 
 
 class _LayerPksm:
@@ -391,12 +523,22 @@ class _LayerPksm:
 
 
 def pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1e-8):
+    """Lockstep multi-layer PKSM (see _pksm_layers_dev)."""
+    _VPOOL_DEPTH[0] += 1
+    try:
+        return _pksm_layers_dev(layers, p, v_node, out, out_scale, krylov_dim, tol)
+    finally:
+        _VPOOL_DEPTH[0] -= 1
+
+
+def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1e-8):
     """out += out_scale * (L_t + delta)^p v for every layer t, summed into out in
     ascending layer order.  The layers' Krylov steps advance in lockstep so
-    each step costs ONE device->host read for all layers (alpha, beta) and
-    one batched host eigh; per layer the arithmetic and its order are those
-    of pksm_layer_dev, so the result is bitwise identical to the sequential
-    loop.  Layers must be single-binding fused kernel layers."""
+    each step costs ONE device->host snapshot for all layers (alpha, beta),
+    read up to MLB_PKSM_DEPTH steps behind the device; per layer the
+    arithmetic and its order are those of pksm_layer_dev, so the result is
+    bitwise identical to the sequential loop.  Layers must be single-binding
+    fused kernel layers."""
     torch = _torch()
     fn = power_fn(p)
     n = v_node.numel()
@@ -404,74 +546,73 @@ def pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1e
     if dim < 1:
         raise ConfigError(f"krylov_dim must be >= 1, got {krylov_dim}")
     T = len(layers)
-    H = torch.empty((T, 2 * dim + 3), dtype=torch.float64, device=v_node.device)
-    st = [_LayerPksm(layer, v_node, dim, H[t]) for t, layer in enumerate(layers)]
+    dev = v_node.device
+    st = [_LayerPksm(layer, v_node, dim, None) for layer in layers]
+    nrm = torch.empty(T, dtype=torch.float64, device=dev)
     for t, x in enumerate(st):
-        dot(x.vs, x.vs, H[t, 0:1])
-    nv2 = H[:, 0].cpu().numpy()
+        dot(x.vs, x.vs, nrm[t:t + 1])
+    nv2 = nrm.cpu().numpy()
+    AB = torch.zeros((T, 2, dim), dtype=torch.float64, device=dev)
+    ABh = _pinned_snapshots((dim, T, 2, dim))
     for t, x in enumerate(st):
         x.nv = float(np.sqrt(nv2[t]))
         if x.nv == 0.0:
             x.done = True
             x.ys = None
         else:
-            x.V = torch.empty((dim, n), dtype=torch.float64, device=v_node.device)
+            x.V = _krylov_basis(dev, t, dim, n)
             axpby(1.0 / x.nv, x.vs, 0.0, x.V[0])
+    stream = torch.cuda.current_stream(dev)
+    for t, x in enumerate(st):
+        if not x.done:
+            x.chain = _Chain(x.V, AB[t], stream, fused=(x.b.ptr, x.a, -1.0, x.K0,
+                                                         _lib.MLB_USE_ISD | _lib.MLB_SORTED))
+    events = [None] * dim
+
+    def issue(j):  # step j of every layer still running at the host's last decision
+        for x in st:
+            if not x.done:
+                x.chain.issue(j)
+        ABh[j].copy_(AB, non_blocking=True)
+        events[j] = torch.cuda.Event()
+        events[j].record(stream)
+
+    depth = _run_ahead()
+    issued = 0
+    while issued < min(depth, dim):
+        issue(issued)
+        issued += 1
     s = 0
-    while True:
-        act = [x for x in st if not x.done]
-        if not act:
-            break
-        for x in act:
-            x.w = x.apply(x.V[s])
-            cgs2(x.V, s + 1, x.w, x.h[: s + 1], x.h[dim:dim + s + 1], x.h[dim + s + 1:dim + s + 2])
-        hb = H[:, dim + s:dim + s + 2].cpu().numpy()  # alpha, ||w||^2 of every layer: one read
-        for x in act:
-            t = st.index(x)
-            x.alphas[s] = hb[t, 0]
-            x.betas[s] = float(np.sqrt(max(hb[t, 1], 0.0)))
+    while any(not x.done for x in st):
+        events[s].synchronize()
+        snap = ABh[s].numpy()
         ss = s + 1
-        Ts = np.zeros((len(act), ss, ss))
-        for i, x in enumerate(act):
-            Ts[i] = np.diag(x.alphas[:ss])
-            if ss > 1:
-                off = x.betas[: ss - 1]
-                Ts[i] += np.diag(off, 1) + np.diag(off, -1)
-        for i, x in enumerate(act):
-            lam, Q = np.linalg.eigh(Ts[i])
+        for t, x in enumerate(st):
+            if x.done:
+                continue
+            x.alphas[s] = snap[t, 0, s]
+            beta = float(np.sqrt(max(snap[t, 1, s], 0.0)))
+            x.betas[s] = beta
+            lam, Q = np.linalg.eigh(_tridiag(x.alphas, x.betas, ss))
             c = x.nv * (Q @ (fn(lam) * Q[0, :]))
             stop = False
             if x.c_prev is not None:
-                diff = c.copy()
-                diff[: ss - 1] -= x.c_prev
-                lhs = np.linalg.norm(diff)
-                rhs = tol * max(np.linalg.norm(c), 1e-300)
-                if rhs > 0 and abs(lhs / rhs - 1.0) < 1e-3:
-                    y = torch.zeros(n, dtype=torch.float64, device=v_node.device)
-                    yp = torch.zeros(n, dtype=torch.float64, device=v_node.device)
-                    gemv_n(x.V, n, ss, _to_dev(c, v_node.device.index), y)
-                    gemv_n(x.V, n, ss - 1, _to_dev(x.c_prev, v_node.device.index), yp)
-                    nb = torch.empty(2, dtype=torch.float64, device=v_node.device)
-                    d = axpby(1.0, y, -1.0, yp)
-                    dot(d, d, nb[0:1])
-                    dot(y, y, nb[1:2])
-                    a2, b2 = nb.cpu().numpy()
-                    lhs, rhs = np.sqrt(a2), tol * max(np.sqrt(b2), 1e-300)
-                stop = lhs <= rhs
-            beta = x.betas[s]
+                stop = _converged(c, x.c_prev, tol, lambda: _exact_test(x.V, n, c, x.c_prev, tol, dev))
             happy = beta <= 1e-13 * max(1.0, np.abs(x.alphas[:ss]).max())
             if stop or happy or ss >= dim:
                 PksmStats.steps.append(ss)
-                x.ys = torch.empty(n, dtype=torch.float64, device=v_node.device)
-                gemv_n(x.V, n, ss, _to_dev(c, v_node.device.index), x.ys)
+                x.ys = torch.empty(n, dtype=torch.float64, device=dev)
+                gemv_n(x.V, n, ss, _to_dev(c, dev.index), x.ys)
                 x.done = True
-                x.V = None
             else:
                 x.c_prev = c
-                axpby(1.0 / beta, x.w, 0.0, x.V[ss])
         s += 1
+        if issued < dim and any(not x.done for x in st):
+            issue(issued)
+            issued += 1
     lib = _lib.lib()
     for x in st:  # ascending layer order, exactly as the sequential loop
+        x.V = None
         if x.ys is None:
             continue
         if out_scale != 1.0:
@@ -541,7 +682,8 @@ def pksm_layer_dev(layer, p, v_node, out, out_scale=1.0, accumulate=True, krylov
             _lib.check(lib.mlb_apply(b.ptr, _lib.ptr(x), _lib.ptr(y), a, -1.0, K0, flags, _sp()))
             return y
 
-        ys = lanczos_fn_apply_dev(apply_sorted, layer.n, vs, fn, krylov_dim, tol)
+        ys = lanczos_fn_apply_dev(apply_sorted, layer.n, vs, fn, krylov_dim, tol,
+                                  fused=(b.ptr, a, -1.0, K0, flags))
         if out_scale != 1.0:
             ys.mul_(out_scale)
         _lib.check(lib.mlb_to_node(b.ptr, _lib.ptr(ys), _lib.ptr(out), int(accumulate), _sp()))

@@ -66,6 +66,22 @@ def test_batched_pksm_is_bitwise_sequential():
         bat = torch.zeros_like(v)
         pksm_layers_dev(layers, p, v, bat, 1.0)
         assert torch.equal(seq, bat)
+    # the device's run-ahead depth changes no value (discarded steps only)
+    import os
+    res = []
+    for depth in ("1", "3"):
+        os.environ["MLB_PKSM_DEPTH"] = depth
+        try:
+            a = torch.zeros_like(v)
+            for layer in layers:
+                pksm_layer_dev(layer, -1.0, v, a, 1.0, True)
+            b = torch.zeros_like(v)
+            pksm_layers_dev(layers, -1.0, v, b, 1.0)
+        finally:
+            del os.environ["MLB_PKSM_DEPTH"]
+        assert torch.equal(a, b)
+        res.append(a)
+    assert torch.equal(res[0], res[1])
 
 
 def test_power_mean_eigs_match_golden():
