@@ -72,7 +72,11 @@ struct StageCfg {
     static constexpr int reach = (r0 > r1 ? (r0 > r2 ? r0 : r2) : (r1 > r2 ? r1 : r2));
     // d = 3: even stride so the broadcast axis-2 row is read as 16-byte pairs
     static constexpr bool vec2 = (D == 3) && (C::NPASS == 1 || C::SP % 2 == 0);
-    static constexpr int pad = vec2 ? (reach + (reach & 1)) : ((reach % 2) ? reach : reach + 1);
+    // d = 2 (grouped lanes, see spread_kernel): stride = 1 mod 8 doubles, so
+    // the 8 point rows x 2 interleaved offsets one load touches are 16
+    // distinct 8-byte bank pairs
+    static constexpr int pad2 = ((C::S + 6) / 8) * 8 + 1;
+    static constexpr int pad = (D == 2) ? pad2 : (vec2 ? (reach + (reach & 1)) : ((reach % 2) ? reach : reach + 1));
 };
 
 struct FsArgs {
@@ -165,8 +169,11 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     const int TL = a.g.TL;
     const int tile = a.tile_cells;
     double* my_tile = smem + (size_t)warp * tile;
-    double* my_stage = smem + (size_t)nw * tile + (size_t)warp * 32 * D * SPAD;
-    for (int i = lane; i < 32 * D * SPAD; i += 32) my_stage[i] = 0.0;
+    // (d = 2: + 8 doubles so the grouped reads of the last row's unused
+    // offsets stay inside the warp's staging)
+    constexpr int STAGE = 32 * D * SPAD + (D == 2 ? 8 : 0);
+    double* my_stage = smem + (size_t)nw * tile + (size_t)warp * STAGE;
+    for (int i = lane; i < STAGE; i += 32) my_stage[i] = 0.0;
     for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
     pdl_wait();  // v (and the partial grids' previous readers) are stream predecessors
 
@@ -178,6 +185,24 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     const int nwarps = gridDim.x * nw;
     const bool sorted = (flags & MLB_SORTED) != 0;
     const bool use_isd = (flags & MLB_USE_ISD) != 0;
+
+    // d = 2: 8 groups of 4 lanes; group g accumulates points g, g + 8, ... of
+    // a sub-chunk, lane (a, b) of a group owns the interleaved stencil block
+    // rows a + 2i x cols b + 2k (GB x GB entries, GB = ceil(S / 2)): per
+    // point 2 GB loads feed GB^2 FMAs, and all 32 lanes are busy.  The groups'
+    // blocks meet by a fixed xor-shuffle tree at every flush.
+    constexpr int GB = (S + 1) / 2;
+    const int g2 = lane >> 2, a2 = (lane >> 1) & 1, b2 = lane & 1;
+    double acc2[(D == 2) ? GB : 1][(D == 2) ? GB : 1];
+    if constexpr (D == 2) {
+#pragma unroll
+        for (int i = 0; i < GB; ++i)
+#pragma unroll
+            for (int k = 0; k < GB; ++k) acc2[i][k] = 0.0;
+    }
+    (void)g2;
+    (void)a2;
+    (void)b2;
 
     for (int pass = 0; pass < C::NPASS; ++pass) {
         const int off2 = pass * C::SP;
@@ -191,6 +216,23 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
         int cur = -1;
 
         auto flush = [&](int cell) {
+            if constexpr (D == 2) {
+                if (cell < 0) return;
+                if (flags & (1u << 18)) return;  // ablation (profiling only)
+#pragma unroll
+                for (int i = 0; i < GB; ++i)
+#pragma unroll
+                    for (int k = 0; k < GB; ++k) {
+                        double v = acc2[i][k];
+                        v += __shfl_xor_sync(0xffffffffu, v, 4);
+                        v += __shfl_xor_sync(0xffffffffu, v, 8);
+                        v += __shfl_xor_sync(0xffffffffu, v, 16);
+                        const int o0 = a2 + 2 * i, o1 = b2 + 2 * k;
+                        if (g2 == 0 && o0 < S && o1 < S) my_tile[cell + o0 * TL1 + o1] += v;
+                        acc2[i][k] = 0.0;
+                    }
+                return;
+            }
             if (!active || cell < 0) return;
             if (flags & (1u << 18)) return;  // ablation (profiling only)
 #pragma unroll
@@ -291,7 +333,21 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
             double f2[D], s2, v2;
             load_data(d2, n2, f2, s2, v2);
             __syncwarp();
-            if (active && !(flags & (1u << 16))) {  // bit 16: ablation (profiling only)
+            if (D == 2 && !(flags & (1u << 16))) {
+                // grouped lanes: 8 points per step (rows past np carry v = 0)
+                for (int j0 = 0; j0 < np; j0 += 8) {
+                    const double* ws = my_stage + (j0 + g2) * D * SPAD;
+                    double w0[GB], w1[GB];
+#pragma unroll
+                    for (int i = 0; i < GB; ++i) w0[i] = ws[a2 + 2 * i];
+#pragma unroll
+                    for (int k = 0; k < GB; ++k) w1[k] = ws[SPAD + b2 + 2 * k];
+#pragma unroll
+                    for (int i = 0; i < GB; ++i)
+#pragma unroll
+                        for (int k = 0; k < GB; ++k) acc2[i][k] = fma(w0[i], w1[k], acc2[i][k]);
+                }
+            } else if (active && !(flags & (1u << 16))) {  // bit 16: ablation (profiling only)
                 // rows past np carry v = 0, so the loop may run to an even count;
                 // the next point's windows are loaded while this one accumulates
                 auto ldw = [&](int j, double* w0, double* w1, double* w2) {
@@ -1044,7 +1100,7 @@ static FsArgs make_args(mlb_binding* b) {
 
 template <int D, int M>
 static size_t spread_smem(int nw, int tile_cells) {
-    return (size_t)nw * tile_cells * 8 + (size_t)nw * 32 * D * StageCfg<D, M>::pad * 8;
+    return (size_t)nw * tile_cells * 8 + (size_t)nw * (32 * D * StageCfg<D, M>::pad + (D == 2 ? 8 : 0)) * 8;
 }
 
 template <int D, int M>
