@@ -156,7 +156,7 @@ __device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps
     return sub_first(a, p.seg + nwarps);
 }
 
-template <int D, int M, bool PERSIST>
+template <int D, int M, bool PERSIST, bool GROUPED = false>
 __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, WinCoef wc,
                                                                     const double* __restrict__ v, unsigned flags,
                                                                     int* __restrict__ work) {
@@ -193,8 +193,9 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     // blocks meet by a fixed xor-shuffle tree at every flush.
     constexpr int GB = (S + 1) / 2;
     const int g2 = lane >> 2, a2 = (lane >> 1) & 1, b2 = lane & 1;
-    double acc2[(D == 2) ? GB : 1][(D == 2) ? GB : 1];
-    if constexpr (D == 2) {
+    constexpr bool G2 = (D == 2) && GROUPED;
+    double acc2[G2 ? GB : 1][G2 ? GB : 1];
+    if constexpr (G2) {
 #pragma unroll
         for (int i = 0; i < GB; ++i)
 #pragma unroll
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
         int cur = -1;
 
         auto flush = [&](int cell) {
-            if constexpr (D == 2) {
+            if constexpr (G2) {
                 if (cell < 0) return;
                 if (flags & (1u << 18)) return;  // ablation (profiling only)
 #pragma unroll
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
             double f2[D], s2, v2;
             load_data(d2, n2, f2, s2, v2);
             __syncwarp();
-            if (D == 2 && !(flags & (1u << 16))) {
+            if (G2 && !(flags & (1u << 16))) {
                 // grouped lanes: 8 points per step (rows past np carry v = 0)
                 for (int j0 = 0; j0 < np; j0 += 8) {
                     const double* ws = my_stage + (j0 + g2) * D * SPAD;
@@ -1116,7 +1117,12 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
         const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
         if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
-        auto kern = spread_kernel<D, M, true>;
+        // grouped d = 2 lanes pay off on large layers (config 4: 622 -> 498
+        // us); at config-2 size the plain lane blocks leave more room for
+        // the concurrently running d = 3 layer (step 3.96 vs 3.86e9)
+        bool grouped = D == 2 && b->n >= (1 << 20);
+        if (const char* env = std::getenv("MLB_D2_GROUPED")) grouped = D == 2 && env[0] == '1';  // tests / tuning
+        auto kern = grouped ? spread_kernel<D, M, true, true> : spread_kernel<D, M, true, false>;
         MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int blocks = std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);
         if (blocks < 1) blocks = 1;

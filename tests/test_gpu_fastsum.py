@@ -84,6 +84,15 @@ def test_stages_match_oracle(d, N, m, sigma):
     idx = np.mod(np.arange(ulo, ulo + L), op.ng)
     sub = full[np.ix_(*([idx] * d))]
     assert rel(grid.cpu().numpy().reshape((L,) * d), sub) < 1e-13
+    if d == 2:  # the grouped-lane spread (large layers) on the same points
+        import os
+        os.environ["MLB_D2_GROUPED"] = "1"
+        try:
+            g2 = torch.zeros_like(grid)
+            _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(vd), _lib.ptr(g2), 0, _lib.stream_ptr()))
+        finally:
+            del os.environ["MLB_D2_GROUPED"]
+        assert rel(g2.cpu().numpy().reshape((L,) * d), sub) < 1e-13
     # convolution
     out = torch.zeros_like(grid)
     _lib.check(lib.mlb_convolve(b.ptr, _lib.ptr(grid), _lib.ptr(out), _lib.stream_ptr()))
