@@ -55,6 +55,8 @@ def _compile(src):
 
 def build(force=False, verbose=False):
     if not force and not needs_build():
+        if verbose:
+            print(f"up to date: {LIB}")
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
