@@ -19,7 +19,7 @@ namespace mlb {
 
 constexpr int kAcMaxM = 32;     // classes
 constexpr int kAcRows = 128;    // rows per tile
-constexpr int kAcBlocks = 148 * 6;  // fixed partition (6 CTAs per SM)
+constexpr int kAcBlocks = 148 * 6;  // partition capacity (6 CTAs per B200 SM); launches use <= this
 
 // well force for one row (m <= kAcMaxM), leave-one-out products as the reference
 __device__ void well_force_row(const double* u, int m, double* t) {
@@ -907,7 +907,7 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
     cudaStream_t st = (cudaStream_t)stream;
     // row partition: ~1k rows per CTA, between one and six CTAs per SM
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(
-        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(148, n / 1024))));
+        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(device_sms(), n / 1024))));
     double* partial = work;
     double* mx = work + (int64_t)kAcBlocks * k * m;
     double* Vc = mx + 2 * kAcBlocks;
@@ -954,7 +954,7 @@ int mlb_ac_step2(const double* Phi, int64_t n, int k, int m, const double* U, co
     if (k < 1 || k * m > 16 * 256) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels need k*m <= 4096");
     cudaStream_t st = (cudaStream_t)stream;
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(
-        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(148, n / 1024))));
+        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(device_sms(), n / 1024))));
     double* partial = work;
     double* mx = work + (int64_t)kAcBlocks * k * m;
     double* Vc = mx + 2 * kAcBlocks;
@@ -1018,7 +1018,7 @@ int mlb_gl_energy_partials(const double* Phi, int64_t n, int k, int m, const dou
 
 int mlb_argmax_rows(const double* U, int64_t n, int m, int32_t* labels, void* stream) {
     if (n <= 0) return MLB_OK;
-    int64_t b = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    int64_t b = std::min<int64_t>((n + 255) / 256, (int64_t)device_sms() * 16);
     argmax_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(U, n, m, labels);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());

@@ -37,6 +37,18 @@ bool pdl_enabled() {
 
 void set_error(const std::string& msg) { g_err = msg; }
 
+int device_sms(int device) {
+    static int cache[64] = {0};
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) return 148;
+    if (device >= 64) device = 63;
+    if (cache[device] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) n = 148;
+        cache[device] = n;
+    }
+    return cache[device];
+}
+
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -112,6 +124,7 @@ int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
     DeviceGuard guard(device);
     mlb_plan* p = new mlb_plan();
     p->device = device;
+    p->nsm = device_sms(device);
     Geom& g = p->g;
     g.d = d;
     g.N = N;
@@ -228,6 +241,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (n < 0 || n >= (int64_t)1 << 31) return fail(MLB_ERR_ARG, "n out of range");
     const Geom& g = plan->g;
     const int d = g.d, Tb = g.Tb, nbr = g.nbr, TL = g.TL;
+    const int nsm = plan->nsm;
     const int bin_lo = g.ulo + g.m;
     // 1. cells and fractional offsets, exactly as _make_binding computes
     //    tx = ng * (x * scale); u = floor(tx) (fastsum.py:343-353, :386)
@@ -357,9 +371,9 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     // segments (one warp's work unit): <= kSegPoints points of one brick,
     // never splitting a chunk; a bit smaller when n is small so every SM
     // gets work
-    // (large n: grow segments so the partial tiles stay ~ 148 x 16 of them)
-    int seg_points = (int)std::max<int64_t>(kSegPoints, n / (148 * 16));
-    while (seg_points > 64 && (n / seg_points) < 148 * 8) seg_points /= 2;
+    // (large n: grow segments so the partial tiles stay ~ nsm x 16 of them)
+    int seg_points = (int)std::max<int64_t>(kSegPoints, n / (nsm * 16));
+    while (seg_points > 64 && (n / seg_points) < nsm * 8) seg_points /= 2;
     if (const char* env = std::getenv("MLB_SEG_POINTS")) seg_points = std::max(32, std::atoi(env));  // tuning
     std::vector<int32_t> seg_chunk, seg_brick, brick_seg(nbricks + 1, 0);
     for (int c = 0; c < nch;) {
@@ -394,7 +408,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (d == 3 && n > 0) {
         // points per block: >= 1024, and at large n about one CTA's share, so
         // a heavy cell splits into few parts (every part is a merge row set)
-        int cap = (int)std::max<int64_t>(1024, ((n / (148 * 2)) + 31) / 32 * 32);
+        int cap = (int)std::max<int64_t>(1024, ((n / (nsm * 2)) + 31) / 32 * 32);
         if (const char* env = std::getenv("MLB_CELL_CAP")) cap = std::max(32, std::atoi(env) / 32 * 32);  // tuning
         brick_blk.assign(nbricks + 1, 0);
         for (int64_t k = 0; k < nkeys; ++k) {
@@ -448,7 +462,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         std::vector<int> iord(items.size());
         for (size_t i = 0; i < items.size(); ++i) iord[i] = (int)i;
         std::stable_sort(iord.begin(), iord.end(), [&](int x, int y) { return items[x].cost > items[y].cost; });
-        ncta_cells = std::min<int>((int)items.size(), 148 * 2);
+        ncta_cells = std::min<int>((int)items.size(), nsm * 2);
         // longest-processing-time-first: each item goes to the least loaded CTA
         std::vector<std::vector<int>> cta_items(ncta_cells);
         {
@@ -597,7 +611,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     if (rc == MLB_OK) rc = dev_upload<int>(&b->work, nullptr, 1);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
     // d <= 2: one partial grid per spread CTA (<= 2 per SM); d = 3: one per segment
-    b->spread_parts_max = 148 * 2;
+    b->spread_parts_max = nsm * 2;
     const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)std::max(1, b->nactive);  // d = 3: brick tiles
     if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, nparts * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells + 2);
@@ -659,7 +673,7 @@ __global__ void scatter_perm_kernel(const int32_t* __restrict__ perm, const doub
 }
 static int grid_for(int64_t n) {
     int64_t b = (n + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > device_sms() * 16) b = device_sms() * 16;
     return (int)(b < 1 ? 1 : b);
 }
 }  // namespace mlb

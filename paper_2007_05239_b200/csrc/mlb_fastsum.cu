@@ -1107,9 +1107,7 @@ static size_t spread_smem(int nw, int tile_cells) {
 template <int D, int M>
 static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st) {
     FsArgs a = make_args(b);
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nsm = device_sms();
     (void)nsm;
     if constexpr (D <= 2) {
         // persistent CTAs of 8 warps, one partial grid per CTA
@@ -1165,12 +1163,7 @@ static int gather_dmp(mlb_binding* b, const double* grid, const double* v, doubl
         MLB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
         if (per_sm < 1) per_sm = 1;
     }
-    int nsm = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = device_sms();
     int blocks = nsm * per_sm;
     const int need = ((D == 3 && PK ? b->ngrp : b->nchunks) + 7) / 8;  // at least one unit per warp
     if (blocks > need) blocks = need;
@@ -1257,7 +1250,7 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     }
     const int64_t total = b->grid_cells;
     int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > device_sms() * 8) blocks = device_sms() * 8;
     if (Tb == 2) reduce_kernel<3, 2><<<(int)blocks, 256, 0, st>>>(a, grid);
     else reduce_kernel<3, 0><<<(int)blocks, 256, 0, st>>>(a, grid);
     note_launches(1);

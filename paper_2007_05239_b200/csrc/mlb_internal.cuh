@@ -22,6 +22,7 @@ int fail(int code, const std::string& msg);
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();  // MLB_NO_PDL=1 disables (A/B)
+int device_sms(int device = -1);  // SM count of `device` (-1: current), cached
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
@@ -79,6 +80,7 @@ struct Geom {
 
 struct mlb_plan {
     int device;
+    int nsm;                     // SM count of the device (grid sizing at bind time)
     mlb::Geom g;
     mlb::WinCoef wc;
     double* fused = nullptr;     // band weights (K^(d-1) x Kh)

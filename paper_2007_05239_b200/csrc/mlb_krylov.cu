@@ -16,7 +16,7 @@ namespace mlb {
 
 constexpr int kRedThreads = 256;
 constexpr int kMaxRowBlocks = 256;
-constexpr int kFusedBlocks = 296;  // fused CGS2 row blocks (2 per SM)
+constexpr int kFusedBlocks = 296;  // CGS2 row-block capacity (2 per B200 SM); launches use min(this, 2 x SMs)
 
 static int row_blocks(int64_t n) {
     int64_t b = (n + 2047) / 2048;
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restric
 
 static int cgs2_fused(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out, double* h1_out,
                       double* nrm2_out, double* work, cudaStream_t st) {
-    const int nb = std::max(1, std::min(kFusedBlocks, (int)((n + kTileRows - 1) / kTileRows)));
+    const int nb = std::max(1, std::min(std::min(kFusedBlocks, 2 * device_sms()), (int)((n + kTileRows - 1) / kTileRows)));
     double* part = work;                              // nb x cols
     double* npart = part + (int64_t)kFusedBlocks * 64;  // nb
     double* h1 = npart + kFusedBlocks;                 // cols
@@ -318,7 +318,7 @@ static int cgs2_fused(const double* V, int64_t ld, int64_t n, int cols, double* 
 
 static int ew_grid(int64_t n) {
     int64_t b = (n + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > device_sms() * 16) b = device_sms() * 16;
     return (int)(b < 1 ? 1 : b);
 }
 
@@ -351,7 +351,7 @@ int mlb_gemv_t(const double* V, int64_t ld, int64_t n, int cols, const double* w
 int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c, double* y, double scale,
                int accumulate, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    const int nb = std::max(1, std::min(148 * 4, (int)((n + 255) / 256)));
+    const int nb = std::max(1, std::min(device_sms() * 4, (int)((n + 255) / 256)));
     gemv_n_kernel<<<nb, 256, cols * sizeof(double), st>>>(V, ld, n, cols, c, y, scale, accumulate, nullptr);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
