@@ -428,19 +428,14 @@ def _lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None
     dim = int(min(krylov_dim, n))
     if dim < 1:
         raise ConfigError(f"krylov_dim must be >= 1, got {krylov_dim}")
-    buf = torch.empty(2, dtype=torch.float64, device=v.device)
-    dot(v, v, buf[0:1])
-    nv = float(np.sqrt(buf[0].item()))
-    if nv == 0.0:
-        if out is None:
-            return torch.zeros_like(v)
-        if not accumulate:
-            out.zero_()
-        return out
+    # AB: h1 row (alpha_j at j) | ||w_j||^2 | <v, v>; V[0] = v / sqrt(<v, v>)
+    # on the device (no start-of-solve sync: <v, v> arrives with step 0)
+    AB = torch.zeros(2 * dim + 1, dtype=torch.float64, device=v.device)
+    vv = AB[2 * dim:2 * dim + 1]
+    dot(v, v, vv)
     V = _krylov_basis(v.device, 0, dim, n)
-    axpby(1.0 / nv, v, 0.0, V[0])
-    AB = torch.zeros((2, dim), dtype=torch.float64, device=v.device)
-    ABh = _pinned_snapshots((dim, 2, dim))
+    scale_by(v, V[0], vv, -0.5)
+    ABh = _pinned_snapshots((dim, 2 * dim + 1))
     stream = torch.cuda.current_stream(v.device)
     chain = _Chain(V, AB, stream, apply_dev=apply_dev, fused=fused)
     events = [None] * dim
@@ -460,10 +455,20 @@ def _lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None
         issued += 1
     c_prev = None
     s = 0
+    nv = None
     while True:
         events[s].synchronize()
-        alphas[s] = ABh[s, 0, s].item()
-        beta = float(np.sqrt(max(ABh[s, 1, s].item(), 0.0)))
+        snap = ABh[s].numpy()
+        if nv is None:
+            nv = float(np.sqrt(snap[2 * dim]))
+            if nv == 0.0:  # (the queued steps ran on v / 0 and are discarded)
+                if out is None:
+                    return torch.zeros_like(v)
+                if not accumulate:
+                    out.zero_()
+                return out
+        alphas[s] = snap[s]
+        beta = float(np.sqrt(max(snap[dim + s], 0.0)))
         betas[s] = beta
         s += 1
         lam, Q = np.linalg.eigh(_tridiag(alphas, betas, s))
@@ -548,25 +553,18 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
     T = len(layers)
     dev = v_node.device
     st = [_LayerPksm(layer, v_node, dim, None) for layer in layers]
-    nrm = torch.empty(T, dtype=torch.float64, device=dev)
-    for t, x in enumerate(st):
-        dot(x.vs, x.vs, nrm[t:t + 1])
-    nv2 = nrm.cpu().numpy()
-    AB = torch.zeros((T, 2, dim), dtype=torch.float64, device=dev)
-    ABh = _pinned_snapshots((dim, T, 2, dim))
-    for t, x in enumerate(st):
-        x.nv = float(np.sqrt(nv2[t]))
-        if x.nv == 0.0:
-            x.done = True
-            x.ys = None
-        else:
-            x.V = _krylov_basis(dev, t, dim, n)
-            axpby(1.0 / x.nv, x.vs, 0.0, x.V[0])
+    # per layer AB row: h1 row (alpha_j at j) | ||w_j||^2 | <v, v>; V[0] on
+    # the device, <v, v> read with step 0 (no start-of-solve sync)
+    AB = torch.zeros((T, 2 * dim + 1), dtype=torch.float64, device=dev)
+    ABh = _pinned_snapshots((dim, T, 2 * dim + 1))
     stream = torch.cuda.current_stream(dev)
     for t, x in enumerate(st):
-        if not x.done:
-            x.chain = _Chain(x.V, AB[t], stream, fused=(x.b.ptr, x.a, -1.0, x.K0,
-                                                         _lib.MLB_USE_ISD | _lib.MLB_SORTED))
+        vv = AB[t, 2 * dim:2 * dim + 1]
+        dot(x.vs, x.vs, vv)
+        x.V = _krylov_basis(dev, t, dim, n)
+        scale_by(x.vs, x.V[0], vv, -0.5)
+        x.chain = _Chain(x.V, AB[t], stream, fused=(x.b.ptr, x.a, -1.0, x.K0,
+                                                     _lib.MLB_USE_ISD | _lib.MLB_SORTED))
     events = [None] * dim
 
     def issue(j):  # step j of every layer still running at the host's last decision
@@ -590,8 +588,14 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
         for t, x in enumerate(st):
             if x.done:
                 continue
-            x.alphas[s] = snap[t, 0, s]
-            beta = float(np.sqrt(max(snap[t, 1, s], 0.0)))
+            if x.nv is None:
+                x.nv = float(np.sqrt(snap[t, 2 * dim]))
+                if x.nv == 0.0:  # zero input: nothing to add (queued steps are discarded)
+                    x.done = True
+                    x.ys = None
+                    continue
+            x.alphas[s] = snap[t, s]
+            beta = float(np.sqrt(max(snap[t, dim + s], 0.0)))
             x.betas[s] = beta
             lam, Q = np.linalg.eigh(_tridiag(x.alphas, x.betas, ss))
             c = x.nv * (Q @ (fn(lam) * Q[0, :]))
