@@ -132,6 +132,22 @@ int mlb_grid_cells(const mlb_binding* b, int64_t* cells, int* L, int* u_lo);
 int mlb_spread(mlb_binding* b, const double* v_dev, double* grid_dev, unsigned flags, void* stream);
 /* the deterministic partial-tile reduction of the last spread into grid_dev */
 int mlb_reduce(mlb_binding* b, double* grid_dev, void* stream);
+
+/* Node-range sharding (the per-matvec sum of the ranks'
+ * sub-box grids; replaces the all-reduce of dist.py's NCCL path): spread
+ * this rank's points and let the final reduction kernel store the grid
+ * straight into every rank's receive buffer -- peer_slots[q] = this rank's
+ * slot (rank * cells) in rank q's buffer, device pointers (own buffer or
+ * CUDA-IPC-mapped peer memory over NVLink), world <= 8.  After a barrier
+ * every rank sums its buffer's slots in rank order (mlb_grid_sum_slots):
+ * bitwise the same grid on all ranks. */
+int mlb_spread_peers(mlb_binding* b, const double* v_dev, double* const* peer_slots, int world, unsigned flags,
+                     void* stream);
+int mlb_grid_sum_slots(const double* recv_dev, int world, int64_t cells, double* grid_dev, void* stream);
+/* CUDA IPC of device buffers (64-byte handles) for the peer slots above */
+int mlb_ipc_handle(const void* dev_ptr, unsigned char* handle64);
+int mlb_ipc_open(const unsigned char* handle64, int device, void** dev_ptr);
+int mlb_ipc_close(void* dev_ptr);
 int mlb_convolve(mlb_binding* b, const double* grid_in_dev, double* grid_out_dev, void* stream);
 int mlb_gather(mlb_binding* b, const double* grid_dev, double* y_dev, unsigned flags, void* stream);
 

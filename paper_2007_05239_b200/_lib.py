@@ -54,6 +54,11 @@ SIGNATURES = {
     "mlb_grid_cells": (I, [P, P, P, P]),
     "mlb_spread": (I, [P, P, P, U, P]),
     "mlb_reduce": (I, [P, P, P]),
+    "mlb_spread_peers": (I, [P, P, P, I, U, P]),
+    "mlb_grid_sum_slots": (I, [P, I, I64, P, P]),
+    "mlb_ipc_handle": (I, [P, P]),
+    "mlb_ipc_open": (I, [P, I, P]),
+    "mlb_ipc_close": (I, [P]),
     "mlb_convolve": (I, [P, P, P, P]),
     "mlb_gather": (I, [P, P, P, U, P]),
     "mlb_band_dft": (I, [P, P, P, I, P]),

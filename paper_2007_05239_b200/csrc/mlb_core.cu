@@ -724,6 +724,58 @@ int mlb_spread(mlb_binding* b, const double* v, double* grid, unsigned flags, vo
     return launch_reduce(b, grid, st);
 }
 
+int mlb_spread_peers(mlb_binding* b, const double* v, double* const* peer_slots, int world, unsigned flags,
+                     void* stream) {
+    if (!b || !peer_slots) return fail(MLB_ERR_ARG, "null argument");
+    if (world < 1 || world > kMaxPeers) return fail(MLB_ERR_ARG, "world size outside [1, 8]");
+    DeviceGuard guard(b->plan->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    PeerOut po{};
+    po.n = world;
+    for (int q = 0; q < world; ++q) {
+        if (!peer_slots[q]) return fail(MLB_ERR_ARG, "null peer slot");
+        po.p[q] = peer_slots[q];
+    }
+    if (b->nseg == 0) {
+        for (int q = 0; q < world; ++q)
+            MLB_CUDA_TRY(cudaMemsetAsync(po.p[q], 0, b->grid_cells * sizeof(double), st));
+        return MLB_OK;
+    }
+    int rc = launch_spread(b, v, flags & ~MLB_SPREAD_ONLY, st);
+    if (rc != MLB_OK) return rc;
+    return launch_reduce(b, nullptr, st, &po);
+}
+
+int mlb_grid_sum_slots(const double* recv, int world, int64_t cells, double* grid, void* stream) {
+    if (!recv || !grid) return fail(MLB_ERR_ARG, "null argument");
+    if (world < 1) return fail(MLB_ERR_ARG, "world size must be >= 1");
+    return launch_slot_sum(recv, world, cells, grid, (cudaStream_t)stream);
+}
+
+int mlb_ipc_handle(const void* dev_ptr, unsigned char* handle64) {
+    if (!dev_ptr || !handle64) return fail(MLB_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    MLB_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    return MLB_OK;
+}
+
+int mlb_ipc_open(const unsigned char* handle64, int device, void** dev_ptr) {
+    if (!handle64 || !dev_ptr) return fail(MLB_ERR_ARG, "null argument");
+    DeviceGuard guard(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    MLB_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return MLB_OK;
+}
+
+int mlb_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return MLB_OK;
+    MLB_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+    return MLB_OK;
+}
+
 int mlb_reduce(mlb_binding* b, double* grid, void* stream) {
     if (!b || !grid) return fail(MLB_ERR_ARG, "null argument");
     DeviceGuard guard(b->plan->device);

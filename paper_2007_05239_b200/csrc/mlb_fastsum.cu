@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick
 // d <= 2: grid[u] = sum over the spread CTAs' partial grids.  Block = 8
 // cells x 32 slices; slice k sums partials k, k+32, ...; the 32 slice sums
 // combine through a fixed shuffle tree -> deterministic.
-__global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, int cells, double* __restrict__ grid) {
+__global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, int cells, PeerOut grid) {
     const int slice = threadIdx.x & 31;
     const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
     double s = 0.0;
@@ -763,13 +763,14 @@ __global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, 
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     pdl_launch();
-    if (slice == 0 && cell < cells) grid[cell] = s;
+    if (slice == 0 && cell < cells) po_store(grid, cell, s);
+    if (grid.n > 1) __threadfence_system();  // peer stores ordered before the exchange barrier
 }
 
 // Stage R2: grid[u] = sum over the (<= 3^d) bricks whose tile covers u of
 // that brick's (first-segment) tile value.  One thread per active cell.
 template <int D, int TBC>
-__global__ void reduce_kernel(FsArgs a, double* __restrict__ grid) {
+__global__ void reduce_kernel(FsArgs a, PeerOut grid) {
     const Geom g = a.g;
     const int L = g.L, nbr = g.nbr;
     const int Tb = TBC ? TBC : g.Tb;
@@ -812,15 +813,16 @@ __global__ void reduce_kernel(FsArgs a, double* __restrict__ grid) {
                     const int s0 = __ldg(a.brick_first + brick);
                     if (s0 >= 0) s += a.partial[(size_t)s0 * a.tile_cells + t];
                 }
-        grid[cidx] = s;
+        po_store(grid, cidx, s);
     }
+    if (grid.n > 1) __threadfence_system();
 }
 
 // Stage R2 for d = 3, block-centric: a CTA covers GB grid blocks of Tb^3
 // cells; the <= R^3 source brick tiles of each grid block are resolved once
 // into smem base pointers, then every cell issues its independent loads.
 template <int TB, int M>
-__global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restrict__ grid) {
+__global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, PeerOut grid) {
     constexpr int CPB = TB * TB * TB;  // cells per grid block
     constexpr int GB = 256 / CPB;      // grid blocks per CTA
     constexpr int TL = TB + 2 * M;
@@ -864,7 +866,8 @@ __global__ void __launch_bounds__(256) reduce3_kernel(FsArgs a, double* __restri
         sum += ok ? __ldcg(p + local) : 0.0;
     }
     pdl_launch();
-    grid[((int64_t)u0 * L + u1) * L + u2] = sum;
+    po_store(grid, ((int64_t)u0 * L + u1) * L + u2, sum);
+    if (grid.n > 1) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ gather --
@@ -1207,8 +1210,15 @@ int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t 
     MLB_DISPATCH_DM(spread_dm, g.d, g.m, b, v, flags, st);
 }
 
-int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
+int launch_reduce(mlb_binding* b, double* grid_local, cudaStream_t st, const PeerOut* peers) {
     FsArgs a = make_args(b);
+    PeerOut grid{};
+    if (peers) {
+        grid = *peers;
+    } else {
+        grid.p[0] = grid_local;
+        grid.n = 1;
+    }
     const Geom& G = b->plan->g;
     if (G.d <= 2) {
         // the spread left one partial grid per CTA
@@ -1253,6 +1263,24 @@ int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st) {
     if (blocks > device_sms() * 8) blocks = device_sms() * 8;
     if (Tb == 2) reduce_kernel<3, 2><<<(int)blocks, 256, 0, st>>>(a, grid);
     else reduce_kernel<3, 0><<<(int)blocks, 256, 0, st>>>(a, grid);
+    note_launches(1);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+// grid[i] = sum over ranks r (in rank order) of recv[r * cells + i]
+__global__ void slot_sum_kernel(const double* __restrict__ recv, int world, int64_t cells, double* __restrict__ grid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cells; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < world; ++r) s += __ldcg(recv + (int64_t)r * cells + i);
+        grid[i] = s;
+    }
+}
+
+int launch_slot_sum(const double* recv, int world, int64_t cells, double* grid, cudaStream_t st) {
+    if (cells <= 0) return MLB_OK;
+    const int blocks = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)device_sms() * 8);
+    slot_sum_kernel<<<blocks, 256, 0, st>>>(recv, world, cells, grid);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;

@@ -22,6 +22,21 @@ int fail(int code, const std::string& msg);
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();  // MLB_NO_PDL=1 disables (A/B)
+
+// Outputs of the final grid reduction (R2): the local grid, or -- node-range
+// sharding over NVLink -- this rank's slot in every peer's receive buffer
+// (P2P stores from the reduction kernel itself: the spread's grid exchange
+// is fused into the kernel that produces the grid).
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+    double* p[kMaxPeers];
+    int n;
+};
+__device__ __forceinline__ void po_store(const PeerOut& o, int64_t i, double v) {
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+        if (q < o.n) o.p[q][i] = v;
+}
 int device_sms(int device = -1);  // SM count of `device` (-1: current), cached
 
 template <typename... KArgs, typename... Args>
@@ -145,7 +160,8 @@ struct mlb_binding {
 namespace mlb {
 // kernels launchers (mlb_fastsum.cu)
 int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st);
-int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st);
+int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st, const PeerOut* peers = nullptr);
+int launch_slot_sum(const double* recv, int world, int64_t cells, double* grid, cudaStream_t st);
 int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_t st);
 int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                   double beta, double gamma, unsigned flags, cudaStream_t st);

@@ -23,6 +23,7 @@ an engine built from the numpy oracle, which is how the partitioning logic
 is verified with gloo at world_size 2 without GPUs.
 """
 
+import ctypes
 import math
 
 import numpy as np
@@ -184,6 +185,15 @@ class BindingEngine:
         _lib.check(_lib.lib().mlb_spread(self.binding.ptr, _lib.ptr(x), _lib.ptr(g), 0, _lib.stream_ptr()))
         return g
 
+    def enable_peer_exchange(self, comm):
+        """Use the fused NVLink peer exchange for the grid sum (PeerGridExchange)."""
+        self.exchange = PeerGridExchange(comm, self.cells, self.device)
+        return self
+
+    def spread_summed(self, x):
+        """The spread grid summed over the ranks through the peer exchange."""
+        return self.exchange.spread_sum(self.binding, x, self.new_grid())
+
     def convolve(self, g):
         out = _torch().empty_like(g)
         _lib.check(_lib.lib().mlb_convolve(self.binding.ptr, _lib.ptr(g), _lib.ptr(out), _lib.stream_ptr()))
@@ -193,6 +203,72 @@ class BindingEngine:
         y = _torch().empty(self.binding.n, dtype=_torch().float64, device=g.device)
         _lib.check(_lib.lib().mlb_gather(self.binding.ptr, _lib.ptr(g), _lib.ptr(y), 0, _lib.stream_ptr()))
         return y
+
+
+class PeerGridExchange:
+    """The per-matvec sum of the ranks' sub-box grids over NVLink peer memory.
+
+    Every rank owns a receive buffer of `world` grid slots; the buffers are
+    mapped into every peer with CUDA IPC once.  Each matvec the final spread
+    reduction kernel of rank r stores its grid straight into slot r of every
+    rank's buffer (mlb_spread_peers: the exchange is fused into the kernel
+    that produces the grid, P2P stores), a one-element NCCL all-reduce on
+    the stream orders those stores before any reader, and each rank sums its
+    slots in rank order (mlb_grid_sum_slots) -- bitwise the same grid
+    everywhere, with no all-gather of the grids through NCCL.
+
+    `slots` may be supplied directly (single-process tests emulate ranks with
+    local buffers); otherwise they are built from IPC handles exchanged over
+    the process group.  Not available (ValueError) for world > 8 or when
+    peer mapping fails; callers then use the NCCL path.
+    """
+
+    def __init__(self, comm, cells, device, recv=None, slots=None):
+        torch = _torch()
+        self.comm, self.cells, self.device = comm, int(cells), int(device)
+        world = 1 if comm is None else comm.world
+        rank = 0 if comm is None else comm.rank
+        if world > 8:
+            raise ValueError("peer grid exchange supports at most 8 ranks")
+        self.world, self.rank = world, rank
+        self.recv = recv if recv is not None else torch.zeros(world * self.cells, dtype=torch.float64,
+                                                               device=f"cuda:{self.device}")
+        self._opened = []
+        if slots is None:
+            lib = _lib.lib()
+            h = (ctypes.c_ubyte * 64)()
+            _lib.check(lib.mlb_ipc_handle(_lib.ptr(self.recv), h))
+            handles = [None] * world
+            comm.dist.all_gather_object(handles, bytes(h), group=comm.group)
+            bases = []
+            for q in range(world):
+                if q == rank:
+                    bases.append(self.recv.data_ptr())
+                    continue
+                ptr = ctypes.c_void_p()
+                buf = (ctypes.c_ubyte * 64).from_buffer_copy(handles[q])
+                _lib.check(lib.mlb_ipc_open(buf, self.device, ctypes.byref(ptr)))
+                self._opened.append(ptr)
+                bases.append(ptr.value)
+            slots = [b + 8 * rank * self.cells for b in bases]
+        self.slots = (ctypes.c_void_p * len(slots))(*slots)
+        self._flag = torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def spread_sum(self, binding, x, grid):
+        """grid = sum over ranks of their spreads (this rank spreads x)."""
+        lib = _lib.lib()
+        sp = _lib.stream_ptr()
+        _lib.check(lib.mlb_spread_peers(binding.ptr, _lib.ptr(x), self.slots, self.world, 0, sp))
+        if self.world > 1:  # every rank's peer stores precede every rank's reads
+            self.comm.dist.all_reduce(self._flag, group=self.comm.group)
+        _lib.check(lib.mlb_grid_sum_slots(_lib.ptr(self.recv), self.world, self.cells, _lib.ptr(grid), sp))
+        return grid
+
+    def close(self):
+        lib = _lib.lib()
+        for ptr in self._opened:
+            lib.mlb_ipc_close(ptr)
+        self._opened = []
 
 
 class ShardedLayer:
@@ -214,11 +290,14 @@ class ShardedLayer:
 
     def w_tilde(self, x):
         """(W~ x)_local: spread local charges, sum grids over ranks, convolve, gather."""
-        g = self.engine.spread(x)
-        if self.deterministic:
-            self.comm.ordered_sum(g)
+        if getattr(self.engine, "exchange", None) is not None:
+            g = self.engine.spread_summed(x)  # fused P2P exchange, rank-order sum
         else:
-            self.comm.all_reduce_sum(g)
+            g = self.engine.spread(x)
+            if self.deterministic:
+                self.comm.ordered_sum(g)
+            else:
+                self.comm.all_reduce_sum(g)
         return self.engine.gather(self.engine.convolve(g))
 
     def matvec(self, x):

@@ -265,8 +265,51 @@ def test_sharded_layer_single_rank_matches_layer():
         vd = torch.from_numpy(v).cuda()
         assert rel(sl.apply_lsym(vd).cpu().numpy(), apply_sym_laplacian(layer, v)) < 1e-12
         assert rel(sharded_pksm(sl, -1.0, vd).cpu().numpy(), pksm_apply(layer, -1.0, v)) < 1e-9
+        # the fused peer exchange (IPC handle of its own buffer, NCCL flag, slot sum)
+        sp = ShardedLayer(BindingEngine(plan, pts).enable_peer_exchange(Comm()), n, 0, n, Comm(), K0=1.0,
+                          shift=math.log(2.0)).build()
+        assert np.array_equal(sp.apply_lsym(vd).cpu().numpy(), sl.apply_lsym(vd).cpu().numpy())
     finally:
         dist.destroy_process_group()
+
+
+def test_peer_grid_exchange_two_emulated_ranks():
+    """mlb_spread_peers + mlb_grid_sum_slots with two ranks emulated on one
+    GPU (their receive buffers are local; the launches run one after the
+    other, nothing waits on another kernel): every rank's buffer ends with the
+    same grid, bitwise, equal to the one-binding spread."""
+    import torch
+    from paper_2007_05239_b200 import KernelSpec, build_plan, bind_points, _lib
+    from paper_2007_05239_b200.dist import PeerGridExchange
+    rng = np.random.default_rng(8)
+    n = 4000
+    for d, N, m in ((3, 32, 4), (2, 32, 4)):
+        pts = np.clip(rng.normal(0, 0.07, size=(n, d)), -0.21875, 0.21875)
+        v = rng.standard_normal(n)
+        plan = build_plan(KernelSpec("gaussian", 0.12), d=d, N=N, m_nfft=m, p_nfft=8)
+        full = bind_points(plan, pts)
+        cells = full.stats()["grid_cells"]
+        ref = torch.zeros(cells, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().mlb_spread(full.ptr, _lib.ptr(torch.from_numpy(v).cuda()), _lib.ptr(ref), 0,
+                                         _lib.stream_ptr()))
+        halves = [(0, n // 2), (n // 2, n)]
+        recv = [torch.full((2 * cells,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(2)]
+        grids = []
+        for r, (lo, hi) in enumerate(halves):
+            b = bind_points(plan, pts[lo:hi])
+            ex = PeerGridExchange(None, cells, 0, recv=recv[r],
+                                  slots=[recv[q].data_ptr() + 8 * r * cells for q in range(2)])
+            ex.world, ex.rank = 2, r
+            _lib.check(_lib.lib().mlb_spread_peers(b.ptr, _lib.ptr(torch.from_numpy(v[lo:hi]).cuda()), ex.slots, 2,
+                                                   0, _lib.stream_ptr()))
+            grids.append(ex)
+        out = []
+        for r in range(2):
+            g = torch.empty(cells, dtype=torch.float64, device="cuda")
+            _lib.check(_lib.lib().mlb_grid_sum_slots(_lib.ptr(recv[r]), 2, cells, _lib.ptr(g), _lib.stream_ptr()))
+            out.append(g.cpu().numpy())
+        assert np.array_equal(out[0], out[1])
+        assert rel(out[0], ref.cpu().numpy()) < 1e-13
 
 
 @pytest.mark.parametrize("d,m", [(1, 4), (2, 4), (3, 4), (3, 5), (3, 6), (3, 3)])
