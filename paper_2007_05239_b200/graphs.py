@@ -18,7 +18,6 @@ import numpy as np
 
 from . import _lib, fastsum
 from .errors import ConfigError, FormatError, NumericalError
-from .kernels import KernelSpec
 
 _SYM_TOL = 1e-12
 

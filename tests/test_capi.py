@@ -1,7 +1,6 @@
 """The C-ABI boundary: libmlb.so loads (no GPU needed) and exports every entry
 point include/multilap_b200.h declares; the ctypes table matches the header."""
 
-import ctypes
 import os
 import re
 

@@ -100,7 +100,7 @@ def _feature_cfg(tmp_path, X, extra=None):
 
 @pytest.mark.gpu
 def test_cli_eig_and_classify_match_the_api(tmp_path):
-    from paper_2007_05239_b200 import (AllenCahnParams, GroupingSpec, GroupSpec, KernelSpec, LabelData,
+    from paper_2007_05239_b200 import (AllenCahnParams, GroupingSpec, GroupSpec, KernelSpec,
                                        PowerMeanConfig, allen_cahn_solve, feature_group, power_mean_eigs,
                                        predict_labels)
     from paper_2007_05239_b200.cli import main

@@ -12,7 +12,6 @@ import pytest
 from numpy.testing import assert_allclose
 
 from conftest import load_golden
-from oracle import fastsum_oracle as fo
 from oracle import solvers_oracle as so
 
 pytestmark = pytest.mark.gpu
