@@ -125,6 +125,14 @@ int mlb_binding_set_isd(mlb_binding* b, const double* isd_dev, void* stream);
 int mlb_apply(mlb_binding* b, const double* v_dev, double* y_dev, double alpha, double beta,
               double gamma, unsigned flags, void* stream);
 
+/* T independent layers applied to one vector (SURVEY 8(b)'s proposed
+ * mlb_apply_lsym_batched; apply_sym_laplacians for C hosts): y[t] = layer
+ * t's mlb_apply of v with coefficients alpha[t], beta[t], gamma[t] (host
+ * arrays).  The layers run concurrently on library-owned streams forked
+ * from and joined back into `stream`; all bindings on one device. */
+int mlb_apply_batched(mlb_binding* const* b, int T, const double* v_dev, double* const* y_dev, const double* alpha,
+                      const double* beta, const double* gamma, unsigned flags, void* stream);
+
 /* Test hooks on the three stages (sub-box grid of L^d cells, row-major):
  * spread (fastsum.py:389-391), convolution rfftn*fused*irfftn
  * (fastsum.py:492-495), gather (fastsum.py:400-406). */

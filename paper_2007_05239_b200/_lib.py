@@ -55,6 +55,7 @@ SIGNATURES = {
     "mlb_spread": (I, [P, P, P, U, P]),
     "mlb_reduce": (I, [P, P, P]),
     "mlb_spread_peers": (I, [P, P, P, I, U, P]),
+    "mlb_apply_batched": (I, [P, I, P, P, P, P, P, U, P]),
     "mlb_grid_sum_slots": (I, [P, I, I64, P, P]),
     "mlb_ipc_handle": (I, [P, P]),
     "mlb_ipc_open": (I, [P, I, P]),

@@ -813,6 +813,42 @@ int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double b
     return rc;
 }
 
+int mlb_apply_batched(mlb_binding* const* b, int T, const double* v, double* const* y, const double* alpha,
+                      const double* beta, const double* gamma, unsigned flags, void* stream) {
+    if (T < 0 || (T > 0 && (!b || !y || !alpha || !beta || !gamma))) return fail(MLB_ERR_ARG, "null argument");
+    if (T == 0) return MLB_OK;
+    if (T == 1) return mlb_apply(b[0], v, y[0], alpha[0], beta[0], gamma[0], flags, stream);
+    for (int t = 0; t < T; ++t)
+        if (!b[t] || b[t]->plan->device != b[0]->plan->device)
+            return fail(MLB_ERR_ARG, "batched layers must be bound on one device");
+    DeviceGuard guard(b[0]->plan->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    // the layers are independent: each runs on its own stream (forked from
+    // and joined back into the caller's stream), so the cheap layers fill
+    // the SMs the costly one leaves idle in its low-occupancy phases
+    static thread_local std::vector<cudaStream_t> pool;
+    static thread_local std::vector<cudaEvent_t> evs;
+    while ((int)pool.size() < T) {
+        cudaStream_t s;
+        MLB_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        pool.push_back(s);
+    }
+    while ((int)evs.size() < T + 1) {
+        cudaEvent_t e;
+        MLB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+    }
+    MLB_CUDA_TRY(cudaEventRecord(evs[T], st));
+    int rc = MLB_OK;
+    for (int t = 0; t < T && rc == MLB_OK; ++t) {
+        MLB_CUDA_TRY(cudaStreamWaitEvent(pool[t], evs[T], 0));
+        rc = mlb_apply(b[t], v, y[t], alpha[t], beta[t], gamma[t], flags, pool[t]);
+        if (rc == MLB_OK) MLB_CUDA_TRY(cudaEventRecord(evs[t], pool[t]));
+    }
+    for (int t = 0; t < T; ++t) MLB_CUDA_TRY(cudaStreamWaitEvent(st, evs[t], 0));
+    return rc;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------ FP64 probe --

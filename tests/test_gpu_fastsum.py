@@ -167,6 +167,43 @@ def test_laplacian_batch_matches_per_layer():
         assert np.array_equal(b2.apply_many(Vp[:1].clone().pin_memory()).numpy(), refs[:1])
 
 
+def test_apply_batched_c_abi_is_bitwise_per_layer():
+    """mlb_apply_batched (layers on library streams, C hosts) == mlb_apply per layer."""
+    import ctypes
+    import torch
+    from paper_2007_05239_b200 import KernelSpec, _lib
+    from paper_2007_05239_b200.graphs import KernelWeights, build_layer, with_shift
+    g = load_golden("solvers")
+    layers = []
+    for key in ("3", "2"):
+        plan = _plan(g["spec" + key])
+        fam, s = FAM[int(g["spec" + key][0])], float(g["spec" + key][1])
+        layers.append(with_shift(build_layer(KernelWeights(g["pts" + key], KernelSpec(fam, s), plan=plan)), 0.4))
+    lib = _lib.lib()
+    v = torch.from_numpy(g["v"]).cuda()
+    bs = [lay.weights._bindings[0] for lay in layers]
+    for lay in layers:
+        lay.weights.set_isd(lay.isd_device(lay.weights.device))
+    coeff = [(1.0 + lay.shift, -1.0, lay.weights.kernel.value_at_zero()) for lay in layers]
+    ref = []
+    for b, (a, bt, gm) in zip(bs, coeff):
+        y = torch.empty_like(v)
+        _lib.check(lib.mlb_apply(b.ptr, _lib.ptr(v), _lib.ptr(y), a, bt, gm, _lib.MLB_USE_ISD, _lib.stream_ptr()))
+        ref.append(y)
+    ys = [torch.full_like(v, float("nan")) for _ in layers]
+    T = len(layers)
+    arr = lambda ctype, vals: (ctype * T)(*vals)  # noqa: E731
+    _lib.check(lib.mlb_apply_batched(arr(ctypes.c_void_p, [b.ptr.value for b in bs]), T, _lib.ptr(v),
+                                     arr(ctypes.c_void_p, [y.data_ptr() for y in ys]),
+                                     arr(ctypes.c_double, [c[0] for c in coeff]),
+                                     arr(ctypes.c_double, [c[1] for c in coeff]),
+                                     arr(ctypes.c_double, [c[2] for c in coeff]), _lib.MLB_USE_ISD,
+                                     _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    for y, r in zip(ys, ref):
+        assert torch.equal(y, r)
+
+
 def test_per_component_blocks_match_oracle():
     from paper_2007_05239_b200 import KernelSpec, build_plan
     from paper_2007_05239_b200.graphs import KernelWeights
