@@ -22,15 +22,34 @@ import scipy.fft as sfft
 from . import fastsum_oracle as fo
 
 
-def _shared(shape):
-    """A float64 array in anonymous shared memory (inherited by forked workers)."""
-    n = int(np.prod(shape))
-    buf = mp.RawArray("d", max(n, 1))
-    return np.frombuffer(buf, dtype=np.float64, count=n).reshape(shape)
+class _Shared:
+    """A float64 array in shared memory: the RawArray travels to the workers
+    (inherited under fork, passed by handle under forkserver), each side
+    makes its own numpy view."""
+
+    def __init__(self, shape):
+        self.shape = tuple(int(x) for x in shape)
+        self.raw = mp.RawArray("d", max(int(np.prod(self.shape)), 1))
+
+    def view(self):
+        n = int(np.prod(self.shape))
+        return np.frombuffer(self.raw, dtype=np.float64, count=n).reshape(self.shape)
 
 
-def _worker(rank, S, conn):
+def _views(R):
+    """Replace every _Shared in the (nested) dict / lists by its numpy view."""
+    if isinstance(R, _Shared):
+        return R.view()
+    if isinstance(R, dict):
+        return {k: _views(v) for k, v in R.items()}
+    if isinstance(R, list):
+        return [_views(v) for v in R]
+    return R
+
+
+def _worker(rank, R, conn):
     """One fixed chunk of the sample: bind once, then serve phase commands."""
+    S = _views(R)
     lo, hi = S["bounds"][rank], S["bounds"][rank + 1]
     P = len(S["bounds"]) - 1
     bindings = [fo.bind(plan, pts[lo:hi], sort=False) if hi > lo else None for plan, pts in S["layers"]]
@@ -74,29 +93,33 @@ class ParallelReference:
     """The shifted normalized-Laplacian matvec of several kernel layers over
     one node sample, on `procs` worker processes (default: every core)."""
 
-    def __init__(self, layer_specs, n, delta, procs=None):
-        """layer_specs: [(OraclePlan, points n x d in box units)]."""
+    def __init__(self, layer_specs, n, delta, procs=None, start_method="fork"):
+        """layer_specs: [(OraclePlan, points n x d in box units)].  `start_method`
+        "forkserver" starts the workers from a clean interpreter (callers whose
+        process already runs CUDA threads, e.g. the GPU tests)."""
         ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
         self.P = P = int(procs or ncpu)
         self.n, self.delta, self.T = n, float(delta), len(layer_specs)
         bounds = [n * r // P for r in range(P + 1)]
-        S = {
+        R = {
             "layers": [(plan, np.ascontiguousarray(pts)) for plan, pts in layer_specs],
             "bounds": bounds,
-            "v": _shared((n,)),
-            "isd": [_shared((n,)) for _ in layer_specs],
-            "deg": [_shared((n,)) for _ in layer_specs],
-            "y": [_shared((n,)) for _ in layer_specs],
-            "parts": [_shared((P, plan.ng ** plan.d)) for plan, _ in layer_specs],
-            "grid": [_shared((plan.ng ** plan.d,)) for plan, _ in layer_specs],
-            "conv": [_shared((plan.ng ** plan.d,)) for plan, _ in layer_specs],
+            "v": _Shared((n,)),
+            "isd": [_Shared((n,)) for _ in layer_specs],
+            "deg": [_Shared((n,)) for _ in layer_specs],
+            "y": [_Shared((n,)) for _ in layer_specs],
+            "parts": [_Shared((P, plan.ng ** plan.d)) for plan, _ in layer_specs],
+            "grid": [_Shared((plan.ng ** plan.d,)) for plan, _ in layer_specs],
+            "conv": [_Shared((plan.ng ** plan.d,)) for plan, _ in layer_specs],
         }
-        self.S = S
-        ctx = mp.get_context("fork")
+        self.S = S = _views(R)
+        ctx = mp.get_context(start_method)
+        if start_method == "forkserver":
+            ctx.set_forkserver_preload(["numpy", "scipy.fft", "oracle.fastsum_oracle"])
         self.conns, self.procs = [], []
         for r in range(P):
             a, b = ctx.Pipe()
-            pr = ctx.Process(target=_worker, args=(r, S, b), daemon=True)
+            pr = ctx.Process(target=_worker, args=(r, R, b), daemon=True)
             pr.start()
             self.conns.append(a)
             self.procs.append(pr)

@@ -29,7 +29,7 @@ def test_config2_full_size_matches_parallel_reference():
         g = GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma))
         Xb, kb, _ = datapipe._scaled_group(wl.X[:, list(ls.columns)], g, 1.0 / 16)
         specs.append((fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p), Xb))
-    ref = ParallelReference(specs, wl.n, delta)
+    ref = ParallelReference(specs, wl.n, delta, start_method="forkserver")  # this process runs CUDA
     try:
         v = np.random.default_rng(3).standard_normal(wl.n)
         want = [y.copy() for y in ref.step(v)]
