@@ -51,15 +51,12 @@ def main(argv=None):
         fastsum.set_fft_workers(args.threads)
         report = COMMANDS[args.command][0](load_config(args.config), args.seed, out_dir=args.out,
                                            threads=args.threads)
-    except ConfigError as exc:
+    except (ConfigError, NumericalError, FormatError) as exc:
         print(f"error: {exc}", file=sys.stderr)
-        return 2
-    except NumericalError as exc:
+        return exc.exit_code
+    except OSError as exc:
         print(f"error: {exc}", file=sys.stderr)
-        return 3
-    except (FormatError, OSError) as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return 4
+        return FormatError.exit_code
     parts = [f"{args.command}: done"]
     if isinstance(report.get("accuracy"), float):
         parts.append(f"accuracy {report['accuracy']:.4f}")
