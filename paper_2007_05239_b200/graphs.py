@@ -389,7 +389,8 @@ class LaplacianBatch:
             cost = [_layer_cost(layer) for layer in graph.layers]
             top = max(range(len(cost)), key=lambda i: cost[i])
             prio = os.environ.get("MLB_NO_STREAM_PRIORITY") is None
-            self._streams = [torch.cuda.Stream(device=dev, priority=(-1 if (prio and i == top) else 0))
+            hi = int(os.environ.get("MLB_STREAM_PRIORITY", "-1"))  # torch range on B200: 0 (low) .. -3 (high)
+            self._streams = [torch.cuda.Stream(device=dev, priority=(hi if (prio and i == top) else 0))
                              for i in range(len(graph.layers))]
             self._fork = torch.cuda.Event()
             self._joins = [torch.cuda.Event() for _ in graph.layers]
