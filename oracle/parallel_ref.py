@@ -166,10 +166,10 @@ class ParallelReference:
             pr.join(timeout=5)
 
 
-def check_against_serial(layer_specs, delta, v, procs=2):
+def check_against_serial(layer_specs, delta, v, procs=2, start_method="fork"):
     """Max relative deviation of the parallel arm from the serial oracle (tests)."""
     from . import solvers_oracle as so
-    par = ParallelReference(layer_specs, len(v), delta, procs=procs)
+    par = ParallelReference(layer_specs, len(v), delta, procs=procs, start_method=start_method)
     try:
         ys = [y.copy() for y in par.step(v)]
     finally:

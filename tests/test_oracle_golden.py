@@ -172,4 +172,7 @@ def test_parallel_reference_arm_matches_serial_oracle():
     for d, N in ((3, 16), (2, 32)):
         pts = np.clip(0.05 * rng.standard_normal((700, d)), -hw, hw)
         specs.append((fo.OraclePlan("gaussian", 0.12, d, N, 4, p=8), pts))
-    assert check_against_serial(specs, math.log(2.0), rng.standard_normal(700), procs=3) < 1e-13
+    v = rng.standard_normal(700)
+    assert check_against_serial(specs, math.log(2.0), v, procs=3) < 1e-13
+    # workers started from a clean interpreter (what CUDA-running callers use)
+    assert check_against_serial(specs, math.log(2.0), v, procs=2, start_method="forkserver") < 1e-13
