@@ -15,6 +15,7 @@
 #include <cstring>
 #include <string>
 #include <queue>
+#include <thread>
 #include <cstdio>
 #include <vector>
 
@@ -80,6 +81,24 @@ template <typename T>
 static void dev_free(T*& p) {
     if (p) cudaFree((void*)p);
     p = nullptr;
+}
+
+// Static partition of [0, n) over host threads for the bind-time loops
+// (results do not depend on the thread count).
+static int host_threads(int64_t n) {
+    return n < ((int64_t)1 << 16) ? 1 : (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+}
+
+template <class F>
+static void parallel_ranges(int64_t n, F&& body) {
+    const int nt = host_threads(n);
+    if (nt == 1) {
+        body(0, (int64_t)0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back([&, t] { body(t, n * t / nt, n * (t + 1) / nt); });
+    for (auto& th : pool) th.join();
 }
 
 static int ipow_h(int b, int e) {
@@ -250,39 +269,61 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     std::vector<int32_t> cell_local((size_t)n), cell_glob((size_t)n);
     const int nloc = ipow_h(Tb, d);
     const int nbricks = ipow_h(nbr, d);
-    for (int64_t i = 0; i < n; ++i) {
-        int brick = 0, local = 0, tcell = 0, gcell = 0;
-        for (int a = 0; a < d; ++a) {
-            const double xt = pts[i * d + a] * scale;
-            const double tx = (double)g.ng * xt;
-            const double fl = std::floor(tx);
-            const int bin = (int)fl - bin_lo;
-            if (!(bin >= 0 && bin < g.nb)) {
-                return fail(MLB_ERR_CONFIG, "point " + std::to_string(i) + " lies outside the plan's admissible box");
+    const int nth = host_threads(n);
+    std::vector<int64_t> first_bad(nth, n);  // per thread: the first point outside the box
+    parallel_ranges(n, [&](int t, int64_t i0, int64_t i1) {
+        for (int64_t i = i0; i < i1; ++i) {
+            int brick = 0, local = 0, tcell = 0, gcell = 0;
+            for (int a = 0; a < d; ++a) {
+                const double xt = pts[i * d + a] * scale;
+                const double tx = (double)g.ng * xt;
+                const double fl = std::floor(tx);
+                const int bin = (int)fl - bin_lo;
+                if (!(bin >= 0 && bin < g.nb)) {
+                    first_bad[t] = i;
+                    return;
+                }
+                f[(size_t)i * d + a] = tx - fl;
+                brick = brick * nbr + bin / Tb;
+                local = local * Tb + bin % Tb;
+                tcell = tcell * TL + bin % Tb;
+                gcell = gcell * g.L + bin;
             }
-            f[(size_t)i * d + a] = tx - fl;
-            brick = brick * nbr + bin / Tb;
-            local = local * Tb + bin % Tb;
-            tcell = tcell * TL + bin % Tb;
-            gcell = gcell * g.L + bin;
+            key[i] = brick * nloc + local;
+            cell_local[i] = tcell;
+            cell_glob[i] = gcell;
         }
-        key[i] = brick * nloc + local;
-        cell_local[i] = tcell;
-        cell_glob[i] = gcell;
-    }
-    // 2. stable counting sort by key
+    });
+    const int64_t bad = *std::min_element(first_bad.begin(), first_bad.end());
+    if (bad < n) return fail(MLB_ERR_CONFIG, "point " + std::to_string(bad) + " lies outside the plan's admissible box");
+    // 2. stable counting sort by key: per-thread histograms of contiguous
+    //    ranges; thread t's points of key k follow those of threads < t, so the
+    //    permutation equals the serial stable sort
     const int64_t nkeys = (int64_t)nbricks * nloc;
+    std::vector<std::vector<int64_t>> hist(nth, std::vector<int64_t>(nkeys, 0));
+    parallel_ranges(n, [&](int t, int64_t i0, int64_t i1) {
+        for (int64_t i = i0; i < i1; ++i) hist[t][key[i]]++;
+    });
     std::vector<int64_t> cnt(nkeys + 1, 0);
-    for (int64_t i = 0; i < n; ++i) cnt[key[i] + 1]++;
-    for (int64_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
-    std::vector<int32_t> perm((size_t)n);
-    {
-        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-        for (int64_t i = 0; i < n; ++i) perm[pos[key[i]]++] = (int32_t)i;
+    for (int64_t k = 0; k < nkeys; ++k) {
+        int64_t c = cnt[k];
+        for (int t = 0; t < nth; ++t) {
+            const int64_t h = hist[t][k];
+            hist[t][k] = c;  // thread t's first slot for key k
+            c += h;
+        }
+        cnt[k + 1] = c;
     }
+    std::vector<int32_t> perm((size_t)n);
+    parallel_ranges(n, [&](int t, int64_t i0, int64_t i1) {
+        std::vector<int64_t>& pos = hist[t];
+        for (int64_t i = i0; i < i1; ++i) perm[pos[key[i]]++] = (int32_t)i;
+    });
     std::vector<int32_t> perm_node(perm);
     if (node_ids)
-        for (int64_t j = 0; j < n; ++j) perm_node[j] = node_ids[perm[j]];
+        parallel_ranges(n, [&](int, int64_t j0, int64_t j1) {
+            for (int64_t j = j0; j < j1; ++j) perm_node[j] = node_ids[perm[j]];
+        });
     // 3. chunks (<= kChunk points of one cell) and segments (<= maxseg chunks of one brick)
     std::vector<int32_t> chunk_start, chunk_cell, chunk_gcell, chunk_brick;
     for (int64_t k = 0; k < nkeys; ++k) {
@@ -555,8 +596,10 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     }
     // frac in sorted order, SoA
     std::vector<double> fs((size_t)n * d);
-    for (int64_t j = 0; j < n; ++j)
-        for (int a = 0; a < d; ++a) fs[(size_t)a * n + j] = f[(size_t)perm[j] * d + a];
+    parallel_ranges(n, [&](int, int64_t j0, int64_t j1) {
+        for (int64_t j = j0; j < j1; ++j)
+            for (int a = 0; a < d; ++a) fs[(size_t)a * n + j] = f[(size_t)perm[j] * d + a];
+    });
 
     DeviceGuard guard(plan->device);
     mlb_binding* b = new mlb_binding();
