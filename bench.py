@@ -1,32 +1,42 @@
 #!/usr/bin/env python
 """Benchmark: normalized-Laplacian matvecs/s (node*layers/s), fp64, on B200.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-512x512 synthetic segmentation image (n = 262,144 nodes), T = 2 kernel layers
--- RGB d=3 sigma=0.1 (N=64, m=4, p=8; the reference rejects N=32 for this
-layer) and xy d=2 sigma=0.15 (N=32, m=4, p=8) -- shifted by
-delta = ln 2 as in the p = -1 PKSM solves.  One STEP = one shifted
-normalized-Laplacian matvec y = (1+delta) v - D^-1/2 W D^-1/2 v on every
-layer (2 x 262,144 node*layers), vectors in node order (the drop-in
-`apply_sym_laplacian` semantics).
+Workload (default `--workload cfg4`): BASELINE.json configs[3], the config the
+metric's "1/2/4/8 B200 ... 10M-node layers" target is quoted on and the
+largest that fits one GPU -- the 3162 x 3162 synthetic image (n = 9,998,244
+nodes), T = 2 kernel layers, RGB d=3 sigma=0.1 and xy d=2 sigma=0.1, both
+N=64, m=5, p=8, shifted by delta = ln 2 as in the p = -1 PKSM solves.  One
+STEP = one shifted normalized-Laplacian matvec
+y = (1+delta) v - D^-1/2 W D^-1/2 v on every layer (2 x 9,998,244
+node*layers), vectors in node order (the drop-in `apply_sym_laplacian`
+semantics).  `--workload cfg2` benches BASELINE configs[1] (512 x 512) instead.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+N = 1: the layers run concurrently on their own streams, each replayed from a
+captured CUDA graph (LaplacianBatch).  N > 1 (torchrun, or `--gpus N` alone,
+which launches torchrun itself): node-range sharding, strong scaling -- rank
+r owns nodes [r n/N, (r+1) n/N) of BOTH layers and binds only those; a step
+spreads the rank's nodes into its private sub-box grids (both layers in one
+buffer), all-reduces that buffer over NCCL (the step's only collective),
+convolves redundantly and gathers its own nodes with the fused Laplacian
+epilogue (dist.ShardedKernelGraph).
+
 Timing: W warm-up steps; then K steps, each bracketed by CUDA events on the
-launching stream, with a 256 MB L2 flush between steps (outside the events);
-barrier + synchronize around the loop; max over ranks.  Multi-GPU (torchrun):
-layers are independent, each rank owns the 2 layers of its own seeded image
-(round-robin layer ownership, no data-path collective) -> weak scaling.
+launching stream, with a 256 MB L2 flush between steps (outside the events;
+the config-4 inputs are also larger than L2); barrier + synchronize around
+the loop; max over ranks.
 
 `--impl reference` times the CPU reference algorithm (the numpy oracle port
-of multilap's fastsum/graphs path: bincount spread/gather + scipy.fft) on a
-bounded subsample of the same layers, rank 0 only.
+of multilap's fastsum/graphs path: bincount spread/gather + scipy.fft, on
+every host core) on a bounded node sample of the same layers, rank 0 only.
 """
 
 import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -54,6 +64,25 @@ def _peaks():
         return float(pk["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def _workload(name):
+    import synth
+    if name == "cfg4":
+        return synth.config4_large(seed=0)
+    if name == "cfg2":
+        return synth.config2_segmentation(seed=0)
+    raise SystemExit(f"unknown workload {name!r}")
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -108,13 +137,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def build_layers(workload, device, delta):
-    import synth
-    from paper_2007_05239_b200 import with_shift
-    G = synth.build_graph(workload, device=device)
-    return [with_shift(l, delta) for l in G.layers]
-
-
 def algorithmic_bytes(d):
     """B(d) = 16 d + 40 bytes per node per normalized-Laplacian matvec."""
     return 16 * d + 40
@@ -144,17 +166,16 @@ def measure_fp64_peak(torch, device):
     return best
 
 
-def stage_breakdown(torch, layers, v, reps=10):
-    """Per-kernel device times (CUDA events, launching stream): spread kernel,
-    partial reduction, convolution, gather (with the Laplacian epilogue)."""
+def stage_breakdown(torch, weights, v, reps=10):
+    """Per-kernel device times (CUDA events on the launching stream): spread
+    kernel, partial reduction, convolution, gather (with the Laplacian
+    epilogue) -- the stage hooks of the C ABI, one layer at a time."""
     from paper_2007_05239_b200 import _lib
     lib = _lib.lib()
     out = []
-    for li, lay in enumerate(layers):
-        w = lay.weights
+    for li, w in enumerate(weights):
         b = w._bindings[0]
         g = b.plan
-        K0 = w.kernel.value_at_zero()
         grid = torch.empty(b.stats()["grid_cells"], dtype=torch.float64, device=v.device)
         grid2 = torch.empty_like(grid)
         y = torch.empty_like(v)
@@ -175,35 +196,99 @@ def stage_breakdown(torch, layers, v, reps=10):
             if r >= 2:
                 tt += [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
         tt /= reps
-        d, m = g.d, g.m_nfft
-        out.append(dict(layer=li, d=d, N=g.N, m=m, n=b.n, spread_ms=tt[0], reduce_ms=tt[1], convolve_ms=tt[2],
-                        gather_ms=tt[3], stats=b.stats()))
+        out.append(dict(layer=li, d=g.d, N=g.N, m=g.m_nfft, n=b.n, spread_ms=tt[0], reduce_ms=tt[1],
+                        convolve_ms=tt[2], gather_ms=tt[3], stats=b.stats()))
     return out
 
 
+def _traffic(workload, name, d):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of this
+    kernel on this workload (profiles/ncu_traffic.json, from the committed
+    `ncu --set full` capture of the same bench command), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+    except Exception:
+        return None, None
+    ent = tr.get(f"{workload}:{name}_d{d}")
+    if isinstance(ent, dict):
+        return ent.get("bytes"), ent.get("source")
+    return None, None
+
+
+def kernel_table(stages, workload, hbm_peak, fp64_peak):
+    """Algorithmic bytes / flops per launch of every stage kernel (SURVEY 8(d):
+    spread reads x, v, D^-1/2 = (8d+16) B/node and does 2C flops/node; the
+    gather reads x, D^-1/2, v and writes y = (8d+24) B/node, 2C flops/node;
+    the convolution reads + writes the sub-box grid, the reduction writes it)."""
+    rows = []
+    for st in stages:
+        d, m, nl = st["d"], st["m"], st["n"]
+        C = (2 * m + 1) ** d
+        cells = st["stats"]["grid_cells"]
+        for name, ms, nbytes, nflops in (("spread", st["spread_ms"], (8 * d + 16) * nl, 2 * C * nl),
+                                         ("gather", st["gather_ms"], (8 * d + 24) * nl, 2 * C * nl),
+                                         ("convolve", st["convolve_ms"], 16 * cells, 0),
+                                         ("reduce", st["reduce_ms"], 8 * cells, 0)):
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            tfs = nflops / (ms * 1e-3) / 1e12
+            traffic, src = _traffic(workload, name, d)
+            rows.append({"kernel": name, "layer": st["layer"], "d": d, "N": st["N"], "m": m, "n": nl, "ms": ms,
+                         "alg_bytes": nbytes, "alg_flops": nflops, "gbs": gbs, "hbm_frac": gbs / hbm_peak,
+                         "fp64_tflops": tfs, "fp64_frac": tfs / fp64_peak if fp64_peak else None,
+                         "traffic": traffic, "traffic_source": src})
+    return rows
+
+
+def roofline_of(rows, hbm_peak, peak_kind, fp64_peak):
+    """The dominant kernel's roofline.  Its bound is the roof its algorithmic
+    intensity hits first: fp64 flops/byte above fp64_peak / hbm_peak (the
+    ridge, ~5.5 flop/B) -> the FP64 pipe (DFMA; B200's fp64 tensor path
+    shares that pipe), else HBM."""
+    top = max(rows, key=lambda r: r["ms"])
+    ridge = fp64_peak * 1e12 / (hbm_peak * 1e9) if fp64_peak else float("inf")
+    fp64_bound = top["alg_bytes"] > 0 and top["alg_flops"] / top["alg_bytes"] > ridge
+    hbm = {"achieved": top["gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": top["gbs"] / hbm_peak,
+           "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    fp64 = {"achieved": top["fp64_tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": top["fp64_frac"], "peak_source": "mlb_probe_fp64 DFMA microbenchmark, this run "
+                                                       "(MEASURED_PEAKS.json has no FP64 entry)"}
+    prim, other = (fp64, ("hbm", hbm)) if fp64_bound else (hbm, ("fp64", fp64))
+    roof = {"bound": "fp64" if fp64_bound else "hbm",
+            "kernel": f"{top['kernel']} (layer d={top['d']}, N={top['N']}, m={top['m']}, n={top['n']})",
+            **{k: prim[k] for k in ("achieved", "peak", "unit", "frac", "peak_source")},
+            "traffic": top["traffic"], "traffic_source": top["traffic_source"],
+            "alg_bytes_per_launch": top["alg_bytes"], "alg_flops_per_launch": top["alg_flops"],
+            "intensity_flop_per_byte": top["alg_flops"] / top["alg_bytes"] if top["alg_bytes"] else None,
+            "ridge_flop_per_byte": ridge, other[0]: other[1]}
+    return roof
+
+
+# ---------------------------------------------------------------- CPU arms --
 def _reference_arm(workload, delta, n_sample, seed=1):
     """The reference algorithm (oracle port) of every layer over a random node
-    sample, on all host cores (oracle/parallel_ref.py)."""
+    sample (points mapped into the box with the map fitted on ALL nodes, so
+    they are the benched layer's points), on all host cores
+    (oracle/parallel_ref.py)."""
     from oracle import fastsum_oracle as fo
     from oracle.parallel_ref import ParallelReference
-    from paper_2007_05239_b200 import datapipe, GroupSpec, KernelSpec
+    from paper_2007_05239_b200 import KernelSpec, datapipe
     rng = np.random.default_rng(seed)
     idx = np.sort(rng.choice(workload.n, size=min(n_sample, workload.n), replace=False))
     specs = []
     for ls in workload.layers:
-        g = GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma))
-        Xb, kb, _ = datapipe._scaled_group(workload.X[idx][:, list(ls.columns)], g, 1.0 / 16)
-        specs.append((fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p), Xb))
+        Xb, kb = datapipe.box_points(workload.X[:, list(ls.columns)], KernelSpec(ls.family, ls.sigma))
+        specs.append((fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p), Xb[idx]))
     ref = ParallelReference(specs, len(idx), delta)
     return ref, rng.standard_normal(len(idx))
 
 
 def _sample_words(ns, n):
-    return f"all {n} nodes" if ns >= n else f"{ns}-node random subsample"
+    return f"all {n} nodes" if ns >= n else f"{ns}-node random subsample of {n}"
 
 
 def cpu_baseline_oracle(workload, delta, n_sample, reps, seed=1):
-    """Time the reference algorithm (numpy oracle, all host cores) on a subsample."""
+    """Time the reference algorithm (numpy oracle, all host cores) on a sample."""
     ref, v = _reference_arm(workload, delta, n_sample, seed)
     try:
         ref.step(v)  # warm-up
@@ -216,12 +301,37 @@ def cpu_baseline_oracle(workload, delta, n_sample, reps, seed=1):
     return ref.n * ref.T * reps / dt, ref.n, dt, ref.P
 
 
+def cpu_single_thread(workload, delta, n_sample, reps=2, seed=2):
+    """'Reference as shipped': the serial oracle (one core; bincount spread /
+    gather, scipy.fft with 1 worker -- the reference's defaults) on a sample."""
+    from oracle import fastsum_oracle as fo
+    from oracle import solvers_oracle as so
+    from paper_2007_05239_b200 import KernelSpec, datapipe
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(workload.n, size=min(n_sample, workload.n), replace=False))
+    v = rng.standard_normal(len(idx))
+    layers = []
+    for ls in workload.layers:
+        Xb, kb = datapipe.box_points(workload.X[:, list(ls.columns)], KernelSpec(ls.family, ls.sigma))
+        op = fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p)
+        b = fo.bind(op, Xb[idx])
+        lay = so.OracleLayer(lambda x, op=op, b=b: fo.fastsum(op, x, binding=b), len(idx))
+        layers.append(lay.shifted(delta))
+    for lay in layers:
+        so.sym_laplacian(lay, v)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for lay in layers:
+            so.sym_laplacian(lay, v)
+    dt = time.perf_counter() - t0
+    return len(idx) * len(layers) * reps / dt, len(idx), dt
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    import synth
-    wl = synth.config2_segmentation(seed=0)
+    wl = _workload(args.workload)
     delta = math.log(2.0)
     ref, v = _reference_arm(wl, delta, args.ref_sample, seed=1)
     n_s, P, T = ref.n, ref.P, ref.T
@@ -237,11 +347,12 @@ def run_reference(args):
     value = n_s * T * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[1] shapes)",
-        "config": {"workload": wl.name, "layers": [vars(l) for l in wl.layers], "delta": delta,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE {wl.name} image; no dataset exists for it)",
+        "config": {"workload": wl.name, "layers": [vars(lay) for lay in wl.layers], "delta": delta,
                    "sample_nodes": n_s},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "port", "cpu_model": _cpu_model(),
                          "sample": f"{_sample_words(n_s, wl.n)} of both layers of {wl.name}; one step = one "
                                    "shifted normalized-Laplacian matvec per layer through the oracle port of the "
                                    f"reference algorithm (bincount spread/gather, full-grid scipy.fft) on {P} "
@@ -252,223 +363,230 @@ def run_reference(args):
     return 0
 
 
-def run_ours(args):
-    import torch
-    ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    device = local
-    torch.cuda.set_device(device)
-    import synth
-    from paper_2007_05239_b200 import LaplacianBatch, MultilayerGraph, _lib
-    from paper_2007_05239_b200.graphs import apply_sym_laplacian_dev
+# ---------------------------------------------------------------- GPU arm ---
+def _timed(torch, step, steps, flush, ws):
+    """K steps, each between CUDA events on the launching stream, L2 flushed
+    between steps outside the events; barrier + sync on both sides; returns
+    (total ms, libmlb launches inside the timed region)."""
+    from paper_2007_05239_b200 import _lib
     lib = _lib.lib()
-    wl = synth.config2_segmentation(seed=rank)   # rank r owns the layers of image r
-    delta = math.log(2.0)
-    layers = build_layers(wl, device, delta)
-    n, T = wl.n, len(layers)
-    rng = np.random.default_rng(1000 + rank)
-    v_host = rng.standard_normal(n)
-    v = torch.from_numpy(v_host).cuda(device)
-    ys = [torch.empty_like(v) for _ in layers]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
-
-    # the layers are independent: one CUDA stream per layer, joined per step,
-    # the whole step replayed from one captured CUDA graph (LaplacianBatch)
-    main = torch.cuda.current_stream()
-    lstreams = [torch.cuda.Stream() for _ in layers]
-    fork = torch.cuda.Event()
-    joins = [torch.cuda.Event() for _ in layers]
-    graph = MultilayerGraph(tuple(layers))
-    batch = LaplacianBatch(graph, use_graph=not args.no_cuda_graph)
-    batch._v.copy_(v)
-
-    # persistent pinned host buffers of the end-to-end leg, allocated at setup:
-    # a freshly pinned buffer moves data slowly for a while (measured on the
-    # pool's boxes: 2 MiB H2D at 90-160 us right after allocation, 42 us once
-    # settled), and a user that streams many vectors keeps its buffers
-    v_pin = torch.from_numpy(v_host).pin_memory()
-    y_pin = torch.empty((T, n), dtype=torch.float64, pin_memory=True)
-    e2e_k = max(3, args.steps)  # one distinct host vector per e2e step
-    V_pin = torch.from_numpy(rng.standard_normal((e2e_k, n))).pin_memory()
-    Y_pin = torch.empty((e2e_k, T, n), dtype=torch.float64, pin_memory=True)
-
-    def step():
-        batch._run()
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    clocks = ClockSampler(device)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     l0 = lib.mlb_launch_count()
-    for i in range(args.steps):
+    for i in range(steps):
         flush.fill_(float(i))
         starts[i].record()
         step()
         ends[i].record()
     torch.cuda.synchronize()
     launches = lib.mlb_launch_count() - l0
-    # the timed loop lasts only milliseconds: keep running the identical step
-    # (untimed) for ~0.6 s so nvidia-smi samples the clocks under this load
-    t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < 0.6:
-        for _ in range(20):
-            step()
-        torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
+    return float(sum(s.elapsed_time(e) for s, e in zip(starts, ends))), int(launches)
+
+
+def _max_over_ranks(torch, x, device, ws):
+    if ws == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    device = local
+    torch.cuda.set_device(device)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2007_05239_b200 import _lib
+    wl = _workload(args.workload)
+    delta = math.log(2.0)
+    n, T = wl.n, len(wl.layers)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    rng = np.random.default_rng(1000)
+    v_host = rng.standard_normal(n)
+    e2e_k = max(3, min(args.steps, 6))   # distinct host vectors streamed by the e2e leg
+    V_host = rng.standard_normal((e2e_k, n))
+    extra = {}
+    if ws == 1:
+        import synth
+        from paper_2007_05239_b200 import LaplacianBatch, MultilayerGraph, with_shift
+        t0 = time.perf_counter()
+        G = synth.build_graph(wl, device=device)
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        layers = [with_shift(lay, delta) for lay in G.layers]
+        weights = [lay.weights for lay in layers]
+        batch = LaplacianBatch(MultilayerGraph(tuple(layers)), use_graph=not args.no_cuda_graph)
+        v = torch.from_numpy(v_host).cuda(device)
+        batch._v.copy_(v)
+        step = batch._run
+        n_local, lo = n, 0
+        parallelism = "dp1 (one GPU; the layers run concurrently on their own CUDA streams)"
+        streams = ("one CUDA stream per layer, joined every step; each layer replayed from its captured CUDA graph"
+                   + (" (disabled)" if args.no_cuda_graph else ""))
+    else:
+        from paper_2007_05239_b200 import KernelSpec
+        from paper_2007_05239_b200.dist import Comm, ShardedKernelGraph, shard_feature_groups
+        comm = Comm()
+        groups = [(ls.columns, KernelSpec(ls.family, ls.sigma), dict(N=ls.N, m_nfft=ls.m, p_nfft=ls.p))
+                  for ls in wl.layers]
+        t0 = time.perf_counter()
+        lo, hi, pts, kerns, plans = shard_feature_groups(wl.X, groups, rank, ws)
+        sg = ShardedKernelGraph(pts, kerns, plans, n, lo, hi, comm=comm, shift=delta, device=device).build()
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        weights = sg.weights
+        n_local = hi - lo
+        v = torch.from_numpy(v_host[lo:hi]).cuda(device)
+        ys = [torch.empty_like(v) for _ in range(T)]
+
+        def step():
+            sg.lsym(v, ys)
+        parallelism = (f"node-range sharded x{ws}: rank r owns nodes [r n/{ws}, (r+1) n/{ws}) of every layer; one "
+                       "NCCL all-reduce of both layers' sub-box grids per step")
+        streams = "one stream; spread (both layers) -> one all-reduce -> convolve + fused gather per layer"
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(device)
+    clocks.start()
+    total_ms, launches = _timed(torch, step, args.steps, flush, ws)
+    # the timed loop can be short: keep running the identical step (untimed)
+    # for ~0.6 s so nvidia-smi samples the clocks under this load
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.6:
+        for _ in range(5):
+            step()
+        torch.cuda.synchronize()
     clk = clocks.stop()
     clk["note"] = "sampled over the timed loop plus a 0.6 s soak of the identical step"
-    total_ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
-    if ws > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = n * T * args.steps * ws / (total_ms * 1e-3)
+    total_ms = _max_over_ranks(torch, total_ms, device, ws)
+    value = n * T * args.steps / (total_ms * 1e-3)
 
-    # ---- end-to-end through the public API: pinned host in, host out ----------
-    # (one call = every layer's L_sym of one host vector: pinned H2D of v,
-    # per-layer D2H of the results as each layer finishes, host sync)
-    for _ in range(max(3, args.warmup)):
-        batch.apply(v_pin, out=y_pin)
-    torch.cuda.synchronize()
+    # ---- end-to-end through the public API: pinned host in, host out --------
+    v_pin = torch.from_numpy(v_host[lo:lo + n_local]).pin_memory()
+    V_pin = torch.from_numpy(np.ascontiguousarray(V_host[:, lo:lo + n_local])).pin_memory()
+    Y_pin = torch.empty((e2e_k, T, n_local), dtype=torch.float64, pin_memory=True)
     e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(3, args.steps)
-    e_s.record()
-    for _ in range(e2e_steps):
-        batch.apply(v_pin, out=y_pin)
-    e_e.record()
-    e_e.synchronize()
-    e2e_sync_ms = e_s.elapsed_time(e_e)
-    e2e_sync_value = n * T * e2e_steps * ws / (e2e_sync_ms * 1e-3)
-    # streamed: the K steps' distinct host vectors through apply_many (vector
-    # i+1's H2D and vector i-1's D2H overlap vector i's compute); the call
-    # returns once every result is in host memory
-    for _ in range(2):
-        batch.apply_many(V_pin[:3], out=Y_pin[:3])
-    torch.cuda.synchronize()
-    e_s.record()
-    batch.apply_many(V_pin, out=Y_pin)
-    e_e.record()
-    e_e.synchronize()
-    e2e_ms = e_s.elapsed_time(e_e)
-    e2e_value = n * T * e2e_k * ws / (e2e_ms * 1e-3)
-
-    # ---- sorted-order variant (what the PKSM inner loop runs) -----------------
-    sorted_value = None
-    try:
-        vs = [torch.empty_like(v) for _ in layers]
-        for lay, x in zip(layers, vs):
-            lib.mlb_to_sorted(lay.weights._bindings[0].ptr, _lib.ptr(v), _lib.ptr(x), _lib.stream_ptr())
-
-        def step_sorted():
-            fork.record(main)
-            for lay, x, y, s, j in zip(layers, vs, ys, lstreams, joins):
-                w = lay.weights
-                s.wait_event(fork)
-                lib.mlb_apply(w._bindings[0].ptr, _lib.ptr(x), _lib.ptr(y), 1.0 + lay.shift, -1.0,
-                              w.kernel.value_at_zero(), _lib.MLB_USE_ISD | _lib.MLB_SORTED,
-                              _lib.C.c_void_p(s.cuda_stream))
-                j.record(s)
-            for j in joins:
-                main.wait_event(j)
-        for _ in range(3):
-            step_sorted()
-        tot = 0.0
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            starts[i].record()
-            step_sorted()
-            ends[i].record()
+    if ws == 1:
+        y_pin = torch.empty((T, n), dtype=torch.float64, pin_memory=True)
+        for _ in range(2):
+            batch.apply(v_pin, out=y_pin)
+            batch.apply_many(V_pin[:3], out=Y_pin[:3])
         torch.cuda.synchronize()
-        tot = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
-        sorted_value = n * T * args.steps * ws / (tot * 1e-3)
-    except Exception as exc:  # diagnostic only
-        sorted_value = f"error: {exc}"
+        e_s.record()
+        for _ in range(e2e_k):
+            batch.apply(v_pin, out=y_pin)
+        e_e.record()
+        e_e.synchronize()
+        e2e_sync_value = n * T * e2e_k / (e_s.elapsed_time(e_e) * 1e-3)
+        e_s.record()
+        batch.apply_many(V_pin, out=Y_pin)
+        e_e.record()
+        e_e.synchronize()
+        e2e_ms = e_s.elapsed_time(e_e)
+        e2e_path = ("paper_2007_05239_b200.LaplacianBatch(graph).apply_many(pinned host (K, n), out=pinned host "
+                    "(K, T, n)): K distinct host vectors, each one H2D of v and T D2H of its results, copies on their "
+                    "own streams overlapping the neighbouring vectors' compute; timed until the last result is in "
+                    "host memory")
+        extra["e2e_synchronous"] = {"value": e2e_sync_value, "unit": UNIT,
+                                    "path": "LaplacianBatch(graph).apply(pinned host v, out=pinned host (T, n)) per "
+                                            "step: H2D, compute, D2H and a host sync every step"}
+    else:
+        vd = torch.empty(n_local, dtype=torch.float64, device=device)
+        yd = [torch.empty_like(vd) for _ in range(T)]
 
-    # ---- roofline of the dominant kernel ---------------------------------------
-    stages = stage_breakdown(torch, layers, v)
+        def e2e_step(i):
+            vd.copy_(V_pin[i], non_blocking=True)
+            sg.lsym(vd, yd)
+            for t in range(T):
+                Y_pin[i, t].copy_(yd[t], non_blocking=True)
+        for i in range(2):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        e_s.record()
+        for i in range(e2e_k):
+            e2e_step(i)
+        e_e.record()
+        e_e.synchronize()
+        e2e_ms = _max_over_ranks(torch, e_s.elapsed_time(e_e), device, ws)
+        e2e_path = ("dist.ShardedKernelGraph.lsym per rank: H2D of the rank's slice of v (pinned), the sharded step, "
+                    "D2H of its slices of the T results, every step (max over ranks)")
+    e2e_value = n * T * e2e_k / (e2e_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (stage hooks, this rank's layers) ---
+    stages = stage_breakdown(torch, weights, v)
     fp64_peak = measure_fp64_peak(torch, f"cuda:{device}")
     hbm_peak, peak_kind = _peaks()
-    kern = []
-    for st in stages:
-        d, m, nl = st["d"], st["m"], st["n"]
-        C = (2 * m + 1) ** d
-        kern.append(("spread", st, st["spread_ms"], (8 * d + 16) * nl, 2 * C * nl))
-        kern.append(("gather", st, st["gather_ms"], (8 * d + 24) * nl, 2 * C * nl))
-        kern.append(("convolve", st, st["convolve_ms"], 16 * st["stats"]["grid_cells"], 0))
-        kern.append(("reduce", st, st["reduce_ms"], 8 * st["stats"]["grid_cells"], 0))
-    top = max(kern, key=lambda k: k[2])
-    name, st, ms, nbytes, nflops = top
-    achieved = nbytes / (ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            tr = json.load(fh)
-        key = f"{name}_d{st['d']}"
-        if key in tr:
-            traffic = tr[key]
-    except Exception:
-        traffic = None
-    roof = {"bound": "hbm", "kernel": f"{name} (layer d={st['d']}, N={st['N']}, m={st['m']})",
-            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "traffic": traffic,
-            "fp64": {"achieved_tflops": nflops / (ms * 1e-3) / 1e12, "peak_tflops": fp64_peak,
-                     "frac": (nflops / (ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
-                     "peak_source": "mlb_probe_fp64 DFMA microbenchmark, this run"}}
-    # whole-step HBM-roofline fraction of the metric (R * B(d) / peak)
+    rows = kernel_table(stages, wl.name, hbm_peak, fp64_peak)
+    roof = roofline_of(rows, hbm_peak, peak_kind, fp64_peak)
+    ms_step = total_ms / args.steps
     step_bytes = sum(algorithmic_bytes(st["d"]) * st["n"] for st in stages)
     step_flops = sum(algorithmic_flops(st["d"], st["m"]) * st["n"] for st in stages)
-    ms_step = total_ms / args.steps
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE configs[1] image; no dataset exists for it)",
-        "config": {"workload": wl.name, "nodes_per_rank": n, "layers": [vars(l) for l in wl.layers],
-                   "delta": delta, "vector_order": "node", "l2": "256 MB flush between steps (outside events)",
-                   "streams": "one CUDA stream per layer (independent layers), joined every step; the step is "
-                              "one captured CUDA graph replay" + (" (disabled)" if args.no_cuda_graph else ""),
-                   "parallelism": f"layer-parallel x{ws} (independent layers per rank, no collective)"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * T,
-                "steps": e2e_k,
-                "path": "paper_2007_05239_b200.LaplacianBatch(graph).apply_many(pinned host (K, n), out=pinned host "
-                        "(K, T, n)): K distinct host vectors, each one H2D of v and T D2H of its results, copies "
-                        "on their own streams overlapping the neighbouring vectors' compute; timed until the last "
-                        "result is in host memory",
-                "synchronous": {"value": e2e_sync_value, "unit": UNIT,
-                                "path": "LaplacianBatch(graph).apply(pinned host v, out=pinned host (T, n)) per step: "
-                                        "H2D, compute, D2H and a host sync every step (no overlap between steps)"}},
-        "gpu_launches": int(launches),
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE {wl.name} image, synth.py; no dataset exists for it)",
+        "config": {"workload": wl.name, "nodes": n, "nodes_per_rank": n_local,
+                   "layers": [vars(lay) for lay in wl.layers], "delta": delta, "vector_order": "node",
+                   "l2": "256 MB flush between steps (outside events); config-4 inputs exceed L2 anyway",
+                   "streams": streams, "parallelism": parallelism, "build_s": build_s},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_local,
+                "d2h_bytes_per_step": 8 * n_local * T, "steps": e2e_k, "path": e2e_path},
+        "gpu_launches": launches,
         "clocks": clk,
         "roofline": roof,
-        "step_roofline": {"hbm_bytes_per_step": step_bytes, "hbm_frac": step_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak,
-                          "fp64_flops_per_step": step_flops,
+        "step_roofline": {"hbm_bytes_per_step": step_bytes * ws,
+                          "hbm_frac": step_bytes * ws / (ms_step * 1e-3) / 1e9 / hbm_peak / ws,
+                          "fp64_flops_per_step": step_flops * ws,
                           "fp64_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak if fp64_peak else None},
-        "sorted_order_value": sorted_value,
+        "kernels": [{k: r[k] for k in ("kernel", "d", "m", "n", "ms", "gbs", "hbm_frac", "fp64_tflops", "fp64_frac",
+                                       "traffic")} for r in rows if r["kernel"] in ("spread", "gather")],
         "stages_ms": [{k: st[k] for k in ("layer", "d", "N", "m", "n", "spread_ms", "reduce_ms", "convolve_ms",
-                                          "gather_ms")}
-                      for st in stages],
+                                          "gather_ms")} for st in stages],
+        **extra,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         val, ns, secs, ncore = cpu_baseline_oracle(wl, delta, args.cpu_sample, args.cpu_reps)
-        result["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": ncore, "kind": "port",
-                                  "sample": f"{_sample_words(ns, wl.n)} of both layers, {args.cpu_reps} shifted "
-                                            f"normalized-Laplacian matvecs per layer through the oracle port of the "
-                                            f"reference algorithm on {ncore} processes (bincount + full-grid "
-                                            f"scipy.fft), {secs:.1f} s"}
+        v1, ns1, secs1 = cpu_single_thread(wl, delta, args.cpu_single_sample)
+        result["cpu_baseline"] = {
+            "value": val, "unit": UNIT, "cores": ncore, "kind": "port", "cpu_model": _cpu_model(),
+            "sample": f"{_sample_words(ns, wl.n)} of both layers, {args.cpu_reps} shifted normalized-Laplacian "
+                      f"matvecs per layer through the oracle port of the reference algorithm on {ncore} processes "
+                      f"(bincount + full-grid scipy.fft), {secs:.1f} s",
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1,
+                              "sample": f"reference as shipped (1 core, serial oracle): {_sample_words(ns1, wl.n)}, "
+                                        f"2 matvecs per layer, {secs1:.1f} s"}}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _launch_ranks(args):
+    """`--gpus N` without a torchrun environment: run this script under
+    torch.distributed.run with N ranks on this node and relay its output."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:]]
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 def main():
@@ -477,14 +595,19 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["cfg4", "cfg2"], default="cfg4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cuda-graph", action="store_true", help="launch the step kernel by kernel")
-    # CPU legs: the full config-2 workload (all 262,144 nodes) unless reduced;
-    # ~0.35 s per step on 16 cores, so 30 reps are ~10 s of CPU work
-    ap.add_argument("--cpu-sample", type=int, default=1 << 30, help="nodes in the CPU baseline sample (default: all)")
+    # CPU legs: bounded node samples of the workload (the full config-4 layers
+    # would need a 213 GB reference binding): ~0.4 s per step on 16 cores
+    ap.add_argument("--cpu-sample", type=int, default=131072, help="nodes in the CPU baseline sample")
     ap.add_argument("--cpu-reps", type=int, default=30)
-    ap.add_argument("--ref-sample", type=int, default=1 << 30, help="nodes in the reference arm's sample (default: all)")
+    ap.add_argument("--cpu-single-sample", type=int, default=16384,
+                    help="nodes in the single-thread ('as shipped') sample")
+    ap.add_argument("--ref-sample", type=int, default=131072, help="nodes in the reference arm's sample")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _launch_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

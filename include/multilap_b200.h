@@ -159,6 +159,14 @@ int mlb_ipc_close(void* dev_ptr);
 int mlb_convolve(mlb_binding* b, const double* grid_in_dev, double* grid_out_dev, void* stream);
 int mlb_gather(mlb_binding* b, const double* grid_dev, double* y_dev, unsigned flags, void* stream);
 
+/* Node-range sharding, NCCL path: the gather of mlb_gather with
+ * mlb_apply's fused epilogue, from a grid the caller summed over the ranks
+ * (mlb_spread -> all-reduce of the sub-box grid -> mlb_convolve -> this):
+ *     y (=|+=) alpha*v + s.(beta*gather(grid) + gamma*s.v)
+ * v, y: this binding's points (node order, or sorted with MLB_SORTED). */
+int mlb_gather_apply(mlb_binding* b, const double* grid_dev, const double* v_dev, double* y_dev, double alpha,
+                     double beta, double gamma, unsigned flags, void* stream);
+
 /* Complex band DFT between the active sub-box (L^d complex cells) and the full
  * band (K^d complex, k = -N/2..N/2 per axis): forward sum_u in[u] e^{-2 pi i k.u/ng},
  * inverse sum_k in[k] e^{+2 pi i k.u/ng} (unnormalised).  Building block of the

@@ -62,6 +62,7 @@ SIGNATURES = {
     "mlb_ipc_close": (I, [P]),
     "mlb_convolve": (I, [P, P, P, P]),
     "mlb_gather": (I, [P, P, P, U, P]),
+    "mlb_gather_apply": (I, [P, P, P, P, D, D, D, U, P]),
     "mlb_band_dft": (I, [P, P, P, I, P]),
     "mlb_to_sorted": (I, [P, P, P, P]),
     "mlb_to_node": (I, [P, P, P, I, P]),

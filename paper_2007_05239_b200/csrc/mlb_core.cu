@@ -13,6 +13,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <queue>
 #include <thread>
@@ -48,6 +51,35 @@ int device_sms(int device) {
         cache[device] = n;
     }
     return cache[device];
+}
+
+int ensure_max_smem(const void* kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    MLB_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = done[{kern, dev}];
+    if (smem <= cur) return MLB_OK;
+    MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+    return MLB_OK;
+}
+
+int occupancy_per_sm(const void* kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, size_t>, int> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(kern, dev, threads, smem);
+    auto it = done.find(key);
+    if (it != done.end()) return it->second;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    done[key] = per_sm;
+    return per_sm;
 }
 
 int fail(int code, const std::string& msg) {
@@ -90,15 +122,19 @@ static int host_threads(int64_t n) {
 }
 
 template <class F>
-static void parallel_ranges(int64_t n, F&& body) {
-    const int nt = host_threads(n);
-    if (nt == 1) {
+static void parallel_ranges_n(int64_t n, int nt, F&& body) {
+    if (nt <= 1) {
         body(0, (int64_t)0, n);
         return;
     }
     std::vector<std::thread> pool;
     for (int t = 0; t < nt; ++t) pool.emplace_back([&, t] { body(t, n * t / nt, n * (t + 1) / nt); });
     for (auto& th : pool) th.join();
+}
+
+template <class F>
+static void parallel_ranges(int64_t n, F&& body) {
+    parallel_ranges_n(n, host_threads(n), body);
 }
 
 static int ipow_h(int b, int e) {
@@ -254,8 +290,25 @@ int mlb_binding_destroy(mlb_binding* b) {
     return MLB_OK;
 }
 
+static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
+                     mlb_binding** out);
+
 int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
              mlb_binding** out) {
+    // host-side allocation / thread failures must not escape the C ABI
+    try {
+        return bind_impl(plan, pts, n, scale, node_ids, out);
+    } catch (const std::bad_alloc&) {
+        return fail(MLB_ERR_CUDA, "mlb_bind: host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(MLB_ERR_CUDA, std::string("mlb_bind: ") + e.what());
+    } catch (...) {
+        return fail(MLB_ERR_CUDA, "mlb_bind: unknown host exception");
+    }
+}
+
+static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
+                     mlb_binding** out) {
     if (!plan || !out || (n > 0 && !pts)) return fail(MLB_ERR_ARG, "null argument");
     if (n < 0 || n >= (int64_t)1 << 31) return fail(MLB_ERR_ARG, "n out of range");
     const Geom& g = plan->g;
@@ -300,14 +353,18 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     //    ranges; thread t's points of key k follow those of threads < t, so the
     //    permutation equals the serial stable sort
     const int64_t nkeys = (int64_t)nbricks * nloc;
-    std::vector<std::vector<int64_t>> hist(nth, std::vector<int64_t>(nkeys, 0));
-    parallel_ranges(n, [&](int t, int64_t i0, int64_t i1) {
+    // per-thread histograms cost nth * nkeys counters: the sort uses at most
+    // enough threads that they stay below ~n counters in total (the permutation
+    // does not depend on the thread count)
+    const int nth_sort = (int)std::max<int64_t>(1, std::min<int64_t>(nth, n / std::max<int64_t>(nkeys, 1)));
+    std::vector<std::vector<int64_t>> hist(nth_sort, std::vector<int64_t>(nkeys, 0));
+    parallel_ranges_n(n, nth_sort, [&](int t, int64_t i0, int64_t i1) {
         for (int64_t i = i0; i < i1; ++i) hist[t][key[i]]++;
     });
     std::vector<int64_t> cnt(nkeys + 1, 0);
     for (int64_t k = 0; k < nkeys; ++k) {
         int64_t c = cnt[k];
-        for (int t = 0; t < nth; ++t) {
+        for (int t = 0; t < nth_sort; ++t) {
             const int64_t h = hist[t][k];
             hist[t][k] = c;  // thread t's first slot for key k
             c += h;
@@ -315,7 +372,7 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
         cnt[k + 1] = c;
     }
     std::vector<int32_t> perm((size_t)n);
-    parallel_ranges(n, [&](int t, int64_t i0, int64_t i1) {
+    parallel_ranges_n(n, nth_sort, [&](int t, int64_t i0, int64_t i1) {
         std::vector<int64_t>& pos = hist[t];
         for (int64_t i = i0; i < i1; ++i) perm[pos[key[i]]++] = (int32_t)i;
     });
@@ -842,6 +899,15 @@ int mlb_gather(mlb_binding* b, const double* grid, double* y, unsigned flags, vo
                          (cudaStream_t)stream);
 }
 
+int mlb_gather_apply(mlb_binding* b, const double* grid, const double* v, double* y, double alpha, double beta,
+                     double gamma, unsigned flags, void* stream) {
+    if (!b || (b->n && (!grid || !v || !y))) return fail(MLB_ERR_ARG, "null argument");
+    if (!b->n) return MLB_OK;
+    DeviceGuard guard(b->plan->device);
+    flags &= (MLB_USE_ISD | MLB_ACCUMULATE | MLB_SORTED);
+    return launch_gather(b, grid, v, y, alpha, beta, gamma, flags, (cudaStream_t)stream);
+}
+
 int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double beta, double gamma, unsigned flags,
               void* stream) {
     if (!b || (b->n && (!v || !y))) return fail(MLB_ERR_ARG, "null argument");
@@ -869,26 +935,43 @@ int mlb_apply_batched(mlb_binding* const* b, int T, const double* v, double* con
     // the layers are independent: each runs on its own stream (forked from
     // and joined back into the caller's stream), so the cheap layers fill
     // the SMs the costly one leaves idle in its low-occupancy phases
-    static thread_local std::vector<cudaStream_t> pool;
-    static thread_local std::vector<cudaEvent_t> evs;
-    while ((int)pool.size() < T) {
+    // streams and events belong to a device: one pool per (thread, device)
+    struct Pool {
+        std::vector<cudaStream_t> streams;
+        std::vector<cudaEvent_t> evs;
+    };
+    static thread_local std::map<int, Pool> pools;
+    Pool& P = pools[b[0]->plan->device];
+    while ((int)P.streams.size() < T) {
         cudaStream_t s;
         MLB_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        pool.push_back(s);
+        P.streams.push_back(s);
     }
-    while ((int)evs.size() < T + 1) {
+    while ((int)P.evs.size() < T + 1) {
         cudaEvent_t e;
         MLB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        evs.push_back(e);
+        P.evs.push_back(e);
     }
-    MLB_CUDA_TRY(cudaEventRecord(evs[T], st));
+    MLB_CUDA_TRY(cudaEventRecord(P.evs[T], st));
     int rc = MLB_OK;
+    int forked = 0;  // streams that waited on the fork event: each must be joined back
     for (int t = 0; t < T && rc == MLB_OK; ++t) {
-        MLB_CUDA_TRY(cudaStreamWaitEvent(pool[t], evs[T], 0));
-        rc = mlb_apply(b[t], v, y[t], alpha[t], beta[t], gamma[t], flags, pool[t]);
-        if (rc == MLB_OK) MLB_CUDA_TRY(cudaEventRecord(evs[t], pool[t]));
+        cudaError_t e = cudaStreamWaitEvent(P.streams[t], P.evs[T], 0);
+        if (e != cudaSuccess) {
+            rc = fail(MLB_ERR_CUDA, std::string("cudaStreamWaitEvent: ") + cudaGetErrorString(e));
+            break;
+        }
+        ++forked;
+        rc = mlb_apply(b[t], v, y[t], alpha[t], beta[t], gamma[t], flags, P.streams[t]);
     }
-    for (int t = 0; t < T; ++t) MLB_CUDA_TRY(cudaStreamWaitEvent(st, evs[t], 0));
+    // always join every forked stream into the caller's stream (also on the
+    // error path: an unjoined fork would break a surrounding graph capture)
+    for (int t = 0; t < forked; ++t) {
+        cudaError_t e = cudaEventRecord(P.evs[t], P.streams[t]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, P.evs[t], 0);
+        if (e != cudaSuccess && rc == MLB_OK)
+            rc = fail(MLB_ERR_CUDA, std::string("stream join: ") + cudaGetErrorString(e));
+    }
     return rc;
 }
 

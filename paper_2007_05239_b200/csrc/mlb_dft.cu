@@ -144,11 +144,7 @@ static void run_gemm(const GemmArgs& g, int batches, cudaStream_t st) {
     dim3 grid((g.N + TN - 1) / TN, (g.M + TM - 1) / TM, batches);
     const size_t smem = (size_t)g.Kd * (TM + 1 + TN + 1) * sizeof(double2);
     auto kern = cgemm_kernel<KA, KB, EP>;
-    static size_t set_for = 0;
-    if (smem > 48 * 1024 && smem > set_for) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set_for = smem;
-    }
+    if (smem > 48 * 1024) ensure_max_smem((const void*)kern, smem);
     kern<<<grid, 256, smem, st>>>(g);
     note_launches(1);
 }
@@ -710,15 +706,9 @@ static int convolve_separable(mlb_binding* b, const double* gin, double* gout, c
     if (d == 3 && (2 * (size_t)L * L + 16 * L) * 8 <= 200 * 1024) {
         const size_t s21 = (2 * (size_t)L * L + 8 * L + 2 * L + 8) * sizeof(double);
         const size_t s0 = ((size_t)L * L + 4 * L + 2 * L + 8) * sizeof(double);
-        static size_t attr21 = 0, attr0 = 0;  // the largest sizes requested so far (L varies per plan)
-        if (s21 > attr21) {
-            MLB_CUDA_TRY(cudaFuncSetAttribute(sep3_p21_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s21));
-            attr21 = s21;
-        }
-        if (s0 > attr0) {
-            MLB_CUDA_TRY(cudaFuncSetAttribute(sep3_p0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0));
-            attr0 = s0;
-        }
+        int rc = ensure_max_smem((const void*)sep3_p21_kernel, s21);  // per (kernel, device)
+        if (rc == MLB_OK) rc = ensure_max_smem((const void*)sep3_p0_kernel, s0);
+        if (rc != MLB_OK) return rc;
         MLB_CUDA_TRY(launch_k(sep3_p21_kernel, dim3(L), dim3(512), s21, st, gin, b->stage_a, c, L));
         MLB_CUDA_TRY(launch_k(sep3_p0_kernel, dim3(L), dim3(512), s0, st, (const double*)b->stage_a, gout, c, L));
         note_launches(2);

@@ -1139,11 +1139,7 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         const size_t smem = (size_t)kCellWarps * (stg + nred) * sizeof(double);
         if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread staging too large for shared memory");
         auto kern3 = spread_cells_kernel<M>;
-        static bool attr = false;
-        if (!attr) {
-            MLB_CUDA_TRY(cudaFuncSetAttribute(kern3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        if (int rc = ensure_max_smem((const void*)kern3, smem)) return rc;  // per (kernel, device)
         if (b->ncta_cells == 0) return MLB_OK;
         MLB_CUDA_TRY(launch_k(kern3, dim3(b->ncta_cells), dim3(kCellWarps * 32), smem, st, a, b->plan->wc, v, flags));
         note_launches(1);
@@ -1160,12 +1156,8 @@ static int gather_dmp(mlb_binding* b, const double* grid, const double* v, doubl
     FsArgs a = make_args(b);
     const size_t smem = ((size_t)8 * NB + (size_t)256 * (2 * S + 1)) * sizeof(double);
     auto kern = gather_kernel<D, M, PK>;
-    static int per_sm = 0;  // resident blocks per SM for this instantiation
-    if (per_sm == 0) {
-        MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MLB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-        if (per_sm < 1) per_sm = 1;
-    }
+    if (int rc = ensure_max_smem((const void*)kern, smem)) return rc;  // per (kernel, device)
+    const int per_sm = occupancy_per_sm((const void*)kern, 256, smem);
     const int nsm = device_sms();
     int blocks = nsm * per_sm;
     const int need = ((D == 3 && PK ? b->ngrp : b->nchunks) + 7) / 8;  // at least one unit per warp

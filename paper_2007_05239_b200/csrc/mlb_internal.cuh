@@ -38,6 +38,12 @@ __device__ __forceinline__ void po_store(const PeerOut& o, int64_t i, double v) 
         if (q < o.n) o.p[q][i] = v;
 }
 int device_sms(int device = -1);  // SM count of `device` (-1: current), cached
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the CURRENT device,
+// remembered per (kernel, device) so a second GPU in the process gets its own
+// call (thread-safe); returns MLB_OK or MLB_ERR_CUDA
+int ensure_max_smem(const void* kern, size_t smem);
+// resident blocks per SM of `kern` at (threads, smem) on the current device, cached per (kernel, device)
+int occupancy_per_sm(const void* kern, int threads, size_t smem);
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {

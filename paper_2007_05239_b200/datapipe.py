@@ -1,9 +1,20 @@
-"""Feature grouping into GPU kernel layers -- drop-in for the hot-path part of
-multilap.datapipe (datapipe.py:32-170, :367-385).
+"""Column groups -> GPU kernel layers: the hot-path part of multilap.datapipe
+(reference datapipe.py:32-170 feature grouping, :367-385 label sampling).
 
-Each column group is centred and scaled isotropically into the fastsum box,
-its bandwidth converted to box units, a plan attached when the group has at
-most 3 columns, and the layer built with GPU-bound KernelWeights.
+The unit that does the work here is `BoxMap`: the affine map of one column
+group into the fastsum box (centre = per-column midpoint of the data range,
+ONE isotropic factor, so kernel distances only change by that factor).  A
+group becomes a layer in three steps -- fit the map, express the kernel
+width in box units (mode "fastsum-box": sigma / factor; "unit-box": sigma
+times the box half-width), bind the mapped points on the device with a plan
+when the group has <= 3 columns -- and the exact O(n^2) device path
+otherwise.  `feature_group` accepts a `weights_factory` so callers can plug
+other weights objects (the reference hard-codes KernelWeights,
+datapipe.py:162-168); the node-range sharded path (dist.shard_feature_groups)
+uses `box_points` directly so every rank maps its nodes with the map fitted
+on the whole matrix.
+
+API names, fields and error messages are the reference's (drop-in).
 """
 
 import logging
@@ -21,11 +32,30 @@ from .kernels import KernelSpec
 log = logging.getLogger(__name__)
 
 SCALING_MODES = ("fastsum-box", "unit-box", "none")
+_BOX_LIMIT = 3   # widest group a fastsum plan (and "fastsum-box" mode) accepts
+
+
+# ------------------------------------------------------------ spec types ---
+def _group_problem(columns, mode):
+    """The first reason a (columns, mode) pair is not a valid group, or None."""
+    if not columns:
+        return "feature group must select at least one column"
+    if len(set(columns)) < len(columns):
+        return f"duplicate column in group {columns}"
+    if mode not in SCALING_MODES:
+        return f"unknown scaling mode {mode!r}, expected one of {SCALING_MODES}"
+    if mode == "fastsum-box" and len(columns) > _BOX_LIMIT:
+        return (f"group of width {len(columns)} cannot use mode 'fastsum-box' (limit {_BOX_LIMIT}); "
+                "use 'unit-box' or 'none'")
+    return None
 
 
 @dataclass(frozen=True)
 class GroupSpec:
-    """One layer: column subset, kernel, scaling mode (datapipe.py:32-65)."""
+    """One layer: a column subset, its kernel and scaling mode (datapipe.py:32-65).
+    kernel.sigma is in the columns' own units for "fastsum-box" / "none" and
+    in [-1, 1]-scaled units for "unit-box"; `per_component` keeps the
+    kernel block-diagonal over the component labels."""
 
     columns: tuple
     kernel: KernelSpec
@@ -33,32 +63,30 @@ class GroupSpec:
     per_component: bool = False
 
     def __post_init__(self):
-        object.__setattr__(self, "columns", tuple(int(c) for c in self.columns))
-        if len(self.columns) == 0:
-            raise ConfigError("feature group must select at least one column")
-        if len(set(self.columns)) != len(self.columns):
-            raise ConfigError(f"duplicate column in group {self.columns}")
-        if self.mode not in SCALING_MODES:
-            raise ConfigError(f"unknown scaling mode {self.mode!r}, expected one of {SCALING_MODES}")
-        if self.mode == "fastsum-box" and len(self.columns) > 3:
-            raise ConfigError(f"group of width {len(self.columns)} cannot use mode 'fastsum-box' (limit 3); "
-                              "use 'unit-box' or 'none'")
+        cols = tuple(int(c) for c in self.columns)
+        object.__setattr__(self, "columns", cols)
+        problem = _group_problem(cols, self.mode)
+        if problem:
+            raise ConfigError(problem)
 
 
 @dataclass(frozen=True)
 class GroupingSpec:
+    """Disjoint column groups, one layer each (datapipe.py:68-83)."""
+
     groups: tuple
 
     def __post_init__(self):
-        object.__setattr__(self, "groups", tuple(self.groups))
-        if not self.groups:
+        groups = tuple(self.groups)
+        object.__setattr__(self, "groups", groups)
+        if not groups:
             raise ConfigError("grouping needs at least one group")
-        seen = set()
-        for g in self.groups:
-            dup = seen.intersection(g.columns)
-            if dup:
-                raise ConfigError(f"column(s) {sorted(dup)} appear in more than one group")
-            seen.update(g.columns)
+        owner = {}
+        for gi, g in enumerate(groups):
+            shared = sorted(c for c in g.columns if owner.get(c, gi) != gi)
+            if shared:
+                raise ConfigError(f"column(s) {shared} appear in more than one group")
+            owner.update((c, gi) for c in g.columns)
 
     @property
     def used_columns(self):
@@ -67,80 +95,125 @@ class GroupingSpec:
 
 @dataclass(frozen=True)
 class ScalingInfo:
+    """x_box = (x - midpoints) / factor (datapipe.py:86-97)."""
+
     midpoints: np.ndarray
     factor: float
     mode: str
 
 
+# ------------------------------------------------------------ box map ------
+@dataclass(frozen=True)
+class BoxMap:
+    """Affine map of a column group into [-s, s]^d, s = 1/4 - eps_b/2
+    (datapipe.py:100-123): x -> clip((x - mid) / half, -1, 1) * s, with
+    `half` the largest half-range over the columns.  A constant group maps
+    to the origin with factor 1."""
+
+    mid: np.ndarray
+    half: float
+    s: float
+
+    @classmethod
+    def fit(cls, X, eps_b=fastsum.DEFAULT_EPS_B):
+        X = np.asarray(X, dtype=float)
+        if X.ndim != 2:
+            raise ConfigError("expected a 2-d feature block")
+        if not np.isfinite(X).all():
+            raise FormatError("non-finite feature values")
+        lo, hi = X.min(axis=0), X.max(axis=0)
+        return cls(mid=0.5 * (lo + hi), half=float((hi - lo).max()) / 2.0, s=fastsum.box_halfwidth(eps_b))
+
+    @property
+    def factor(self):
+        """Original units per box unit (1 for a constant group)."""
+        return 1.0 if self.half == 0.0 else self.half / self.s
+
+    def __call__(self, X):
+        X = np.asarray(X, dtype=float)
+        if self.half == 0.0:
+            return np.zeros_like(X)
+        # the clip absorbs the one-ulp overshoot at the extremes; with a
+        # dyadic s the product then stays inside the box
+        return np.clip((X - self.mid) / self.half, -1.0, 1.0) * self.s
+
+    def info(self):
+        return ScalingInfo(midpoints=self.mid, factor=self.factor, mode="fastsum-box")
+
+    def kernel_in_box(self, kernel, mode):
+        """The group's kernel with sigma in box units (datapipe.py:126-133)."""
+        sigma = kernel.sigma / self.factor if mode == "fastsum-box" else kernel.sigma * self.s
+        return KernelSpec(family=kernel.family, sigma=sigma)
+
+
 def scale_for_fastsum(X, eps_b=fastsum.DEFAULT_EPS_B):
-    """Centre at column midpoints, one isotropic factor into the box (datapipe.py:100-123)."""
-    X = np.asarray(X, dtype=float)
-    if X.ndim != 2:
-        raise ConfigError("expected a 2-d feature block")
-    if not np.all(np.isfinite(X)):
-        raise FormatError("non-finite feature values")
-    s = fastsum.box_halfwidth(eps_b)
-    lo, hi = X.min(axis=0), X.max(axis=0)
-    mid = 0.5 * (lo + hi)
-    half = float(np.max(hi - lo)) / 2.0
-    if half == 0.0:
-        return np.zeros_like(X), ScalingInfo(midpoints=mid, factor=1.0, mode="fastsum-box")
-    unit = np.clip((X - mid) / half, -1.0, 1.0)
-    return unit * s, ScalingInfo(midpoints=mid, factor=half / s, mode="fastsum-box")
+    """(box coordinates, ScalingInfo) of one column group (datapipe.py:100-123)."""
+    bm = BoxMap.fit(X, eps_b)
+    return bm(X), bm.info()
 
 
-def _scaled_group(Xg, g, eps_b):
-    Xb, info = scale_for_fastsum(Xg, eps_b)
-    if g.mode == "fastsum-box":
-        sigma_box = g.kernel.sigma / info.factor
-    else:
-        sigma_box = g.kernel.sigma * fastsum.box_halfwidth(eps_b)
-    return Xb, KernelSpec(family=g.kernel.family, sigma=sigma_box), info
+def box_points(Xg, kernel, mode="fastsum-box", eps_b=fastsum.DEFAULT_EPS_B):
+    """(box coordinates, box-unit kernel) of one column group."""
+    bm = BoxMap.fit(Xg, eps_b)
+    return bm(Xg), bm.kernel_in_box(kernel, mode)
 
 
-def feature_group(X, spec, components=None, fastsum_params=None, device=None):
-    """One GPU graph layer per column group (datapipe.py:136-170)."""
+# ------------------------------------------------------------ layers -------
+def _checked_matrix(X, spec):
     X = np.asarray(X, dtype=float)
     if X.ndim != 2:
         raise ConfigError("feature matrix must be 2-d")
-    n, d = X.shape
-    for g in spec.groups:
-        bad = [c for c in g.columns if c < 0 or c >= d]
-        if bad:
-            raise ConfigError(f"column index {bad[0]} out of range for {d} feature columns")
-    unused = sorted(set(range(d)) - set(spec.used_columns))
+    d = X.shape[1]
+    out_of_range = [c for g in spec.groups for c in g.columns if not 0 <= c < d]
+    if out_of_range:
+        raise ConfigError(f"column index {out_of_range[0]} out of range for {d} feature columns")
+    unused = sorted(set(range(d)).difference(spec.used_columns))
     if unused:
         log.info("dropping %d unused feature column(s): %s", len(unused), unused)
+    return X
+
+
+def _group_weights(X, g, components, params, device, factory):
+    Xg = X[:, list(g.columns)]
+    comp = components if g.per_component else None
+    if g.mode == "none":          # original units, exact sums
+        return factory(Xg, g.kernel, plan=None, components=comp, device=device)
+    Xb, kernel_box = box_points(Xg, g.kernel, g.mode, params.get("eps_b", fastsum.DEFAULT_EPS_B))
+    plan = fastsum.build_plan(kernel_box, d=len(g.columns), **params) if len(g.columns) <= _BOX_LIMIT else None
+    return factory(Xb, kernel_box, plan=plan, components=comp, device=device)
+
+
+def feature_group(X, spec, components=None, fastsum_params=None, device=None, weights_factory=None):
+    """One graph layer per column group (datapipe.py:136-170), bound on the GPU.
+
+    `weights_factory(points, kernel, plan=, components=, device=)` replaces
+    KernelWeights (default) for every group."""
+    X = _checked_matrix(X, spec)
     params = dict(fastsum_params or {})
-    eps_b = params.get("eps_b", fastsum.DEFAULT_EPS_B)
-    layers = []
-    for g in spec.groups:
-        Xg = X[:, list(g.columns)]
-        comp = components if g.per_component else None
-        if g.mode == "none":
-            weights = KernelWeights(Xg, g.kernel, plan=None, components=comp, device=device)
-        else:
-            Xb, kern_box, _ = _scaled_group(Xg, g, eps_b)
-            plan = fastsum.build_plan(kern_box, d=len(g.columns), **params) if len(g.columns) <= 3 else None
-            weights = KernelWeights(Xb, kern_box, plan=plan, components=comp, device=device)
-        layers.append(build_layer(weights))
-    return MultilayerGraph(tuple(layers))
+    factory = KernelWeights if weights_factory is None else weights_factory
+    return MultilayerGraph(tuple(build_layer(_group_weights(X, g, components, params, device, factory))
+                                 for g in spec.groups))
 
 
+# ------------------------------------------------------------ labels -------
 def sample_labels(truth, fraction, seed, omega0=1000.0):
-    """Per class ceil(fraction * size) labelled nodes, default_rng(seed) (datapipe.py:367-385)."""
+    """Known labels: per class c = 0..m-1 in order, ceil(fraction * |c|)
+    members (at least one) drawn without replacement by one
+    default_rng(seed) stream (datapipe.py:367-385)."""
     truth = np.asarray(truth)
     if not 0.0 < fraction <= 1.0:
         raise ConfigError(f"label fraction {fraction} outside (0, 1]")
     m = int(truth.max()) + 1
     if truth.min() < 0:
         raise ConfigError("ground truth must label every node (no negatives)")
+    sizes = np.bincount(truth.astype(np.int64), minlength=m)
+    if (sizes == 0).any():
+        raise ConfigError(f"class {int(np.argmin(sizes > 0))} absent from ground truth")
+    by_class = np.argsort(truth, kind="stable")        # members of class c, ascending node index
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
     rng = np.random.default_rng(seed)
     ids = np.full(truth.shape[0], -1)
     for c in range(m):
-        members = np.flatnonzero(truth == c)
-        if members.size == 0:
-            raise ConfigError(f"class {c} absent from ground truth")
-        count = max(1, math.ceil(fraction * members.size))
-        ids[rng.choice(members, size=count, replace=False)] = c
+        members = by_class[bounds[c]:bounds[c + 1]]
+        ids[rng.choice(members, size=max(1, math.ceil(fraction * sizes[c])), replace=False)] = c
     return LabelData.from_class_ids(ids, m, omega0)

@@ -231,37 +231,53 @@ class PeerGridExchange:
         if world > 8:
             raise ValueError("peer grid exchange supports at most 8 ranks")
         self.world, self.rank = world, rank
-        self.recv = recv if recv is not None else torch.zeros(world * self.cells, dtype=torch.float64,
-                                                               device=f"cuda:{self.device}")
+        # two receive buffers, alternated per call (write-after-read safety:
+        # rank r's stores of call k+2 into buffer (k mod 2) follow call k+1's
+        # barrier, which every peer reaches only after its slot sum of call k)
+        if recv is None:
+            recv = [torch.zeros(world * self.cells, dtype=torch.float64, device=f"cuda:{self.device}")
+                    for _ in range(2)]
+        elif not isinstance(recv, (list, tuple)):
+            recv = [recv]
+        self.recv = list(recv)
         self._opened = []
         if slots is None:
             lib = _lib.lib()
-            h = (ctypes.c_ubyte * 64)()
-            _lib.check(lib.mlb_ipc_handle(_lib.ptr(self.recv), h))
-            handles = [None] * world
-            comm.dist.all_gather_object(handles, bytes(h), group=comm.group)
-            bases = []
-            for q in range(world):
-                if q == rank:
-                    bases.append(self.recv.data_ptr())
-                    continue
-                ptr = ctypes.c_void_p()
-                buf = (ctypes.c_ubyte * 64).from_buffer_copy(handles[q])
-                _lib.check(lib.mlb_ipc_open(buf, self.device, ctypes.byref(ptr)))
-                self._opened.append(ptr)
-                bases.append(ptr.value)
-            slots = [b + 8 * rank * self.cells for b in bases]
-        self.slots = (ctypes.c_void_p * len(slots))(*slots)
+            slots = []
+            for buf_local in self.recv:
+                h = (ctypes.c_ubyte * 64)()
+                _lib.check(lib.mlb_ipc_handle(_lib.ptr(buf_local), h))
+                handles = [None] * world
+                comm.dist.all_gather_object(handles, bytes(h), group=comm.group)
+                bases = []
+                for q in range(world):
+                    if q == rank:
+                        bases.append(buf_local.data_ptr())
+                        continue
+                    ptr = ctypes.c_void_p()
+                    buf = (ctypes.c_ubyte * 64).from_buffer_copy(handles[q])
+                    _lib.check(lib.mlb_ipc_open(buf, self.device, ctypes.byref(ptr)))
+                    self._opened.append(ptr)
+                    bases.append(ptr.value)
+                slots.append([b + 8 * rank * self.cells for b in bases])
+        elif slots and not isinstance(slots[0], (list, tuple)):
+            slots = [slots]
+        if len(slots) != len(self.recv):
+            raise ValueError("one slot list per receive buffer")
+        self.slots = [(ctypes.c_void_p * len(sl))(*sl) for sl in slots]
+        self._calls = 0
         self._flag = torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.device}")
 
-    def spread_sum(self, binding, x, grid):
+    def spread_sum(self, binding, x, grid, flags=0):
         """grid = sum over ranks of their spreads (this rank spreads x)."""
         lib = _lib.lib()
         sp = _lib.stream_ptr()
-        _lib.check(lib.mlb_spread_peers(binding.ptr, _lib.ptr(x), self.slots, self.world, 0, sp))
+        k = self._calls % len(self.recv)
+        self._calls += 1
+        _lib.check(lib.mlb_spread_peers(binding.ptr, _lib.ptr(x), self.slots[k], self.world, int(flags), sp))
         if self.world > 1:  # every rank's peer stores precede every rank's reads
             self.comm.dist.all_reduce(self._flag, group=self.comm.group)
-        _lib.check(lib.mlb_grid_sum_slots(_lib.ptr(self.recv), self.world, self.cells, _lib.ptr(grid), sp))
+        _lib.check(lib.mlb_grid_sum_slots(_lib.ptr(self.recv[k]), self.world, self.cells, _lib.ptr(grid), sp))
         return grid
 
     def close(self):
@@ -389,3 +405,150 @@ def sharded_pksm(layer, p, v, krylov_dim=50, tol=1e-8):
     if p == 0:
         raise ConfigError("p must be nonzero")
     return sharded_lanczos_fn(layer, v, power_fn(p), krylov_dim, tol)
+
+
+# ------------------------------- 2b. node-range sharded multilayer graph ----
+class ShardedKernelGraph:
+    """Every layer of a multilayer kernel graph split by the SAME node range
+    over the ranks: rank r owns nodes [lo, hi)
+    of every layer and binds only those points (the active sub-box of a
+    plan is fixed by the plan's admissible box, so every rank's grid has the
+    same layout).
+
+    One normalized-Laplacian step (every layer's L_sym + delta of one vector):
+      per layer   mlb_spread of the rank's nodes (D^-1/2 folded in) into that
+                  layer's slice of ONE buffer holding all layers' sub-box grids;
+      once        all-reduce (sum) of that buffer over the ranks -- the only
+                  collective of the step (NCCL over NVLink on the box);
+      per layer   mlb_convolve (redundant on every rank: the band-limited
+                  convolution of a <= 700 KB sub-box) and mlb_gather_apply,
+                  the gather with the fused epilogue
+                  y = (1+delta) v - D^-1/2 W~ D^-1/2 v + K0 D^-1 v on the
+                  rank's nodes (fastsum.py:475-497, graphs.py:197-201).
+    With one rank it is the single-GPU matvec (no collective).
+
+    layer_points: per layer the (n_local x d_t) box-unit points of this
+    rank's nodes; kernels / plans: per layer KernelSpec (box units) and
+    FastsumPlan.  Build the pieces with `shard_feature_groups`.
+    """
+
+    def __init__(self, layer_points, kernels, plans, n_global, lo, hi, comm=None, shift=0.0, device=None):
+        from .graphs import KernelWeights
+        torch = _torch()
+        self.comm = comm
+        self.world = 1 if comm is None else comm.world
+        self.n, self.lo, self.hi = int(n_global), int(lo), int(hi)
+        self.shift = float(shift)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.dev = torch.device("cuda", self.device)
+        self.weights = [KernelWeights(pts, k, plan=pl, device=self.device)
+                        for pts, k, pl in zip(layer_points, kernels, plans)]
+        for w in self.weights:
+            if w.n != self.n_local:
+                raise ConfigError("every layer must hold this rank's node range")
+        self.T = len(self.weights)
+        self.K0 = [w.kernel.value_at_zero() for w in self.weights]
+        cells = [w._bindings[0].stats()["grid_cells"] for w in self.weights]
+        self.offsets = np.concatenate([[0], np.cumsum(cells)]).astype(np.int64)
+        self.grids = torch.zeros(int(self.offsets[-1]), dtype=torch.float64, device=self.dev)
+        self.conv = torch.zeros_like(self.grids)
+        self.degrees = None
+        self.isd = None
+
+    @property
+    def n_local(self):
+        return self.hi - self.lo
+
+    def _grid(self, buf, t):
+        return buf[int(self.offsets[t]):int(self.offsets[t + 1])]
+
+    def _all_reduce(self):
+        if self.comm is not None:   # (a world-size-1 group still runs the collective)
+            self.comm.all_reduce_sum(self.grids)
+
+    def spread_local(self, v, flags):
+        """Every layer's spread of this rank's nodes into self.grids."""
+        lib = _lib.lib()
+        sp = _lib.stream_ptr()
+        spread_flags = int(flags) & (_lib.MLB_USE_ISD | _lib.MLB_SORTED)
+        for t, w in enumerate(self.weights):
+            _lib.check(lib.mlb_spread(w._bindings[0].ptr, _lib.ptr(v), _lib.ptr(self._grid(self.grids, t)),
+                                      spread_flags, sp))
+
+    def _step(self, v, ys, coef, flags):
+        """ys[t] (=|+=) coef[t] combination for every layer; ONE collective."""
+        self.spread_local(v, flags)
+        self._all_reduce()
+        return self.finish(v, ys, coef, flags)
+
+    def finish(self, v, ys, coef, flags):
+        """Convolve the summed grids and gather this rank's nodes (fused epilogue)."""
+        lib = _lib.lib()
+        sp = _lib.stream_ptr()
+        for t, w in enumerate(self.weights):
+            b = w._bindings[0].ptr
+            g_in, g_out = self._grid(self.grids, t), self._grid(self.conv, t)
+            _lib.check(lib.mlb_convolve(b, _lib.ptr(g_in), _lib.ptr(g_out), sp))
+            a, be, ga = coef[t]
+            _lib.check(lib.mlb_gather_apply(b, _lib.ptr(g_out), _lib.ptr(v), _lib.ptr(ys[t]), float(a), float(be),
+                                            float(ga), int(flags), sp))
+        return ys
+
+    def build(self):
+        """Degrees W 1 of every layer (graphs.py:168-183) through the sharded
+        matvec; a zero degree on any rank raises NumericalError naming the
+        first global node; then D^-1/2 is stored in every binding."""
+        torch = _torch()
+        ones = torch.ones(self.n_local, dtype=torch.float64, device=self.dev)
+        degs = [torch.empty_like(ones) for _ in range(self.T)]
+        self._step(ones, degs, [(-k0, 1.0, 0.0) for k0 in self.K0], 0)
+        first = torch.tensor([float(self.n)], dtype=torch.float64, device=self.dev)
+        for d in degs:
+            bad = torch.nonzero(d <= 1e-300)
+            if bad.numel():
+                first = torch.minimum(first, (bad[0].to(torch.float64) + self.lo).reshape(1))
+        if self.world > 1:
+            self.comm.dist.all_reduce(first, op=self.comm.dist.ReduceOp.MIN, group=self.comm.group)
+        if int(first.item()) < self.n:
+            raise NumericalError(f"node {int(first.item())} has zero degree; the normalized Laplacian is undefined")
+        return self.set_degrees(degs)
+
+    def set_degrees(self, degs):
+        """Store this rank's degrees and D^-1/2 (1 / sqrt, as graphs.py:159-165)."""
+        torch = _torch()
+        self.degrees = degs
+        self.isd = [1.0 / torch.sqrt(d) for d in degs]
+        for w, s in zip(self.weights, self.isd):
+            w.set_isd(s)
+        return self
+
+    def lsym(self, v, ys, accumulate=False):
+        """ys[t] = (L_sym,t + shift) v for every layer t (local rows)."""
+        flags = _lib.MLB_USE_ISD | (_lib.MLB_ACCUMULATE if accumulate else 0)
+        return self._step(v, ys, [(1.0 + self.shift, -1.0, k0) for k0 in self.K0], flags)
+
+    def weighted(self, v, ys):
+        """ys[t] = D^-1/2 W D^-1/2 v (the apply_one_minus_L1 term, powermean.py:75-76)."""
+        return self._step(v, ys, [(0.0, 1.0, -k0) for k0 in self.K0], _lib.MLB_USE_ISD)
+
+
+def shard_feature_groups(X, groups, rank, world, eps_b=None):
+    """Box-scaled points of this rank's node range for every column group.
+
+    groups: [(columns, KernelSpec in feature units, fastsum params dict)].
+    The box scaling uses the WHOLE feature matrix (every rank holds X), so
+    each rank's points and kernel widths are those of the unsharded layer
+    (datapipe.feature_group's scaling).  Returns (lo, hi, points, kernels, plans).
+    """
+    from . import datapipe, fastsum
+    n = X.shape[0]
+    lo, hi = shard_range(n, rank, world)
+    pts, kerns, plans = [], [], []
+    for columns, kernel, params in groups:
+        params = dict(params or {})
+        eb = params.get("eps_b", fastsum.DEFAULT_EPS_B) if eps_b is None else eps_b
+        Xb, kb = datapipe.box_points(X[:, list(columns)], kernel, "fastsum-box", eb)
+        pts.append(np.ascontiguousarray(Xb[lo:hi]))
+        kerns.append(kb)
+        plans.append(fastsum.build_plan(kb, d=len(columns), **params))
+    return lo, hi, pts, kerns, plans

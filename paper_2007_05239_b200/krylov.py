@@ -283,16 +283,20 @@ class PksmStats:
 _PINNED = {}
 
 
-def _pinned_snapshots(shape):
+def _pinned_snapshots(shape, device):
     """Reused pinned host buffer for the per-step alpha / beta snapshots (a
-    fresh pinned allocation per solve costs far more than the solve's reads;
-    reuse is safe: every read waits for its own step's event, which follows
-    any earlier copy into the buffer on the stream)."""
+    fresh pinned allocation per solve costs far more than the solve's reads).
+    Keyed like the Krylov bases by (device, nesting level, shape): a solve
+    nested inside an operator of another solve, or a solve on another device
+    or thread-stream, never shares the outer solve's rows.  Reuse by the NEXT
+    solve at the same level is safe: every read waits for its own step's
+    event, which follows any earlier copy into the buffer on the stream."""
     torch = _torch()
-    buf = _PINNED.get(shape)
+    key = (int(device.index if hasattr(device, "index") else device), _VPOOL_DEPTH[0], tuple(shape))
+    buf = _PINNED.get(key)
     if buf is None:
         buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
-        _PINNED[shape] = buf
+        _PINNED[key] = buf
     return buf
 
 
@@ -435,7 +439,7 @@ def _lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None
     dot(v, v, vv)
     V = _krylov_basis(v.device, 0, dim, n)
     scale_by(v, V[0], vv, -0.5)
-    ABh = _pinned_snapshots((dim, 2 * dim + 1))
+    ABh = _pinned_snapshots((dim, 2 * dim + 1), v.device)
     stream = torch.cuda.current_stream(v.device)
     chain = _Chain(V, AB, stream, apply_dev=apply_dev, fused=fused)
     events = [None] * dim
@@ -556,7 +560,7 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
     # per layer AB row: h1 row (alpha_j at j) | ||w_j||^2 | <v, v>; V[0] on
     # the device, <v, v> read with step 0 (no start-of-solve sync)
     AB = torch.zeros((T, 2 * dim + 1), dtype=torch.float64, device=dev)
-    ABh = _pinned_snapshots((dim, T, 2 * dim + 1))
+    ABh = _pinned_snapshots((dim, T, 2 * dim + 1), dev)
     stream = torch.cuda.current_stream(dev)
     for t, x in enumerate(st):
         vv = AB[t, 2 * dim:2 * dim + 1]

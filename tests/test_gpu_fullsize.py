@@ -19,15 +19,14 @@ def test_config2_full_size_matches_parallel_reference():
     import synth
     from oracle import fastsum_oracle as fo
     from oracle.parallel_ref import ParallelReference
-    from paper_2007_05239_b200 import GroupSpec, KernelSpec, LaplacianBatch, MultilayerGraph, datapipe, with_shift
+    from paper_2007_05239_b200 import KernelSpec, LaplacianBatch, MultilayerGraph, datapipe, with_shift
     wl = synth.config2_segmentation(seed=0)
     delta = math.log(2.0)
     G = synth.build_graph(wl, device=0)
     graph = MultilayerGraph(tuple(with_shift(layer, delta) for layer in G.layers))
     specs = []
     for ls in wl.layers:
-        g = GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma))
-        Xb, kb, _ = datapipe._scaled_group(wl.X[:, list(ls.columns)], g, 1.0 / 16)
+        Xb, kb = datapipe.box_points(wl.X[:, list(ls.columns)], KernelSpec(ls.family, ls.sigma))
         specs.append((fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p), Xb))
     ref = ParallelReference(specs, wl.n, delta, start_method="forkserver")  # this process runs CUDA
     try:

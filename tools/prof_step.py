@@ -1,5 +1,8 @@
-"""Small driver for ncu: build the config-2 layers, run a few fused
-normalized-Laplacian steps (no timing, no CPU baseline)."""
+"""Small driver for ncu: build a workload's layers, run a few fused
+normalized-Laplacian steps (no timing, no CPU baseline).
+
+    python tools/prof_step.py [steps] [side|cfg4]   (default: 3 steps of config 2 at 512)
+"""
 import math
 import os
 import sys
@@ -17,9 +20,12 @@ from paper_2007_05239_b200.graphs import apply_sym_laplacian_dev
 
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-    side = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    which = sys.argv[2] if len(sys.argv) > 2 else "512"
     torch.cuda.set_device(0)
-    wl = synth.config2_segmentation(seed=0, side=side)
+    if which == "cfg4":
+        wl = synth.config4_large(seed=0)
+    else:
+        wl = synth.config2_segmentation(seed=0, side=int(which))
     G = synth.build_graph(wl, device=0)
     layers = [with_shift(l, math.log(2.0)) for l in G.layers]
     v = torch.from_numpy(np.random.default_rng(1).standard_normal(wl.n)).cuda()
