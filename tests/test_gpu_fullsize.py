@@ -10,6 +10,8 @@ import math
 import numpy as np
 import pytest
 
+from oracle import fastsum_oracle as fo
+
 pytestmark = pytest.mark.gpu
 
 
@@ -42,3 +44,37 @@ def test_config2_full_size_matches_parallel_reference():
     for t in range(graph.T):
         err = np.linalg.norm(got[t] - want[t]) / np.linalg.norm(want[t])
         assert err < 1e-11, (t, err)
+
+
+def test_config4_full_size_matches_c_oracle():
+    """BASELINE configs[3] at FULL size (3162 x 3162, n = 9,998,244; RGB d=3
+    and xy d=2, N=64, m=5): the layers' degrees and L_sym v for two seeded
+    vectors through the GPU path (the m=5 d=3 spread, the grouped d=2 lanes
+    of n >= 2^20, heavy-cell block splitting, the batched two-stream step)
+    against the C restatement of the reference spread / gather on every host
+    core with the scipy FFT stage (oracle/c_oracle.py; the chunked oracle of
+    SURVEY 8(c): the reference binding would need 213 GB).  North-star bar:
+    1e-8 relative; observed ~1e-13."""
+    import torch
+
+    import synth
+    from oracle import c_oracle as co
+    from paper_2007_05239_b200 import KernelSpec, LaplacianBatch, MultilayerGraph, datapipe, with_shift
+    wl = synth.config4_large(seed=0)
+    delta = math.log(2.0)
+    G = synth.build_graph(wl, device=0)
+    graph = MultilayerGraph(tuple(with_shift(layer, delta) for layer in G.layers))
+    rng = np.random.default_rng(44)
+    V = rng.standard_normal((2, wl.n))
+    batch = LaplacianBatch(graph)
+    got = [batch.apply(torch.from_numpy(v).pin_memory()).numpy().copy() for v in V]
+    for t, ls in enumerate(wl.layers):
+        Xb, kb = datapipe.box_points(wl.X[:, list(ls.columns)], KernelSpec(ls.family, ls.sigma))
+        op = fo.OraclePlan(ls.family, kb.sigma, len(ls.columns), ls.N, ls.m, p=ls.p)
+        deg, L = co.laplacian_layer(op, Xb, V, delta)
+        derr = np.linalg.norm(G.layers[t].degrees - deg) / np.linalg.norm(deg)
+        assert derr <= 1e-10, (t, derr)
+        for k in range(2):
+            err = np.linalg.norm(got[k][t] - L[k]) / np.linalg.norm(L[k])
+            assert err <= 1e-8, (t, k, err)
+            print(f"config 4 layer {t} vector {k}: rel err {err:.2e} (degrees {derr:.2e})")

@@ -68,6 +68,21 @@ def test_fastsum_matches_reference(name):
     assert np.linalg.norm(got_c - ref) <= 1e-13 * np.linalg.norm(ref)
     if name + "/direct" in g.files:
         assert_allclose(fo.direct(pts, v, fam, s), g[name + "/direct"], atol=1e-11)
+    # the C restatement (full-size chunked oracle, oracle/c/mlb_oracle.c): W v and W 1
+    # in one pass, on 3 host threads (a different summation order)
+    from oracle import c_oracle as co
+    both = co.fastsum_many(plan, pts, np.stack([v, np.ones(len(v))]), threads=3)
+    assert np.linalg.norm(both[0] - ref) <= 1e-13 * np.linalg.norm(ref)
+    assert_allclose(both[1], g[name + "/ones"], rtol=1e-12)
+
+
+def test_c_oracle_window_matches_reference():
+    from oracle import c_oracle as co
+    g = load_golden("window")
+    for m in (2, 3, 4, 5, 6):
+        ref = g[f"phi_m{m}"]
+        got = co.window(g[f"t_m{m}"], m, 1.5 * math.pi)
+        assert np.abs(got - ref).max() <= 4e-16 * np.abs(ref).max(), m
 
 
 def test_two_point_case():
