@@ -229,6 +229,16 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
 int mlb_ac_step2(const double* Phi, int64_t n, int k, int m, const double* U, const double* F, const double* fid,
                  const double* denom, double c_dt, double dt_2eps, double dt, int first, double* U_next,
                  double* stats, double* work, void* stream);
+/* the multiclass step split for node-range sharding: this
+   rank's rows only.  rhs_partial: PtR (k x m, device) = Phi^T R(U) over the n
+   local rows (fixed-order block sums); the caller all-reduces PtR over the
+   ranks; update_from: Vc = PtR / denom, U_next = proj_simplex(Phi Vc), stats =
+   the local [max |dU_i|^2, max |U_next_i|^2] (the caller max-reduces them).
+   work: mlb_ac_work_size doubles. */
+int mlb_ac_rhs_partial(const double* Phi, int64_t n, int k, int m, const double* U, const double* F, const double* fid,
+                       double c_dt, double dt_2eps, double dt, double* PtR, double* work, void* stream);
+int mlb_ac_update_from(const double* Phi, int64_t n, int k, int m, const double* PtR, const double* denom,
+                       const double* U, double* U_next, double* stats, double* work, void* stream);
 /* one binary Allen-Cahn step (allencahn.py:261-309): v_next = (lead v - dt/eps Phi^T u^3
    - dt Phi^T (fid (u - f))) / denom, u_next = Phi v_next; stats = (max (u_next-u)^2, max u_next^2);
    work: mlb_ac_work_size(n, k, 1) doubles */

@@ -80,6 +80,8 @@ SIGNATURES = {
     "mlb_ac_step": (I, [P, I64, I, I, P, P, P, P, D, D, D, P, P, P, P]),
     "mlb_argmax_rows": (I, [P, I64, I, P, P]),
     "mlb_ac_step2": (I, [P, I64, I, I, P, P, P, P, D, D, D, I, P, P, P, P]),
+    "mlb_ac_rhs_partial": (I, [P, I64, I, I, P, P, P, D, D, D, P, P, P]),
+    "mlb_ac_update_from": (I, [P, I64, I, I, P, P, P, P, P, P, P]),
     "mlb_bac_step": (I, [P, I64, I, P, P, P, P, P, D, D, D, P, P, P, P, P]),
     "mlb_gl_energy_work_size": (I64, [I, I]),
     "mlb_gl_energy_partials": (I, [P, I64, I, I, P, P, P, P, P, P]),

@@ -567,7 +567,7 @@ __global__ void ac_finish_kernel(const double* __restrict__ partial, int nb, int
     for (int b = lane; b < nb; b += 32) s += partial[(int64_t)b * k * m + o];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-    if (lane == 0) Vc[o] = s / denom[o / m];
+    if (lane == 0) Vc[o] = denom ? s / denom[o / m] : s;  // (no denom: the plain sum, sharded partials)
 }
 
 __global__ void ac_update_kernel(const double* __restrict__ Phi, int64_t n, int k, int m,
@@ -940,6 +940,65 @@ int mlb_ac_step(const double* Phi, int64_t n, int k, int m, const double* U, con
     note_launches(3);
     ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
     note_launches(1);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_ac_rhs_partial(const double* Phi, int64_t n, int k, int m, const double* U, const double* F, const double* fid,
+                       double c_dt, double dt_2eps, double dt, double* PtR, double* work, void* stream) {
+    if (m < 2 || m > kAcMaxM) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels support 2 <= m <= 32 classes");
+    if (k < 1 || k * m > 16 * 256) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels need k*m <= 4096");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) {
+        MLB_CUDA_TRY(cudaMemsetAsync(PtR, 0, (size_t)k * m * sizeof(double), st));
+        return MLB_OK;
+    }
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(
+        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(device_sms(), n / 1024))));
+    double* partial = work;
+    const size_t sm1 = std::max((size_t)256 * (k + 2 * m), (size_t)256 * 32) * sizeof(double);
+    const size_t sm2 = std::max((size_t)kTile * (m + k), (size_t)256 * 32) * sizeof(double);
+    if (sm1 > 200 * 1024 || sm2 > 200 * 1024) return fail(MLB_ERR_CONFIG, "Allen-Cahn tiles too large (k, m)");
+    if (m <= 8) {
+        auto rhs = m <= 4 ? ac_rhs3_kernel<4> : ac_rhs3_kernel<8>;
+        if (int rc = ensure_max_smem((const void*)rhs, sm1)) return rc;
+        rhs<<<nb, 256, sm1, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
+    } else {
+        if (int rc = ensure_max_smem((const void*)ac_rhs2_kernel, sm2)) return rc;
+        ac_rhs2_kernel<<<nb, 256, sm2, st>>>(Phi, n, k, m, U, F, fid, c_dt, dt_2eps, dt, partial);
+    }
+    ac_finish_kernel<<<(k * m * 32 + 255) / 256, 256, 0, st>>>(partial, nb, k, m, nullptr, PtR);
+    note_launches(2);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_ac_update_from(const double* Phi, int64_t n, int k, int m, const double* PtR, const double* denom,
+                       const double* U, double* U_next, double* stats, double* work, void* stream) {
+    if (m < 2 || m > kAcMaxM) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels support 2 <= m <= 32 classes");
+    if (k < 1 || k * m > 16 * 256) return fail(MLB_ERR_CONFIG, "Allen-Cahn kernels need k*m <= 4096");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(
+        (n + kAcRows - 1) / kAcRows, std::min<int64_t>(kAcBlocks, std::max<int64_t>(device_sms(), n / 1024))));
+    double* mx = work + (int64_t)kAcBlocks * k * m;
+    double* Vc = mx + 2 * kAcBlocks;
+    ac_finish_kernel<<<(k * m * 32 + 255) / 256, 256, 0, st>>>(PtR, 1, k, m, denom, Vc);
+    note_launches(1);
+    if (n == 0) {
+        MLB_CUDA_TRY(cudaMemsetAsync(stats, 0, 2 * sizeof(double), st));
+        return MLB_OK;
+    }
+    const size_t sm3 = ((size_t)((k * m + 1) & ~1) + (size_t)256 * (k + m)) * sizeof(double);
+    if (m <= 8) {
+        auto upd = m <= 4 ? ac_update3_kernel<4> : ac_update3_kernel<8>;
+        if (sm3 > 200 * 1024) return fail(MLB_ERR_CONFIG, "Allen-Cahn tiles too large (k, m)");
+        if (int rc = ensure_max_smem((const void*)upd, sm3)) return rc;
+        upd<<<nb, 256, sm3, st>>>(Phi, n, k, m, Vc, U, U_next, mx);
+    } else {
+        ac_update_kernel<<<nb, 256, (size_t)k * m * sizeof(double), st>>>(Phi, n, k, m, Vc, U, U_next, mx);
+    }
+    ac_max_finish<<<1, 32, 0, st>>>(mx, nb, stats);
+    note_launches(2);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }

@@ -354,57 +354,25 @@ class ShardedLayer:
         return float(sum(float(p.item()) for p in parts))   # rank order: deterministic
 
 
-def sharded_lanczos_fn(layer, v, fn, krylov_dim=50, tol=1e-8):
-    """Lanczos f(A) v (krylov.py:172-216) on node-sharded vectors.
-
-    The basis is sharded with the nodes; every inner product is a global sum
-    over ranks (rank order), so all ranks take identical decisions.
-    """
+def sharded_pksm(layer, p, v, krylov_dim=50, tol=1e-8):
+    """(L_sym + delta)^p v on node-sharded vectors (krylov.py:219-244) for a
+    ShardedLayer: the solver of sharded.py (two fused reductions per step)
+    with this layer's Laplacian; numpy in -> numpy out (CPU engines), CUDA
+    tensor in -> CUDA tensor out."""
+    from .sharded import ShardContext
+    from .sharded import sharded_pksm as _pksm
     torch = _torch()
     is_t = isinstance(v, torch.Tensor)
-    nv = math.sqrt(layer.dot(v, v))
-    if nv == 0.0:
-        return v * 0.0
-    dim = int(min(krylov_dim, layer.n))
-    V = [v / nv]
-    alphas, betas = [], []
-    y_prev = None
-    while True:
-        s = len(V) - 1
-        w = layer.apply_lsym(V[s])
-        alphas.append(layer.dot(V[s], w))
-        # CGS2 against V[0..s] with global dot products (krylov.py:65-71)
-        for _ in range(2):
-            h = [layer.dot(Vj, w) for Vj in V]
-            for Vj, hj in zip(V, h):
-                w = w - hj * Vj
-        beta = math.sqrt(layer.dot(w, w))
-        betas.append(beta)
-        m = len(alphas)
-        T = np.diag(alphas)
-        if m > 1:
-            T += np.diag(betas[: m - 1], 1) + np.diag(betas[: m - 1], -1)
-        lam, Q = np.linalg.eigh(T)
-        c = nv * (Q @ (fn(lam) * Q[0, :]))
-        y = c[0] * V[0]
-        for j in range(1, m):
-            y = y + c[j] * V[j]
-        if y_prev is not None:
-            d = y - y_prev
-            if math.sqrt(layer.dot(d, d)) <= tol * max(math.sqrt(layer.dot(y, y)), 1e-300):
-                return y
-        if beta <= 1e-13 * max(1.0, float(np.abs(alphas).max())) or m >= dim:
-            return y
-        y_prev = y
-        V.append(w / beta)
+    dev = v.device.index if is_t and v.is_cuda else None
+    ctx = ShardContext(layer.comm, layer.n, layer.lo, layer.hi, dev)
 
-
-def sharded_pksm(layer, p, v, krylov_dim=50, tol=1e-8):
-    """(L_sym + delta)^p v on node-sharded vectors (krylov.py:219-244)."""
-    from .krylov import power_fn
-    if p == 0:
-        raise ConfigError("p must be nonzero")
-    return sharded_lanczos_fn(layer, v, power_fn(p), krylov_dim, tol)
+    def apply(x):
+        if dev is None:
+            return torch.from_numpy(np.ascontiguousarray(layer.apply_lsym(x.numpy()), dtype=np.float64))
+        return layer.apply_lsym(x)
+    x = v if is_t else torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
+    y = _pksm(ctx, apply, p, x, krylov_dim, tol)
+    return y if is_t else y.numpy()
 
 
 # ------------------------------- 2b. node-range sharded multilayer graph ----
@@ -521,6 +489,38 @@ class ShardedKernelGraph:
         for w, s in zip(self.weights, self.isd):
             w.set_isd(s)
         return self
+
+    def _step_layer(self, t, v, y, coef, flags):
+        """One layer alone: its spread, the all-reduce of ITS grid slice only,
+        convolution and fused gather (the per-layer operator of PKSM)."""
+        lib = _lib.lib()
+        sp = _lib.stream_ptr()
+        b = self.weights[t]._bindings[0].ptr
+        g_in, g_out = self._grid(self.grids, t), self._grid(self.conv, t)
+        _lib.check(lib.mlb_spread(b, _lib.ptr(v), _lib.ptr(g_in), int(flags) & (_lib.MLB_USE_ISD | _lib.MLB_SORTED),
+                                  sp))
+        if self.comm is not None:
+            self.comm.all_reduce_sum(g_in)
+        _lib.check(lib.mlb_convolve(b, _lib.ptr(g_in), _lib.ptr(g_out), sp))
+        a, be, ga = coef
+        _lib.check(lib.mlb_gather_apply(b, _lib.ptr(g_out), _lib.ptr(v), _lib.ptr(y), float(a), float(be), float(ga),
+                                        int(flags), sp))
+        return y
+
+    def layer_ops(self):
+        """Per layer (ascending): (x -> (L_sym,t + shift) x, x -> D^-1/2 W D^-1/2 x)
+        on this rank's rows, each a new tensor -- the operators of
+        sharded.sharded_power_mean_eigs."""
+        torch = _torch()
+        ops = []
+        for t, k0 in enumerate(self.K0):
+            def lsym(x, t=t, k0=k0):
+                return self._step_layer(t, x, torch.empty_like(x), (1.0 + self.shift, -1.0, k0), _lib.MLB_USE_ISD)
+
+            def weighted(x, t=t, k0=k0):
+                return self._step_layer(t, x, torch.empty_like(x), (0.0, 1.0, -k0), _lib.MLB_USE_ISD)
+            ops.append((lsym, weighted))
+        return ops
 
     def lsym(self, v, ys, accumulate=False):
         """ys[t] = (L_sym,t + shift) v for every layer t (local rows)."""

@@ -337,7 +337,7 @@ def test_peer_grid_exchange_two_emulated_ranks():
             ex = PeerGridExchange(None, cells, 0, recv=recv[r],
                                   slots=[recv[q].data_ptr() + 8 * r * cells for q in range(2)])
             ex.world, ex.rank = 2, r
-            _lib.check(_lib.lib().mlb_spread_peers(b.ptr, _lib.ptr(torch.from_numpy(v[lo:hi]).cuda()), ex.slots, 2,
+            _lib.check(_lib.lib().mlb_spread_peers(b.ptr, _lib.ptr(torch.from_numpy(v[lo:hi]).cuda()), ex.slots[0], 2,
                                                    0, _lib.stream_ptr()))
             grids.append(ex)
         out = []
