@@ -110,3 +110,49 @@ def test_sharded_graph_emulated_ranks_match_oracle(world):
         assert _rel(got_deg[t], deg) < 1e-12
         ref = so.sym_laplacian(lay.shifted(delta), v)
         assert _rel(got[t], ref) < 1e-11, (t, _rel(got[t], ref))
+
+
+def test_sharded_eigensolver_and_allen_cahn_nccl_world1():
+    """sharded.sharded_power_mean_eigs + sharded_allen_cahn through the NCCL
+    process group (world size 1: every reduction is a real collective call)
+    against the single-GPU power_mean_eigs / allen_cahn_solve of the same
+    graph: eigenvalues <= 1e-9, projectors <= 1e-7, identical labels."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2007_05239_b200 import (AllenCahnParams, LabelData, PowerMeanConfig, allen_cahn_solve,
+                                       power_mean_eigs, predict_labels, sample_labels)
+    from paper_2007_05239_b200.dist import Comm, ShardedKernelGraph, shard_feature_groups
+    from paper_2007_05239_b200.powermean import SpectralBasis
+    from paper_2007_05239_b200.sharded import ShardContext, sharded_allen_cahn, sharded_power_mean_eigs
+    wl = _small_cfg4(side=64)
+    delta = math.log(2.0)
+    k = 4
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        comm = Comm()
+        lo, hi, pts, kerns, plans = shard_feature_groups(wl.X, _groups(wl), 0, 1)
+        sg = ShardedKernelGraph(pts, kerns, plans, wl.n, lo, hi, comm=comm, shift=delta, device=0).build()
+        ctx = ShardContext(comm, wl.n, lo, hi, device=0)
+        vals, vecs = sharded_power_mean_eigs(ctx, sg.layer_ops(), PowerMeanConfig(p=-1.0), k, seed=0)
+        G = synth.build_graph(wl, device=0)
+        ref = power_mean_eigs(G, PowerMeanConfig(p=-1.0), k, seed=0)
+        assert np.max(np.abs(vals - ref.values) / np.abs(ref.values)) <= 1e-9
+        V = vecs.cpu().numpy()
+        z = np.random.default_rng(3).standard_normal((wl.n, 2))
+        d = np.linalg.norm(V @ (V.T @ z) - ref.vectors @ (ref.vectors.T @ z)) / np.linalg.norm(z)
+        assert d <= 1e-7, d
+        lab = sample_labels(wl.truth, 0.02, seed=0)
+        U, it, conv = sharded_allen_cahn(ctx, vals, vecs, LabelData(F=lab.F, fidelity=lab.fidelity, m=lab.m),
+                                         AllenCahnParams(max_iter=100))
+        res = allen_cahn_solve(SpectralBasis(values=vals, vectors=V), lab, AllenCahnParams(max_iter=100))
+        assert it == res.iterations and conv == res.converged
+        assert np.abs(U.cpu().numpy() - res.scores).max() <= 1e-12
+        assert np.array_equal(predict_labels(U.cpu().numpy()), predict_labels(res.scores))
+    finally:
+        dist.destroy_process_group()
