@@ -104,6 +104,26 @@ int mlb_plan_destroy(mlb_plan* plan);
  * mlb_apply -- one binding per component block (graphs.py:99-129). */
 int mlb_bind(const mlb_plan* plan, const double* points_host, int64_t n, double scale,
              const int32_t* node_ids_host, mlb_binding** out);
+/* The same binding from a row-major point / feature matrix on the host OR the
+ * device, with the box map of feature_group folded in (datapipe.py:100-123:
+ * x_box = clip((x - mid) / half, -1, 1) * box_s per column, then the torus
+ * scale) and validate_box (fastsum.py:66-80) done on the device.  Every
+ * per-point step (map, check, cells, stable sort, sorted offsets) runs on
+ * the GPU; the host builds the cell-level work tables from per-cell counts. */
+typedef struct mlb_bind_desc {
+    const double* points;     /* n rows of ld doubles */
+    int points_on_device;     /* 1: device pointer, 0: host pointer */
+    int64_t n;
+    int ld;                   /* row stride in doubles */
+    const int* cols;          /* nullable, host: the d columns of a row (default 0..d-1) */
+    double scale;             /* 1/sqrt(d) for the fastsum box, 1 for the bare torus transforms */
+    const double* box_mid;    /* nullable, host, d values: raw features -> box (mode "fastsum-box") */
+    double box_half, box_s;   /* half-range and box half-width of that map */
+    double box_hw;            /* > 0: reject |x_box|_inf > box_hw + 1e-12 (ConfigError, validate_box) */
+    const int32_t* node_ids;  /* nullable, host: point -> node index (component blocks) */
+    void* stream;             /* the bind's stream (it synchronises it) */
+} mlb_bind_desc;
+int mlb_bind_ex(const mlb_plan* plan, const mlb_bind_desc* desc, mlb_binding** out);
 int mlb_binding_destroy(mlb_binding* b);
 int64_t mlb_binding_n(const mlb_binding* b);
 /* sorted position -> original node index (int32, host out, n entries) */

@@ -33,6 +33,12 @@ class PlanDesc(C.Structure):
                 ("conv_kernel", P), ("sep_kernel", P)]
 
 
+class BindDesc(C.Structure):
+    """mlb_bind_desc (include/multilap_b200.h)."""
+    _fields_ = [("points", P), ("points_on_device", I), ("n", I64), ("ld", I), ("cols", P), ("scale", D),
+                ("box_mid", P), ("box_half", D), ("box_s", D), ("box_hw", D), ("node_ids", P), ("stream", P)]
+
+
 # name -> (restype, argtypes); mirrors include/multilap_b200.h
 SIGNATURES = {
     "mlb_abi_version": (I, []),
@@ -45,6 +51,7 @@ SIGNATURES = {
     "mlb_plan_create": (I, [C.POINTER(PlanDesc), I, C.POINTER(P)]),
     "mlb_plan_destroy": (I, [P]),
     "mlb_bind": (I, [P, P, I64, D, P, C.POINTER(P)]),
+    "mlb_bind_ex": (I, [P, C.POINTER(BindDesc), C.POINTER(P)]),
     "mlb_binding_destroy": (I, [P]),
     "mlb_binding_n": (I64, [P]),
     "mlb_binding_perm": (I, [P, P]),

@@ -18,7 +18,6 @@
 #include <tuple>
 #include <string>
 #include <queue>
-#include <thread>
 #include <cstdio>
 #include <vector>
 
@@ -113,28 +112,6 @@ template <typename T>
 static void dev_free(T*& p) {
     if (p) cudaFree((void*)p);
     p = nullptr;
-}
-
-// Static partition of [0, n) over host threads for the bind-time loops
-// (results do not depend on the thread count).
-static int host_threads(int64_t n) {
-    return n < ((int64_t)1 << 16) ? 1 : (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
-}
-
-template <class F>
-static void parallel_ranges_n(int64_t n, int nt, F&& body) {
-    if (nt <= 1) {
-        body(0, (int64_t)0, n);
-        return;
-    }
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nt; ++t) pool.emplace_back([&, t] { body(t, n * t / nt, n * (t + 1) / nt); });
-    for (auto& th : pool) th.join();
-}
-
-template <class F>
-static void parallel_ranges(int64_t n, F&& body) {
-    parallel_ranges_n(n, host_threads(n), body);
 }
 
 static int ipow_h(int b, int e) {
@@ -290,14 +267,12 @@ int mlb_binding_destroy(mlb_binding* b) {
     return MLB_OK;
 }
 
-static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
-                     mlb_binding** out);
+static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding** out);
 
-int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
-             mlb_binding** out) {
-    // host-side allocation / thread failures must not escape the C ABI
+static int bind_guarded(const mlb_plan* plan, const BindPointsIn& in, mlb_binding** out) {
+    // host-side allocation failures must not escape the C ABI
     try {
-        return bind_impl(plan, pts, n, scale, node_ids, out);
+        return bind_impl(plan, in, out);
     } catch (const std::bad_alloc&) {
         return fail(MLB_ERR_CUDA, "mlb_bind: host allocation failed");
     } catch (const std::exception& e) {
@@ -307,88 +282,97 @@ int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, c
     }
 }
 
-static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
-                     mlb_binding** out) {
-    if (!plan || !out || (n > 0 && !pts)) return fail(MLB_ERR_ARG, "null argument");
+int mlb_bind(const mlb_plan* plan, const double* pts, int64_t n, double scale, const int32_t* node_ids,
+             mlb_binding** out) {
+    if (!plan) return fail(MLB_ERR_ARG, "null argument");
+    BindPointsIn in{};
+    in.points = pts;
+    in.points_on_device = 0;
+    in.n = n;
+    in.ld = plan->g.d;
+    in.scale = scale;
+    in.node_ids = node_ids;
+    return bind_guarded(plan, in, out);
+}
+
+int mlb_bind_ex(const mlb_plan* plan, const mlb_bind_desc* desc, mlb_binding** out) {
+    if (!plan || !desc) return fail(MLB_ERR_ARG, "null argument");
+    const int d = plan->g.d;
+    if (desc->ld < d && !desc->cols) return fail(MLB_ERR_ARG, "row stride smaller than the dimension");
+    if (desc->cols)
+        for (int a = 0; a < d; ++a)
+            if (desc->cols[a] < 0 || desc->cols[a] >= desc->ld) return fail(MLB_ERR_ARG, "column outside the row");
+    if (desc->box_mid && !(desc->box_half > 0.0)) return fail(MLB_ERR_ARG, "box map needs half > 0");
+    BindPointsIn in{};
+    in.points = desc->points;
+    in.points_on_device = desc->points_on_device;
+    in.n = desc->n;
+    in.ld = desc->ld;
+    in.cols = desc->cols;
+    in.scale = desc->scale;
+    in.box_mid = desc->box_mid;
+    in.box_half = desc->box_half;
+    in.box_s = desc->box_s;
+    in.box_hw = desc->box_hw;
+    in.node_ids = desc->node_ids;
+    in.stream = desc->stream;
+    return bind_guarded(plan, in, out);
+}
+
+static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding** out) {
+    if (!plan || !out || (in.n > 0 && !in.points)) return fail(MLB_ERR_ARG, "null argument");
+    const int64_t n = in.n;
     if (n < 0 || n >= (int64_t)1 << 31) return fail(MLB_ERR_ARG, "n out of range");
     const Geom& g = plan->g;
     const int d = g.d, Tb = g.Tb, nbr = g.nbr, TL = g.TL;
     const int nsm = plan->nsm;
-    const int bin_lo = g.ulo + g.m;
-    // 1. cells and fractional offsets, exactly as _make_binding computes
-    //    tx = ng * (x * scale); u = floor(tx) (fastsum.py:343-353, :386)
-    std::vector<int32_t> key((size_t)n);
-    std::vector<double> f((size_t)n * d);
-    std::vector<int32_t> cell_local((size_t)n), cell_glob((size_t)n);
     const int nloc = ipow_h(Tb, d);
     const int nbricks = ipow_h(nbr, d);
-    const int nth = host_threads(n);
-    std::vector<int64_t> first_bad(nth, n);  // per thread: the first point outside the box
-    parallel_ranges(n, [&](int t, int64_t i0, int64_t i1) {
-        for (int64_t i = i0; i < i1; ++i) {
-            int brick = 0, local = 0, tcell = 0, gcell = 0;
-            for (int a = 0; a < d; ++a) {
-                const double xt = pts[i * d + a] * scale;
-                const double tx = (double)g.ng * xt;
-                const double fl = std::floor(tx);
-                const int bin = (int)fl - bin_lo;
-                if (!(bin >= 0 && bin < g.nb)) {
-                    first_bad[t] = i;
-                    return;
-                }
-                f[(size_t)i * d + a] = tx - fl;
-                brick = brick * nbr + bin / Tb;
-                local = local * Tb + bin % Tb;
-                tcell = tcell * TL + bin % Tb;
-                gcell = gcell * g.L + bin;
-            }
-            key[i] = brick * nloc + local;
-            cell_local[i] = tcell;
-            cell_glob[i] = gcell;
+    DeviceGuard guard(plan->device);
+    // 1-2. per point on the device (mlb_bind.cu): box map / box check, cell
+    //      and fractional offsets exactly as _make_binding computes them
+    //      (fastsum.py:343-353, :386), stable radix sort by (brick, cell)
+    //      key, sorted SoA offsets; the host gets the per-key point counts
+    BindPointsOut dev;
+    struct Owned {  // device arrays not yet handed to the binding
+        BindPointsOut* o;
+        ~Owned() {
+            if (o->perm) cudaFree(o->perm);
+            if (o->frac) cudaFree(o->frac);
         }
-    });
-    const int64_t bad = *std::min_element(first_bad.begin(), first_bad.end());
-    if (bad < n) return fail(MLB_ERR_CONFIG, "point " + std::to_string(bad) + " lies outside the plan's admissible box");
-    // 2. stable counting sort by key: per-thread histograms of contiguous
-    //    ranges; thread t's points of key k follow those of threads < t, so the
-    //    permutation equals the serial stable sort
-    const int64_t nkeys = (int64_t)nbricks * nloc;
-    // per-thread histograms cost nth * nkeys counters: the sort uses at most
-    // enough threads that they stay below ~n counters in total (the permutation
-    // does not depend on the thread count)
-    const int nth_sort = (int)std::max<int64_t>(1, std::min<int64_t>(nth, n / std::max<int64_t>(nkeys, 1)));
-    std::vector<std::vector<int64_t>> hist(nth_sort, std::vector<int64_t>(nkeys, 0));
-    parallel_ranges_n(n, nth_sort, [&](int t, int64_t i0, int64_t i1) {
-        for (int64_t i = i0; i < i1; ++i) hist[t][key[i]]++;
-    });
-    std::vector<int64_t> cnt(nkeys + 1, 0);
-    for (int64_t k = 0; k < nkeys; ++k) {
-        int64_t c = cnt[k];
-        for (int t = 0; t < nth_sort; ++t) {
-            const int64_t h = hist[t][k];
-            hist[t][k] = c;  // thread t's first slot for key k
-            c += h;
+    } owned{&dev};
+    if (int rc = bind_points_device(in, g, &dev)) return rc;
+    const int64_t nkeys = dev.nkeys;
+    const std::vector<int64_t>& cnt = dev.cnt;
+    // cell of a key: tile-local (TL^d) and sub-box (L^d) flat indices, the
+    // digits of key = brick * nloc + local (axis 0 most significant)
+    auto key_cells = [&](int64_t k, int32_t* tcell, int32_t* gcell) {
+        int64_t brick = k / nloc, local = k % nloc;
+        int bins[3], locs[3];
+        for (int a = d - 1; a >= 0; --a) {
+            locs[a] = (int)(local % Tb);
+            bins[a] = (int)(brick % nbr) * Tb + locs[a];
+            local /= Tb;
+            brick /= nbr;
         }
-        cnt[k + 1] = c;
-    }
-    std::vector<int32_t> perm((size_t)n);
-    parallel_ranges_n(n, nth_sort, [&](int t, int64_t i0, int64_t i1) {
-        std::vector<int64_t>& pos = hist[t];
-        for (int64_t i = i0; i < i1; ++i) perm[pos[key[i]]++] = (int32_t)i;
-    });
-    std::vector<int32_t> perm_node(perm);
-    if (node_ids)
-        parallel_ranges(n, [&](int, int64_t j0, int64_t j1) {
-            for (int64_t j = j0; j < j1; ++j) perm_node[j] = node_ids[perm[j]];
-        });
+        int32_t t = 0, gc = 0;
+        for (int a = 0; a < d; ++a) {
+            t = t * TL + locs[a];
+            gc = gc * g.L + bins[a];
+        }
+        if (tcell) *tcell = t;
+        if (gcell) *gcell = gc;
+    };
+    auto tcell_of = [&](int64_t k) { int32_t t; key_cells(k, &t, nullptr); return t; };
+    auto gcell_of = [&](int64_t k) { int32_t gc; key_cells(k, nullptr, &gc); return gc; };
     // 3. chunks (<= kChunk points of one cell) and segments (<= maxseg chunks of one brick)
     std::vector<int32_t> chunk_start, chunk_cell, chunk_gcell, chunk_brick;
     for (int64_t k = 0; k < nkeys; ++k) {
         const int64_t lo = cnt[k], hi = cnt[k + 1];
         for (int64_t s = lo; s < hi; s += kChunk) {
             chunk_start.push_back((int32_t)s);
-            chunk_cell.push_back(cell_local[perm[s]]);
-            chunk_gcell.push_back(cell_glob[perm[s]]);
+            chunk_cell.push_back(tcell_of(k));
+            chunk_gcell.push_back(gcell_of(k));
             chunk_brick.push_back((int32_t)(k / nloc));
         }
     }
@@ -416,12 +400,12 @@ static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double 
     }
     if (packed) {
         if (n >= ((int64_t)1 << 29)) return fail(MLB_ERR_CONFIG, "d = 3 bindings hold fewer than 2^29 points");
-        struct Lane { int32_t a, b; int dc; };
+        struct Lane { int32_t a, b; int dc; int64_t k; };
         std::vector<Lane> lanes;
         int lo = 0, hi = 0;  // the pencil's occupied axis-2 range: one staging serves all its groups
         auto emit = [&](const std::vector<Lane>& ls, bool two) {
             // grid index of the first staged cell: any member's cell minus its offset
-            const int32_t gb = cell_glob[perm[ls[0].a]] - (ls[0].dc - lo);
+            const int32_t gb = gcell_of(ls[0].k) - (ls[0].dc - lo);
             ggrp.push_back(gb);
             ggrp.push_back((hi - lo + 1) | (two ? 256 : 0));
             const size_t base = gslot.size();
@@ -444,7 +428,7 @@ static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double 
                     hi = std::max(hi, dc);
                 }
                 for (int64_t s = cnt[kk]; s < cnt[kk + 1]; s += 2)
-                    lanes.push_back({(int32_t)s, s + 1 < cnt[kk + 1] ? (int32_t)(s + 1) : -1, dc});
+                    lanes.push_back({(int32_t)s, s + 1 < cnt[kk + 1] ? (int32_t)(s + 1) : -1, dc, kk});
             }
             for (size_t g0 = 0; g0 < lanes.size(); g0 += 32) {
                 const size_t g1 = std::min(lanes.size(), g0 + 32);
@@ -454,8 +438,8 @@ static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double 
                 if (g1 == lanes.size() && pts <= 32) {  // tail: one point per lane
                     std::vector<Lane> one;
                     for (const Lane& l : ls) {
-                        one.push_back({l.a, -1, l.dc});
-                        if (l.b >= 0) one.push_back({l.b, -1, l.dc});
+                        one.push_back({l.a, -1, l.dc, l.k});
+                        if (l.b >= 0) one.push_back({l.b, -1, l.dc, l.k});
                     }
                     emit(one, false);
                 } else {
@@ -518,7 +502,7 @@ static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double 
             for (int64_t s0 = lo; s0 < hi; s0 += per) {
                 cblk.push_back((int32_t)s0);
                 cblk.push_back((int32_t)std::min<int64_t>(per, hi - s0));
-                cblk.push_back(cell_local[perm[s0]]);
+                cblk.push_back(tcell_of(k));
                 cblk.push_back((int32_t)(k / nloc));
                 brick_blk[k / nloc + 1]++;
             }
@@ -651,14 +635,6 @@ static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double 
                     (int)(cblk.size() / 4), items.size(), ncta_cells, active_brick.size(), merge_pairs.size() / 2, mx);
         }
     }
-    // frac in sorted order, SoA
-    std::vector<double> fs((size_t)n * d);
-    parallel_ranges(n, [&](int, int64_t j0, int64_t j1) {
-        for (int64_t j = j0; j < j1; ++j)
-            for (int a = 0; a < d; ++a) fs[(size_t)a * n + j] = f[(size_t)perm[j] * d + a];
-    });
-
-    DeviceGuard guard(plan->device);
     mlb_binding* b = new mlb_binding();
     b->plan = plan;
     b->n = n;
@@ -682,8 +658,10 @@ static int bind_impl(const mlb_plan* plan, const double* pts, int64_t n, double 
     }
     b->stage_elems = std::max<int64_t>(2 * st, b->grid_cells);  // >= one real grid (separable passes)
     int rc = MLB_OK;
-    if (rc == MLB_OK) rc = dev_upload(&b->perm, perm_node.data(), (size_t)n);
-    if (rc == MLB_OK) rc = dev_upload(&b->frac, fs.data(), (size_t)n * d);
+    b->perm = dev.perm;  // the device binding's arrays move into the binding
+    b->frac = dev.frac;
+    dev.perm = nullptr;
+    dev.frac = nullptr;
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_start, chunk_start.data(), chunk_start.size());
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_cell, chunk_cell.data(), chunk_cell.size());
     if (rc == MLB_OK) rc = dev_upload(&b->chunk_gcell, chunk_gcell.data(), chunk_gcell.size());

@@ -164,6 +164,29 @@ struct mlb_binding {
 };
 
 namespace mlb {
+// device half of the binding (mlb_bind.cu)
+struct BindPointsIn {
+    const double* points;     // n rows of `ld` doubles; columns cols[0..d) (or 0..d) are the coordinates
+    int points_on_device;
+    int64_t n;
+    int ld;
+    const int* cols;          // nullable (host)
+    double scale;             // torus scale
+    const double* box_mid;    // nullable (host, d): affine box map of raw features
+    double box_half, box_s;
+    double box_hw;            // > 0: validate_box on the box coordinates
+    const int32_t* node_ids;  // nullable (host)
+    void* stream;
+};
+struct BindPointsOut {
+    int nkeys = 0;
+    std::vector<int64_t> cnt;  // nkeys + 1: first sorted position of every key
+    int32_t* perm = nullptr;   // device, sorted -> node (owned by the caller afterwards)
+    double* frac = nullptr;    // device, d x n SoA
+    double worst = 0.0;        // max |box coordinate|
+};
+int bind_points_device(const BindPointsIn& in, const Geom& g, BindPointsOut* out);
+
 // kernels launchers (mlb_fastsum.cu)
 int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st);
 int launch_reduce(mlb_binding* b, double* grid, cudaStream_t st, const PeerOut* peers = nullptr);

@@ -115,13 +115,19 @@ class BoxMap:
     s: float
 
     @classmethod
-    def fit(cls, X, eps_b=fastsum.DEFAULT_EPS_B):
+    def fit(cls, X, eps_b=fastsum.DEFAULT_EPS_B, columns=None):
+        """Fit on a feature block, or on `columns` of a wider matrix (column
+        by column on strided views: no copy of the block)."""
         X = np.asarray(X, dtype=float)
         if X.ndim != 2:
             raise ConfigError("expected a 2-d feature block")
-        if not np.isfinite(X).all():
-            raise FormatError("non-finite feature values")
-        lo, hi = X.min(axis=0), X.max(axis=0)
+        cols = range(X.shape[1]) if columns is None else columns
+        lo, hi = np.empty(len(cols)), np.empty(len(cols))
+        for i, c in enumerate(cols):
+            col = X[:, c]
+            if not np.isfinite(col).all():
+                raise FormatError("non-finite feature values")
+            lo[i], hi[i] = col.min(), col.max()
         return cls(mid=0.5 * (lo + hi), half=float((hi - lo).max()) / 2.0, s=fastsum.box_halfwidth(eps_b))
 
     @property
@@ -173,25 +179,41 @@ def _checked_matrix(X, spec):
     return X
 
 
-def _group_weights(X, g, components, params, device, factory):
-    Xg = X[:, list(g.columns)]
+def _group_weights(X, X_dev, g, components, params, device, factory):
     comp = components if g.per_component else None
+    eps_b = params.get("eps_b", fastsum.DEFAULT_EPS_B)
     if g.mode == "none":          # original units, exact sums
-        return factory(Xg, g.kernel, plan=None, components=comp, device=device)
-    Xb, kernel_box = box_points(Xg, g.kernel, g.mode, params.get("eps_b", fastsum.DEFAULT_EPS_B))
-    plan = fastsum.build_plan(kernel_box, d=len(g.columns), **params) if len(g.columns) <= _BOX_LIMIT else None
+        return factory(X[:, list(g.columns)], g.kernel, plan=None, components=comp, device=device)
+    planned = len(g.columns) <= _BOX_LIMIT
+    if planned and factory is KernelWeights:
+        # the box map runs on the device inside the bind, reading the group's
+        # columns straight from the (device copy of the) feature matrix
+        bm = BoxMap.fit(X, eps_b, columns=g.columns)
+        kernel_box = bm.kernel_in_box(g.kernel, g.mode)
+        plan = fastsum.build_plan(kernel_box, d=len(g.columns), **params)
+        return KernelWeights(X if X_dev is None else X_dev, kernel_box, plan=plan, components=comp, device=device,
+                             box_map=bm, columns=g.columns, host_points=X)
+    Xb, kernel_box = box_points(X[:, list(g.columns)], g.kernel, g.mode, eps_b)
+    plan = fastsum.build_plan(kernel_box, d=len(g.columns), **params) if planned else None
     return factory(Xb, kernel_box, plan=plan, components=comp, device=device)
 
 
 def feature_group(X, spec, components=None, fastsum_params=None, device=None, weights_factory=None):
     """One graph layer per column group (datapipe.py:136-170), bound on the GPU.
 
+    The feature matrix goes to the device once; every planned group binds
+    from that copy (box map, box check, cells and sort on the GPU).
     `weights_factory(points, kernel, plan=, components=, device=)` replaces
-    KernelWeights (default) for every group."""
+    KernelWeights for every group (it receives box coordinates)."""
     X = _checked_matrix(X, spec)
     params = dict(fastsum_params or {})
     factory = KernelWeights if weights_factory is None else weights_factory
-    return MultilayerGraph(tuple(build_layer(_group_weights(X, g, components, params, device, factory))
+    X_dev = None
+    if factory is KernelWeights and any(g.mode != "none" and len(g.columns) <= _BOX_LIMIT for g in spec.groups):
+        import torch
+        dev = torch.cuda.current_device() if device is None else int(device)
+        X_dev = torch.from_numpy(np.ascontiguousarray(X)).to(f"cuda:{dev}")
+    return MultilayerGraph(tuple(build_layer(_group_weights(X, X_dev, g, components, params, device, factory))
                                  for g in spec.groups))
 
 

@@ -374,24 +374,55 @@ class PointBinding:
     """Device binding of one point set (replaces PointBinding, fastsum.py:320-330).
 
     Holds the libmlb binding: cell-sorted permutation, fractional offsets,
-    chunk/segment tables and scratch.  `node_ids` places the points inside a
-    longer node vector (component blocks, graphs.py:99-129).
+    chunk/segment tables and scratch, built by mlb_bind_ex with every
+    per-point step on the GPU.  `points`: an (n, >= d) float64 array (host)
+    or CUDA tensor (device-resident points are bound in place); `columns`
+    picks the d coordinate columns of a wider feature matrix; `box_map`
+    (datapipe.BoxMap) maps raw feature columns into the box on the device
+    (feature_group's scaling folded into the bind); `validate` runs
+    validate_box (fastsum.py:66-80) on the device.  `node_ids` places the
+    points inside a longer node vector (component blocks, graphs.py:99-129).
     """
 
-    def __init__(self, plan, points, scale, domain="box", device=None, node_ids=None):
+    def __init__(self, plan, points, scale, domain="box", device=None, node_ids=None, box_map=None,
+                 columns=None, validate=False):
         import torch
         self.plan = plan
         self.device = torch.cuda.current_device() if device is None else int(device)
-        pts = np.ascontiguousarray(points, dtype=float)
-        self.n, self.d = pts.shape
+        if isinstance(points, torch.Tensor):
+            src = points.to(device=f"cuda:{self.device}", dtype=torch.float64).contiguous()
+            on_dev, ptr = 1, src.data_ptr()
+        else:
+            src = np.ascontiguousarray(points, dtype=float)
+            on_dev, ptr = 0, src.ctypes.data
+        if src.ndim != 2:
+            raise ConfigError(f"points must be a 2-d array, got shape {tuple(src.shape)}")
+        self.n = int(src.shape[0])
+        self.d = plan.d
+        cols = None if columns is None else np.ascontiguousarray(columns, dtype=np.int32)
+        if cols is None and src.shape[1] != plan.d:
+            raise ConfigError(f"points have dimension {src.shape[1]}, plan expects {plan.d}")
+        if cols is not None and cols.shape != (plan.d,):
+            raise ConfigError(f"expected {plan.d} coordinate columns, got {len(cols)}")
         self.n_grid = plan.n_grid
         self.grid_size = plan.n_grid ** plan.d
         self._plan_handle = plan.device_plan(self.device, domain)
-        lib = _lib.lib()
         ids = None if node_ids is None else np.ascontiguousarray(node_ids, dtype=np.int32)
+        mid = None if box_map is None else np.ascontiguousarray(np.broadcast_to(box_map.mid, (plan.d,)), dtype=float)
+        desc = _lib.BindDesc(
+            points=ptr if self.n else None, points_on_device=on_dev, n=self.n, ld=int(src.shape[1]),
+            cols=None if cols is None else cols.ctypes.data, scale=float(scale),
+            box_mid=None if mid is None else mid.ctypes.data,
+            box_half=0.0 if box_map is None else float(box_map.half),
+            box_s=0.0 if box_map is None else float(box_map.s),
+            box_hw=box_halfwidth(plan.eps_b) if validate else 0.0,
+            node_ids=None if ids is None else ids.ctypes.data,
+            stream=torch.cuda.current_stream(self.device).cuda_stream)
+        if box_map is not None and box_map.half == 0.0:
+            raise ConfigError("a constant column group maps to the origin; bind its zero points instead")
         out = C.c_void_p()
-        _lib.check(lib.mlb_bind(self._plan_handle.ptr, pts.ctypes.data if self.n else None, self.n,
-                                float(scale), None if ids is None else ids.ctypes.data, C.byref(out)))
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().mlb_bind_ex(self._plan_handle.ptr, C.byref(desc), C.byref(out)))
         self.ptr = out
 
     def stats(self):
@@ -419,10 +450,15 @@ def bind_points(plan, points, sort=None, device=None, node_ids=None):
     `sort` is accepted for compatibility: the device binding always orders
     points by cell.
     """
-    points = validate_box(points, plan.eps_b)
+    import torch
+    if not isinstance(points, torch.Tensor):
+        points = np.asarray(points, dtype=float)
+    if points.ndim != 2:
+        raise ConfigError(f"points must be a 2-d array, got shape {tuple(points.shape)}")
     if points.shape[1] != plan.d:
         raise ConfigError(f"points have dimension {points.shape[1]}, plan expects {plan.d}")
-    return PointBinding(plan, points, plan.ball_scale, "box", device, node_ids)
+    # validate_box (non-finite values, |x|_inf <= 1/4 - eps_b/2) runs on the device inside the bind
+    return PointBinding(plan, points, plan.ball_scale, "box", device, node_ids, validate=True)
 
 
 # ------------------------------------------------------------------ apply --

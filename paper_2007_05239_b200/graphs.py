@@ -55,17 +55,35 @@ class KernelWeights:
     device kernel (direct.py) is used.
     """
 
-    def __init__(self, points, kernel, plan=None, components=None, device=None):
-        points = np.asarray(points, dtype=float)
-        if points.ndim != 2:
-            raise ConfigError(f"points must be a 2-d array, got {points.shape}")
-        if not np.all(np.isfinite(points)):
-            raise ConfigError("points contain non-finite values")
-        self.points = points
+    def __init__(self, points, kernel, plan=None, components=None, device=None, box_map=None, columns=None,
+                 host_points=None):
+        """`points`: (n, d) box coordinates (the reference's argument), or --
+        the feature_group fast path -- a raw feature matrix (host array or
+        CUDA tensor) with `columns` naming the group's columns and `box_map`
+        (datapipe.BoxMap) the map into the box, applied on the device inside
+        the bind; the box coordinates are then materialised on the host only
+        if `.points` is read (from `host_points`, the host copy of a device
+        feature matrix, when given)."""
+        torch = _torch()
         self.kernel = kernel
         self.plan = plan
-        self.n = points.shape[0]
         self.device = _current_device() if device is None else int(device)
+        self._box_map, self._columns = box_map, None if columns is None else tuple(int(c) for c in columns)
+        if box_map is None and columns is None and not _is_tensor(points):
+            points = np.asarray(points, dtype=float)
+            if points.ndim != 2:
+                raise ConfigError(f"points must be a 2-d array, got {points.shape}")
+            if not np.all(np.isfinite(points)):
+                raise ConfigError("points contain non-finite values")
+            self._points = points
+            self._src = None
+        else:
+            if tuple(points.shape).__len__() != 2:
+                raise ConfigError(f"points must be a 2-d array, got {tuple(points.shape)}")
+            self._points = None
+            self._src = points          # raw features (host or device), mapped lazily
+        self.n = int(points.shape[0])
+        d = len(self._columns) if self._columns is not None else int(points.shape[1])
         if components is None:
             self._blocks = [np.arange(self.n)]
         else:
@@ -75,12 +93,43 @@ class KernelWeights:
             self._blocks = [np.flatnonzero(components == c) for c in np.unique(components)]
         self._isd_dev = None
         if plan is not None:
-            if plan.d != points.shape[1]:
-                raise ConfigError(f"plan dimension {plan.d} does not match points ({points.shape[1]})")
-            self._bindings = [fastsum.bind_points(plan, points[idx], device=self.device,
-                                                  node_ids=idx.astype(np.int32)) for idx in self._blocks]
+            if plan.d != d:
+                raise ConfigError(f"plan dimension {plan.d} does not match points ({d})")
+            if self._src is None:
+                self._bindings = [fastsum.bind_points(plan, self._points[idx], device=self.device,
+                                                      node_ids=idx.astype(np.int32)) for idx in self._blocks]
+            else:
+                bm = box_map if (box_map is not None and box_map.half > 0.0) else None
+                self._bindings = []
+                for idx in self._blocks:
+                    if len(self._blocks) == 1:
+                        src = self._src
+                    elif _is_tensor(self._src):
+                        src = self._src[torch.from_numpy(idx).to(self._src.device)]
+                    else:
+                        src = self._src[idx]
+                    if box_map is not None and bm is None:   # constant group: every point at the origin
+                        src = np.zeros((len(idx), d))
+                        cols = None
+                    else:
+                        cols = self._columns
+                    self._bindings.append(fastsum.PointBinding(plan, src, plan.ball_scale, "box", self.device,
+                                                               idx.astype(np.int32), box_map=bm, columns=cols,
+                                                               validate=True))
         else:
             self._bindings = None
+        if host_points is not None:
+            self._src = host_points     # do not keep the device copy alive
+
+    @property
+    def points(self):
+        """(n, d) box coordinates (graphs.py:89-95): the reference attribute."""
+        if self._points is None:
+            src = self._src.cpu().numpy() if _is_tensor(self._src) else np.asarray(self._src, dtype=float)
+            if self._columns is not None:
+                src = src[:, list(self._columns)]
+            self._points = self._box_map(src) if self._box_map is not None else np.ascontiguousarray(src)
+        return self._points
 
     # -- device interface ---------------------------------------------------
     @property

@@ -367,3 +367,35 @@ def test_tiny_and_ragged_sizes_match_oracle(d, m):
         # scale by |v| too: for n = 1 the result is the O(1e-8) NFFT residual of W v = 0
         err = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), np.linalg.norm(v))
         assert err < 1e-11, (n, err)
+
+
+def test_device_bind_paths_agree_and_validate():
+    """mlb_bind_ex: host points, device points and the device box map of raw
+    feature columns (feature_group's scaling folded into the bind) give the
+    same binding -- identical permutation, bitwise identical degrees -- and
+    the device-side validate_box raises the reference's ConfigErrors."""
+    import torch
+    from paper_2007_05239_b200 import (ConfigError, GroupingSpec, GroupSpec, KernelSpec, KernelWeights, bind_points,
+                                       build_layer, build_plan, datapipe, feature_group)
+    from paper_2007_05239_b200.fastsum import PointBinding
+    rng = np.random.default_rng(77)
+    n = 20000
+    X = np.concatenate([rng.normal(0.3, 0.1, (n, 3)), rng.uniform(-5, 7, (n, 2))], axis=1)
+    spec = GroupingSpec((GroupSpec((0, 1, 2), KernelSpec("gaussian", 0.1)), GroupSpec((3, 4), KernelSpec("gaussian", 1.0))))
+    params = dict(N=32, m_nfft=4, p_nfft=8)
+    G = feature_group(X, spec, fastsum_params=params)
+    for g, layer in zip(spec.groups, G.layers):
+        Xb, kb = datapipe.box_points(X[:, list(g.columns)], g.kernel)
+        plan = build_plan(kb, d=len(g.columns), **params)
+        ref = build_layer(KernelWeights(Xb, kb, plan=plan))
+        assert np.array_equal(layer.degrees, ref.degrees)
+        assert np.array_equal(layer.weights._bindings[0].sorted_perm(), ref.weights._bindings[0].sorted_perm())
+        assert np.array_equal(layer.weights.points, Xb)           # lazily materialised box coordinates
+        bd = PointBinding(plan, torch.from_numpy(Xb).cuda(), plan.ball_scale, validate=True)
+        assert np.array_equal(bd.sorted_perm(), ref.weights._bindings[0].sorted_perm())
+    plan = build_plan(KernelSpec("gaussian", 0.1), d=2, N=16, m_nfft=4, p_nfft=8)
+    with pytest.raises(ConfigError, match="points exceed the admissible box"):
+        bind_points(plan, np.array([[0.0, 0.1], [0.3, 0.0]]))
+    with pytest.raises(ConfigError, match="non-finite"):
+        bind_points(plan, np.array([[0.0, np.nan]]))
+    assert bind_points(plan, np.zeros((0, 2))).n == 0

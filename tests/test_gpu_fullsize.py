@@ -77,4 +77,9 @@ def test_config4_full_size_matches_c_oracle():
         for k in range(2):
             err = np.linalg.norm(got[k][t] - L[k]) / np.linalg.norm(L[k])
             assert err <= 1e-8, (t, k, err)
-            print(f"config 4 layer {t} vector {k}: rel err {err:.2e} (degrees {derr:.2e})")
+            # the kernel part alone, D^-1/2 W D^-1/2 v = (1+delta) v - L v (the diagonal term would hide its error)
+            kw, kw_ref = (1.0 + delta) * V[k] - got[k][t], (1.0 + delta) * V[k] - L[k]
+            kerr = np.linalg.norm(kw - kw_ref) / np.linalg.norm(kw_ref)
+            assert kerr <= 1e-8, (t, k, kerr)
+            print(f"config 4 layer {t} vector {k}: L_sym rel err {err:.2e}, D^-1/2 W D^-1/2 v rel err {kerr:.2e} "
+                  f"(degrees {derr:.2e})")
