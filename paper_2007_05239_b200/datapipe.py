@@ -115,19 +115,26 @@ class BoxMap:
     s: float
 
     @classmethod
-    def fit(cls, X, eps_b=fastsum.DEFAULT_EPS_B, columns=None):
-        """Fit on a feature block, or on `columns` of a wider matrix (column
-        by column on strided views: no copy of the block)."""
-        X = np.asarray(X, dtype=float)
-        if X.ndim != 2:
-            raise ConfigError("expected a 2-d feature block")
-        cols = range(X.shape[1]) if columns is None else columns
-        lo, hi = np.empty(len(cols)), np.empty(len(cols))
-        for i, c in enumerate(cols):
-            col = X[:, c]
-            if not np.isfinite(col).all():
+    def fit(cls, X, eps_b=fastsum.DEFAULT_EPS_B, columns=None, X_dev=None):
+        """Fit on a feature block, or on `columns` of a wider matrix.  With
+        `X_dev` (the device copy of X) the column ranges are reduced on the
+        GPU (min / max are exact: the same map as the host reduction)."""
+        if X_dev is not None:
+            import torch
+            cols = range(X_dev.shape[1]) if columns is None else columns
+            sub = X_dev[:, list(cols)]
+            if not bool(torch.isfinite(sub).all()):
                 raise FormatError("non-finite feature values")
-            lo[i], hi[i] = col.min(), col.max()
+            lo_t, hi_t = torch.aminmax(sub, dim=0)
+            lo, hi = lo_t.cpu().numpy(), hi_t.cpu().numpy()
+        else:
+            X = np.asarray(X, dtype=float)
+            if X.ndim != 2:
+                raise ConfigError("expected a 2-d feature block")
+            Xg = X if columns is None else X[:, list(columns)]
+            if not np.isfinite(Xg).all():
+                raise FormatError("non-finite feature values")
+            lo, hi = Xg.min(axis=0), Xg.max(axis=0)
         return cls(mid=0.5 * (lo + hi), half=float((hi - lo).max()) / 2.0, s=fastsum.box_halfwidth(eps_b))
 
     @property
@@ -188,7 +195,7 @@ def _group_weights(X, X_dev, g, components, params, device, factory):
     if planned and factory is KernelWeights:
         # the box map runs on the device inside the bind, reading the group's
         # columns straight from the (device copy of the) feature matrix
-        bm = BoxMap.fit(X, eps_b, columns=g.columns)
+        bm = BoxMap.fit(X, eps_b, columns=g.columns, X_dev=X_dev)
         kernel_box = bm.kernel_in_box(g.kernel, g.mode)
         plan = fastsum.build_plan(kernel_box, d=len(g.columns), **params)
         return KernelWeights(X if X_dev is None else X_dev, kernel_box, plan=plan, components=comp, device=device,

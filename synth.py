@@ -150,11 +150,17 @@ def build_graph(workload, device=None, layer_ids=None):
     """GPU multilayer graph of a workload: one feature_group call per layer so
     each layer keeps its own plan parameters (N differs between layers)."""
     from paper_2007_05239_b200 import GroupingSpec, GroupSpec, KernelSpec, MultilayerGraph, feature_group
+    ids = list(range(len(workload.layers)) if layer_ids is None else layer_ids)
+    params = [dict(N=workload.layers[i].N, m_nfft=workload.layers[i].m, p_nfft=workload.layers[i].p) for i in ids]
+    if all(p == params[0] for p in params):   # one feature_group call: the matrix goes to the device once
+        spec = GroupingSpec(tuple(GroupSpec(workload.layers[i].columns,
+                                            KernelSpec(workload.layers[i].family, workload.layers[i].sigma))
+                                  for i in ids))
+        return feature_group(workload.X, spec, fastsum_params=params[0], device=device)
     layers = []
-    ids = range(len(workload.layers)) if layer_ids is None else layer_ids
-    for i in ids:
+    for i, prm in zip(ids, params):
         ls = workload.layers[i]
         spec = GroupingSpec((GroupSpec(ls.columns, KernelSpec(ls.family, ls.sigma)),))
-        G = feature_group(workload.X, spec, fastsum_params=dict(N=ls.N, m_nfft=ls.m, p_nfft=ls.p), device=device)
+        G = feature_group(workload.X, spec, fastsum_params=prm, device=device)
         layers.append(G.layers[0])
     return MultilayerGraph(tuple(layers))

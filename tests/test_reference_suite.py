@@ -1,0 +1,53 @@
+"""The reference's OWN tests, run against the reference package with the
+INTEGRATION.md shim installed (integration/gpu_weights.py: bind_points,
+fastsum_apply, direct_apply and KernelWeights of `multilap` routed through
+libmlb's C ABI).  The unmodified reference lives in baseline/_ref
+(tools/install_reference.sh: pip install --target, plus a copy of its tests);
+the test skips when that install is absent.
+
+Covered: pkg/tests/test_fastsum.py (fastsum vs direct / dense oracles,
+two-point sum, Laplacian kernel, blocking, expansion degree, degrees,
+bitwise repeated applies, box validation; fastsum.py:153-270 of the tests)
+and pkg/tests/test_graphs.py (KernelWeights vs dense kernel matrix,
+per-component blocks, Laplacian identities; :47-151)."""
+
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+TESTS = os.path.join(REF, "multilap_tests")
+
+
+@pytest.mark.gpu
+def test_reference_tests_pass_through_the_shim():
+    if not os.path.isdir(os.path.join(REF, "multilap")) or not os.path.isdir(TESTS):
+        pytest.skip("reference not installed in baseline/_ref (tools/install_reference.sh)")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, ROOT]))
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "integration.pytest_b200_shim",
+           "-c", os.path.join(ROOT, "integration", "pytest_ref.ini"), "--rootdir", TESTS,
+           os.path.join(TESTS, "test_fastsum.py"), os.path.join(TESTS, "test_graphs.py")]
+    r = subprocess.run(cmd, cwd=TESTS, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    print(out[-3000:])
+    assert r.returncode == 0, out[-4000:]
+    m = re.search(r"libmlb kernel launches during the reference tests: (\d+)", out)
+    assert m and int(m.group(1)) > 0, "the shim did not reach libmlb"
+    assert re.search(r"(\d+) passed", out)
+
+
+def test_shim_declares_the_full_plan_desc():
+    """INTEGRATION.md's reference-side PlanDesc carries all 13 fields of
+    mlb_plan_desc, in header order (no GPU needed)."""
+    sys.path.insert(0, ROOT)
+    from integration.gpu_weights import PlanDesc
+    with open(os.path.join(ROOT, "include", "multilap_b200.h")) as fh:
+        hdr = fh.read()
+    body = hdr[hdr.index("typedef struct mlb_plan_desc {"):hdr.index("} mlb_plan_desc;")]
+    names = re.findall(r"\b(\w+)\s*;", body.replace("int d, N, m, ng;", "int d; int N; int m; int ng;")
+                       .replace("int bin_lo, bin_hi;", "int bin_lo; int bin_hi;"))
+    assert [f[0] for f in PlanDesc._fields_] == names
