@@ -20,6 +20,7 @@ formed once at the end.  Borderline steps (ratio within
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -354,14 +355,6 @@ def _exact_test(V, n, c, c_prev, tol, device):
     return np.sqrt(a2), tol * max(np.sqrt(b2), 1e-300)
 
 
-def _tridiag(alphas, betas, s):
-    T = np.diag(alphas[:s])
-    if s > 1:
-        off = betas[: s - 1]
-        T += np.diag(off, 1) + np.diag(off, -1)
-    return T
-
-
 class _Chain:
     """Device side of one Lanczos chain: step j = matvec of V[j], CGS2 against
     V[:j+1] (alpha_j = first-pass coefficient, ||w||^2 into AB), and
@@ -475,8 +468,7 @@ def _lanczos_fn_apply_dev(apply_dev, n, v, fn, krylov_dim=50, tol=1e-8, out=None
         beta = float(np.sqrt(max(snap[dim + s], 0.0)))
         betas[s] = beta
         s += 1
-        lam, Q = np.linalg.eigh(_tridiag(alphas, betas, s))
-        c = nv * (Q @ (fn(lam) * Q[0, :]))
+        c = _coeffs(alphas[None, :], betas[None, :], s, np.array([nv]), fn)[0]
         stop = False
         if c_prev is not None:
             stop = _converged(c, c_prev, tol, lambda: _exact_test(V, n, c, c_prev, tol, v.device))
@@ -540,14 +532,84 @@ def pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1e
         _VPOOL_DEPTH[0] -= 1
 
 
+def _coeffs(alphas, betas, s, nv, fn):
+    """c = ||v|| Q f(Lambda) Q[0, :] for a stack of tridiagonal T_s (rows of
+    alphas / betas: one Lanczos chain each) -- krylov.py:200-206 -- with one
+    batched eigh and one batched product (the stack's entries are independent:
+    a one-chain stack gives the bitwise same c)."""
+    Ta = alphas.shape[0]
+    T = np.zeros((Ta, s, s))
+    ix = np.arange(s)
+    T[:, ix, ix] = alphas[:, :s]
+    if s > 1:
+        T[:, ix[:-1], ix[1:]] = betas[:, : s - 1]
+        T[:, ix[1:], ix[:-1]] = betas[:, : s - 1]
+    lam, Q = np.linalg.eigh(T)
+    fl = np.stack([fn(lam[t]) for t in range(Ta)]) if Ta > 1 else fn(lam[0])[None, :]
+    return nv[:, None] * np.matmul(Q, (fl * Q[:, 0, :])[:, :, None])[:, :, 0]
+
+
+_LOCK_POOL = {}
+_LOCK_GRAPHS = {}
+
+
+def _graphs_enabled():
+    return os.environ.get("MLB_PKSM_GRAPHS", "1") != "0"
+
+
+def _lock_buffers(dev, T, dim, n):
+    """Per (device, nesting level, T, dim, n): the lockstep solve's device
+    buffers at FIXED addresses (AB rows, w, h, reduction scratch per layer;
+    the bases come from _krylov_basis), so captured step graphs replay on any
+    later solve of the same shape."""
+    torch = _torch()
+    key = (dev.index, _VPOOL_DEPTH[0], T, dim, n)
+    P = _LOCK_POOL.get(key)
+    if P is None:
+        need = max(int(_lib.lib().mlb_krylov_work_size(n, dim + 2)), 1 << 16)
+        P = dict(AB=torch.zeros((T, 2 * dim + 1), dtype=torch.float64, device=dev),
+                 w=torch.empty((T, n), dtype=torch.float64, device=dev),
+                 h=torch.empty((T, dim + 1), dtype=torch.float64, device=dev),
+                 work=torch.empty((T, need), dtype=torch.float64, device=dev),
+                 ABh=torch.empty((dim, T, 2 * dim + 1), dtype=torch.float64, pin_memory=True),
+                 streams=[torch.cuda.Stream(device=dev) for _ in range(min(T, 8))])
+        _LOCK_POOL[key] = P
+    return P
+
+
+def _issue_layer_step(x, t, j, P, dim, n, sp):
+    """Step j of layer t's chain on stream `sp`: matvec of V[j] (fused
+    Laplacian, sorted order), CGS2 against V[:j+1] (alpha_j and ||w||^2 into
+    its AB row), V[j+1] = w / ||w|| on the device."""
+    lib = _lib.lib()
+    v0 = x.V.data_ptr()
+    row = lambda k: C.c_void_p(v0 + 8 * n * k)  # noqa: E731
+    w = C.c_void_p(P["w"][t].data_ptr())
+    ab0 = P["AB"][t].data_ptr()
+    nrm = C.c_void_p(ab0 + 8 * (dim + j))
+    _lib.check(lib.mlb_apply(x.b.ptr, row(j), w, x.a, -1.0, x.K0, _lib.MLB_USE_ISD | _lib.MLB_SORTED, sp))
+    _lib.check(lib.mlb_cgs2(C.c_void_p(v0), n, n, j + 1, w, C.c_void_p(P["h"][t].data_ptr()), C.c_void_p(ab0),
+                            nrm, C.c_void_p(P["work"][t].data_ptr()), sp))
+    if j + 1 < dim:
+        _lib.check(lib.mlb_scale_by(w, row(j + 1), n, nrm, -0.5, sp))
+
+
 def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1e-8):
     """out += out_scale * (L_t + delta)^p v for every layer t, summed into out in
-    ascending layer order.  The layers' Krylov steps advance in lockstep so
-    each step costs ONE device->host snapshot for all layers (alpha, beta),
-    read up to MLB_PKSM_DEPTH steps behind the device; per layer the
-    arithmetic and its order are those of pksm_layer_dev, so the result is
-    bitwise identical to the sequential loop.  Layers must be single-binding
-    fused kernel layers."""
+    ascending layer order.  The layers' Krylov steps advance in lockstep:
+
+    * device: step j of ALL layers is one replay of a CUDA graph captured
+      once per (layer set, j) and cached across solves -- the layers' chains
+      on up to 8 forked streams inside the graph, then one D2H snapshot of
+      every layer's (alpha_j, ||w_j||^2) -- so a step costs one graph launch
+      instead of ~3 C-ABI calls per layer; layers that already stopped keep
+      iterating inside the graph (their results were taken at their stop);
+    * host: up to MLB_PKSM_DEPTH steps behind the device, one batched eigh
+      of every running layer's T_s and the coefficient-space stopping test
+      (krylov.py:200-216; exact re-test near the threshold).
+    Per layer the arithmetic and its order are those of a one-layer solve, so
+    results do not depend on the layer set.  Layers must be single-binding
+    fused kernel layers.  MLB_PKSM_GRAPHS=0 issues the steps eagerly."""
     torch = _torch()
     fn = power_fn(p)
     n = v_node.numel()
@@ -557,68 +619,114 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
     T = len(layers)
     dev = v_node.device
     st = [_LayerPksm(layer, v_node, dim, None) for layer in layers]
-    # per layer AB row: h1 row (alpha_j at j) | ||w_j||^2 | <v, v>; V[0] on
-    # the device, <v, v> read with step 0 (no start-of-solve sync)
-    AB = torch.zeros((T, 2 * dim + 1), dtype=torch.float64, device=dev)
-    ABh = _pinned_snapshots((dim, T, 2 * dim + 1), dev)
+    P = _lock_buffers(dev, T, dim, n)
+    AB, ABh = P["AB"], P["ABh"]
+    AB.zero_()
     stream = torch.cuda.current_stream(dev)
     for t, x in enumerate(st):
         vv = AB[t, 2 * dim:2 * dim + 1]
         dot(x.vs, x.vs, vv)
         x.V = _krylov_basis(dev, t, dim, n)
         scale_by(x.vs, x.V[0], vv, -0.5)
-        x.chain = _Chain(x.V, AB[t], stream, fused=(x.b.ptr, x.a, -1.0, x.K0,
-                                                     _lib.MLB_USE_ISD | _lib.MLB_SORTED))
+    use_graphs = _graphs_enabled()
+    gkey = (dev.index, _VPOOL_DEPTH[0], dim, n, tuple(int(x.b.ptr.value) for x in st),
+            tuple((x.a, x.K0) for x in st), tuple(x.V.data_ptr() for x in st), AB.data_ptr())
+    graphs = None
+    if use_graphs:
+        graphs = _LOCK_GRAPHS.get(gkey)
+        if graphs is None:
+            graphs = _LOCK_GRAPHS[gkey] = {}
+            # the graphs bake in the bindings' device pointers: drop them when a binding dies
+            for x in st:
+                weakref.finalize(x.b, _LOCK_GRAPHS.pop, gkey, None)
     events = [None] * dim
+    lib = _lib.lib()
 
-    def issue(j):  # step j of every layer still running at the host's last decision
-        for x in st:
-            if not x.done:
-                x.chain.issue(j)
-        ABh[j].copy_(AB, non_blocking=True)
+    def issue(j):
+        if not use_graphs:
+            for t, x in enumerate(st):
+                if not x.done:
+                    _issue_layer_step(x, t, j, P, dim, n, C.c_void_p(stream.cuda_stream))
+            ABh[j].copy_(AB, non_blocking=True)
+        else:
+            if j not in graphs:
+                if j == 0:  # kernel attributes / first-use setup outside any capture
+                    torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                cap = torch.cuda.Stream(device=dev)
+                l0 = lib.mlb_launch_count()
+                with torch.cuda.graph(g, stream=cap):
+                    fork = torch.cuda.Event()
+                    fork.record(cap)
+                    ss = P["streams"]
+                    for s_ in ss:
+                        s_.wait_event(fork)
+                    for t, x in enumerate(st):
+                        s_ = ss[t % len(ss)]
+                        _issue_layer_step(x, t, j, P, dim, n, C.c_void_p(s_.cuda_stream))
+                    for s_ in ss:
+                        e = torch.cuda.Event()
+                        e.record(s_)
+                        cap.wait_event(e)
+                    ABh[j].copy_(AB, non_blocking=True)
+                graphs[j] = (g, int(lib.mlb_launch_count() - l0))
+            g, cnt = graphs[j]
+            g.replay()
+            lib.mlb_note_launches(cnt)
         events[j] = torch.cuda.Event()
         events[j].record(stream)
 
+    if use_graphs and 0 not in graphs:
+        # first solve of this layer set: step 0 eagerly once (sets kernel
+        # attributes outside capture), then graphs from step 0 on
+        for t, x in enumerate(st):
+            _issue_layer_step(x, t, 0, P, dim, n, C.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize(dev)   # (re-running step 0 from the graph recomputes the same values)
     depth = _run_ahead()
     issued = 0
     while issued < min(depth, dim):
         issue(issued)
         issued += 1
+    alphas = np.zeros((T, dim))
+    betas = np.zeros((T, dim))
+    nv = np.full(T, np.nan)
+    c_prev = [None] * T
     s = 0
     while any(not x.done for x in st):
         events[s].synchronize()
         snap = ABh[s].numpy()
         ss = s + 1
         for t, x in enumerate(st):
-            if x.done:
+            if x.done or x.nv is not None:
                 continue
-            if x.nv is None:
-                x.nv = float(np.sqrt(snap[t, 2 * dim]))
-                if x.nv == 0.0:  # zero input: nothing to add (queued steps are discarded)
-                    x.done = True
-                    x.ys = None
-                    continue
-            x.alphas[s] = snap[t, s]
-            beta = float(np.sqrt(max(snap[t, dim + s], 0.0)))
-            x.betas[s] = beta
-            lam, Q = np.linalg.eigh(_tridiag(x.alphas, x.betas, ss))
-            c = x.nv * (Q @ (fn(lam) * Q[0, :]))
+            x.nv = float(np.sqrt(snap[t, 2 * dim]))
+            nv[t] = x.nv
+            if x.nv == 0.0:  # zero input: nothing to add (queued steps are discarded)
+                x.done = True
+                x.ys = None
+        act = [t for t, x in enumerate(st) if not x.done]
+        if not act:
+            break
+        alphas[act, s] = snap[act, s]
+        betas[act, s] = np.sqrt(np.maximum(snap[act, dim + s], 0.0))
+        cs = _coeffs(alphas[act], betas[act], ss, nv[act], fn)
+        for c, t in zip(cs, act):
+            x = st[t]
             stop = False
-            if x.c_prev is not None:
-                stop = _converged(c, x.c_prev, tol, lambda: _exact_test(x.V, n, c, x.c_prev, tol, dev))
-            happy = beta <= 1e-13 * max(1.0, np.abs(x.alphas[:ss]).max())
+            if c_prev[t] is not None:
+                stop = _converged(c, c_prev[t], tol, lambda: _exact_test(x.V, n, c, c_prev[t], tol, dev))
+            happy = betas[t, s] <= 1e-13 * max(1.0, np.abs(alphas[t, :ss]).max())
             if stop or happy or ss >= dim:
                 PksmStats.steps.append(ss)
                 x.ys = torch.empty(n, dtype=torch.float64, device=dev)
                 gemv_n(x.V, n, ss, _to_dev(c, dev.index), x.ys)
                 x.done = True
             else:
-                x.c_prev = c
+                c_prev[t] = c
         s += 1
         if issued < dim and any(not x.done for x in st):
             issue(issued)
             issued += 1
-    lib = _lib.lib()
     for x in st:  # ascending layer order, exactly as the sequential loop
         x.V = None
         if x.ys is None:

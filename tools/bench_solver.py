@@ -54,12 +54,30 @@ def main():
     pred = predict_labels(res.scores).cpu().numpy()
     t_ac = time.perf_counter() - t0
     acc = float(np.mean(pred == wl.truth))
+    # the raw batched matvec rate of the same layers (every layer's shifted
+    # L_sym of one vector per step, LaplacianBatch), for the in-solver ratio
+    from paper_2007_05239_b200 import LaplacianBatch, MultilayerGraph, with_shift
+    batch = LaplacianBatch(MultilayerGraph(tuple(with_shift(l, math.log(2.0)) for l in G.layers)))
+    vv = torch.from_numpy(np.random.default_rng(3).standard_normal(wl.n)).cuda()
+    for _ in range(3):
+        batch.apply_dev(vv)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record()
+    for _ in range(reps):
+        batch.apply_dev(vv)
+    e1.record()
+    e1.synchronize()
+    raw_rate = wl.n * len(G.layers) * reps / (e0.elapsed_time(e1) * 1e-3)
     out = {
         "workload": wl.name, "n": wl.n, "layers": len(G.layers), "k": k,
         "t_build_s": t_build, "t_eig_s": t_eig, "t_ac_s": t_ac,
         "outer_matvecs": stats.get("matvecs"), "restarts": stats.get("restarts"),
         "pksm_calls": len(PksmStats.steps), "layer_matvecs": int(sum(PksmStats.steps)),
         "node_layers_per_s_in_solver": wl.n * sum(PksmStats.steps) / t_eig if t_eig > 0 else None,
+        "raw_batched_node_layers_per_s": raw_rate,
+        "in_solver_over_raw": (wl.n * sum(PksmStats.steps) / t_eig) / raw_rate if t_eig > 0 else None,
         "ac_iterations": res.iterations, "ac_converged": res.converged, "accuracy": acc,
         "values": [float(x) for x in basis.values], "libmlb_launches": int(_lib.lib().mlb_launch_count() - l0),
     }
