@@ -234,6 +234,14 @@ int mlb_hadamard(const double* x, const double* y, double* z, int64_t n, void* s
 int mlb_direct(const double* X, int64_t n, int d, int family, double sigma, const double* v, const double* s,
                double* y, double alpha, double beta, double gamma, int accumulate, void* stream);
 
+/* Exact sums at nt targets Xt (nt x d, device): yt[t] = sum_j K(|Xt_t - X_j|) v_j
+ * over ALL n sources (a target that is also a source includes its K(0) v
+ * term); the accuracy check of run_fastsum_bench (runner.py:496-512).  work:
+ * mlb_direct_targets_work_size(nt) doubles. */
+int64_t mlb_direct_targets_work_size(int64_t nt);
+int mlb_direct_targets(const double* X, int64_t n, int d, int family, double sigma, const double* v, const double* Xt,
+                       int64_t nt, double* yt, double* work, void* stream);
+
 /* ---- Allen-Cahn (allencahn.py:172-223) ----------------------------------
  * Phi: n x k row-major, U/F: n x m row-major, fid: n.  One iteration:
  *   R = (1+c dt) U - dt/(2 eps) T(U) - dt fid (U-F);  Vc = Phi^T R / denom;

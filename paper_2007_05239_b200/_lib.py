@@ -83,6 +83,8 @@ SIGNATURES = {
     "mlb_scale_by": (I, [P, P, I64, P, D, P]),
     "mlb_hadamard": (I, [P, P, P, I64, P]),
     "mlb_direct": (I, [P, I64, I, I, D, P, P, P, D, D, D, I, P]),
+    "mlb_direct_targets_work_size": (I64, [I64]),
+    "mlb_direct_targets": (I, [P, I64, I, I, D, P, P, I64, P, P, P]),
     "mlb_ac_work_size": (I64, [I64, I, I]),
     "mlb_ac_step": (I, [P, I64, I, I, P, P, P, P, D, D, D, P, P, P, P]),
     "mlb_argmax_rows": (I, [P, I64, I, P, P]),

@@ -888,11 +888,80 @@ __global__ void direct_kernel(const double* __restrict__ X, int64_t n, int d, in
     }
 }
 
+// exact sums at a target subset (the accuracy check of run_fastsum_bench,
+// runner.py:496-512, on a 2,000-target sample of up to 10^7 sources): block
+// (bx, sy) sums sources [sy*chunk, (sy+1)*chunk) for targets bx*128.. into
+// partial[sy * nt + t]; direct_targets_finish sums the slices in slice order
+__global__ void direct_targets_kernel(const double* __restrict__ X, int64_t n, int d, int family, double inv_sigma,
+                                      const double* __restrict__ v, const double* __restrict__ Xt, int64_t nt,
+                                      int64_t chunk, double* __restrict__ partial) {
+    extern __shared__ double tile[];  // 128 x (d + 1)
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = t < nt;
+    double xt[16];
+    const int dd = d < 16 ? d : 16;
+    for (int a = 0; a < dd; ++a) xt[a] = live ? Xt[t * d + a] : 0.0;
+    const int64_t s0 = blockIdx.y * chunk, s1 = min(n, s0 + chunk);
+    double acc = 0.0;
+    for (int64_t j0 = s0; j0 < s1; j0 += 128) {
+        const int cnt = (int)min((int64_t)128, s1 - j0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+            for (int a = 0; a < d; ++a) tile[e * (d + 1) + a] = X[(j0 + e) * d + a];
+            tile[e * (d + 1) + d] = v[j0 + e];
+        }
+        __syncthreads();
+        if (live)
+            for (int e = 0; e < cnt; ++e) {
+                double r2 = 0.0;
+                for (int a = 0; a < d; ++a) {
+                    const double xa = (a < 16) ? xt[a] : Xt[t * d + a];
+                    const double df = (xa - tile[e * (d + 1) + a]) * inv_sigma;
+                    r2 = fma(df, df, r2);
+                }
+                acc = fma((family == 0) ? exp(-r2) : exp(-sqrt(r2)), tile[e * (d + 1) + d], acc);
+            }
+    }
+    if (live) partial[(int64_t)blockIdx.y * nt + t] = acc;
+}
+
+__global__ void direct_targets_finish(const double* __restrict__ partial, int slices, int64_t nt,
+                                      double* __restrict__ yt) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    double acc = 0.0;
+    for (int sl = 0; sl < slices; ++sl) acc += partial[(int64_t)sl * nt + t];
+    yt[t] = acc;
+}
+
 }  // namespace mlb
 
 using namespace mlb;
 
 extern "C" {
+
+int64_t mlb_direct_targets_work_size(int64_t nt) { return 1024 * nt; }
+
+int mlb_direct_targets(const double* X, int64_t n, int d, int family, double sigma, const double* v, const double* Xt,
+                       int64_t nt, double* yt, double* work, void* stream) {
+    if (nt <= 0) return MLB_OK;
+    if (d < 1 || d > 4096) return fail(MLB_ERR_CONFIG, "direct kernel needs 1 <= d <= 4096");
+    const size_t smem = (size_t)128 * (d + 1) * sizeof(double);
+    if (smem > 200 * 1024) return fail(MLB_ERR_CONFIG, "direct kernel: d too large for the smem tile");
+    if (int rc = ensure_max_smem((const void*)direct_targets_kernel, smem)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t tx = (nt + 127) / 128;
+    // enough source slices to fill the GPU several times over (<= 1024 slices)
+    int64_t slices = std::max<int64_t>(1, std::min<int64_t>(1024, (int64_t)device_sms() * 8 / std::max<int64_t>(tx, 1)));
+    slices = std::min<int64_t>(slices, std::max<int64_t>(1, (n + 127) / 128));
+    const int64_t chunk = (n + slices - 1) / slices;
+    direct_targets_kernel<<<dim3((unsigned)tx, (unsigned)slices), 128, smem, st>>>(X, n, d, family, 1.0 / sigma, v, Xt,
+                                                                                    nt, chunk, work);
+    direct_targets_finish<<<(unsigned)tx, 128, 0, st>>>(work, (int)slices, nt, yt);
+    note_launches(2);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
 
 int64_t mlb_ac_work_size(int64_t n, int k, int m) {
     (void)n;  // (m = 1: the binary scheme's 2k partials + maxima fit as well)

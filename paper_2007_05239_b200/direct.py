@@ -70,3 +70,28 @@ def direct_apply_dev(weights, v, y, alpha, beta, gamma, s=None, accumulate=False
         direct_sum_dev(Xb, vb, weights.kernel, yb, alpha, beta, gamma, sb, accumulate)
         y.index_copy_(0, ib, yb)
     return y
+
+
+def direct_at_targets(points, v, kernel, targets):
+    """Exact (W v)[t] for the target rows `targets` (zero diagonal), one
+    device pass over all sources per target tile (mlb_direct_targets): the
+    reference's accuracy check of fastsum against direct_apply
+    (runner.py:496-512) on a target sample when n is too large for O(n^2)."""
+    torch = _torch()
+    x = np.ascontiguousarray(points, dtype=float)
+    v = np.ascontiguousarray(v, dtype=float)
+    tg = np.asarray(targets, dtype=np.int64)
+    if x.ndim != 2 or v.shape != (x.shape[0],):
+        raise ConfigError("points / v shapes do not match")
+    dev = torch.cuda.current_device()
+    Xd = torch.from_numpy(x).to(f"cuda:{dev}")
+    vd = torch.from_numpy(v).to(f"cuda:{dev}")
+    Xt = torch.from_numpy(np.ascontiguousarray(x[tg])).to(f"cuda:{dev}")
+    yt = torch.empty(len(tg), dtype=torch.float64, device=f"cuda:{dev}")
+    lib = _lib.lib()
+    work = torch.empty(max(int(lib.mlb_direct_targets_work_size(len(tg))), 1), dtype=torch.float64,
+                       device=f"cuda:{dev}")
+    _lib.check(lib.mlb_direct_targets(_lib.ptr(Xd), x.shape[0], x.shape[1], _family(kernel), float(kernel.sigma),
+                                      _lib.ptr(vd), _lib.ptr(Xt), len(tg), _lib.ptr(yt), _lib.ptr(work),
+                                      _lib.stream_ptr()))
+    return yt.cpu().numpy() - kernel.value_at_zero() * v[tg]
