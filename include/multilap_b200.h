@@ -211,6 +211,17 @@ int mlb_gemv_t(const double* V, int64_t ld, int64_t n, int cols, const double* w
  * nrm2_out = ||w||^2 after (device, 1, nullable) */
 int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out,
              double* h1_out, double* nrm2_out, double* work, void* stream);
+/* CGS2 of T Lanczos chains in one launch per phase (the lockstep PKSM of many
+ * layers): chain t has basis V[t] (same ld, n, cols for all), w[t] is
+ * orthogonalised in place; h_out[t] = h1 + h2, h1_out[t] = first-pass
+ * projections, nrm2_out[t][0] = ||w||^2 after; with vnext (nullable) also
+ * V[t] column `cols` = w / sqrt(||w||^2).  Pointer arrays are DEVICE arrays of
+ * T device pointers; cols <= 64.  Per chain bitwise the same as mlb_cgs2 +
+ * mlb_scale_by.  work: mlb_cgs2_batched_work_size(T) doubles. */
+int64_t mlb_cgs2_batched_work_size(int T);
+int mlb_cgs2_batched(int T, const double* const* V, int64_t ld, int64_t n, int cols, double* const* w,
+                     double* const* h_out, double* const* h1_out, double* const* nrm2_out, double* const* vnext,
+                     double* work, void* stream);
 /* y = V[:, :cols] c  (c device) ; out may alias nothing */
 int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c, double* y,
                double scale, int accumulate, void* stream);

@@ -177,8 +177,8 @@ __device__ __forceinline__ void ld4(const double* p, bool ok, double* v) {
 }
 
 // part[j * nb + b] = sum over block b's rows of V[j][i] w[i]
-__global__ void __launch_bounds__(256) cgs_dot_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
-                                                      const double* __restrict__ w, double* __restrict__ part) {
+__device__ __forceinline__ void cgs_dot_block(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                                              const double* __restrict__ w, double* __restrict__ part) {
     __shared__ double acc[8][64];  // per warp, per column (tiles accumulate in order)
     const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t per = ((n + nb - 1) / nb + 3) & ~(int64_t)3;
@@ -231,13 +231,38 @@ __global__ void __launch_bounds__(256) cgs_dot_kernel(const double* __restrict__
     }
 }
 
+__global__ void __launch_bounds__(256) cgs_dot_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                                                      const double* __restrict__ w, double* __restrict__ part) {
+    cgs_dot_block(V, ld, n, cols, w, part);
+}
+
+// The lockstep PKSM's CGS2 of T chains in ONE launch per phase: chain t =
+// blockIdx.y, its pointers from device arrays (every chain has the same n and
+// column count; the row partition and every sum order are those of the
+// single-chain kernels, so each chain's result is bitwise the same).
+struct CgsBatch {
+    const double* const* V;
+    double* const* w;
+    double* const* h_out;    // h1 + h2 (nullable entries not allowed: give scratch)
+    double* const* h1_out;   // first-pass projections (alpha at cols - 1)
+    double* const* nrm2;     // ||w||^2 after
+    double* const* vnext;    // nullable array: V[t] column `cols` = w / sqrt(nrm2)
+    double* work;            // T x per-chain scratch
+    int64_t work_stride;
+};
+
+__global__ void __launch_bounds__(256) cgs_dot_batched(CgsBatch B, int64_t ld, int64_t n, int cols) {
+    const int t = blockIdx.y;
+    cgs_dot_block(B.V[t], ld, n, cols, B.w[t], B.work + t * B.work_stride);
+}
+
 // h[j] = sum_b part_in[j * nb + b] (warp per column, same in every block);
 // w -= V h on the block's rows; npart[b] = the block's partial of ||w||^2.
 // Block 0 stores h into h_save and h_prev + h into h_sum.
-__global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
-                                                         const double* __restrict__ part_in, double* __restrict__ w,
-                                                         double* __restrict__ npart, double* __restrict__ h_save,
-                                                         const double* __restrict__ h_prev, double* __restrict__ h_sum) {
+__device__ __forceinline__ void cgs_update_block(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                                                 const double* __restrict__ part_in, double* __restrict__ w,
+                                                 double* __restrict__ npart, double* __restrict__ h_save,
+                                                 const double* __restrict__ h_prev, double* __restrict__ h_sum) {
     __shared__ double h[64];
     __shared__ double sh[8];
     const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -294,6 +319,40 @@ __global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restric
             npart[blockIdx.x] = t;
         }
     }
+}
+
+__global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
+                                                         const double* __restrict__ part_in, double* __restrict__ w,
+                                                         double* __restrict__ npart, double* __restrict__ h_save,
+                                                         const double* __restrict__ h_prev, double* __restrict__ h_sum) {
+    cgs_update_block(V, ld, n, cols, part_in, w, npart, h_save, h_prev, h_sum);
+}
+
+// pass = 0: w -= V h1, h1 -> h1_out[t];  pass = 1: w -= V h2, h_out = h1 + h2, ||w||^2 partials
+__global__ void __launch_bounds__(256) cgs_update_batched(CgsBatch B, int64_t ld, int64_t n, int cols, int pass) {
+    const int t = blockIdx.y;
+    double* wk = B.work + t * B.work_stride;
+    double* npart = wk + (int64_t)kFusedBlocks * 64;
+    if (pass == 0)
+        cgs_update_block(B.V[t], ld, n, cols, wk, B.w[t], nullptr, B.h1_out[t], nullptr, nullptr);
+    else
+        cgs_update_block(B.V[t], ld, n, cols, wk, B.w[t], npart, nullptr, B.h1_out[t], B.h_out[t]);
+}
+
+// ||w||^2 of every chain (fixed-order sum of its block partials), then
+// V[cols] = w / sqrt(||w||^2): grid (blocks, T)
+__global__ void cgs_norm_scale_batched(CgsBatch B, int64_t ld, int64_t n, int cols, int nb) {
+    const int t = blockIdx.y;
+    const double* npart = B.work + t * B.work_stride + (int64_t)kFusedBlocks * 64;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += npart[b];   // the order of finish_partial
+    if (blockIdx.x == 0 && threadIdx.x == 0) B.nrm2[t][0] = s;
+    if (!B.vnext) return;
+    const double f = 1.0 / sqrt(s);               // scale_by_kernel's factor
+    const double* w = B.w[t];
+    double* y = B.vnext[t] + (int64_t)cols * ld;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = w[i] * f;
 }
 
 static int cgs2_fused(const double* V, int64_t ld, int64_t n, int cols, double* w, double* h_out, double* h1_out,
@@ -392,6 +451,27 @@ int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double
         note_launches(1);
     }
     if (h1_out) MLB_CUDA_TRY(cudaMemcpyAsync(h1_out, h1, cols * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int64_t mlb_cgs2_batched_work_size(int T) { return (int64_t)T * ((int64_t)kFusedBlocks * (64 + 1) + 64); }
+
+int mlb_cgs2_batched(int T, const double* const* V, int64_t ld, int64_t n, int cols, double* const* w,
+                     double* const* h_out, double* const* h1_out, double* const* nrm2_out, double* const* vnext,
+                     double* work, void* stream) {
+    if (T <= 0 || cols <= 0 || n <= 0) return MLB_OK;
+    if (cols > 64 || (ld & 1)) return fail(MLB_ERR_ARG, "batched CGS2 needs cols <= 64 and an even leading dimension");
+    if (!V || !w || !h_out || !h1_out || !nrm2_out || !work) return fail(MLB_ERR_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = std::max(1, std::min(std::min(kFusedBlocks, 2 * device_sms()), (int)((n + kTileRows - 1) / kTileRows)));
+    CgsBatch B{V, w, h_out, h1_out, nrm2_out, vnext, work, (int64_t)kFusedBlocks * (64 + 1) + 64};
+    cgs_dot_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols);
+    cgs_update_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols, 0);
+    cgs_dot_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols);
+    cgs_update_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols, 1);
+    cgs_norm_scale_batched<<<dim3(ew_grid(n) / std::max(1, T / 8) + 1, T), 256, 0, st>>>(B, ld, n, cols, nb);
+    note_launches(5);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }

@@ -566,15 +566,45 @@ def _lock_buffers(dev, T, dim, n):
     key = (dev.index, _VPOOL_DEPTH[0], T, dim, n)
     P = _LOCK_POOL.get(key)
     if P is None:
-        need = max(int(_lib.lib().mlb_krylov_work_size(n, dim + 2)), 1 << 16)
+        lib = _lib.lib()
+        need = max(int(lib.mlb_krylov_work_size(n, dim + 2)), 1 << 16)
         P = dict(AB=torch.zeros((T, 2 * dim + 1), dtype=torch.float64, device=dev),
                  w=torch.empty((T, n), dtype=torch.float64, device=dev),
                  h=torch.empty((T, dim + 1), dtype=torch.float64, device=dev),
                  work=torch.empty((T, need), dtype=torch.float64, device=dev),
+                 bwork=torch.empty(int(lib.mlb_cgs2_batched_work_size(T)), dtype=torch.float64, device=dev),
                  ABh=torch.empty((dim, T, 2 * dim + 1), dtype=torch.float64, pin_memory=True),
                  streams=[torch.cuda.Stream(device=dev) for _ in range(min(T, 8))])
+        # device pointer arrays of the batched CGS2 (fixed per pool; nrm2 per step j)
+        ab0 = P["AB"].data_ptr()
+        rows = [ab0 + 8 * (2 * dim + 1) * t for t in range(T)]
+        P["p_w"] = torch.tensor([P["w"][t].data_ptr() for t in range(T)], dtype=torch.int64, device=dev)
+        P["p_h"] = torch.tensor([P["h"][t].data_ptr() for t in range(T)], dtype=torch.int64, device=dev)
+        P["p_h1"] = torch.tensor(rows, dtype=torch.int64, device=dev)
+        P["p_nrm"] = torch.tensor([[r + 8 * (dim + j) for r in rows] for j in range(dim)], dtype=torch.int64,
+                                  device=dev)
         _LOCK_POOL[key] = P
     return P
+
+
+def _batched_cgs_ok(dim, n):
+    return dim <= 64 and n % 2 == 0 and os.environ.get("MLB_PKSM_BATCHED_CGS", "1") != "0"
+
+
+def _issue_matvec(x, t, j, P, n, sp):
+    """w_t = (L_t + delta) V_t[j] (fused Laplacian, sorted order) on stream sp."""
+    v0 = x.V.data_ptr()
+    _lib.check(_lib.lib().mlb_apply(x.b.ptr, C.c_void_p(v0 + 8 * n * j), C.c_void_p(P["w"][t].data_ptr()), x.a,
+                                    -1.0, x.K0, _lib.MLB_USE_ISD | _lib.MLB_SORTED, sp))
+
+
+def _issue_cgs_batched(P, p_V, T, j, dim, n, sp):
+    """CGS2 of every chain's w against its V[:j+1] in 5 launches, then
+    V[j+1] = w / ||w|| (mlb_cgs2_batched: per chain bitwise the single path)."""
+    _lib.check(_lib.lib().mlb_cgs2_batched(
+        T, C.c_void_p(p_V.data_ptr()), n, n, j + 1, C.c_void_p(P["p_w"].data_ptr()),
+        C.c_void_p(P["p_h"].data_ptr()), C.c_void_p(P["p_h1"].data_ptr()), C.c_void_p(P["p_nrm"][j].data_ptr()),
+        C.c_void_p(p_V.data_ptr()) if j + 1 < dim else None, C.c_void_p(P["bwork"].data_ptr()), sp))
 
 
 def _issue_layer_step(x, t, j, P, dim, n, sp):
@@ -630,7 +660,8 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
         scale_by(x.vs, x.V[0], vv, -0.5)
     use_graphs = _graphs_enabled()
     gkey = (dev.index, _VPOOL_DEPTH[0], dim, n, tuple(int(x.b.ptr.value) for x in st),
-            tuple((x.a, x.K0) for x in st), tuple(x.V.data_ptr() for x in st), AB.data_ptr())
+            tuple((x.a, x.K0) for x in st), tuple(x.V.data_ptr() for x in st), AB.data_ptr(),
+            _batched_cgs_ok(dim, n))
     graphs = None
     if use_graphs:
         graphs = _LOCK_GRAPHS.get(gkey)
@@ -641,6 +672,18 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
                 weakref.finalize(x.b, _LOCK_GRAPHS.pop, gkey, None)
     events = [None] * dim
     lib = _lib.lib()
+
+    batched = _batched_cgs_ok(dim, n)
+    p_V = None
+    if batched:   # the bases' pointer array at a fixed address (captured graphs read it)
+        vptrs = [x.V.data_ptr() for x in st]
+        if "p_V" not in P:
+            P["p_V"] = torch.tensor(vptrs, dtype=torch.int64, device=dev)
+            P["p_V_key"] = vptrs
+        elif P["p_V_key"] != vptrs:
+            P["p_V"].copy_(torch.tensor(vptrs, dtype=torch.int64))
+            P["p_V_key"] = vptrs
+        p_V = P["p_V"]
 
     def issue(j):
         if not use_graphs:
@@ -663,11 +706,16 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
                         s_.wait_event(fork)
                     for t, x in enumerate(st):
                         s_ = ss[t % len(ss)]
-                        _issue_layer_step(x, t, j, P, dim, n, C.c_void_p(s_.cuda_stream))
+                        if batched:    # the layers' matvecs concurrently, then ONE batched CGS2
+                            _issue_matvec(x, t, j, P, n, C.c_void_p(s_.cuda_stream))
+                        else:
+                            _issue_layer_step(x, t, j, P, dim, n, C.c_void_p(s_.cuda_stream))
                     for s_ in ss:
                         e = torch.cuda.Event()
                         e.record(s_)
                         cap.wait_event(e)
+                    if batched:
+                        _issue_cgs_batched(P, p_V, len(st), j, dim, n, C.c_void_p(cap.cuda_stream))
                     ABh[j].copy_(AB, non_blocking=True)
                 graphs[j] = (g, int(lib.mlb_launch_count() - l0))
             g, cnt = graphs[j]
