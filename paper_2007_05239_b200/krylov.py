@@ -704,8 +704,11 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
                     ss = P["streams"]
                     for s_ in ss:
                         s_.wait_event(fork)
+                    # one stream per binding: a binding's scratch grids must not be shared by
+                    # concurrent chains (the same layer may appear twice in a layer set)
+                    slot = {}
                     for t, x in enumerate(st):
-                        s_ = ss[t % len(ss)]
+                        s_ = ss[slot.setdefault(int(x.b.ptr.value), len(slot)) % len(ss)]
                         if batched:    # the layers' matvecs concurrently, then ONE batched CGS2
                             _issue_matvec(x, t, j, P, n, C.c_void_p(s_.cuda_stream))
                         else:
