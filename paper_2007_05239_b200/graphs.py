@@ -439,8 +439,15 @@ class LaplacianBatch:
             top = max(range(len(cost)), key=lambda i: cost[i])
             prio = os.environ.get("MLB_NO_STREAM_PRIORITY") is None
             hi = int(os.environ.get("MLB_STREAM_PRIORITY", "-1"))  # torch range on B200: 0 (low) .. -3 (high)
-            self._streams = [torch.cuda.Stream(device=dev, priority=(hi if (prio and i == top) else 0))
-                             for i in range(len(graph.layers))]
+            # one stream per weights object: a binding's scratch grids must not be shared
+            # by concurrent layers (a graph may hold the same weights twice)
+            by_w = {}
+            self._streams = []
+            for i, layer in enumerate(graph.layers):
+                key = id(layer.weights)
+                if key not in by_w:
+                    by_w[key] = torch.cuda.Stream(device=dev, priority=(hi if (prio and i == top) else 0))
+                self._streams.append(by_w[key])
             self._fork = torch.cuda.Event()
             self._joins = [torch.cuda.Event() for _ in graph.layers]
         self._pin_in = None
