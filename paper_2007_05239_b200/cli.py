@@ -14,7 +14,7 @@ from .runner import run_classify, run_eig, run_fastsum_bench, run_sbm_bench, run
 
 COMMANDS = {
     "classify": (run_classify, "semi-supervised classification from features or edge lists"),
-    "segment-image": (run_segment_image, "pixel classification of PNG images (not in the B200 backend)"),
+    "segment-image": (run_segment_image, "pixel classification of RGB PNG images"),
     "sbm-bench": (run_sbm_bench, "stochastic block model benchmark (not in the B200 backend)"),
     "fastsum-bench": (run_fastsum_bench, "fast summation accuracy and scaling tables"),
     "eig": (run_eig, "write the k smallest power mean eigenvalues"),

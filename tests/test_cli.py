@@ -66,7 +66,7 @@ def test_cli_exit_codes(tmp_path, capsys):
     assert "unknown config key: eig.kk" in capsys.readouterr().err
     assert main(["eig", "--config", str(tmp_path / "missing.json")]) == 2
     assert main(["eig"]) == 2  # no graph input
-    assert main(["segment-image"]) == 2
+    assert main(["segment-image"]) == 2   # no input.images
     assert main(["sbm-bench"]) == 2
     X = tmp_path / "x.csv"
     X.write_text("1,2\nx,3\n")
