@@ -27,7 +27,7 @@ def main():
     G = synth.build_graph(wl, device=0)
     layers = [with_shift(l, math.log(2.0)) for l in G.layers]
     v = torch.from_numpy(np.random.default_rng(1).standard_normal(wl.n)).cuda()
-    for st in bench.stage_breakdown(torch, layers, v, reps=5):
+    for st in bench.stage_breakdown(torch, [l.weights for l in layers], v, reps=10):
         st.pop("stats", None)
         print({k: (round(x * 1e3, 1) if k.endswith("_ms") else x) for k, x in st.items()})
 
