@@ -574,7 +574,8 @@ def _lock_buffers(dev, T, dim, n):
                  work=torch.empty((T, need), dtype=torch.float64, device=dev),
                  bwork=torch.empty(int(lib.mlb_cgs2_batched_work_size(T)), dtype=torch.float64, device=dev),
                  ABh=torch.empty((dim, T, 2 * dim + 1), dtype=torch.float64, pin_memory=True),
-                 streams=[torch.cuda.Stream(device=dev) for _ in range(min(T, 8))])
+                 streams=[torch.cuda.Stream(device=dev)
+                          for _ in range(min(T, int(os.environ.get("MLB_PKSM_STREAMS", "8"))))])
         # device pointer arrays of the batched CGS2 (fixed per pool; nrm2 per step j)
         ab0 = P["AB"].data_ptr()
         rows = [ab0 + 8 * (2 * dim + 1) * t for t in range(T)]
