@@ -17,8 +17,6 @@ namespace mlb {
 constexpr int kRedThreads = 256;
 constexpr int kMaxRowBlocks = 256;
 constexpr int kFusedBlocks = 296;  // CGS2 row-block capacity (2 per B200 SM); launches use min(this, 2 x SMs)
-// CGS2 scratch: part1 (kFusedBlocks x 64) | npart (kFusedBlocks) | h1 (64) | part2 (kFusedBlocks x 64)
-constexpr int64_t kCgsPart2 = (int64_t)kFusedBlocks * 65 + 64;
 
 static int row_blocks(int64_t n) {
     int64_t b = (n + 2047) / 2048;
@@ -323,104 +321,6 @@ __device__ __forceinline__ void cgs_update_block(const double* __restrict__ V, i
     }
 }
 
-// Pass-1 update fused with the pass-2 projections: w -= V h1 on the block's
-// rows (h1 = fixed-order sum of part_in, as cgs_update_block), then the same
-// thread's 4 rows of V are re-read (L1-resident: just loaded) against the new w
-// and reduced exactly as cgs_dot_block does (same rows per thread, same
-// shuffle tree, tiles in order, warps in order) into part_out: one DRAM pass
-// over V instead of two, bitwise the same h2.
-__device__ __forceinline__ void cgs_update_dot_block(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
-                                                     const double* __restrict__ part_in, double* __restrict__ w,
-                                                     double* __restrict__ h_save, double* __restrict__ part_out) {
-    __shared__ double h[64];
-    __shared__ double acc[8][64];
-    const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = warp; j < cols; j += 8) {
-        double s = 0.0;
-        for (int b = lane; b < nb; b += 32) s += __ldcg(part_in + (int64_t)j * nb + b);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-        if (lane == 0) {
-            h[j] = s;
-            if (blockIdx.x == 0 && h_save) h_save[j] = s;
-        }
-    }
-    for (int j = threadIdx.x; j < 8 * 64; j += blockDim.x) (&acc[0][0])[j] = 0.0;
-    __syncthreads();
-    const int64_t per = ((n + nb - 1) / nb + 3) & ~(int64_t)3;
-    const int64_t r0 = min(n, blockIdx.x * per), r1 = min(n, r0 + per);
-    for (int64_t t0 = r0; t0 < r1; t0 += kTileRows) {
-        const int64_t i0 = t0 + 4 * threadIdx.x;
-        const bool full = i0 + 3 < r1;
-        double x[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-        for (int j = 0; j < cols; ++j) {
-            const double* col = V + (int64_t)j * ld + i0;
-            const double hj = h[j];
-            double v[4];
-            if (full) {
-                ld4(col, true, v);
-            } else {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) v[r] = (i0 + r < r1) ? __ldg(col + r) : 0.0;
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r) x[r] = fma(v[r], hj, x[r]);
-        }
-        double wr[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int64_t i = i0 + r;
-            if (i < r1) {
-                const double wn = w[i] - x[r];
-                w[i] = wn;
-                wr[r] = wn;
-            } else {
-                wr[r] = 0.0;
-            }
-        }
-        for (int j0 = 0; j0 < cols; j0 += 4) {
-            double vr[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double* col = V + (int64_t)min(j0 + q, cols - 1) * ld + i0;
-                if (full) {
-                    ld4(col, true, vr[q]);
-                } else {
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) vr[q][r] = (i0 + r < r1) ? __ldg(col + r) : 0.0;
-                }
-            }
-            double sq[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                sq[q] = 0.0;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) sq[q] = fma(vr[q][r], wr[r], sq[q]);
-            }
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) sq[q] += __shfl_down_sync(0xffffffffu, sq[q], o);
-            if (lane == 0)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (j0 + q < cols) acc[warp][j0 + q] += sq[q];
-        }
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < cols; j += blockDim.x) {
-        double t = 0.0;
-        for (int k = 0; k < 8; ++k) t += acc[k][j];
-        part_out[(int64_t)j * nb + blockIdx.x] = t;
-    }
-}
-
-__global__ void __launch_bounds__(256) cgs_update_dot_kernel(const double* __restrict__ V, int64_t ld, int64_t n,
-                                                             int cols, const double* __restrict__ part_in,
-                                                             double* __restrict__ w, double* __restrict__ h_save,
-                                                             double* __restrict__ part_out) {
-    cgs_update_dot_block(V, ld, n, cols, part_in, w, h_save, part_out);
-}
-
 __global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restrict__ V, int64_t ld, int64_t n, int cols,
                                                          const double* __restrict__ part_in, double* __restrict__ w,
                                                          double* __restrict__ npart, double* __restrict__ h_save,
@@ -428,17 +328,15 @@ __global__ void __launch_bounds__(256) cgs_update_kernel(const double* __restric
     cgs_update_block(V, ld, n, cols, part_in, w, npart, h_save, h_prev, h_sum);
 }
 
-
-// pass 0: w -= V h1, h1 -> h1_out[t], and the pass-2 partials into part2 (fused);
-// pass 1: w -= V h2 (h2 from part2), h_out = h1 + h2, ||w||^2 partials
+// pass = 0: w -= V h1, h1 -> h1_out[t];  pass = 1: w -= V h2, h_out = h1 + h2, ||w||^2 partials
 __global__ void __launch_bounds__(256) cgs_update_batched(CgsBatch B, int64_t ld, int64_t n, int cols, int pass) {
     const int t = blockIdx.y;
     double* wk = B.work + t * B.work_stride;
     double* npart = wk + (int64_t)kFusedBlocks * 64;
     if (pass == 0)
-        cgs_update_dot_block(B.V[t], ld, n, cols, wk, B.w[t], B.h1_out[t], wk + kCgsPart2);
+        cgs_update_block(B.V[t], ld, n, cols, wk, B.w[t], nullptr, B.h1_out[t], nullptr, nullptr);
     else
-        cgs_update_block(B.V[t], ld, n, cols, wk + kCgsPart2, B.w[t], npart, nullptr, B.h1_out[t], B.h_out[t]);
+        cgs_update_block(B.V[t], ld, n, cols, wk, B.w[t], npart, nullptr, B.h1_out[t], B.h_out[t]);
 }
 
 // ||w||^2 of every chain (fixed-order sum of its block partials), then
@@ -463,11 +361,11 @@ static int cgs2_fused(const double* V, int64_t ld, int64_t n, int cols, double* 
     double* part = work;                              // nb x cols
     double* npart = part + (int64_t)kFusedBlocks * 64;  // nb
     double* h1 = npart + kFusedBlocks;                 // cols
-    double* part2 = work + kCgsPart2;                  // nb x cols
     cgs_dot_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, w, part);
-    cgs_update_dot_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, part, w, h1, part2);   // update 1 + projections 2
-    cgs_update_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, part2, w, npart, nullptr, h1, h_out);
-    note_launches(3);
+    cgs_update_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, part, w, nullptr, h1, nullptr, nullptr);
+    cgs_dot_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, w, part);
+    cgs_update_kernel<<<nb, 256, 0, st>>>(V, ld, n, cols, part, w, npart, nullptr, h1, h_out);
+    note_launches(4);
     if (nrm2_out) {
         finish_partial<<<1, 64, 0, st>>>(npart, nb, 1, nrm2_out, nullptr);
         note_launches(1);
@@ -492,7 +390,7 @@ extern "C" {
 int64_t mlb_krylov_work_size(int64_t n, int maxcols) {
     (void)n;
     const int64_t unfused = (int64_t)kMaxRowBlocks * (maxcols + 2) + 2 * (maxcols + 2);
-    const int64_t fused = kCgsPart2 + (int64_t)kFusedBlocks * 64;
+    const int64_t fused = (int64_t)kFusedBlocks * (64 + 1) + 64;
     return std::max(unfused, fused);
 }
 
@@ -557,7 +455,7 @@ int mlb_cgs2(const double* V, int64_t ld, int64_t n, int cols, double* w, double
     return MLB_OK;
 }
 
-int64_t mlb_cgs2_batched_work_size(int T) { return (int64_t)T * (kCgsPart2 + (int64_t)kFusedBlocks * 64); }
+int64_t mlb_cgs2_batched_work_size(int T) { return (int64_t)T * ((int64_t)kFusedBlocks * (64 + 1) + 64); }
 
 int mlb_cgs2_batched(int T, const double* const* V, int64_t ld, int64_t n, int cols, double* const* w,
                      double* const* h_out, double* const* h1_out, double* const* nrm2_out, double* const* vnext,
@@ -567,12 +465,13 @@ int mlb_cgs2_batched(int T, const double* const* V, int64_t ld, int64_t n, int c
     if (!V || !w || !h_out || !h1_out || !nrm2_out || !work) return fail(MLB_ERR_ARG, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
     const int nb = std::max(1, std::min(std::min(kFusedBlocks, 2 * device_sms()), (int)((n + kTileRows - 1) / kTileRows)));
-    CgsBatch B{V, w, h_out, h1_out, nrm2_out, vnext, work, kCgsPart2 + (int64_t)kFusedBlocks * 64};
+    CgsBatch B{V, w, h_out, h1_out, nrm2_out, vnext, work, (int64_t)kFusedBlocks * (64 + 1) + 64};
     cgs_dot_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols);
-    cgs_update_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols, 0);   // update 1 + projections 2
+    cgs_update_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols, 0);
+    cgs_dot_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols);
     cgs_update_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols, 1);
     cgs_norm_scale_batched<<<dim3(ew_grid(n) / std::max(1, T / 8) + 1, T), 256, 0, st>>>(B, ld, n, cols, nb);
-    note_launches(4);
+    note_launches(5);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }
