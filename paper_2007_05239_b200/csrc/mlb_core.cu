@@ -648,6 +648,7 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     b->nblk = (int)(cblk.size() / 4);
     b->ncta_cells = ncta_cells;
     b->nactive = (int)active_brick.size();
+    if (const char* env = std::getenv("MLB_SPREAD_ATOMIC")) b->spread_atomic = (d == 3 && env[0] == '1');
     b->grid_cells = 1;
     for (int a = 0; a < d; ++a) b->grid_cells *= g.L;
     int64_t st = (int64_t)g.Kh;
@@ -792,9 +793,10 @@ int mlb_spread(mlb_binding* b, const double* v, double* grid, unsigned flags, vo
     if (!b || !grid) return fail(MLB_ERR_ARG, "null argument");
     DeviceGuard guard(b->plan->device);
     cudaStream_t st = (cudaStream_t)stream;
+    b->atomic_target = grid;
     int rc = launch_spread(b, v, flags & ~MLB_SPREAD_ONLY, st);
     if (rc != MLB_OK) return rc;
-    if (flags & MLB_SPREAD_ONLY) return MLB_OK;
+    if (flags & MLB_SPREAD_ONLY || b->spread_atomic) return MLB_OK;
     if (b->nseg == 0) {
         MLB_CUDA_TRY(cudaMemsetAsync(grid, 0, b->grid_cells * sizeof(double), st));
         return MLB_OK;
@@ -819,6 +821,7 @@ int mlb_spread_peers(mlb_binding* b, const double* v, double* const* peer_slots,
             MLB_CUDA_TRY(cudaMemsetAsync(po.p[q], 0, b->grid_cells * sizeof(double), st));
         return MLB_OK;
     }
+    b->atomic_target = nullptr;   // (the peer exchange always takes the deterministic blocks)
     int rc = launch_spread(b, v, flags & ~MLB_SPREAD_ONLY, st);
     if (rc != MLB_OK) return rc;
     return launch_reduce(b, nullptr, st, &po);
@@ -857,6 +860,7 @@ int mlb_ipc_close(void* dev_ptr) {
 int mlb_reduce(mlb_binding* b, double* grid, void* stream) {
     if (!b || !grid) return fail(MLB_ERR_ARG, "null argument");
     DeviceGuard guard(b->plan->device);
+    if (b->spread_atomic) return MLB_OK;   // the atomic spread wrote the grid itself
     if (b->nseg == 0) {
         MLB_CUDA_TRY(cudaMemsetAsync(grid, 0, b->grid_cells * sizeof(double), (cudaStream_t)stream));
         return MLB_OK;
@@ -893,8 +897,9 @@ int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double b
     DeviceGuard guard(b->plan->device);
     cudaStream_t st = (cudaStream_t)stream;
     flags &= (MLB_USE_ISD | MLB_ACCUMULATE | MLB_SORTED);  // the public bits only
+    b->atomic_target = b->grid;
     int rc = launch_spread(b, v, flags, st);
-    if (rc == MLB_OK) rc = launch_reduce(b, b->grid, st);
+    if (rc == MLB_OK && !b->spread_atomic) rc = launch_reduce(b, b->grid, st);
     if (rc == MLB_OK) rc = launch_convolve(b, b->grid, b->grid2, st);
     if (rc == MLB_OK) rc = launch_gather(b, b->grid2, v, y, alpha, beta, gamma, flags, st);
     return rc;

@@ -112,7 +112,21 @@ struct FsArgs {
     int tile_cells;
     int nchunks;
     int nseg;
+    // d = 3 atomic mode (MLB_SPREAD_ATOMIC=1, A/B only): cell blocks are added
+    // into this zeroed sub-box grid with red.global.add.f64 (no merge / R2;
+    // not bitwise reproducible); nullptr: the deterministic blocks
+    double* agrid;
 };
+
+// sub-box index of element (o01 = o0*S + o1, o2) of d = 3 cell block `blk`
+__device__ __forceinline__ int64_t block_grid_index(const FsArgs& a, int blk, int o01, int o2) {
+    const int4 cb = __ldg(a.cblk + blk);
+    const int S = a.g.S, TL = a.g.TL, Tb = a.g.Tb, nbr = a.g.nbr, L = a.g.L;
+    const int c0 = cb.z / (TL * TL), c1 = (cb.z / TL) % TL, c2 = cb.z % TL;
+    const int B0 = cb.w / (nbr * nbr), B1 = (cb.w / nbr) % nbr, B2 = cb.w % nbr;
+    const int u0 = B0 * Tb + c0 + o01 / S, u1 = B1 * Tb + c1 + o01 % S, u2 = B2 * Tb + c2 + o2;
+    return ((int64_t)u0 * L + u1) * L + u2;
+}
 
 // ----------------------------------------------------------------- spread --
 // Warps own segments statically (gw, gw + W, ...).  A segment is a list of
@@ -627,7 +641,10 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
                     double* out = a.blocks + (size_t)blk * (S * S * S);
                     for (int t = lane; t < NRED; t += 32) {
                         const int o01 = t / C::SP, k = t % C::SP;
-                        if (off2 + k < S) out[o01 * S + off2 + k] = stage[t];
+                        if (off2 + k < S) {
+                            if (a.agrid) atomicAdd(a.agrid + block_grid_index(a, blk, o01, off2 + k), stage[t]);
+                            else out[o01 * S + off2 + k] = stage[t];
+                        }
                     }
                     __syncwarp();
                 }
@@ -658,7 +675,10 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
                             double sum = 0.0;
                             for (int r = 0; r < nw; ++r) sum += red[(wlo + r) * NRED + t];
                             const int o01 = t / C::SP, k = t % C::SP;
-                            if (off2 + k < S) out[o01 * S + off2 + k] = sum;
+                            if (off2 + k < S) {
+                                if (a.agrid) atomicAdd(a.agrid + block_grid_index(a, bk, o01, off2 + k), sum);
+                                else out[o01 * S + off2 + k] = sum;
+                            }
                         }
                     }
                 }
@@ -907,7 +927,24 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     const int c_hi = (int)(((long long)nunits * (gw + 1)) / nwt);
     const int64_t rs = (D == 3) ? (int64_t)L * L : (int64_t)L;  // stride of axis 0
     long long cur = -1;
+    // m >= 5 d = 3 chunks (one CTA per SM, registers to spare): the epilogue's
+    // gathers are issued at the chunk's start (EPF) and the NEXT chunk's
+    // offsets are loaded while this chunk contracts (PF)
+    constexpr bool EPF = D == 3 && M >= 5;
+    constexpr bool PF = D == 3 && !PK && M >= 5;
+    double nf[6] = {0.5, 0.5, 0.5, 0.5, 0.5, 0.5};
+    auto load_frac = [&](int c) {
+        const int q0 = a.chunk_start[c];
+        const int qn = a.chunk_start[c + 1] - q0;
+        const bool oA = lane < qn, oB = lane + 32 < qn;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            nf[2 * ax] = oA ? __ldg(a.frac + ax * a.n + q0 + lane) : 0.5;
+            nf[2 * ax + 1] = oB ? __ldg(a.frac + ax * a.n + q0 + 32 + lane) : 0.5;
+        }
+    };
     pdl_wait();  // the grid (convolution) and v come from stream predecessors
+    if (PF && c_lo < c_hi) load_frac(c_lo);
     for (int ch = c_lo; ch < c_hi; ++ch) {
         int gbase, wst = S, dcA = 0, pA, pB;
         bool okA, okB, two;
@@ -934,12 +971,31 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             pB = p0 + 32 + lane;
         }
         const long long key = (long long)gbase * 16 + wst;
+        // d = 3: the epilogue's gathers (node index, D^-1/2, then v[node]) are
+        // issued now and consumed after the contraction -- a random v[perm[p]]
+        // read costs a full DRAM round trip that 2 warps per SMSP cannot hide
+        int nodeA = 0, nodeB = 0;
+        double sA = 1.0, sB = 1.0;
+        if (EPF) {
+            nodeA = (flags & MLB_SORTED) ? pA : (okA ? __ldg(a.perm + pA) : 0);
+            nodeB = (flags & MLB_SORTED) ? pB : (okB ? __ldg(a.perm + pB) : 0);
+            if (flags & MLB_USE_ISD) {
+                sA = okA ? __ldg(a.isd + pA) : 1.0;
+                sB = okB ? __ldg(a.isd + pB) : 1.0;
+            }
+        }
         // issue the point loads before (possibly) restaging the neighbourhood
-        const double fA0 = okA ? __ldg(a.frac + pA) : 0.5, fB0 = okB ? __ldg(a.frac + pB) : 0.5;
-        const double fA1 = (D >= 2 && okA) ? __ldg(a.frac + a.n + pA) : 0.5;
-        const double fB1 = (D >= 2 && okB) ? __ldg(a.frac + a.n + pB) : 0.5;
-        const double fA2 = (D == 3 && okA) ? __ldg(a.frac + 2 * a.n + pA) : 0.5;
-        const double fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
+        double fA0, fB0, fA1, fB1, fA2, fB2;
+        if (PF) {
+            fA0 = nf[0]; fB0 = nf[1]; fA1 = nf[2]; fB1 = nf[3]; fA2 = nf[4]; fB2 = nf[5];
+        } else {
+            fA0 = okA ? __ldg(a.frac + pA) : 0.5;
+            fB0 = okB ? __ldg(a.frac + pB) : 0.5;
+            fA1 = (D >= 2 && okA) ? __ldg(a.frac + a.n + pA) : 0.5;
+            fB1 = (D >= 2 && okB) ? __ldg(a.frac + a.n + pB) : 0.5;
+            fA2 = (D == 3 && okA) ? __ldg(a.frac + 2 * a.n + pA) : 0.5;
+            fB2 = (D == 3 && okB) ? __ldg(a.frac + 2 * a.n + pB) : 0.5;
+        }
         if (key != cur && !(flags & (1u << 18))) {  // bit 18: ablation (profiling only): no restaging
             __syncwarp();
             if (D == 3 && PK) {
@@ -979,13 +1035,19 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
                 for (int q = 0; q < S; ++q) wB0[q] = wB1[q] = wB2[q] = 0.0;
             }
         }
+        double vA = 0.0, vB = 0.0;
         if (D == 3) {
 #pragma unroll
             for (int q = 0; q < S; ++q) {
                 w0s[q] = wA0[q];
                 w0s[S + q] = wB0[q];
             }
+            if (EPF && v) {  // (the node indices have arrived during the window evaluation)
+                vA = okA ? __ldg(v + nodeA) : 0.0;
+                vB = okB ? __ldg(v + nodeB) : 0.0;
+            }
         }
+        if (PF && ch + 1 < c_hi) load_frac(ch + 1);
         double accA = 0.0, accB = 0.0;
         if (flags & (1u << 16)) {  // ablation (profiling only): skip the contraction
             accA = wA0[0] + wA1[S - 1] + wA2[1];
@@ -1054,9 +1116,17 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             if (!ok) continue;
             const int p = h ? pB : pA;
             const double acc = h ? accB : accA;
-            const int node = (flags & MLB_SORTED) ? p : __ldg(a.perm + p);
-            const double vv = v ? __ldg(v + node) : 0.0;
-            const double s = (flags & MLB_USE_ISD) ? __ldg(a.isd + p) : 1.0;
+            int node;
+            double vv, s;
+            if (EPF) {
+                node = h ? nodeB : nodeA;
+                vv = h ? vB : vA;
+                s = h ? sB : sA;
+            } else {
+                node = (flags & MLB_SORTED) ? p : __ldg(a.perm + p);
+                vv = v ? __ldg(v + node) : 0.0;
+                s = (flags & MLB_USE_ISD) ? __ldg(a.isd + p) : 1.0;
+            }
             double res = alpha * vv + s * (beta * acc + gamma * s * vv);
             if (flags & MLB_ACCUMULATE) res += y[node];
             y[node] = res;
@@ -1086,6 +1156,7 @@ static FsArgs make_args(mlb_binding* b) {
     a.merge_off = b->merge_off;
     a.merge_pairs = b->merge_pairs;
     a.blocks = b->blocks;
+    a.agrid = nullptr;
     a.ggrp = reinterpret_cast<const int2*>(b->ggrp);
     a.gslot = b->gslot;
     a.ngrp = b->ngrp;
@@ -1141,6 +1212,10 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         auto kern3 = spread_cells_kernel<M>;
         if (int rc = ensure_max_smem((const void*)kern3, smem)) return rc;  // per (kernel, device)
         if (b->ncta_cells == 0) return MLB_OK;
+        if (b->spread_atomic && b->atomic_target) {   // A/B mode: zero the target grid, blocks added atomically
+            MLB_CUDA_TRY(cudaMemsetAsync(b->atomic_target, 0, b->grid_cells * sizeof(double), st));
+            a.agrid = b->atomic_target;
+        }
         MLB_CUDA_TRY(launch_k(kern3, dim3(b->ncta_cells), dim3(kCellWarps * 32), smem, st, a, b->plan->wc, v, flags));
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());

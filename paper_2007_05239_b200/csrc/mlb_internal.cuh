@@ -161,6 +161,10 @@ struct mlb_binding {
     int tile_cells = 0;              // TL^d
     int64_t grid_cells = 0;          // L^d
     int max_seg_chunks = 0;
+    // d = 3 A/B mode (env MLB_SPREAD_ATOMIC=1 at bind time): the spread adds
+    // cell blocks into atomic_target with red.global.add (no merge / R2)
+    int spread_atomic = 0;
+    double* atomic_target = nullptr;
 };
 
 namespace mlb {
