@@ -21,7 +21,7 @@ oracle (oracle/c/mlb_oracle.c).
 
 The output keeps what the parity tests check and stays small:
 eigenvalues, the Allen-Cahn predicted labels, iterations, the degrees of
-every layer (float64 for n <= 50k, else a 4096-node seeded sample), and a
+every layer (all nodes when n x layers <= 2e5, else a 4096-node seeded sample), and a
 sketch of the eigenvector subspace: P z = Phi (Phi^T z) for two seeded
 Gaussian z (float32), which compares projectors independently of the
 eigenvectors' signs / rotations inside clusters.
@@ -93,9 +93,9 @@ def main():
     n = wl.n
     Z = sketch_seeds(n)
     sketch = (basis.vectors @ (basis.vectors.T @ Z)).astype(np.float32)
-    if n <= 50_000:
+    if n * len(layers) <= 200_000:
         deg_idx = np.arange(n)
-    else:
+    else:   # a seeded 4096-node sample keeps the fixture small
         deg_idx = degree_sample(n)
     degs = np.stack([lay.degrees[deg_idx] for lay in layers])
     tag = f"cfg{a.config}" + ("" if a.side is None else f"_side{a.side}")
