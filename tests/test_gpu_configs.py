@@ -8,6 +8,11 @@ labels identical on >= 99.9% of the nodes.  Also: the degrees of every layer
 (<= 1e-12), the eigenvector subspace through a projector sketch P z for two
 seeded z (<= 1e-6 relative; signs / rotations inside clusters cancel), the
 Allen-Cahn iteration count.
+
+cfg4_side1000 (n = 10^6) comes from oracle/gen_golden_cfg4_large.py: the
+reference's own solvers with the layers' W v computed by the multi-process
+oracle of the reference algorithm (the reference's KernelWeights would need
+a 21 GB binding at this size).
 """
 
 import os
@@ -19,7 +24,8 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("cfg3", 3, None), ("cfg2", 2, None), ("cfg4_side500", 4, 500), ("cfg4_side100", 4, 100)]
+CASES = [("cfg3", 3, None), ("cfg2", 2, None), ("cfg4_side500", 4, 500), ("cfg4_side100", 4, 100),
+         ("cfg4_side1000", 4, 1000)]
 
 
 def _golden(tag):
