@@ -691,12 +691,7 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
     // d <= 2: one partial grid per spread CTA (<= 2 per SM); d = 3: one per segment
     b->spread_parts_max = nsm * 2;
-    // d <= 2: one partial grid per spread CTA, or per warp (8 per CTA) when the
-    // sub-box is too large for shared-memory tiles (global per-warp tiles)
-    const bool gtile = d <= 2 && (size_t)b->tile_cells * 8 * 8 > (size_t)64 * 1024;
-    b->gtile_ok = gtile ? 1 : 0;
-    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max * (gtile ? 8 : 1))
-                                   : (size_t)std::max(1, b->nactive);  // d = 3: brick tiles
+    const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)std::max(1, b->nactive);  // d = 3: brick tiles
     if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, nparts * b->tile_cells);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells + 2);

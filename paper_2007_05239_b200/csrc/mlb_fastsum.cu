@@ -170,8 +170,8 @@ __device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps
     return sub_first(a, p.seg + nwarps);
 }
 
-template <int D, int M, bool PERSIST, bool GROUPED = false, bool GTILE = false>
-__global__ void __launch_bounds__(PERSIST ? 256 : 64, GTILE ? 2 : 1) spread_kernel(FsArgs a, WinCoef wc,
+template <int D, int M, bool PERSIST, bool GROUPED = false>
+__global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, WinCoef wc,
                                                                     const double* __restrict__ v, unsigned flags,
                                                                     int* __restrict__ work) {
     using C = SpreadCfg<D, M>;
@@ -182,15 +182,11 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64, GTILE ? 2 : 1) spread_kern
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TL = a.g.TL;
     const int tile = a.tile_cells;
-    // GTILE (large d <= 2 sub-boxes, PERSIST): the warp's sub-box tile lives in
-    // global memory (L2) -- it is only touched when the cell changes -- and IS
-    // the warp's partial grid, so shared memory holds just the staging and 8
-    // warps per CTA (several CTAs per SM) fit instead of 3
-    double* my_tile = GTILE ? a.partial + (size_t)(blockIdx.x * nw + warp) * tile : smem + (size_t)warp * tile;
+    double* my_tile = smem + (size_t)warp * tile;
     // (d = 2: + 8 doubles so the grouped reads of the last row's unused
     // offsets stay inside the warp's staging)
     constexpr int STAGE = 32 * D * SPAD + (D == 2 ? 8 : 0);
-    double* my_stage = smem + (GTILE ? 0 : (size_t)nw * tile) + (size_t)warp * STAGE;
+    double* my_stage = smem + (size_t)nw * tile + (size_t)warp * STAGE;
     for (int i = lane; i < STAGE; i += 32) my_stage[i] = 0.0;
     for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
     pdl_wait();  // v (and the partial grids' previous readers) are stream predecessors
@@ -447,7 +443,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64, GTILE ? 2 : 1) spread_kern
         }
     }
     pdl_launch();
-    if (PERSIST && !GTILE) {
+    if (PERSIST) {
         __syncthreads();
         double* out = a.partial + (size_t)blockIdx.x * tile;
         for (int i = threadIdx.x; i < tile; i += blockDim.x) {
@@ -1191,24 +1187,18 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         // persistent CTAs of 8 warps, one partial grid per CTA
         int nw = 8;
         while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
-        // a large sub-box leaves few warps per CTA: its tiles go to global
-        // memory instead (one partial grid per warp, summed by grid_sum)
-        bool gtile = nw < 8 && b->gtile_ok && b->n >= (1 << 20);
-        if (const char* env = std::getenv("MLB_D2_GTILE")) gtile = b->gtile_ok && env[0] == '1';  // A/B
-        if (gtile) nw = 8;
-        const size_t smem = gtile ? spread_smem<D, M>(nw, 0) : spread_smem<D, M>(nw, b->tile_cells);
+        const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
         if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
         // grouped d = 2 lanes pay off on large layers (config 4: 622 -> 498
         // us); at config-2 size the plain lane blocks leave more room for
         // the concurrently running d = 3 layer (step 3.96 vs 3.86e9)
         bool grouped = D == 2 && b->n >= (1 << 20);
         if (const char* env = std::getenv("MLB_D2_GROUPED")) grouped = D == 2 && env[0] == '1';  // tests / tuning
-        auto kern = gtile ? (grouped ? spread_kernel<D, M, true, true, true> : spread_kernel<D, M, true, false, true>)
-                          : (grouped ? spread_kernel<D, M, true, true> : spread_kernel<D, M, true, false>);
-        if (int rc = ensure_max_smem((const void*)kern, smem)) return rc;
+        auto kern = grouped ? spread_kernel<D, M, true, true> : spread_kernel<D, M, true, false>;
+        MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int blocks = std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);
         if (blocks < 1) blocks = 1;
-        b->spread_parts = gtile ? blocks * nw : blocks;
+        b->spread_parts = blocks;
         MLB_CUDA_TRY(launch_k(kern, dim3(blocks), dim3(nw * 32), smem, st, a, b->plan->wc, v, flags, b->work));
         note_launches(1);
         MLB_CUDA_TRY(cudaGetLastError());

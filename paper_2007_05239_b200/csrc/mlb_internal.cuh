@@ -164,7 +164,6 @@ struct mlb_binding {
     // d = 3 A/B mode (env MLB_SPREAD_ATOMIC=1 at bind time): the spread adds
     // cell blocks into atomic_target with red.global.add (no merge / R2)
     int spread_atomic = 0;
-    int gtile_ok = 0;                // d <= 2: `partial` holds one tile per spread warp (global tiles possible)
     double* atomic_target = nullptr;
 };
 
