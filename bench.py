@@ -411,7 +411,9 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
     rng = np.random.default_rng(1000)
     v_host = rng.standard_normal(n)
-    e2e_k = max(3, min(args.steps, 6))   # distinct host vectors streamed by the e2e leg
+    # distinct host vectors streamed by the e2e leg: the K steps' own vectors,
+    # capped so the pinned input + outputs stay under ~1.5 GB (config 4: 6)
+    e2e_k = max(3, min(args.steps, int(1.5e9 // (8 * n * (1 + T)))))
     V_host = rng.standard_normal((e2e_k, n))
     extra = {}
     if ws == 1:

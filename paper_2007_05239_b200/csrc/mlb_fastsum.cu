@@ -930,15 +930,17 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     // m >= 5 d = 3 chunks (one CTA per SM, registers to spare): the epilogue's
     // gathers are issued at the chunk's start (EPF) and the NEXT chunk's
     // offsets are loaded while this chunk contracts (PF)
-    constexpr bool EPF = D == 3 && M >= 5;
-    constexpr bool PF = D == 3 && !PK && M >= 5;
+    // (d = 2: the axis-0 windows go to shared memory like d = 3's, which
+    // leaves the registers for both prefetches at 128 registers per thread)
+    constexpr bool EPF = (D == 3 && M >= 5) || D == 2;
+    constexpr bool PF = ((D == 3 && M >= 5) || D == 2) && !PK;
     double nf[6] = {0.5, 0.5, 0.5, 0.5, 0.5, 0.5};
     auto load_frac = [&](int c) {
         const int q0 = a.chunk_start[c];
         const int qn = a.chunk_start[c + 1] - q0;
         const bool oA = lane < qn, oB = lane + 32 < qn;
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
+        for (int ax = 0; ax < D; ++ax) {
             nf[2 * ax] = oA ? __ldg(a.frac + ax * a.n + q0 + lane) : 0.5;
             nf[2 * ax + 1] = oB ? __ldg(a.frac + ax * a.n + q0 + 32 + lane) : 0.5;
         }
@@ -1036,7 +1038,7 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             }
         }
         double vA = 0.0, vB = 0.0;
-        if (D == 3) {
+        if (D >= 2) {
 #pragma unroll
             for (int q = 0; q < S; ++q) {
                 w0s[q] = wA0[q];
@@ -1069,8 +1071,8 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
                     rA = fma(wA1[j], gv, rA);
                     rB = fma(wB1[j], gv, rB);
                 }
-                accA = fma(wA0[i], rA, accA);
-                accB = fma(wB0[i], rB, accB);
+                accA = fma(w0s[i], rA, accA);
+                accB = fma(w0s[S + i], rB, accB);
             }
         } else if (!two) {
 #pragma unroll 1
