@@ -127,7 +127,8 @@ class ShardContext:
         """out[:k] = (V[:s]^T S[:s, :k])^T: Ritz / restart vectors (local rows)."""
         torch = _torch()
         if not self.gpu:
-            out[:k] = (V[:s].T @ S[:s, :k]).T
+            Sk = S[:s, :k] if isinstance(S, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(S[:s, :k]))
+            out[:k] = (V[:s].T @ Sk).T
             return out
         Sd = torch.from_numpy(np.asfortranarray(np.asarray(S[:s, :k].cpu() if isinstance(S, torch.Tensor)
                                                            else S[:s, :k])).ravel(order="F")).to(self.device)
