@@ -166,7 +166,7 @@ def measure_fp64_peak(torch, device):
     return best
 
 
-def stage_breakdown(torch, weights, v, reps=10):
+def stage_breakdown(torch, weights, v, reps=10, sorted_order=False):
     """Per-kernel device times (CUDA events on the launching stream): spread
     kernel, partial reduction, convolution, gather (with the Laplacian
     epilogue) -- the stage hooks of the C ABI, one layer at a time."""
@@ -184,13 +184,15 @@ def stage_breakdown(torch, weights, v, reps=10):
         sp = _lib.stream_ptr()
         for r in range(reps + 2):
             ev[0].record()
-            _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD | _lib.MLB_SPREAD_ONLY, sp))
+            so = _lib.MLB_SORTED if sorted_order else 0
+            _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(v), _lib.ptr(grid), _lib.MLB_USE_ISD | _lib.MLB_SPREAD_ONLY | so,
+                                      sp))
             ev[1].record()
             _lib.check(lib.mlb_reduce(b.ptr, _lib.ptr(grid), sp))
             ev[2].record()
             _lib.check(lib.mlb_convolve(b.ptr, _lib.ptr(grid), _lib.ptr(grid2), sp))
             ev[3].record()
-            _lib.check(lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), 0, sp))
+            _lib.check(lib.mlb_gather(b.ptr, _lib.ptr(grid2), _lib.ptr(y), so, sp))
             ev[4].record()
             ev[4].synchronize()
             if r >= 2:

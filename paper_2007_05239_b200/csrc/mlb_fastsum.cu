@@ -218,6 +218,14 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     (void)g2;
     (void)a2;
     (void)b2;
+    // d = 1: every lane owns its point (sub-chunks never straddle a cell) and
+    // accumulates its S windows in registers; the warp's S sums meet by a
+    // fixed xor-shuffle tree only when the cell changes (dense cells: a few
+    // times per segment).  No staging, no shared-memory traffic per point.
+    constexpr bool R1 = (D == 1);
+    double acc1[R1 ? S : 1];
+#pragma unroll
+    for (int o = 0; o < (R1 ? S : 1); ++o) acc1[o] = 0.0;
 
     for (int pass = 0; pass < C::NPASS; ++pass) {
         const int off2 = pass * C::SP;
@@ -231,6 +239,18 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
         int cur = -1;
 
         auto flush = [&](int cell) {
+            if constexpr (R1) {
+                if (cell < 0) return;
+#pragma unroll
+                for (int o = 0; o < S; ++o) {
+                    double t = acc1[o];
+#pragma unroll
+                    for (int sh = 16; sh > 0; sh >>= 1) t += __shfl_xor_sync(0xffffffffu, t, sh);
+                    if (lane == 0 && !(flags & (1u << 18))) my_tile[cell + o] += t;
+                    acc1[o] = 0.0;
+                }
+                return;
+            }
             if constexpr (G2) {
                 if (cell < 0) return;
                 if (flags & (1u << 18)) return;  // ablation (profiling only)
@@ -330,7 +350,13 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
                 cur = cell;
             }
             __syncwarp();
-            if (!(flags & (1u << 17))) {  // bit 17: ablation (profiling only)
+            if (R1 && !(flags & (1u << 17))) {
+                const double sv0 = (lane < np && p0.sub >= 0) ? s0 * v0 : 0.0;
+                double w[S];
+                kb_windows<M>(f0[0], wc, w);
+#pragma unroll
+                for (int o = 0; o < S; ++o) acc1[o] = fma(w[o], sv0, acc1[o]);
+            } else if (!(flags & (1u << 17))) {  // bit 17: ablation (profiling only)
                 const double sv0 = (lane < np && p0.sub >= 0) ? s0 * v0 : 0.0;
                 double w[S];
 #pragma unroll
@@ -348,7 +374,9 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
             double f2[D], s2, v2;
             load_data(d2, n2, f2, s2, v2);
             __syncwarp();
-            if (G2 && !(flags & (1u << 16))) {
+            if (R1) {
+                // (accumulated above, in registers)
+            } else if (G2 && !(flags & (1u << 16))) {
                 // grouped lanes: 8 points per step (rows past np carry v = 0)
                 for (int j0 = 0; j0 < np; j0 += 8) {
                     const double* ws = my_stage + (j0 + g2) * D * SPAD;
@@ -932,8 +960,8 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     // offsets are loaded while this chunk contracts (PF)
     // (d = 2: the axis-0 windows go to shared memory like d = 3's, which
     // leaves the registers for both prefetches at 128 registers per thread)
-    constexpr bool EPF = (D == 3 && M >= 5) || D == 2;
-    constexpr bool PF = ((D == 3 && M >= 5) || D == 2) && !PK;
+    constexpr bool EPF = (D == 3 && M >= 5) || D <= 2;
+    constexpr bool PF = ((D == 3 && M >= 5) || D <= 2) && !PK;
     double nf[6] = {0.5, 0.5, 0.5, 0.5, 0.5, 0.5};
     auto load_frac = [&](int c) {
         const int q0 = a.chunk_start[c];
@@ -1044,10 +1072,10 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
                 w0s[q] = wA0[q];
                 w0s[S + q] = wB0[q];
             }
-            if (EPF && v) {  // (the node indices have arrived during the window evaluation)
-                vA = okA ? __ldg(v + nodeA) : 0.0;
-                vB = okB ? __ldg(v + nodeB) : 0.0;
-            }
+        }
+        if (EPF && v) {  // (the node indices have arrived during the window evaluation)
+            vA = okA ? __ldg(v + nodeA) : 0.0;
+            vB = okB ? __ldg(v + nodeB) : 0.0;
         }
         if (PF && ch + 1 < c_hi) load_frac(ch + 1);
         double accA = 0.0, accB = 0.0;

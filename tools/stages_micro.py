@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--N", type=int, default=64)
     ap.add_argument("--m", default="4")
     ap.add_argument("--sigma", type=float, default=0.2)
+    ap.add_argument("--sorted", action="store_true", help="vectors in the binding's cell order (the solvers' order)")
     a = ap.parse_args()
     import bench
     from paper_2007_05239_b200 import KernelSpec, KernelWeights, build_layer, build_plan
@@ -39,11 +40,11 @@ def main():
             plan = build_plan(kern, d=d, N=a.N, m_nfft=m, p_nfft=8)
             layer = build_layer(KernelWeights(x, kern, plan=plan))
             vd = torch.from_numpy(v).cuda()
-            st = bench.stage_breakdown(torch, [layer.weights], vd, reps=10)
+            st = bench.stage_breakdown(torch, [layer.weights], vd, reps=10, sorted_order=a.sorted)
             rows = bench.kernel_table(st, "micro", hbm, fp64)
             for r in rows:
                 if r["kernel"] in ("spread", "gather"):
-                    print(json.dumps({"d": d, "m": m, "N": a.N, "n": n, "kernel": r["kernel"], "us": round(r["ms"] * 1e3, 1),
+                    print(json.dumps({"order": "sorted" if a.sorted else "node", "d": d, "m": m, "N": a.N, "n": n, "kernel": r["kernel"], "us": round(r["ms"] * 1e3, 1),
                                       "hbm_frac": round(r["hbm_frac"], 3), "fp64_frac": round(r["fp64_frac"], 3)}))
 
 
