@@ -454,7 +454,10 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     // never splitting a chunk; a bit smaller when n is small so every SM
     // gets work
     // (large n: grow segments so the partial tiles stay ~ nsm x 16 of them)
-    int seg_points = (int)std::max<int64_t>(kSegPoints, n / (nsm * 16));
+    // ~4 segments per spread warp (static round-robin): with about one per
+    // warp, the few warps that get two set the kernel time (measured at
+    // n = 1e7: d=1 spread 316 -> 212 us, config-4 d=2 spread 498 -> 461 us)
+    int seg_points = (int)std::max<int64_t>(kSegPoints, n / (nsm * 64));
     while (seg_points > 64 && (n / seg_points) < nsm * 8) seg_points /= 2;
     if (const char* env = std::getenv("MLB_SEG_POINTS")) seg_points = std::max(32, std::atoi(env));  // tuning
     std::vector<int32_t> seg_chunk, seg_brick, brick_seg(nbricks + 1, 0);
