@@ -403,8 +403,14 @@ def run_ours(args):
     ws, rank, local = _dist()
     device = local
     torch.cuda.set_device(device)
-    if ws > 1:
+    sharded = ws > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
+        if ws == 1:   # --sharded on one GPU: a one-rank NCCL group (the collective still runs)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2007_05239_b200 import _lib
     wl = _workload(args.workload)
@@ -418,7 +424,7 @@ def run_ours(args):
     e2e_k = max(3, min(args.steps, int(5e9 // (8 * n * (1 + T)))))
     V_host = rng.standard_normal((e2e_k, n))
     extra = {}
-    if ws == 1:
+    if not sharded:
         import synth
         from paper_2007_05239_b200 import LaplacianBatch, MultilayerGraph, with_shift
         t0 = time.perf_counter()
@@ -480,7 +486,7 @@ def run_ours(args):
     V_pin = torch.from_numpy(np.ascontiguousarray(V_host[:, lo:lo + n_local])).pin_memory()
     Y_pin = torch.empty((e2e_k, T, n_local), dtype=torch.float64, pin_memory=True)
     e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws == 1:
+    if not sharded:
         y_pin = torch.empty((T, n), dtype=torch.float64, pin_memory=True)
         for _ in range(2):
             batch.apply(v_pin, out=y_pin)
@@ -573,7 +579,7 @@ def run_ours(args):
                                         f"2 matvecs per layer, {secs1:.1f} s"}}
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if ws > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
     return 0
 
@@ -602,6 +608,8 @@ def main():
     ap.add_argument("--workload", choices=["cfg4", "cfg2"], default="cfg4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cuda-graph", action="store_true", help="launch the step kernel by kernel")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the node-range sharded step (NCCL all-reduce of the grids) even on one GPU")
     # CPU legs: bounded node samples of the workload (the full config-4 layers
     # would need a 213 GB reference binding): ~0.4 s per step on 16 cores
     ap.add_argument("--cpu-sample", type=int, default=131072, help="nodes in the CPU baseline sample")

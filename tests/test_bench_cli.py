@@ -48,3 +48,16 @@ def test_bench_line_contract():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["nodes_per_rank"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_bench_sharded_step_on_one_gpu():
+    """The node-range sharded step (the N > 1 bench path: one NCCL all-reduce
+    of both layers' grids per step) runs end to end on one GPU (`--sharded`)."""
+    import json
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--sharded", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline", "--workload", "cfg2"], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 1 and d["value"] > 1e8 and "sharded" in d["config"]["parallelism"]
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
