@@ -399,3 +399,34 @@ def test_device_bind_paths_agree_and_validate():
     with pytest.raises(ConfigError, match="non-finite"):
         bind_points(plan, np.array([[0.0, np.nan]]))
     assert bind_points(plan, np.zeros((0, 2))).n == 0
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_bare_nfft_matches_naive_dft_and_oracle(d):
+    """The reference's own naive-DFT checks of nfft_adjoint / nfft_forward
+    (test_fastsum.py:48-73, there for d = 1, 2) extended to d = 3: GPU
+    transforms vs the naive sums (<= 1e-9, the reference's bar) and vs the
+    numpy oracle of the reference algorithm (<= 1e-12); adjointness."""
+    from paper_2007_05239_b200 import KernelSpec, build_plan
+    from paper_2007_05239_b200.fastsum import nfft_adjoint, nfft_forward
+    rng = np.random.default_rng(10 + d)
+    N, n = 16, 37
+    plan = build_plan(KernelSpec("gaussian", 0.2), d=d, N=N)
+    oplan = fo.OraclePlan("gaussian", 0.2, d, N, 5, p=5)
+    pts = rng.uniform(-0.5, 0.4999, size=(n, d))
+    v = rng.standard_normal(n)
+    ax = np.fft.fftfreq(N) * N
+    freqs = np.stack([m.ravel() for m in np.meshgrid(*([ax] * d), indexing="ij")], axis=1)
+    adj = nfft_adjoint(pts, v, plan)
+    naive = np.exp(-2j * np.pi * (freqs @ pts.T)) @ v
+    assert np.abs(adj.ravel() - naive).max() <= 1e-9 * np.abs(naive).max()
+    ref = fo.nfft_adjoint(oplan, pts, v)
+    assert np.abs(adj - ref).max() <= 1e-12 * np.abs(ref).max()
+    c = rng.standard_normal((N,) * d) + 1j * rng.standard_normal((N,) * d)
+    fwd = nfft_forward(c, pts, plan)
+    naive = np.exp(+2j * np.pi * (pts @ freqs.T)) @ c.ravel()
+    assert np.abs(fwd - naive).max() <= 1e-9 * np.abs(naive).max()
+    ref = fo.nfft_forward(oplan, c, pts)
+    assert np.abs(fwd - ref).max() <= 1e-12 * np.abs(ref).max()
+    lhs, rhs = np.sum(fwd * v), np.sum(c * np.conj(adj))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
