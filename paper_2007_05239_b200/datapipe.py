@@ -246,3 +246,75 @@ def sample_labels(truth, fraction, seed, omega0=1000.0):
         members = by_class[bounds[c]:bounds[c + 1]]
         ids[rng.choice(members, size=max(1, math.ceil(fraction * sizes[c])), replace=False)] = c
     return LabelData.from_class_ids(ids, m, omega0)
+
+
+# ------------------------------------------------------------ images -------
+@dataclass(frozen=True)
+class ImageStack:
+    """Vectorised images (datapipe.py:285-297): rgb (n x 3), xy (n x 2: column,
+    row), component id per pixel, (h, w) per image."""
+
+    rgb: np.ndarray
+    xy: np.ndarray
+    components: np.ndarray
+    shapes: tuple
+
+    @property
+    def n(self):
+        return self.rgb.shape[0]
+
+
+def image_to_features(images):
+    """One image or a list of 8-bit RGB images, pixels row-major (datapipe.py:300-325)."""
+    X, comps, shapes = image_features(images)
+    return ImageStack(rgb=X[:, :3], xy=X[:, 3:], components=comps, shapes=shapes)
+
+
+def load_image(path):
+    """8-bit RGB PNG -> (h, w, 3) uint8 (datapipe.py:341-352)."""
+    from PIL import Image
+    try:
+        with Image.open(path) as img:
+            if img.mode != "RGB":
+                raise FormatError(f"{path}: expected an 8-bit RGB image, got mode {img.mode!r}")
+            return np.asarray(img, dtype=np.uint8)
+    except (FileNotFoundError, FormatError):
+        raise
+    except Exception as exc:
+        raise FormatError(f"{path}: cannot decode image ({exc})") from exc
+
+
+def save_image(path, array):
+    from PIL import Image
+    a = np.asarray(array).astype(np.uint8)
+    Image.fromarray(a, mode="L" if a.ndim == 2 else "RGB").save(path)
+
+
+def image_features(images):
+    """Row-major pixel features of a list of RGB images (datapipe.py:300-325):
+    (n x 5 [r, g, b, col, row], component id per pixel, shapes)."""
+    if isinstance(images, np.ndarray):
+        images = [images]
+    if not images:
+        raise ConfigError("need at least one image")
+    feats, comps, shapes = [], [], []
+    for k, img in enumerate(images):
+        img = np.asarray(img)
+        if img.ndim != 3 or img.shape[2] != 3 or img.dtype != np.uint8:
+            raise FormatError(f"image {k}: expected 8-bit RGB of shape (h, w, 3), got {img.dtype} {img.shape}")
+        h, w = img.shape[:2]
+        rows, cols = np.divmod(np.arange(h * w), w)
+        feats.append(np.column_stack([img.reshape(-1, 3).astype(float), cols.astype(float), rows.astype(float)]))
+        comps.append(np.full(h * w, k))
+        shapes.append((h, w))
+    return np.vstack(feats), np.concatenate(comps), tuple(shapes)
+
+
+def masks_from_labels(labels, shapes):
+    """Per image (h, w) label arrays (datapipe.py:328-338)."""
+    labels = np.asarray(labels)
+    ends = np.cumsum([h * w for h, w in shapes])
+    if (ends[-1] if len(ends) else 0) != labels.shape[0]:
+        raise ConfigError(f"label vector length {labels.shape[0]} does not match shapes {shapes}")
+    starts = np.concatenate([[0], ends[:-1]])
+    return [labels[a:b].reshape(h, w) for a, b, (h, w) in zip(starts, ends, shapes)]

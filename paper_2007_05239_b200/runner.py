@@ -19,7 +19,8 @@ import numpy as np
 from . import fastsum
 from .allencahn import AllenCahnParams, LabelData, allen_cahn_solve, predict_labels
 from .csvio import load_features_csv, load_labels_csv, write_matrix_csv, write_predictions_csv
-from .datapipe import GroupingSpec, GroupSpec, feature_group, sample_labels
+from .datapipe import (GroupingSpec, GroupSpec, feature_group, image_features, load_image, masks_from_labels,
+                       sample_labels, save_image)
 from .errors import ConfigError, FormatError
 from .graphs import MultilayerGraph, build_layer, load_edge_list
 from .kernels import KernelSpec
@@ -256,57 +257,6 @@ def run_classify(cfg, seed, out_dir=".", threads=1):
     report.update(_scores(pred, truth, labels))
     report["config"] = cfg
     return _finish(out_dir, report, clock, outputs)
-
-
-# ------------------------------------------------------------ images -------
-def load_image(path):
-    """8-bit RGB PNG -> (h, w, 3) uint8 (datapipe.py:341-352)."""
-    from PIL import Image
-    try:
-        with Image.open(path) as img:
-            if img.mode != "RGB":
-                raise FormatError(f"{path}: expected an 8-bit RGB image, got mode {img.mode!r}")
-            return np.asarray(img, dtype=np.uint8)
-    except (FileNotFoundError, FormatError):
-        raise
-    except Exception as exc:
-        raise FormatError(f"{path}: cannot decode image ({exc})") from exc
-
-
-def save_image(path, array):
-    from PIL import Image
-    a = np.asarray(array).astype(np.uint8)
-    Image.fromarray(a, mode="L" if a.ndim == 2 else "RGB").save(path)
-
-
-def image_features(images):
-    """Row-major pixel features of a list of RGB images (datapipe.py:300-325):
-    (n x 5 [r, g, b, col, row], component id per pixel, shapes)."""
-    if isinstance(images, np.ndarray):
-        images = [images]
-    if not images:
-        raise ConfigError("need at least one image")
-    feats, comps, shapes = [], [], []
-    for k, img in enumerate(images):
-        img = np.asarray(img)
-        if img.ndim != 3 or img.shape[2] != 3 or img.dtype != np.uint8:
-            raise FormatError(f"image {k}: expected 8-bit RGB of shape (h, w, 3), got {img.dtype} {img.shape}")
-        h, w = img.shape[:2]
-        rows, cols = np.divmod(np.arange(h * w), w)
-        feats.append(np.column_stack([img.reshape(-1, 3).astype(float), cols.astype(float), rows.astype(float)]))
-        comps.append(np.full(h * w, k))
-        shapes.append((h, w))
-    return np.vstack(feats), np.concatenate(comps), tuple(shapes)
-
-
-def masks_from_labels(labels, shapes):
-    """Per image (h, w) label arrays (datapipe.py:328-338)."""
-    labels = np.asarray(labels)
-    ends = np.cumsum([h * w for h, w in shapes])
-    if (ends[-1] if len(ends) else 0) != labels.shape[0]:
-        raise ConfigError(f"label vector length {labels.shape[0]} does not match shapes {shapes}")
-    starts = np.concatenate([[0], ends[:-1]])
-    return [labels[a:b].reshape(h, w) for a, b, (h, w) in zip(starts, ends, shapes)]
 
 
 def run_segment_image(cfg, seed, out_dir=".", threads=1):
