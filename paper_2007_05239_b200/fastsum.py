@@ -186,6 +186,49 @@ def _embed_axis(arr, axis, N, n_grid, split_nyquist):
     return np.moveaxis(out, 0, axis)
 
 
+def _full_fused(coeffs, d, N, n_grid, m, b):
+    """fused_weights of the reference (fastsum.py:282-294): b-hat (real part)
+    embedded in ng^d with the Nyquist value halved onto +-N/2, times the
+    squared KB deconvolution on |k| <= N/2 (0 outside) per axis, times ng^d;
+    the rfftn half of the last axis."""
+    full = coeffs.real
+    for ax in range(d):
+        full = _embed_axis(full, ax, N, n_grid, True)
+    fq = np.fft.fftfreq(n_grid) * n_grid
+    band = np.abs(fq) <= N // 2
+    wfull = np.zeros(n_grid)
+    wfull[band] = _kb_deconv(fq[band], n_grid, m, b) ** 2
+    for ax in range(d):
+        sh = [1] * d
+        sh[ax] = n_grid
+        full = full * wfull.reshape(sh)
+    full = full * float(n_grid) ** d
+    return np.ascontiguousarray(full[..., : n_grid // 2 + 1])
+
+
+def _band_weights(coeffs, d, N, n_grid, m, b):
+    """The same values as fused_weights on the band only: k = -N/2..N/2 on the
+    first d-1 axes, k = 0..N/2 on the last, with the identical per-element
+    operation order (Nyquist halving -- exact --, the axis-0, 1, 2 deconvolution
+    factors in order, then ng^d): the device tables without the ng^d arrays."""
+    h = N // 2
+    kf = np.arange(-h, h + 1)
+    kh = np.arange(0, h + 1)
+    c = coeffs.real
+    ks = [kf] * (d - 1) + [kh]
+    vals = c[np.ix_(*[np.mod(k, N) for k in ks])]
+    for ax, k in enumerate(ks):   # embed: the Nyquist entries carry 0.5 (power of two: exact in any order)
+        sh = [1] * d
+        sh[ax] = len(k)
+        vals = vals * np.where(np.abs(k) == h, 0.5, 1.0).reshape(sh)
+    w = _kb_deconv(np.arange(-h, h + 1).astype(float), n_grid, m, b) ** 2     # indexed by k + h
+    for ax, k in enumerate(ks):
+        sh = [1] * d
+        sh[ax] = len(k)
+        vals = vals * w[k + h].reshape(sh)
+    return vals * float(n_grid) ** d
+
+
 @dataclass
 class FastsumPlan:
     """Plan for fast sums of one kernel in one dimension (fastsum.py:183-216).
@@ -208,11 +251,20 @@ class FastsumPlan:
     window_shape: float
     coeffs: np.ndarray
     deconv_axis: np.ndarray = field(repr=False)
-    fused_weights: np.ndarray = field(repr=False)
+    _fused: np.ndarray = field(default=None, repr=False, compare=False)
     K0: float = 1.0
     win_coef: np.ndarray = field(default=None, repr=False)
     win_deg: int = 14
     _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def fused_weights(self):
+        """rfftn-layout fused weights (ng,)*(d-1) x (ng/2+1) (fastsum.py:282-294),
+        built on first access: the device path only needs the |k| <= N/2
+        band (_band_weights), so plan construction skips the ng^d arrays."""
+        if self._fused is None:
+            self._fused = _full_fused(self.coeffs, self.d, self.N, self.n_grid, self.m_nfft, self.window_shape)
+        return self._fused
 
     def describe(self):
         return {"kernel": self.kernel.family, "sigma": self.kernel.sigma, "d": self.d, "N": self.N,
@@ -239,14 +291,17 @@ class FastsumPlan:
         kfull = np.arange(-N // 2, N // 2 + 1)
         khalf = np.arange(0, N // 2 + 1)
         idx = [np.mod(kfull, ng)] * (d - 1) + [khalf]
-        band = self.fused_weights[np.ix_(*idx)] / float(ng) ** d
+        Fb = _band_weights(self.coeffs, d, N, ng, m, self.window_shape)   # K^(d-1) x Kh, k_last >= 0
+        band = Fb / float(ng) ** d
         u = np.arange(ulo, ulo + L)
         ph = np.mod(np.outer(u, kfull), ng).astype(float) * (2.0 * math.pi / ng)
         tw = np.empty((L, N + 1, 2))
         tw[..., 0] = np.cos(ph)
         tw[..., 1] = -np.sin(ph)
-        idx_full = [np.mod(kfull, ng)] * d
-        Ffull = self.fused_weights_full()[np.ix_(*idx_full)] / float(ng) ** d   # K^d band
+        # the full K^d band: negative last-axis frequencies by the reflection
+        # F(k', -k_last) = F(-k', k_last) of fused_weights_full (F is even)
+        Fneg = Fb[..., 1:][tuple([slice(None, None, -1)] * (d - 1) + [slice(None, None, -1)])]
+        Ffull = np.concatenate([Fneg, Fb], axis=-1) / float(ng) ** d
         D = np.arange(-(L - 1), L)
         A = np.exp(2j * math.pi * np.outer(kfull, D) / ng)                       # K x (2L-1)
         conv = None
@@ -347,25 +402,12 @@ def build_plan(kernel, d, N=DEFAULT_N, m_nfft=DEFAULT_M, eps_b=DEFAULT_EPS_B, p_
     leak = np.max(np.abs(coeffs.imag)) if coeffs.size else 0.0
     if leak > 1e-12 * max(1.0, np.max(np.abs(coeffs.real))):
         raise NumericalError("kernel coefficients are not real; kernel not even?")
-    full = coeffs.real
-    for ax in range(d):
-        full = _embed_axis(full, ax, N, n_grid, True)
-    fq = np.fft.fftfreq(n_grid) * n_grid
-    band = np.abs(fq) <= N // 2
-    wfull = np.zeros(n_grid)
-    wfull[band] = _kb_deconv(fq[band], n_grid, m_nfft, b) ** 2
-    for ax in range(d):
-        sh = [1] * d
-        sh[ax] = n_grid
-        full = full * wfull.reshape(sh)
-    full = full * float(n_grid) ** d
-    fused = np.ascontiguousarray(full[..., : n_grid // 2 + 1])
     win_coef, win_deg = (None, 14)
     if m_nfft <= 6:
         win_coef, win_deg = window_polynomials(m_nfft, b)
     return FastsumPlan(kernel=kernel, d=d, N=N, m_nfft=m_nfft, eps_b=eps_b, p_nfft=p_nfft, rho=rho,
                        n_grid=n_grid, ball_scale=ball_scale, kernel_eff=kernel_eff, window="kaiser-bessel",
-                       window_shape=b, coeffs=coeffs, deconv_axis=deconv_axis, fused_weights=fused,
+                       window_shape=b, coeffs=coeffs, deconv_axis=deconv_axis,
                        K0=kernel.value_at_zero(), win_coef=win_coef, win_deg=win_deg)
 
 
