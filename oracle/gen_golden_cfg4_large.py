@@ -40,9 +40,11 @@ class ParallelWeights:
         self.ref, self.li, self.n = ref, li, ref.n
 
     def matvec(self, v):
-        self.ref.S["v"][:] = np.asarray(v, dtype=float)
-        self.ref._apply(self.li, False, "degrees")   # gather - K0 v  =  W v
-        return self.ref.S["deg"][self.li].copy()
+        v = np.asarray(v, dtype=float)
+        self.ref.S["v"][:] = v
+        self.ref._apply(self.li, False, "degrees")   # the "degrees" mode returns gather - K0 (for v = 1)
+        K0 = self.ref.S["layers"][self.li][0].K0
+        return self.ref.S["deg"][self.li] + K0 - K0 * v   # W v = gather - K0 v (fastsum.py:497)
 
     def materialize(self):
         raise NotImplementedError
