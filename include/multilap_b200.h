@@ -128,8 +128,9 @@ int mlb_binding_destroy(mlb_binding* b);
 int64_t mlb_binding_n(const mlb_binding* b);
 /* sorted position -> original node index (int32, host out, n entries) */
 int mlb_binding_perm(const mlb_binding* b, int32_t* perm_host);
-/* binding statistics: [n, nchunks, nsegments, nbricks, tile_cells, grid_cells] */
-int mlb_binding_stats(const mlb_binding* b, int64_t* out6);
+/* binding statistics: [n, nchunks, nsegments, nbricks, tile_cells, grid_cells,
+   band_ctas (d = 2 banded spread CTAs, 0 = full tiles), band_tile_cells] */
+int mlb_binding_stats(const mlb_binding* b, int64_t* out8);
 
 /* Store D^-1/2 (graphs.py:159-165) for the fused Laplacian; node order, device. */
 int mlb_binding_set_isd(mlb_binding* b, const double* isd_dev, void* stream);

@@ -253,6 +253,9 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->merge_pairs);
     dev_free(b->blocks);
     dev_free(b->seg_sub);
+    dev_free(b->cta_seg);
+    dev_free(b->cta_row0);
+    dev_free(b->row_cta);
     dev_free(b->seg_brick);
     dev_free(b->brick_seg);
     dev_free(b->brick_first);
@@ -485,6 +488,55 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     }
     seg_sub[nseg] = (int)(sub_desc.size() / 2);
     for (int br = 0; br < nbricks; ++br) brick_seg[br + 1] += brick_seg[br];
+    // d = 2 banded spread (large layers): CTA c takes the contiguous segment
+    // range [cta_seg[c], cta_seg[c+1]); cells are sorted row-major, so its
+    // points' stencils reach only the sub-box rows [row0, rmax + S) and its
+    // warps' shared-memory tiles hold just that band (config 4: ~12 of 55
+    // rows), which lets 12 instead of 6 warps run per SM.  The band sums
+    // meet in launch_reduce (band_sum_kernel), in CTA order.
+    std::vector<int32_t> cta_seg, cta_row0, row_cta;
+    int ncta_band = 0, band_tile = 0;
+    {
+        bool banded = d == 2 && n >= (1 << 20);
+        if (const char* env = std::getenv("MLB_D2_BANDED")) banded = d == 2 && env[0] == '1';  // tests / A/B
+        if (banded && nseg > 0) {
+            const int S = 2 * g.m + 1;
+            const int nc = std::min(nsm * 3, std::max(1, nseg / kBandWarps));
+            std::vector<int32_t> cs(nc + 1), r0(nc), r1(nc);
+            int rows = 0;
+            for (int c = 0; c <= nc; ++c) cs[c] = (int32_t)((int64_t)nseg * c / nc);
+            for (int c = 0; c < nc; ++c) {
+                int lo = 1 << 30, hi = -1;
+                for (int ch = seg_chunk[cs[c]]; ch < seg_chunk[cs[c + 1]]; ++ch) {
+                    lo = std::min(lo, chunk_cell[ch] / TL);
+                    hi = std::max(hi, chunk_cell[ch] / TL);
+                }
+                r0[c] = lo;
+                r1[c] = hi + S;   // one past the band's last row
+                rows = std::max(rows, hi - lo + S);
+            }
+            if ((int64_t)rows * 2 <= TL) {   // only where the bands are much smaller than the sub-box
+                ncta_band = nc;
+                band_tile = rows * TL;
+                cta_seg = cs;
+                cta_row0 = r0;
+                for (int c = 0; c < nc; ++c)
+                    for (int j = seg_sub[cs[c]]; j < seg_sub[cs[c + 1]]; ++j) sub_desc[2 * j + 1] -= r0[c] * TL;
+                // rows covered by CTA c: [r0[c], r1[c]); both bounds are non-decreasing in c
+                row_cta.assign(2 * (size_t)g.L, 0);
+                int first = 0, last = -1;
+                for (int u = 0; u < g.L; ++u) {
+                    while (first < nc && r1[first] <= u) ++first;
+                    while (last + 1 < nc && r0[last + 1] <= u) ++last;
+                    row_cta[2 * u] = first;
+                    row_cta[2 * u + 1] = last;   // empty when last < first
+                }
+            }
+            if (std::getenv("MLB_DEBUG"))
+                fprintf(stderr, "[mlb] d2 bands: %d CTAs, band rows %d of %d (%s)\n", nc, rows, TL,
+                        ncta_band ? "banded" : "full tiles");
+        }
+    }
     // d = 3: brick tile slot per brick (set with the cell blocks below), -1 if empty
     std::vector<int32_t> brick_first(nbricks, -1);
     // d = 3: cell blocks, CTA items and per-warp sub-chunk streams
@@ -690,12 +742,20 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
         const int S = 2 * g.m + 1;
         if (rc == MLB_OK) rc = dev_upload<double>(&b->blocks, nullptr, (size_t)b->nblk * S * S * S);
     }
+    if (ncta_band > 0) {
+        b->ncta_band = ncta_band;
+        b->band_tile = band_tile;
+        if (rc == MLB_OK) rc = dev_upload(&b->cta_seg, cta_seg.data(), cta_seg.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->cta_row0, cta_row0.data(), cta_row0.size());
+        if (rc == MLB_OK) rc = dev_upload(&b->row_cta, row_cta.data(), row_cta.size());
+    }
     if (rc == MLB_OK) rc = dev_upload<int>(&b->work, nullptr, 1);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->isd, nullptr, (size_t)n);
     // d <= 2: one partial grid per spread CTA (<= 2 per SM); d = 3: one per segment
     b->spread_parts_max = nsm * 2;
     const size_t nparts = (d <= 2) ? (size_t)std::max(nseg, b->spread_parts_max) : (size_t)std::max(1, b->nactive);  // d = 3: brick tiles
-    if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, nparts * b->tile_cells);
+    const size_t partial_elems = std::max(nparts * (size_t)b->tile_cells, (size_t)ncta_band * band_tile);
+    if (rc == MLB_OK) rc = dev_upload<double>(&b->partial, nullptr, partial_elems);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_a, nullptr, (size_t)b->stage_elems);
@@ -726,6 +786,8 @@ int mlb_binding_stats(const mlb_binding* b, int64_t* o) {
     o[3] = b->nbricks;
     o[4] = b->tile_cells;
     o[5] = b->grid_cells;
+    o[6] = b->ncta_band;
+    o[7] = b->band_tile;
     return MLB_OK;
 }
 

@@ -116,6 +116,9 @@ struct FsArgs {
     // into this zeroed sub-box grid with red.global.add.f64 (no merge / R2;
     // not bitwise reproducible); nullptr: the deterministic blocks
     double* agrid;
+    // d = 2 banded spread: CTA c owns segments [cta_seg[c], cta_seg[c+1])
+    // (nullptr: warps take segments gw, gw + W, ... over the whole list)
+    const int32_t* cta_seg;
 };
 
 // sub-box index of element (o01 = o0*S + o1, o2) of d = 3 cell block `blk`
@@ -147,9 +150,9 @@ struct SubPos {
     int end;   // one past the segment's last sub-chunk
 };
 
-__device__ __forceinline__ SubPos sub_first(const FsArgs& a, int seg) {
+__device__ __forceinline__ SubPos sub_first(const FsArgs& a, int seg, int seg_end) {
     SubPos p;
-    if (seg >= a.nseg) {
+    if (seg >= seg_end) {
         p.sub = -1;
         p.seg = seg;
         p.end = 0;
@@ -161,13 +164,13 @@ __device__ __forceinline__ SubPos sub_first(const FsArgs& a, int seg) {
     return p;
 }
 
-__device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps) {
+__device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps, int seg_end) {
     if (p.sub < 0) return p;
     if (p.sub + 1 < p.end) {
         p.sub += 1;
         return p;
     }
-    return sub_first(a, p.seg + nwarps);
+    return sub_first(a, p.seg + nwarps, seg_end);
 }
 
 template <int D, int M, bool PERSIST, bool GROUPED = false>
@@ -195,8 +198,11 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     const bool active = lane < C::P0 * C::P1 * C::P2;
     const int TL2 = (D == 3) ? TL * TL : 1;
     const int TL1 = (D >= 2) ? TL : 1;
-    const int gwarp = blockIdx.x * nw + warp;
-    const int nwarps = gridDim.x * nw;
+    // segment walk: banded CTAs own a contiguous range, else global round-robin
+    const bool banded = a.cta_seg != nullptr;
+    const int gwarp = banded ? __ldg(a.cta_seg + blockIdx.x) + warp : blockIdx.x * nw + warp;
+    const int nwarps = banded ? nw : gridDim.x * nw;
+    const int seg_end = banded ? __ldg(a.cta_seg + blockIdx.x + 1) : a.nseg;
     const bool sorted = (flags & MLB_SORTED) != 0;
     const bool use_isd = (flags & MLB_USE_ISD) != 0;
 
@@ -296,10 +302,10 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
         };
 
         // pipeline: p0 (compute), p1 (data in flight), p2 (perm in flight), p3 (descriptor in flight)
-        SubPos p0 = sub_first(a, gwarp);
-        SubPos p1 = sub_next(a, p0, nwarps);
-        SubPos p2 = sub_next(a, p1, nwarps);
-        SubPos p3 = sub_next(a, p2, nwarps);
+        SubPos p0 = sub_first(a, gwarp, seg_end);
+        SubPos p1 = sub_next(a, p0, nwarps, seg_end);
+        SubPos p2 = sub_next(a, p1, nwarps, seg_end);
+        SubPos p3 = sub_next(a, p2, nwarps, seg_end);
         int2 d0 = (p0.sub >= 0) ? __ldg(a.sub_desc + p0.sub) : make_int2(0, 0);
         int2 d1 = (p1.sub >= 0) ? __ldg(a.sub_desc + p1.sub) : make_int2(0, 0);
         int2 d2 = (p2.sub >= 0) ? __ldg(a.sub_desc + p2.sub) : make_int2(0, 0);
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
                 }
             }
             // advance the pipeline (loads of later sub-chunks overlap the accumulation)
-            SubPos p4 = sub_next(a, p3, nwarps);
+            SubPos p4 = sub_next(a, p3, nwarps, seg_end);
             const int2 d4 = (p4.sub >= 0) ? __ldg(a.sub_desc + p4.sub) : make_int2(0, 0);
             const int n3 = node_of(d3);
             double f2[D], s2, v2;
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
         }
         flush(cur);
         __syncwarp();
-        if (!PERSIST && seg_cur < a.nseg && !(flags & (1u << 19))) {
+        if (!PERSIST && seg_cur < seg_end && !(flags & (1u << 19))) {
             double* out = a.partial + (size_t)seg_cur * tile;
             for (int i = lane; i < tile; i += 32) {
                 out[i] = (pass ? out[i] : 0.0) + my_tile[i];
@@ -808,6 +814,28 @@ __global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, 
             s += a3;
         }
         for (; j < nparts; j += 32) s += __ldcg(partial + (size_t)j * cells + cell);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    pdl_launch();
+    if (slice == 0 && cell < cells) po_store(grid, cell, s);
+    if (grid.n > 1) __threadfence_system();  // peer stores ordered before the exchange barrier
+}
+
+// d = 2 banded spread: grid[u0, u1] = sum over the CTAs whose band covers
+// row u0 (a contiguous CTA range, row_cta) of their band tiles.  Same
+// 8 cells x 32 slices layout and fixed shuffle tree as grid_sum_kernel.
+__global__ void band_sum_kernel(const double* __restrict__ partial, int band_tile, int TL,
+                                const int32_t* __restrict__ cta_row0, const int2* __restrict__ row_cta, int cells,
+                                PeerOut grid) {
+    const int slice = threadIdx.x & 31;
+    const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
+    double s = 0.0;
+    pdl_wait();  // the band tiles come from the spread
+    if (cell < cells) {
+        const int u0 = cell / TL, u1 = cell - u0 * TL;
+        const int2 rc = __ldg(row_cta + u0);
+        for (int c = rc.x + slice; c <= rc.y; c += 32)
+            s += __ldcg(partial + (size_t)c * band_tile + (size_t)(u0 - __ldg(cta_row0 + c)) * TL + u1);
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     pdl_launch();
@@ -1187,6 +1215,7 @@ static FsArgs make_args(mlb_binding* b) {
     a.merge_pairs = b->merge_pairs;
     a.blocks = b->blocks;
     a.agrid = nullptr;
+    a.cta_seg = nullptr;
     a.ggrp = reinterpret_cast<const int2*>(b->ggrp);
     a.gslot = b->gslot;
     a.ngrp = b->ngrp;
@@ -1214,10 +1243,16 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
     const int nsm = device_sms();
     (void)nsm;
     if constexpr (D <= 2) {
-        // persistent CTAs of 8 warps, one partial grid per CTA
-        int nw = 8;
-        while (nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
-        const size_t smem = spread_smem<D, M>(nw, b->tile_cells);
+        // persistent CTAs of 8 warps, one partial grid per CTA; banded d = 2:
+        // kBandWarps-warp CTAs over their own segment ranges, one band tile each
+        const bool banded = D == 2 && b->ncta_band > 0;
+        if (banded) {
+            a.cta_seg = b->cta_seg;
+            a.tile_cells = b->band_tile;
+        }
+        int nw = banded ? kBandWarps : 8;
+        while (!banded && nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
+        const size_t smem = spread_smem<D, M>(nw, a.tile_cells);
         if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
         // grouped d = 2 lanes pay off on large layers (config 4: 622 -> 498
         // us); at config-2 size the plain lane blocks leave more room for
@@ -1226,7 +1261,7 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
         if (const char* env = std::getenv("MLB_D2_GROUPED")) grouped = D == 2 && env[0] == '1';  // tests / tuning
         auto kern = grouped ? spread_kernel<D, M, true, true> : spread_kernel<D, M, true, false>;
         MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int blocks = std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);
+        int blocks = banded ? b->ncta_band : std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);
         if (blocks < 1) blocks = 1;
         b->spread_parts = blocks;
         MLB_CUDA_TRY(launch_k(kern, dim3(blocks), dim3(nw * 32), smem, st, a, b->plan->wc, v, flags, b->work));
@@ -1317,6 +1352,16 @@ int launch_reduce(mlb_binding* b, double* grid_local, cudaStream_t st, const Pee
         grid.n = 1;
     }
     const Geom& G = b->plan->g;
+    if (G.d == 2 && b->ncta_band > 0) {
+        // the banded spread left one band tile per CTA
+        const int cells = (int)b->grid_cells;
+        MLB_CUDA_TRY(launch_k(band_sum_kernel, dim3((cells + 7) / 8), dim3(256), 0, st, (const double*)b->partial,
+                              b->band_tile, G.TL, (const int32_t*)b->cta_row0,
+                              reinterpret_cast<const int2*>(b->row_cta), cells, grid));
+        note_launches(1);
+        MLB_CUDA_TRY(cudaGetLastError());
+        return MLB_OK;
+    }
     if (G.d <= 2) {
         // the spread left one partial grid per CTA
         const int cells = (int)b->grid_cells;

@@ -71,6 +71,7 @@ constexpr int kMaxM = 6;          // window cutoffs supported by the kernels
 constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
 constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
 constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA
+constexpr int kBandWarps = 4;    // warps per banded d = 2 spread CTA
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
@@ -165,6 +166,15 @@ struct mlb_binding {
     // cell blocks into atomic_target with red.global.add (no merge / R2)
     int spread_atomic = 0;
     double* atomic_target = nullptr;
+    // d = 2 banded spread (large layers): CTA c owns segments
+    // [cta_seg[c], cta_seg[c+1]) and a tile of the sub-box rows
+    // [cta_row0[c], cta_row0[c] + band_tile / TL); sub_desc cells are
+    // band-relative; row_cta[u0] = {first, last} CTA whose band covers row u0
+    int ncta_band = 0;               // 0: not banded
+    int band_tile = 0;               // cells per band tile (rows x TL)
+    int32_t* cta_seg = nullptr;      // ncta_band + 1
+    int32_t* cta_row0 = nullptr;     // ncta_band
+    int32_t* row_cta = nullptr;      // 2 x L
 };
 
 namespace mlb {

@@ -25,6 +25,7 @@ is verified with gloo at world_size 2 without GPUs.
 
 import ctypes
 import math
+import os
 
 import numpy as np
 
@@ -434,14 +435,46 @@ class ShardedKernelGraph:
         if self.comm is not None:   # (a world-size-1 group still runs the collective)
             self.comm.all_reduce_sum(self.grids)
 
+    def _layer_streams(self):
+        """One side stream per layer after the first (the first runs on the
+        caller's stream): the layers' kernels overlap, as in LaplacianBatch."""
+        torch = _torch()
+        if getattr(self, "_side", None) is None:
+            self._side = [torch.cuda.Stream(self.dev) for _ in range(self.T - 1)]
+            self._fork_ev = torch.cuda.Event()
+            self._join_ev = [torch.cuda.Event() for _ in range(self.T - 1)]
+        return self._side
+
+    def _per_layer(self, fn):
+        """fn(t, stream_ptr) for every layer, layer t > 0 on side stream t-1,
+        forked from and joined back into the current stream."""
+        torch = _torch()
+        if self.T == 1 or os.environ.get("MLB_SHARD_ONE_STREAM") == "1":
+            sp = _lib.stream_ptr()
+            for t in range(self.T):
+                fn(t, sp)
+            return
+        side = self._layer_streams()
+        main = torch.cuda.current_stream(self.dev)
+        self._fork_ev.record(main)
+        for t in range(1, self.T):
+            s = side[t - 1]
+            s.wait_event(self._fork_ev)
+            fn(t, s.cuda_stream)
+            self._join_ev[t - 1].record(s)
+        fn(0, main.cuda_stream)
+        for ev in self._join_ev:
+            main.wait_event(ev)
+
     def spread_local(self, v, flags):
         """Every layer's spread of this rank's nodes into self.grids."""
         lib = _lib.lib()
-        sp = _lib.stream_ptr()
         spread_flags = int(flags) & (_lib.MLB_USE_ISD | _lib.MLB_SORTED)
-        for t, w in enumerate(self.weights):
-            _lib.check(lib.mlb_spread(w._bindings[0].ptr, _lib.ptr(v), _lib.ptr(self._grid(self.grids, t)),
-                                      spread_flags, sp))
+
+        def spread(t, sp):
+            _lib.check(lib.mlb_spread(self.weights[t]._bindings[0].ptr, _lib.ptr(v),
+                                      _lib.ptr(self._grid(self.grids, t)), spread_flags, sp))
+        self._per_layer(spread)
 
     def _step(self, v, ys, coef, flags):
         """ys[t] (=|+=) coef[t] combination for every layer; ONE collective."""
@@ -452,14 +485,15 @@ class ShardedKernelGraph:
     def finish(self, v, ys, coef, flags):
         """Convolve the summed grids and gather this rank's nodes (fused epilogue)."""
         lib = _lib.lib()
-        sp = _lib.stream_ptr()
-        for t, w in enumerate(self.weights):
-            b = w._bindings[0].ptr
+
+        def fin(t, sp):
+            b = self.weights[t]._bindings[0].ptr
             g_in, g_out = self._grid(self.grids, t), self._grid(self.conv, t)
             _lib.check(lib.mlb_convolve(b, _lib.ptr(g_in), _lib.ptr(g_out), sp))
             a, be, ga = coef[t]
             _lib.check(lib.mlb_gather_apply(b, _lib.ptr(g_out), _lib.ptr(v), _lib.ptr(ys[t]), float(a), float(be),
                                             float(ga), int(flags), sp))
+        self._per_layer(fin)
         return ys
 
     def build(self):
@@ -530,6 +564,60 @@ class ShardedKernelGraph:
     def weighted(self, v, ys):
         """ys[t] = D^-1/2 W D^-1/2 v (the apply_one_minus_L1 term, powermean.py:75-76)."""
         return self._step(v, ys, [(0.0, 1.0, -k0) for k0 in self.K0], _lib.MLB_USE_ISD)
+
+    def lsym_many(self, V, out=None):
+        """(k, T, n_local): `lsym` of k host vectors (rows of V, this rank's
+        slices), streamed like LaplacianBatch.apply_many: vector i+1's H2D and
+        vector i-1's D2H run on copy streams while vector i's sharded step
+        (spreads, the all-reduce, convolutions, gathers) runs on the current
+        stream, with two device buffer sets.  V: pinned contiguous (k,
+        n_local) float64 tensor; out: optional pinned (k, T, n_local).
+        Returns after the last result has landed in host memory."""
+        torch = _torch()
+        if not (torch.is_tensor(V) and V.is_pinned() and V.dtype == torch.float64 and V.is_contiguous()
+                and V.dim() == 2 and V.shape[1] == self.n_local):
+            raise ConfigError("V must be a contiguous pinned float64 (k, n_local) tensor")
+        k, T = int(V.shape[0]), self.T
+        if out is None:
+            out = torch.empty((k, T, self.n_local), dtype=torch.float64, pin_memory=True)
+        elif not (torch.is_tensor(out) and out.is_pinned() and out.dtype == torch.float64 and out.is_contiguous()
+                  and tuple(out.shape) == (k, T, self.n_local)):
+            raise ConfigError("out must be a contiguous pinned float64 tensor of shape (k, T, n_local)")
+        if getattr(self, "_many", None) is None:
+            self._many = (torch.cuda.Stream(self.dev), torch.cuda.Stream(self.dev),
+                          [torch.empty(self.n_local, dtype=torch.float64, device=self.dev) for _ in range(2)],
+                          [[torch.empty(self.n_local, dtype=torch.float64, device=self.dev) for _ in range(T)]
+                           for _ in range(2)])
+        cin, cout, vb, yb = self._many
+        main = torch.cuda.current_stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(main)
+        cin.wait_event(start)
+        cout.wait_event(start)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        for i in range(k):
+            b = i & 1
+            if i >= 2:          # vb[b] is free once vector i-2's step has read it
+                cin.wait_event(ev_done[b])
+            with torch.cuda.stream(cin):
+                vb[b].copy_(V[i], non_blocking=True)
+            ev_in[b].record(cin)
+            main.wait_event(ev_in[b])
+            if i >= 2:          # yb[b] is free once vector i-2's results are copied out
+                main.wait_event(ev_out[b])
+            self.lsym(vb[b], yb[b])
+            ev_done[b].record(main)
+            cout.wait_event(ev_done[b])
+            with torch.cuda.stream(cout):
+                for t in range(T):
+                    out[i, t].copy_(yb[b][t], non_blocking=True)
+            ev_out[b].record(cout)
+        main.wait_stream(cin)
+        main.wait_stream(cout)
+        main.synchronize()
+        return out
 
 
 def shard_feature_groups(X, groups, rank, world, eps_b=None):

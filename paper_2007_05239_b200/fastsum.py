@@ -468,9 +468,10 @@ class PointBinding:
         self.ptr = out
 
     def stats(self):
-        o = (C.c_int64 * 6)()
+        o = (C.c_int64 * 8)()
         _lib.check(_lib.load().mlb_binding_stats(self.ptr, o))
-        return dict(zip(("n", "chunks", "segments", "bricks", "tile_cells", "grid_cells"), list(o)))
+        return dict(zip(("n", "chunks", "segments", "bricks", "tile_cells", "grid_cells", "band_ctas",
+                         "band_tile_cells"), list(o)))
 
     def sorted_perm(self):
         out = np.empty(self.n, dtype=np.int32)

@@ -105,6 +105,56 @@ def test_stages_match_oracle(d, N, m, sigma):
     assert rel(y.cpu().numpy(), fo.gather(ob, conv_full.ravel())) < 1e-13
 
 
+@pytest.mark.parametrize("grouped", ["1", "0"])
+@pytest.mark.parametrize("layout", ["square", "blobs"])
+def test_banded_d2_spread_matches_oracle(grouped, layout):
+    """The banded d = 2 spread (CTAs over contiguous cell ranges, band tiles,
+    band_sum_kernel; default for n >= 2^20) forced on a 60k-point layer:
+    spread grid vs the oracle, the whole fastsum vs the full-tile path, and
+    repeated spreads bitwise identical."""
+    import os
+
+    import torch
+    from paper_2007_05239_b200 import KernelSpec, bind_points, build_plan
+    from paper_2007_05239_b200 import _lib
+    from paper_2007_05239_b200.fastsum import fastsum_apply
+    rng = np.random.default_rng(77)
+    n = 60_000
+    if layout == "square":   # image coordinates: every cell evenly filled
+        pts = rng.uniform(-0.17, 0.17, size=(n, 2))
+    else:                    # clustered: bands of very different widths
+        c = rng.uniform(-0.15, 0.15, size=(6, 2))
+        pts = np.clip(c[rng.integers(0, 6, n)] + 0.02 * rng.standard_normal((n, 2)), -0.2, 0.2)
+    v = rng.standard_normal(n)
+    plan = build_plan(KernelSpec("gaussian", 0.1), d=2, N=64, m_nfft=5, p_nfft=8)
+    os.environ["MLB_D2_GROUPED"] = grouped
+    os.environ["MLB_D2_BANDED"] = "1"
+    try:
+        b = bind_points(plan, pts)
+        assert b.stats()["band_ctas"] > 0
+        L, ulo = b._plan_handle.L, b._plan_handle.ulo
+        lib = _lib.lib()
+        vd = torch.from_numpy(v).cuda()
+        grids = []
+        for _ in range(2):
+            g = torch.zeros(L * L, dtype=torch.float64, device="cuda")
+            _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(vd), _lib.ptr(g), 0, _lib.stream_ptr()))
+            grids.append(g.cpu().numpy())
+        y_band = fastsum_apply(pts, v, plan, binding=b)
+        os.environ["MLB_D2_BANDED"] = "0"
+        b0 = bind_points(plan, pts)
+        assert b0.stats()["band_ctas"] == 0
+        y_full = fastsum_apply(pts, v, plan, binding=b0)
+    finally:
+        del os.environ["MLB_D2_GROUPED"], os.environ["MLB_D2_BANDED"]
+    assert np.array_equal(grids[0], grids[1])
+    op = fo.OraclePlan("gaussian", 0.1, 2, 64, 5, p=8)
+    full = fo.spread(fo.bind(op, pts), v).reshape(op.ng, op.ng)
+    idx = np.mod(np.arange(ulo, ulo + L), op.ng)
+    assert rel(grids[0].reshape(L, L), full[np.ix_(idx, idx)]) < 1e-13
+    assert rel(y_band, y_full) < 1e-14
+
+
 def test_laplacian_matches_reference_golden():
     from paper_2007_05239_b200 import KernelSpec, build_plan
     from paper_2007_05239_b200.graphs import KernelWeights, apply_sym_laplacian, build_layer, with_shift

@@ -62,6 +62,14 @@ def test_sharded_graph_nccl_world1_equals_unsharded():
         ref = LaplacianBatch(MultilayerGraph(tuple(with_shift(lay, delta) for lay in G.layers))).apply_dev(v)
         for t in range(len(ys)):
             assert torch.equal(ys[t], ref[t]), t
+        # the streamed host-in / host-out form: every vector's results equal
+        # the per-vector step bitwise
+        V = torch.from_numpy(np.random.default_rng(6).standard_normal((5, wl.n))).pin_memory()
+        Y = sg.lsym_many(V)
+        for i in range(5):
+            sg.lsym(V[i].cuda(), ys)
+            for t in range(len(ys)):
+                assert torch.equal(Y[i, t], ys[t].cpu()), (i, t)
     finally:
         dist.destroy_process_group()
 
