@@ -361,7 +361,7 @@ def run_reference(args):
                                    "processes (point chunks, fixed-order grid sum, FFT on all cores)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_OUT, flush=True)
     return 0
 
 
@@ -472,9 +472,10 @@ def run_ours(args):
 
         def step():
             sg.lsym(v, ys)
-        parallelism = (f"node-range sharded x{ws}: rank r owns nodes [r n/{ws}, (r+1) n/{ws}) of every layer; one "
-                       "NCCL all-reduce of both layers' sub-box grids per step")
-        streams = "one stream; spread (both layers) -> one all-reduce -> convolve + fused gather per layer"
+        parallelism = (f"node-range sharded x{ws}: rank r owns nodes [r n/{ws}, (r+1) n/{ws}) of every layer; per "
+                       "layer one NCCL all-reduce of its sub-box grid per step")
+        streams = ("one stream per layer (the d=3 layer at high priority, the cheap layer issued first): spread -> "
+                   "NCCL all-reduce of the layer's grid -> convolve -> fused gather")
 
     # the e2e leg's pinned host buffers are allocated at setup: a freshly
     # pinned buffer transfers 2-3x slower for a while on the pool's boxes
@@ -588,7 +589,7 @@ def run_ours(args):
                               "sample": f"reference as shipped (1 core, serial oracle): {_sample_words(ns1, wl.n)}, "
                                         f"2 matvecs per layer, {secs1:.1f} s"}}
     if rank == 0:
-        print(json.dumps(result), flush=True)
+        print(json.dumps(result), file=_OUT, flush=True)
     if sharded:
         torch.distributed.destroy_process_group()
     return 0
@@ -607,6 +608,9 @@ def _launch_ranks(args):
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
     cmd += [a for a in sys.argv[1:]]
     return subprocess.call(cmd, cwd=ROOT)
+
+
+_OUT = sys.stdout
 
 
 def main():
@@ -630,6 +634,12 @@ def main():
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return _launch_ranks(args)
+    # stdout carries exactly the one JSON line: anything libraries print to
+    # fd 1 (NCCL's version banner under NCCL_DEBUG=VERSION, ...) goes to stderr
+    global _OUT
+    _OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -384,12 +384,14 @@ class ShardedKernelGraph:
     plan is fixed by the plan's admissible box, so every rank's grid has the
     same layout).
 
-    One normalized-Laplacian step (every layer's L_sym + delta of one vector):
-      per layer   mlb_spread of the rank's nodes (D^-1/2 folded in) into that
-                  layer's slice of ONE buffer holding all layers' sub-box grids;
-      once        all-reduce (sum) of that buffer over the ranks -- the only
-                  collective of the step (NCCL over NVLink on the box);
-      per layer   mlb_convolve (redundant on every rank: the band-limited
+    One normalized-Laplacian step (every layer's L_sym + delta of one vector),
+    per layer on its own stream (cheapest layer issued first):
+      mlb_spread of the rank's nodes (D^-1/2 folded in) into that layer's
+                  slice of one buffer holding all layers' sub-box grids;
+      all-reduce (sum) of that slice over the ranks -- the layer's only
+                  collective (NCCL over NVLink on the box; the cheap layers'
+                  collectives overlap the costly layer's spread);
+      mlb_convolve (redundant on every rank: the band-limited
                   convolution of a <= 700 KB sub-box) and mlb_gather_apply,
                   the gather with the fused epilogue
                   y = (1+delta) v - D^-1/2 W~ D^-1/2 v + K0 D^-1 v on the
@@ -436,35 +438,44 @@ class ShardedKernelGraph:
             self.comm.all_reduce_sum(self.grids)
 
     def _layer_streams(self):
-        """One side stream per layer after the first (the first runs on the
-        caller's stream): the layers' kernels overlap, as in LaplacianBatch."""
+        """One stream per layer, the costliest layer's at high priority (as in
+        LaplacianBatch), and the issue order: cheapest layer first, so that the
+        collectives, which one communicator runs in issue order, come in the
+        order the layers' spreads finish."""
         torch = _torch()
-        if getattr(self, "_side", None) is None:
-            self._side = [torch.cuda.Stream(self.dev) for _ in range(self.T - 1)]
+        if getattr(self, "_streams", None) is None:
+            cost = [w.n * (2 * w.plan.m_nfft + 1) ** w.plan.d for w in self.weights]
+            top = int(np.argmax(cost))
+            prio = os.environ.get("MLB_NO_STREAM_PRIORITY") != "1"
+            self._streams = [torch.cuda.Stream(self.dev, priority=-1 if (prio and t == top) else 0)
+                             for t in range(self.T)]
+            self._order = [int(t) for t in np.argsort(cost, kind="stable")]
             self._fork_ev = torch.cuda.Event()
-            self._join_ev = [torch.cuda.Event() for _ in range(self.T - 1)]
-        return self._side
+            self._join_ev = [torch.cuda.Event() for _ in range(self.T)]
+        return self._streams
 
     def _per_layer(self, fn):
-        """fn(t, stream_ptr) for every layer, layer t > 0 on side stream t-1,
-        forked from and joined back into the current stream."""
+        """fn(t, stream_ptr) for every layer on its own stream (the current
+        torch stream inside fn, so collectives issued there order against the
+        layer's kernels), forked from and joined back into the caller's stream.
+        MLB_SHARD_ONE_STREAM=1: every layer in order on the caller's stream."""
         torch = _torch()
         if self.T == 1 or os.environ.get("MLB_SHARD_ONE_STREAM") == "1":
             sp = _lib.stream_ptr()
             for t in range(self.T):
                 fn(t, sp)
             return
-        side = self._layer_streams()
+        streams = self._layer_streams()
         main = torch.cuda.current_stream(self.dev)
         self._fork_ev.record(main)
-        for t in range(1, self.T):
-            s = side[t - 1]
+        for t in self._order:
+            s = streams[t]
             s.wait_event(self._fork_ev)
-            fn(t, s.cuda_stream)
-            self._join_ev[t - 1].record(s)
-        fn(0, main.cuda_stream)
-        for ev in self._join_ev:
-            main.wait_event(ev)
+            with torch.cuda.stream(s):
+                fn(t, s.cuda_stream)
+            self._join_ev[t].record(s)
+        for t in self._order:
+            main.wait_event(self._join_ev[t])
 
     def spread_local(self, v, flags):
         """Every layer's spread of this rank's nodes into self.grids."""
@@ -476,24 +487,45 @@ class ShardedKernelGraph:
                                       _lib.ptr(self._grid(self.grids, t)), spread_flags, sp))
         self._per_layer(spread)
 
+    def _finish_layer(self, t, v, y, coef, flags, sp):
+        lib = _lib.lib()
+        b = self.weights[t]._bindings[0].ptr
+        g_in, g_out = self._grid(self.grids, t), self._grid(self.conv, t)
+        _lib.check(lib.mlb_convolve(b, _lib.ptr(g_in), _lib.ptr(g_out), sp))
+        a, be, ga = coef
+        _lib.check(lib.mlb_gather_apply(b, _lib.ptr(g_out), _lib.ptr(v), _lib.ptr(y), float(a), float(be),
+                                        float(ga), int(flags), sp))
+
     def _step(self, v, ys, coef, flags):
-        """ys[t] (=|+=) coef[t] combination for every layer; ONE collective."""
+        """ys[t] (=|+=) coef[t] combination for every layer.
+
+        Default: every layer's chain -- spread, all-reduce of ITS grid slice,
+        convolution, fused gather -- on its own stream, so a cheap layer's
+        whole chain (and its collective) runs under the costly layer's spread
+        and fills the costly layer's merge / all-reduce gaps.
+        MLB_SHARD_JOINED=1 (or one stream): both spreads, ONE all-reduce of all
+        layers' grids, then the convolutions and gathers."""
+        if self.T > 1 and os.environ.get("MLB_SHARD_JOINED") != "1" and \
+                os.environ.get("MLB_SHARD_ONE_STREAM") != "1":
+            lib = _lib.lib()
+            spread_flags = int(flags) & (_lib.MLB_USE_ISD | _lib.MLB_SORTED)
+
+            def chain(t, sp):
+                g_in = self._grid(self.grids, t)
+                _lib.check(lib.mlb_spread(self.weights[t]._bindings[0].ptr, _lib.ptr(v), _lib.ptr(g_in),
+                                          spread_flags, sp))
+                if self.comm is not None:
+                    self.comm.all_reduce_sum(g_in)
+                self._finish_layer(t, v, ys[t], coef[t], flags, sp)
+            self._per_layer(chain)
+            return ys
         self.spread_local(v, flags)
         self._all_reduce()
         return self.finish(v, ys, coef, flags)
 
     def finish(self, v, ys, coef, flags):
         """Convolve the summed grids and gather this rank's nodes (fused epilogue)."""
-        lib = _lib.lib()
-
-        def fin(t, sp):
-            b = self.weights[t]._bindings[0].ptr
-            g_in, g_out = self._grid(self.grids, t), self._grid(self.conv, t)
-            _lib.check(lib.mlb_convolve(b, _lib.ptr(g_in), _lib.ptr(g_out), sp))
-            a, be, ga = coef[t]
-            _lib.check(lib.mlb_gather_apply(b, _lib.ptr(g_out), _lib.ptr(v), _lib.ptr(ys[t]), float(a), float(be),
-                                            float(ga), int(flags), sp))
-        self._per_layer(fin)
+        self._per_layer(lambda t, sp: self._finish_layer(t, v, ys[t], coef[t], flags, sp))
         return ys
 
     def build(self):
@@ -529,16 +561,12 @@ class ShardedKernelGraph:
         convolution and fused gather (the per-layer operator of PKSM)."""
         lib = _lib.lib()
         sp = _lib.stream_ptr()
-        b = self.weights[t]._bindings[0].ptr
-        g_in, g_out = self._grid(self.grids, t), self._grid(self.conv, t)
-        _lib.check(lib.mlb_spread(b, _lib.ptr(v), _lib.ptr(g_in), int(flags) & (_lib.MLB_USE_ISD | _lib.MLB_SORTED),
-                                  sp))
+        g_in = self._grid(self.grids, t)
+        _lib.check(lib.mlb_spread(self.weights[t]._bindings[0].ptr, _lib.ptr(v), _lib.ptr(g_in),
+                                  int(flags) & (_lib.MLB_USE_ISD | _lib.MLB_SORTED), sp))
         if self.comm is not None:
             self.comm.all_reduce_sum(g_in)
-        _lib.check(lib.mlb_convolve(b, _lib.ptr(g_in), _lib.ptr(g_out), sp))
-        a, be, ga = coef
-        _lib.check(lib.mlb_gather_apply(b, _lib.ptr(g_out), _lib.ptr(v), _lib.ptr(y), float(a), float(be), float(ga),
-                                        int(flags), sp))
+        self._finish_layer(t, v, y, coef, flags, sp)
         return y
 
     def layer_ops(self):

@@ -26,6 +26,7 @@ def test_reference_arm_line():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                         "--warmup", "1", "--ref-sample", "3000"], capture_output=True, text=True, cwd=ROOT)
     assert r.returncode == 0, r.stderr
+    assert len(r.stdout.strip().splitlines()) == 1   # stdout is the one JSON line
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
@@ -52,12 +53,15 @@ def test_bench_line_contract():
 
 @pytest.mark.gpu
 def test_bench_sharded_step_on_one_gpu():
-    """The node-range sharded step (the N > 1 bench path: one NCCL all-reduce
-    of both layers' grids per step) runs end to end on one GPU (`--sharded`)."""
+    """The node-range sharded step (the N > 1 bench path: per layer one NCCL
+    all-reduce of its grid per step) runs end to end on one GPU (`--sharded`);
+    stdout holds only the JSON line even with NCCL's version banner on."""
     import json
+    env = dict(os.environ, NCCL_DEBUG="VERSION")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--sharded", "--steps", "3", "--warmup", "3",
-                        "--no-cpu-baseline", "--workload", "cfg2"], capture_output=True, text=True, cwd=ROOT)
+                        "--no-cpu-baseline", "--workload", "cfg2"], capture_output=True, text=True, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
+    assert len(r.stdout.strip().splitlines()) == 1, r.stdout[:500]
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["n_gpus"] == 1 and d["value"] > 1e8 and "sharded" in d["config"]["parallelism"]
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
