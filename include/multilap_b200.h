@@ -223,6 +223,15 @@ int64_t mlb_cgs2_batched_work_size(int T);
 int mlb_cgs2_batched(int T, const double* const* V, int64_t ld, int64_t n, int cols, double* const* w,
                      double* const* h_out, double* const* h1_out, double* const* nrm2_out, double* const* vnext,
                      double* work, void* stream);
+/* Lockstep PKSM coefficients of step j for T chains (krylov.py:196-216),
+ * one warp per chain, no host eigh: AB row t (device, ld >= 2 dim + 5
+ * doubles) = [h1 (alpha_j at j) | ||w_j||^2 at dim + j | <v,v> at 2 dim |
+ * stats out: min eigenvalue, ||c||^2, ||c - [c_prev; 0]||^2, status];
+ * hist (device, T x 2 dim) receives alpha_j / beta_j; C (device, T x dim x
+ * dim) receives c_j = ||v|| Q f(Lambda) Q[0,:]^T of T_{j+1} with f = max(.,0)^p,
+ * eigenpairs by implicit QL.  status 1 = QL did not converge (recompute). */
+int mlb_tridiag_fn_batched(int T, double* AB, int64_t ld, int dim, int j, double p, double* hist, double* C,
+                           void* stream);
 /* y = V[:, :cols] c  (c device) ; out may alias nothing */
 int mlb_gemv_n(const double* V, int64_t ld, int64_t n, int cols, const double* c, double* y,
                double scale, int accumulate, void* stream);

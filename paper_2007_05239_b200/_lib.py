@@ -79,6 +79,7 @@ SIGNATURES = {
     "mlb_gemv_n": (I, [P, I64, I64, I, P, P, D, I, P]),
     "mlb_cgs2_batched_work_size": (I64, [I]),
     "mlb_cgs2_batched": (I, [I, P, I64, I64, I, P, P, P, P, P, P, P]),
+    "mlb_tridiag_fn_batched": (I, [I, P, I64, I, I, D, P, P, P]),
     "mlb_gemm_vs": (I, [P, I64, I64, I, P, I, P, I64, P]),
     "mlb_dot": (I, [P, P, I64, P, P, P]),
     "mlb_axpby": (I, [D, P, D, P, I64, P]),

@@ -381,6 +381,142 @@ static int ew_grid(int64_t n) {
     return (int)(b < 1 ? 1 : b);
 }
 
+
+// ------------------------------------------------------ PKSM coefficients --
+// The lockstep PKSM's per-step coefficients on the device (krylov.py:196-216:
+// eigh(T_s), f(Lambda), y = ||v|| V_s Q f(Lambda) Q[0,:]), one warp per
+// chain, so no host eigh sits between two graph replays.  Step j of chain t:
+//   * record alpha_j = ab[j] and beta_j = sqrt(max(ab[dim + j], 0)) (the
+//     CGS2 just wrote them) into the chain's history;
+//   * T_s (s = j + 1) = tridiag(beta, alpha, beta) -> eigenvalues and
+//     eigenvectors by implicit QL with shifts (the EISPACK tql2 scheme): the
+//     scalar recurrence is evaluated redundantly by every lane, lane 0 writes
+//     the diagonal / off-diagonal back, and each rotation updates the
+//     eigenvector matrix in shared memory with one lane per row;
+//   * c = nv Q f(max(Lambda, 0)) Q[0,:]^T into C[t][j][0..s);
+//   * stats after the row's <v,v> entry: min eigenvalue (unclamped), ||c||^2,
+//     ||c - [c_{j-1}; 0]||^2 (fixed-order warp sums), status (1 = QL did not
+//     converge in 60 sweeps: the host recomputes that step).
+constexpr int kTriMax = 64;
+constexpr int kTriLd = kTriMax + 1;
+
+__device__ __forceinline__ double tri_f(double lam, double p) {
+    lam = fmax(lam, 0.0);
+    if (p == -1.0) return 1.0 / lam;   // numpy's fast paths for these powers
+    if (p == 1.0) return lam;
+    if (p == 2.0) return lam * lam;
+    if (p == 0.5) return sqrt(lam);
+    return pow(lam, p);
+}
+
+__global__ void __launch_bounds__(32) tridiag_fn_kernel(double* __restrict__ AB, int ld, int dim, int j, double p,
+                                                        double* __restrict__ hist, double* __restrict__ Cc) {
+    __shared__ double Q[kTriMax * kTriLd];
+    __shared__ double dg[kTriMax], of[kTriMax];
+    const int t = blockIdx.x, lane = threadIdx.x;
+    double* ab = AB + (size_t)t * ld;
+    double* al = hist + (size_t)t * 2 * dim;
+    double* be = al + dim;
+    const int s = j + 1;
+    if (lane == 0) {
+        al[j] = ab[j];
+        be[j] = sqrt(fmax(ab[dim + j], 0.0));
+    }
+    __syncwarp();
+    for (int i = lane; i < s; i += 32) {
+        dg[i] = al[i];
+        of[i] = (i + 1 < s) ? be[i] : 0.0;
+        for (int k = 0; k < s; ++k) Q[i * kTriLd + k] = (i == k) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    int status = 0;
+    for (int l = 0; l < s && !status; ++l) {
+        for (int iter = 0;; ++iter) {
+            int m = l;
+            for (; m < s - 1; ++m) {   // first negligible off-diagonal at or after l
+                const double e = fabs(of[m]);
+                if (e == 0.0 || e <= 2.220446049250313e-16 * (fabs(dg[m]) + fabs(dg[m + 1]))) break;
+            }
+            if (m == l) break;
+            if (iter == 60) {
+                status = 1;
+                break;
+            }
+            double g = (dg[l + 1] - dg[l]) / (2.0 * of[l]);
+            double r = hypot(g, 1.0);
+            g = dg[m] - dg[l] + of[l] / (g + copysign(r, g));
+            double sn = 1.0, cs = 1.0, pp = 0.0;
+            bool split = false;
+            for (int i = m - 1; i >= l; --i) {
+                const double ei = of[i], di = dg[i], di1 = dg[i + 1];
+                __syncwarp();
+                const double f = sn * ei, b = cs * ei;
+                r = hypot(f, g);
+                if (lane == 0) of[i + 1] = r;
+                if (r == 0.0) {   // the rotation underflowed: deflate and restart at l
+                    if (lane == 0) {
+                        dg[i + 1] = di1 - pp;
+                        of[m] = 0.0;
+                    }
+                    split = true;
+                    __syncwarp();
+                    break;
+                }
+                sn = f / r;
+                cs = g / r;
+                g = di1 - pp;
+                r = (di - g) * sn + 2.0 * cs * b;
+                pp = sn * r;
+                if (lane == 0) dg[i + 1] = g + pp;
+                g = cs * r - b;
+                for (int k = lane; k < s; k += 32) {   // columns i, i+1 of the eigenvector matrix
+                    double* q = Q + k * kTriLd;
+                    const double qi = q[i], qi1 = q[i + 1];
+                    q[i + 1] = sn * qi + cs * qi1;
+                    q[i] = cs * qi - sn * qi1;
+                }
+                __syncwarp();
+            }
+            if (split) continue;
+            if (lane == 0) {
+                dg[l] -= pp;
+                of[l] = g;
+                of[m] = 0.0;
+            }
+            __syncwarp();
+        }
+    }
+    // f(Lambda) Q[0,:] into `of`, then c = nv Q (f Q[0,:]) with one lane per row
+    double lmin = dg[0];
+    for (int k = 1; k < s; ++k) lmin = fmin(lmin, dg[k]);
+    __syncwarp();
+    for (int k = lane; k < s; k += 32) of[k] = tri_f(dg[k], p) * Q[k];
+    __syncwarp();
+    const double nv = sqrt(ab[2 * dim]);
+    double* c = Cc + ((size_t)t * dim + j) * dim;
+    const double* cp = Cc + ((size_t)t * dim + (j > 0 ? j - 1 : 0)) * dim;
+    double c2 = 0.0, d2 = 0.0;
+    for (int i = lane; i < s; i += 32) {
+        double acc = 0.0;
+        for (int k = 0; k < s; ++k) acc = fma(Q[i * kTriLd + k], of[k], acc);
+        const double ci = nv * acc;
+        c[i] = ci;
+        const double di = ci - ((j > 0 && i < s - 1) ? cp[i] : 0.0);
+        c2 = fma(ci, ci, c2);
+        d2 = fma(di, di, d2);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+    }
+    if (lane == 0) {
+        ab[2 * dim + 1] = lmin;
+        ab[2 * dim + 2] = c2;
+        ab[2 * dim + 3] = d2;
+        ab[2 * dim + 4] = (double)status;
+    }
+}
+
 }  // namespace mlb
 
 using namespace mlb;
@@ -472,6 +608,18 @@ int mlb_cgs2_batched(int T, const double* const* V, int64_t ld, int64_t n, int c
     cgs_update_batched<<<dim3(nb, T), 256, 0, st>>>(B, ld, n, cols, 1);
     cgs_norm_scale_batched<<<dim3(ew_grid(n) / std::max(1, T / 8) + 1, T), 256, 0, st>>>(B, ld, n, cols, nb);
     note_launches(5);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int mlb_tridiag_fn_batched(int T, double* AB, int64_t ld, int dim, int j, double p, double* hist, double* C,
+                           void* stream) {
+    if (T <= 0) return MLB_OK;
+    if (dim < 1 || dim > kTriMax || j < 0 || j >= dim) return fail(MLB_ERR_ARG, "tridiagonal step needs 0 <= j < dim <= 64");
+    if (ld < 2 * (int64_t)dim + 5) return fail(MLB_ERR_ARG, "AB rows need 2 dim + 5 entries");
+    if (!AB || !hist || !C) return fail(MLB_ERR_ARG, "null argument");
+    tridiag_fn_kernel<<<T, 32, 0, (cudaStream_t)stream>>>(AB, (int)ld, dim, j, p, hist, C);
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }

@@ -568,17 +568,20 @@ def _lock_buffers(dev, T, dim, n):
     if P is None:
         lib = _lib.lib()
         need = max(int(lib.mlb_krylov_work_size(n, dim + 2)), 1 << 16)
-        P = dict(AB=torch.zeros((T, 2 * dim + 1), dtype=torch.float64, device=dev),
+        ld = _ab_ld(dim)
+        P = dict(AB=torch.zeros((T, ld), dtype=torch.float64, device=dev),
+                 hist=torch.zeros((T, 2 * dim), dtype=torch.float64, device=dev),
+                 Cc=torch.zeros((T, dim, dim), dtype=torch.float64, device=dev),
                  w=torch.empty((T, n), dtype=torch.float64, device=dev),
                  h=torch.empty((T, dim + 1), dtype=torch.float64, device=dev),
                  work=torch.empty((T, need), dtype=torch.float64, device=dev),
                  bwork=torch.empty(int(lib.mlb_cgs2_batched_work_size(T)), dtype=torch.float64, device=dev),
-                 ABh=torch.empty((dim, T, 2 * dim + 1), dtype=torch.float64, pin_memory=True),
+                 ABh=torch.empty((dim, T, ld), dtype=torch.float64, pin_memory=True),
                  streams=[torch.cuda.Stream(device=dev)
                           for _ in range(min(T, int(os.environ.get("MLB_PKSM_STREAMS", "8"))))])
         # device pointer arrays of the batched CGS2 (fixed per pool; nrm2 per step j)
         ab0 = P["AB"].data_ptr()
-        rows = [ab0 + 8 * (2 * dim + 1) * t for t in range(T)]
+        rows = [ab0 + 8 * ld * t for t in range(T)]
         P["p_w"] = torch.tensor([P["w"][t].data_ptr() for t in range(T)], dtype=torch.int64, device=dev)
         P["p_h"] = torch.tensor([P["h"][t].data_ptr() for t in range(T)], dtype=torch.int64, device=dev)
         P["p_h1"] = torch.tensor(rows, dtype=torch.int64, device=dev)
@@ -586,6 +589,24 @@ def _lock_buffers(dev, T, dim, n):
                                   device=dev)
         _LOCK_POOL[key] = P
     return P
+
+
+def _ab_ld(dim):
+    """Lockstep AB row: h1 (dim) | ||w||^2 (dim) | <v,v> | 4 device-coefficient stats."""
+    return 2 * dim + 5
+
+
+def _device_coeffs_ok(dim):
+    """Lockstep PKSM coefficients on the device (mlb_tridiag_fn_batched):
+    dim <= 64; MLB_PKSM_DEVICE_COEFFS=0 keeps the host's batched eigh."""
+    return dim <= 64 and os.environ.get("MLB_PKSM_DEVICE_COEFFS", "1") != "0"
+
+
+def _issue_coeffs(P, T, j, dim, p, sp):
+    """Every chain's step-j coefficients and stop statistics on the device."""
+    _lib.check(_lib.lib().mlb_tridiag_fn_batched(T, C.c_void_p(P["AB"].data_ptr()), _ab_ld(dim), dim, j, float(p),
+                                                 C.c_void_p(P["hist"].data_ptr()), C.c_void_p(P["Cc"].data_ptr()),
+                                                 sp))
 
 
 def _batched_cgs_ok(dim, n):
@@ -660,9 +681,10 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
         x.V = _krylov_basis(dev, t, dim, n)
         scale_by(x.vs, x.V[0], vv, -0.5)
     use_graphs = _graphs_enabled()
+    dev_coeffs = _device_coeffs_ok(dim)
     gkey = (dev.index, _VPOOL_DEPTH[0], dim, n, tuple(int(x.b.ptr.value) for x in st),
             tuple((x.a, x.K0) for x in st), tuple(x.V.data_ptr() for x in st), AB.data_ptr(),
-            _batched_cgs_ok(dim, n))
+            _batched_cgs_ok(dim, n), dev_coeffs, float(p) if dev_coeffs else None)
     graphs = None
     if use_graphs:
         graphs = _LOCK_GRAPHS.get(gkey)
@@ -691,6 +713,8 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
             for t, x in enumerate(st):
                 if not x.done:
                     _issue_layer_step(x, t, j, P, dim, n, C.c_void_p(stream.cuda_stream))
+            if dev_coeffs:
+                _issue_coeffs(P, T, j, dim, p, C.c_void_p(stream.cuda_stream))
             ABh[j].copy_(AB, non_blocking=True)
         else:
             if j not in graphs:
@@ -720,6 +744,8 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
                         cap.wait_event(e)
                     if batched:
                         _issue_cgs_batched(P, p_V, len(st), j, dim, n, C.c_void_p(cap.cuda_stream))
+                    if dev_coeffs:
+                        _issue_coeffs(P, T, j, dim, p, C.c_void_p(cap.cuda_stream))
                     ABh[j].copy_(AB, non_blocking=True)
                 graphs[j] = (g, int(lib.mlb_launch_count() - l0))
             g, cnt = graphs[j]
@@ -733,6 +759,8 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
         # attributes outside capture), then graphs from step 0 on
         for t, x in enumerate(st):
             _issue_layer_step(x, t, 0, P, dim, n, C.c_void_p(stream.cuda_stream))
+        if dev_coeffs:
+            _issue_coeffs(P, T, 0, dim, p, C.c_void_p(stream.cuda_stream))
         torch.cuda.synchronize(dev)   # (re-running step 0 from the graph recomputes the same values)
     depth = _run_ahead()
     issued = 0
@@ -761,20 +789,23 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
             break
         alphas[act, s] = snap[act, s]
         betas[act, s] = np.sqrt(np.maximum(snap[act, dim + s], 0.0))
-        cs = _coeffs(alphas[act], betas[act], ss, nv[act], fn)
-        for c, t in zip(cs, act):
-            x = st[t]
-            stop = False
-            if c_prev[t] is not None:
-                stop = _converged(c, c_prev[t], tol, lambda: _exact_test(x.V, n, c, c_prev[t], tol, dev))
-            happy = betas[t, s] <= 1e-13 * max(1.0, np.abs(alphas[t, :ss]).max())
-            if stop or happy or ss >= dim:
-                PksmStats.steps.append(ss)
-                x.ys = torch.empty(n, dtype=torch.float64, device=dev)
-                gemv_n(x.V, n, ss, _to_dev(c, dev.index), x.ys)
-                x.done = True
-            else:
-                c_prev[t] = c
+        if dev_coeffs:
+            _dev_coeff_step(st, act, snap, s, dim, n, p, fn, tol, alphas, betas, nv, P, dev)
+        else:
+            cs = _coeffs(alphas[act], betas[act], ss, nv[act], fn)
+            for c, t in zip(cs, act):
+                x = st[t]
+                stop = False
+                if c_prev[t] is not None:
+                    stop = _converged(c, c_prev[t], tol, lambda: _exact_test(x.V, n, c, c_prev[t], tol, dev))
+                happy = betas[t, s] <= 1e-13 * max(1.0, np.abs(alphas[t, :ss]).max())
+                if stop or happy or ss >= dim:
+                    PksmStats.steps.append(ss)
+                    x.ys = torch.empty(n, dtype=torch.float64, device=dev)
+                    gemv_n(x.V, n, ss, _to_dev(c, dev.index), x.ys)
+                    x.done = True
+                else:
+                    c_prev[t] = c
         s += 1
         if issued < dim and any(not x.done for x in st):
             issue(issued)
@@ -787,6 +818,52 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
             x.ys.mul_(out_scale)
         _lib.check(lib.mlb_to_node(x.b.ptr, _lib.ptr(x.ys), _lib.ptr(out), 1, _sp()))
     return out
+
+
+def _check_spectrum(low, p):
+    """power_fn's PSD / positivity checks (krylov.py:230-242) on a minimum eigenvalue."""
+    if low < -1e-10:
+        raise NumericalError(f"operator is not positive semidefinite (eigenvalue {low:.3e})")
+    if p < 0 and max(low, 0.0) <= 0.0:
+        raise NumericalError("zero eigenvalue encountered with a negative power; "
+                             "a positive shift delta is required")
+
+
+def _dev_coeff_step(st, act, snap, s, dim, n, p, fn, tol, alphas, betas, nv, P, dev):
+    """Host side of one lockstep step with device coefficients: the stop test
+    of krylov.py:205-216 on the per-chain statistics the device wrote
+    (min eigenvalue, ||c||^2, ||c - c_prev||^2), exact re-test near the
+    threshold on the device vectors; y = V_s c_s from the device's c."""
+    torch = _torch()
+    ss = s + 1
+    Cc = P["Cc"]
+    for t in act:
+        x = st[t]
+        low, c2, d2, status = snap[t, 2 * dim + 1: 2 * dim + 5]
+        if status != 0:   # QL did not converge: this chain's step on the host
+            c = _coeffs(alphas[t:t + 1], betas[t:t + 1], ss, nv[t:t + 1], fn)[0]
+            cd = _to_dev(c, dev.index)
+            Cc[t, s, :ss].copy_(cd)
+            c2 = float(c @ c)
+            diff = c.copy()
+            if s > 0:
+                diff[:s] -= Cc[t, s - 1, :s].cpu().numpy()
+            d2 = float(diff @ diff)
+        else:
+            _check_spectrum(float(low), p)
+        c_dev = Cc[t, s, :ss]
+        stop = False
+        if s > 0:
+            lhs, rhs = float(np.sqrt(d2)), tol * max(float(np.sqrt(c2)), 1e-300)
+            if rhs > 0 and abs(lhs / rhs - 1.0) < 1e-3:
+                lhs, rhs = _exact_test(x.V, n, c_dev, Cc[t, s - 1, :s], tol, dev)
+            stop = lhs <= rhs
+        happy = betas[t, s] <= 1e-13 * max(1.0, np.abs(alphas[t, :ss]).max())
+        if stop or happy or ss >= dim:
+            PksmStats.steps.append(ss)
+            x.ys = torch.empty(n, dtype=torch.float64, device=dev)
+            gemv_n(x.V, n, ss, c_dev.contiguous(), x.ys)
+            x.done = True
 
 
 def batchable_layers(layers):

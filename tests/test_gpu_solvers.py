@@ -48,8 +48,12 @@ def test_pksm_and_power_operators_match_golden():
 
 
 def test_batched_pksm_is_bitwise_sequential():
-    """The lockstep multi-layer PKSM (one host read per step for all layers)
-    reproduces the per-layer loop bit for bit, including the layer-order sum."""
+    """The lockstep multi-layer PKSM (one graph replay and one host read per
+    step for all layers) reproduces the per-layer loop: bit for bit with the
+    host's batched eigh (MLB_PKSM_DEVICE_COEFFS=0), to rounding (<= 1e-13)
+    with the coefficients on the device (default); the layer-order sum too."""
+    import os
+
     import torch
     from paper_2007_05239_b200 import with_shift
     from paper_2007_05239_b200.krylov import pksm_layer_dev, pksm_layers_dev
@@ -64,10 +68,16 @@ def test_batched_pksm_is_bitwise_sequential():
             pksm_layer_dev(layer, p, v, seq, 1.0, True)
         bat = torch.zeros_like(v)
         pksm_layers_dev(layers, p, v, bat, 1.0)
-        assert torch.equal(seq, bat)
+        assert rel(bat.cpu().numpy(), seq.cpu().numpy()) < 1e-13
+        os.environ["MLB_PKSM_DEVICE_COEFFS"] = "0"
+        try:
+            hb = torch.zeros_like(v)
+            pksm_layers_dev(layers, p, v, hb, 1.0)
+        finally:
+            del os.environ["MLB_PKSM_DEVICE_COEFFS"]
+        assert torch.equal(seq, hb)
     # the device's run-ahead depth changes no value (discarded steps only)
-    import os
-    res = []
+    res, resb = [], []
     for depth in ("1", "3"):
         os.environ["MLB_PKSM_DEPTH"] = depth
         try:
@@ -78,9 +88,65 @@ def test_batched_pksm_is_bitwise_sequential():
             pksm_layers_dev(layers, -1.0, v, b, 1.0)
         finally:
             del os.environ["MLB_PKSM_DEPTH"]
-        assert torch.equal(a, b)
+        assert rel(b.cpu().numpy(), a.cpu().numpy()) < 1e-13
         res.append(a)
-    assert torch.equal(res[0], res[1])
+        resb.append(b)
+    assert torch.equal(res[0], res[1]) and torch.equal(resb[0], resb[1])
+
+
+@pytest.mark.parametrize("p", [-1.0, -3.0, 0.5, 2.0])
+def test_device_tridiagonal_coefficients_match_host_eigh(p):
+    """mlb_tridiag_fn_batched (implicit QL per warp) against the host's batched
+    eigh (krylov._coeffs, the reference's krylov.py:200-206 arithmetic) on
+    random Lanczos-like tridiagonals, every step j of dim = 64 chains, plus the
+    stop statistics and the min eigenvalue of an indefinite chain."""
+    import ctypes as C
+
+    import torch
+    from paper_2007_05239_b200 import _lib
+    from paper_2007_05239_b200.krylov import _coeffs
+    rng = np.random.default_rng(11)
+    T, dim = 5, 64
+    ld = 2 * dim + 5
+    al = rng.uniform(2.0, 3.0, (T, dim))               # Gershgorin: lambda >= 0.2
+    be = rng.uniform(0.0, 0.9, (T, dim))
+    be[1, 7] = 0.0                                   # an exactly split matrix
+    al[4, :] = rng.uniform(-1.0, 1.0, dim)           # indefinite chain
+    vv = rng.uniform(0.5, 4.0, T)
+    AB = torch.zeros((T, ld), dtype=torch.float64, device="cuda")
+    hist = torch.zeros((T, 2 * dim), dtype=torch.float64, device="cuda")
+    Cc = torch.zeros((T, dim, dim), dtype=torch.float64, device="cuda")
+    lib = _lib.lib()
+    fn = lambda lam: np.maximum(lam, 0.0) ** p   # noqa: E731
+    prev = None
+    for j in range(dim):
+        row = np.zeros((T, ld))
+        row[:, j] = al[:, j]
+        row[:, dim + j] = be[:, j] ** 2
+        row[:, 2 * dim] = vv
+        AB.copy_(torch.from_numpy(row))
+        _lib.check(lib.mlb_tridiag_fn_batched(T, C.c_void_p(AB.data_ptr()), ld, dim, j, p,
+                                              C.c_void_p(hist.data_ptr()), C.c_void_p(Cc.data_ptr()), _lib.stream_ptr()))
+        out = AB.cpu().numpy()
+        s = j + 1
+        lam = np.array([np.linalg.eigvalsh(np.diag(al[t, :s]) + np.diag(be[t, :s - 1], 1) + np.diag(be[t, :s - 1], -1))
+                        for t in range(T)])
+        assert np.all(out[:, 2 * dim + 4] == 0)
+        assert np.allclose(out[:, 2 * dim + 1], lam.min(axis=1), rtol=0, atol=1e-13 * np.abs(lam).max())
+        ok = [t for t in range(T) if lam[t].min() > 1e-3]   # the power is defined on these chains
+        ref = _coeffs(al[ok], be[ok], s, np.sqrt(vv[ok]), fn)
+        got = Cc[ok, j, :s].cpu().numpy()
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), j
+        assert np.allclose(out[ok, 2 * dim + 2], (ref * ref).sum(axis=1), rtol=1e-12)
+        if prev is not None:
+            d = ref.copy()
+            d[:, :s - 1] -= prev
+            # ||c - c_prev|| to rounding relative to ||c|| (what the stop test compares it with)
+            err = np.abs(np.sqrt(out[ok, 2 * dim + 3]) - np.sqrt((d * d).sum(axis=1)))
+            assert np.all(err <= 1e-13 * np.sqrt((ref * ref).sum(axis=1)))
+        prev = ref
+    assert np.array_equal(hist[:, :dim].cpu().numpy(), al)
+    assert np.array_equal(hist[:, dim:].cpu().numpy(), np.sqrt(be ** 2))
 
 
 def test_power_mean_eigs_match_golden():

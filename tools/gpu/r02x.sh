@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02x; mkdir -p $O
+timeout 600 python tools/stages_micro.py --d 1,2 --m 4 > $O/micro_node.log 2>&1; echo "micro rc=$?" >> $O/rc.txt
+timeout 600 python tools/stages_micro.py --d 1,2 --m 4 --sorted > $O/micro_sorted.log 2>&1; echo "micro sorted rc=$?" >> $O/rc.txt
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"spread_kernel|gather_kernel" -s 2 -c 2 -o $O/d1_sorted python tools/stages_micro.py --d 1 --m 4 --sorted > $O/ncu_d1.log 2>&1; echo "ncu rc=$?" >> $O/rc.txt
