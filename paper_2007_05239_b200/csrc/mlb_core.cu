@@ -254,6 +254,7 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->blocks);
     dev_free(b->seg_sub);
     dev_free(b->cta_seg);
+    dev_free(b->key_start);
     dev_free(b->cta_row0);
     dev_free(b->row_cta);
     dev_free(b->seg_brick);
@@ -741,6 +742,12 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
         if (packed && rc == MLB_OK) rc = dev_upload(&b->gslot, gslot.data(), gslot.size());
         const int S = 2 * g.m + 1;
         if (rc == MLB_OK) rc = dev_upload<double>(&b->blocks, nullptr, (size_t)b->nblk * S * S * S);
+    }
+    const char* s1 = std::getenv("MLB_D1_STREAM");   // A/B: 0 = the sub-chunk kernels
+    if (d == 1 && n > 0 && !(s1 && s1[0] == '0')) {   // per-cell starts for the streaming d = 1 kernels
+        std::vector<int32_t> ks(cnt.begin(), cnt.end());
+        b->nkeys = (int)nkeys;
+        if (rc == MLB_OK) rc = dev_upload(&b->key_start, ks.data(), ks.size());
     }
     if (ncta_band > 0) {
         b->ncta_band = ncta_band;

@@ -119,6 +119,9 @@ struct FsArgs {
     // d = 2 banded spread: CTA c owns segments [cta_seg[c], cta_seg[c+1])
     // (nullptr: warps take segments gw, gw + W, ... over the whole list)
     const int32_t* cta_seg;
+    // d = 1 streaming spread / gather: first sorted point of every cell (nkeys + 1)
+    const int32_t* key_start;
+    int nkeys;
 };
 
 // sub-box index of element (o01 = o0*S + o1, o2) of d = 3 cell block `blk`
@@ -364,13 +367,24 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
                 for (int o = 0; o < S; ++o) acc1[o] = fma(w[o], sv0, acc1[o]);
             } else if (!(flags & (1u << 17))) {  // bit 17: ablation (profiling only)
                 const double sv0 = (lane < np && p0.sub >= 0) ? s0 * v0 : 0.0;
-                double w[S];
+                if constexpr (G2) {
+                    double w[D][S];
+                    kb_windows_k<M, D>(f0, wc, w);   // both axes at once (one coefficient read each)
 #pragma unroll
-                for (int ax = 0; ax < D; ++ax) {
-                    kb_windows<M>(f0[ax], wc, w);
-                    double* dst = my_stage + (lane * D + ax) * SPAD;
+                    for (int ax = 0; ax < D; ++ax) {
+                        double* dst = my_stage + (lane * D + ax) * SPAD;
 #pragma unroll
-                    for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * sv0 : w[o];
+                        for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[ax][o] * sv0 : w[ax][o];
+                    }
+                } else {   // (plain lanes: the joint form costs the 2-CTA residency on config 2)
+                    double w[S];
+#pragma unroll
+                    for (int ax = 0; ax < D; ++ax) {
+                        kb_windows<M>(f0[ax], wc, w);
+                        double* dst = my_stage + (lane * D + ax) * SPAD;
+#pragma unroll
+                        for (int o = 0; o < S; ++o) dst[o] = (ax == 0) ? w[o] * sv0 : w[o];
+                    }
                 }
             }
             // advance the pipeline (loads of later sub-chunks overlap the accumulation)
@@ -488,6 +502,225 @@ __global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, Wi
     }
 }
 
+// ------------------------------------------------- d = 1: streaming kernels --
+// d = 1 layers put 10^3..10^5 points in a cell, so per-32-point descriptors
+// are pure overhead and the window polynomials are the work.  Each warp
+// streams a contiguous range of the sorted points, K1 points per lane per
+// step (lane l takes base + l + 32u): coalesced loads one step ahead (point
+// indices two ahead), the lane's K1 windows formed together (one
+// coefficient read feeds K1 FMAs) and consumed as they are formed.  A
+// point's cell comes from the per-cell start table (cells are sorted).
+constexpr int K1 = 4;
+constexpr int K1STEP = 32 * K1;
+
+__device__ __forceinline__ void warp_range(int64_t n, int64_t& lo, int64_t& hi) {
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5;
+    const int64_t W = (int64_t)gridDim.x * nw, gw = (int64_t)blockIdx.x * nw + warp;
+    const int64_t per = ((n + W - 1) / W + K1STEP - 1) / K1STEP * K1STEP;
+    lo = gw * per;
+    hi = lo + per < n ? lo + per : n;
+}
+
+// last key whose start is <= p
+__device__ __forceinline__ int key_of(const FsArgs& a, int64_t p) {
+    int kl = 0, kh = a.nkeys;
+    while (kh - kl > 1) {
+        const int mid = (kl + kh) >> 1;
+        if (__ldg(a.key_start + mid) <= p) kl = mid;
+        else kh = mid;
+    }
+    return kl;
+}
+
+// Spread: the lane's K1 points accumulate into registers for the warp's
+// current cell; a step whose 32 K1 points all lie in it (almost every step)
+// takes the fast path, otherwise the step is replayed slot by slot with a
+// flush (fixed xor-shuffle tree, lane 0 adds to the warp's tile) at every
+// cell boundary.  The CTA sums its warp tiles (grid_sum_kernel then sums the
+// CTAs): deterministic.
+template <int M>
+__global__ void __launch_bounds__(256, 2) spread1_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v,
+                                                         unsigned flags) {
+    constexpr int S = 2 * M + 1;
+    extern __shared__ double smem[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = a.tile_cells;
+    double* my_tile = smem + (size_t)warp * tile;
+    for (int i = lane; i < tile; i += 32) my_tile[i] = 0.0;
+    const bool sorted = (flags & MLB_SORTED) != 0, use_isd = (flags & MLB_USE_ISD) != 0;
+    int64_t lo, hi;
+    warp_range(a.n, lo, hi);
+    pdl_wait();  // v (and D^-1/2) may come from the stream predecessor
+    if (lo < hi) {
+        int cur = key_of(a, lo);
+        int64_t cstart = __ldg(a.key_start + cur), nxt = __ldg(a.key_start + cur + 1);
+        double acc[S];
+#pragma unroll
+        for (int o = 0; o < S; ++o) acc[o] = 0.0;
+        auto flush = [&]() {
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                double t = acc[o];
+#pragma unroll
+                for (int sh = 16; sh > 0; sh >>= 1) t += __shfl_xor_sync(0xffffffffu, t, sh);
+                if (lane == 0) my_tile[cur + o] += t;
+                acc[o] = 0.0;
+            }
+        };
+        auto ld_node = [&](int64_t base, int (&nd)[K1]) {
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                const int64_t p = base + 32 * u + lane;
+                nd[u] = (p < hi) ? (sorted ? (int)p : __ldg(a.perm + p)) : 0;
+            }
+        };
+        // raw loads only: the product s v is formed when the step consumes them,
+        // so the loads stay in flight across the previous step's arithmetic
+        auto ld_data = [&](int64_t base, const int (&nd)[K1], double (&f)[K1], double (&sc)[K1], double (&vv)[K1]) {
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                const int64_t p = base + 32 * u + lane;
+                const bool ok = p < hi;
+                f[u] = ok ? __ldg(a.frac + p) : 0.5;
+                sc[u] = (ok && use_isd) ? __ldg(a.isd + p) : 1.0;
+                vv[u] = ok ? __ldg(v + nd[u]) : 0.0;
+            }
+        };
+        int nd[K1];
+        double f[K1], sc[K1], vv[K1];
+        ld_node(lo, nd);
+        ld_data(lo, nd, f, sc, vv);
+        ld_node(lo + K1STEP, nd);
+        for (int64_t base = lo; base < hi; base += K1STEP) {
+            double fc[K1], svc[K1];
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                fc[u] = f[u];
+                svc[u] = sc[u] * vv[u];
+            }
+            if (base + K1STEP < hi) ld_data(base + K1STEP, nd, f, sc, vv);   // next step's data
+            if (base + 2 * K1STEP < hi) ld_node(base + 2 * K1STEP, nd);   // and the indices after it
+            const int64_t last = (base + K1STEP < hi ? base + K1STEP : hi) - 1;
+            if (last < nxt) {
+                kb_accumulate_k<M, K1>(fc, svc, wc, acc);
+                continue;
+            }
+#pragma unroll 1
+            for (int u = 0; u < K1; ++u) {   // a cell boundary inside this step
+                const int64_t g0 = base + 32 * u;
+                if (g0 >= hi) break;
+                const int64_t g1 = (g0 + 32 < hi ? g0 + 32 : hi) - 1;
+                const int64_t p = g0 + lane;
+                double fsel = fc[0], ssel = svc[0];   // slot u's values (constant indices: no stack)
+#pragma unroll
+                for (int k = 1; k < K1; ++k)
+                    if (u == k) {
+                        fsel = fc[k];
+                        ssel = svc[k];
+                    }
+                const double fu[1] = {fsel};
+                while (true) {
+                    const double su[1] = {(p <= g1 && p >= cstart && p < nxt) ? ssel : 0.0};
+                    kb_accumulate_k<M, 1>(fu, su, wc, acc);
+                    if (g1 < nxt) break;
+                    flush();
+                    cstart = nxt;   // the next non-empty cell starts here
+                    do {
+                        ++cur;
+                        nxt = __ldg(a.key_start + cur + 1);
+                    } while (nxt <= cstart);
+                }
+            }
+        }
+        flush();
+    }
+    pdl_launch();
+    __syncthreads();
+    double* out = a.partial + (size_t)blockIdx.x * tile;
+    for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += smem[(size_t)w * tile + i];
+        out[i] = t;
+    }
+}
+
+// Gather: the whole (tiny) d = 1 grid sits in shared memory; every lane
+// tracks its own points' cells (its points only move forward); epilogue
+// y = alpha v + s (beta acc + gamma s v).
+template <int M>
+__global__ void __launch_bounds__(256, 2) gather1_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
+                                                         const double* __restrict__ v, double* __restrict__ y,
+                                                         double alpha, double beta, double gamma, unsigned flags) {
+    extern __shared__ double gs[];
+    const int lane = threadIdx.x & 31;
+    const bool sorted = (flags & MLB_SORTED) != 0, use_isd = (flags & MLB_USE_ISD) != 0;
+    pdl_wait();  // the grid (convolution) and v come from stream predecessors
+    for (int i = threadIdx.x; i < a.g.L; i += blockDim.x) gs[i] = __ldcg(grid + i);
+    __syncthreads();
+    int64_t lo, hi;
+    warp_range(a.n, lo, hi);
+    if (lo < hi) {
+        int lc = key_of(a, lo + lane < hi ? lo + lane : hi - 1);
+        int64_t lnxt = __ldg(a.key_start + lc + 1);
+        auto ld_node = [&](int64_t base, int (&nd)[K1]) {
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                const int64_t p = base + 32 * u + lane;
+                nd[u] = (p < hi) ? (sorted ? (int)p : __ldg(a.perm + p)) : 0;
+            }
+        };
+        auto ld_data = [&](int64_t base, const int (&nd)[K1], double (&f)[K1], double (&sc)[K1], double (&vv)[K1]) {
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                const int64_t p = base + 32 * u + lane;
+                const bool ok = p < hi;
+                f[u] = ok ? __ldg(a.frac + p) : 0.5;
+                sc[u] = (ok && use_isd) ? __ldg(a.isd + p) : 1.0;
+                vv[u] = (ok && v) ? __ldg(v + nd[u]) : 0.0;
+            }
+        };
+        int nd[K1], ndn[K1];
+        double f[K1], sc[K1], vv[K1];
+        ld_node(lo, nd);
+        ld_data(lo, nd, f, sc, vv);
+        ld_node(lo + K1STEP, ndn);
+        for (int64_t base = lo; base < hi; base += K1STEP) {
+            double fc[K1], scc[K1], vc[K1];
+            int ndc[K1], cell[K1];
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                fc[u] = f[u];
+                scc[u] = sc[u];
+                vc[u] = vv[u];
+                ndc[u] = nd[u];
+                nd[u] = ndn[u];
+                const int64_t p = base + 32 * u + lane;
+                while (p < hi && p >= lnxt) {   // this lane's cell (points only move forward)
+                    ++lc;
+                    lnxt = __ldg(a.key_start + lc + 1);
+                }
+                cell[u] = lc;
+            }
+            if (base + K1STEP < hi) ld_data(base + K1STEP, nd, f, sc, vv);
+            if (base + 2 * K1STEP < hi) ld_node(base + 2 * K1STEP, ndn);
+            double acc[K1];
+#pragma unroll
+            for (int u = 0; u < K1; ++u) acc[u] = 0.0;
+            kb_dot_k<M, K1>(fc, wc, gs, cell, acc);
+#pragma unroll
+            for (int u = 0; u < K1; ++u) {
+                const int64_t p = base + 32 * u + lane;
+                if (p >= hi) continue;
+                const int node = ndc[u];
+                double res = alpha * vc[u] + scc[u] * (beta * acc[u] + gamma * scc[u] * vc[u]);
+                if (flags & MLB_ACCUMULATE) res += y[node];
+                y[node] = res;
+            }
+        }
+    }
+    pdl_launch();
+}
+
 // ------------------------------------------------------ spread d=3: cells --
 // The d = 3 spread works per CELL: all points of a cell (or of a part of at
 // most cell_cap points of a heavy cell) share one (2m+1)^3 stencil position,
@@ -565,7 +798,7 @@ __global__ void __launch_bounds__(256, (M >= 5) ? 1 : 2) spread_cells_kernel(FsA
                 const double sv = (lane < np) ? s0 * v0 : 0.0;
                 double w[S];
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
+                for (int ax = 0; ax < 3; ++ax) {   // (the joint 3-axis form spills at m = 4, gains nothing at m = 5)
                     kb_windows<M>(f0[ax], wc, w);
                     double* dst = stage + (lane * 3 + ax) * SPAD;
 #pragma unroll
@@ -1076,22 +1309,42 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
             __syncwarp();
             cur = key;
         }
-        double wA0[S], wA1[S], wA2[S], wB0[S], wB1[S], wB2[S];
+        // windows of both points and all axes: [A0 A1 A2 | B0 B1 B2] (first D of each)
+        double wAB[2 * D][S];
+        double (&wA0)[S] = wAB[0];
+        double (&wA1)[S] = wAB[D >= 2 ? 1 : 0];
+        double (&wA2)[S] = wAB[D == 3 ? 2 : 0];
+        double (&wB0)[S] = wAB[D];
+        double (&wB1)[S] = wAB[D >= 2 ? D + 1 : D];
+        double (&wB2)[S] = wAB[D == 3 ? D + 2 : D];
         if (flags & (1u << 17)) {  // ablation (profiling only): constant windows
 #pragma unroll
-            for (int q = 0; q < S; ++q) wA0[q] = wB0[q] = wA1[q] = wB1[q] = wA2[q] = wB2[q] = fA0 + fB1 + fA2;
-        } else {
-            kb_windows<M>(fA0, wc, wA0);
-            if (D >= 2) kb_windows<M>(fA1, wc, wA1);
-            if (D == 3) kb_windows<M>(fA2, wc, wA2);
-            if (two) {
-                kb_windows<M>(fB0, wc, wB0);
-                if (D >= 2) kb_windows<M>(fB1, wc, wB1);
-                if (D == 3) kb_windows<M>(fB2, wc, wB2);
-            } else {
+            for (int k = 0; k < 2 * D; ++k)
 #pragma unroll
-                for (int q = 0; q < S; ++q) wB0[q] = wB1[q] = wB2[q] = 0.0;
+                for (int q = 0; q < S; ++q) wAB[k][q] = fA0 + fB1 + fA2;
+        } else if (two) {   // one coefficient read feeds 2D FMAs
+            double fk[2 * D];
+            const double fa[3] = {fA0, fA1, fA2}, fb[3] = {fB0, fB1, fB2};
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                fk[k] = fa[k];
+                fk[D + k] = fb[k];
             }
+            kb_windows_k<M, 2 * D>(fk, wc, wAB);
+        } else {
+            double fk[D];
+            const double fa[3] = {fA0, fA1, fA2};
+#pragma unroll
+            for (int k = 0; k < D; ++k) fk[k] = fa[k];
+            double wa[D][S];
+            kb_windows_k<M, D>(fk, wc, wa);
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+#pragma unroll
+                for (int q = 0; q < S; ++q) {
+                    wAB[k][q] = wa[k][q];
+                    wAB[D + k][q] = 0.0;
+                }
         }
         double vA = 0.0, vB = 0.0;
         if (D >= 2) {
@@ -1216,6 +1469,8 @@ static FsArgs make_args(mlb_binding* b) {
     a.blocks = b->blocks;
     a.agrid = nullptr;
     a.cta_seg = nullptr;
+    a.key_start = b->key_start;
+    a.nkeys = b->nkeys;
     a.ggrp = reinterpret_cast<const int2*>(b->ggrp);
     a.gslot = b->gslot;
     a.ngrp = b->ngrp;
@@ -1242,6 +1497,18 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
     FsArgs a = make_args(b);
     const int nsm = device_sms();
     (void)nsm;
+    if constexpr (D == 1) {
+        if (b->key_start && b->n >= kStream1MinN) {   // streaming d = 1 spread
+            const size_t smem = (size_t)8 * b->tile_cells * sizeof(double);
+            if (int rc = ensure_max_smem((const void*)spread1_kernel<M>, smem)) return rc;
+            const int blocks = std::max(1, std::min(2 * nsm, (int)((b->n + 8 * K1STEP - 1) / (8 * K1STEP))));
+            b->spread_parts = blocks;
+            MLB_CUDA_TRY(launch_k(spread1_kernel<M>, dim3(blocks), dim3(256), smem, st, a, b->plan->wc, v, flags));
+            note_launches(1);
+            MLB_CUDA_TRY(cudaGetLastError());
+            return MLB_OK;
+        }
+    }
     if constexpr (D <= 2) {
         // persistent CTAs of 8 warps, one partial grid per CTA; banded d = 2:
         // kBandWarps-warp CTAs over their own segment ranges, one band tile each
@@ -1312,6 +1579,20 @@ static int gather_dmp(mlb_binding* b, const double* grid, const double* v, doubl
 template <int D, int M>
 static int gather_dm(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                      double beta, double gamma, unsigned flags, cudaStream_t st) {
+    if constexpr (D == 1) {
+        if (b->key_start && b->n >= kStream1MinN) {   // streaming d = 1 gather
+            FsArgs a = make_args(b);
+            const size_t smem = (size_t)b->plan->g.L * sizeof(double);
+            if (int rc = ensure_max_smem((const void*)gather1_kernel<M>, smem)) return rc;
+            const int nsm = device_sms();
+            const int blocks = std::max(1, std::min(2 * nsm, (int)((b->n + 8 * K1STEP - 1) / (8 * K1STEP))));
+            MLB_CUDA_TRY(launch_k(gather1_kernel<M>, dim3(blocks), dim3(256), smem, st, a, b->plan->wc, grid, v, y,
+                                  alpha, beta, gamma, flags));
+            note_launches(1);
+            MLB_CUDA_TRY(cudaGetLastError());
+            return MLB_OK;
+        }
+    }
     if (D == 3 && b->gather_packed) return gather_dmp<D, M, true>(b, grid, v, y, alpha, beta, gamma, flags, st);
     return gather_dmp<D, M, false>(b, grid, v, y, alpha, beta, gamma, flags, st);
 }

@@ -72,6 +72,7 @@ constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
 constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
 constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA
 constexpr int kBandWarps = 4;    // warps per banded d = 2 spread CTA
+constexpr int64_t kStream1MinN = 1 << 16;  // d = 1: streaming kernels from this many points
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
 
@@ -175,6 +176,9 @@ struct mlb_binding {
     int32_t* cta_seg = nullptr;      // ncta_band + 1
     int32_t* cta_row0 = nullptr;     // ncta_band
     int32_t* row_cta = nullptr;      // 2 x L
+    // d = 1 streaming spread / gather: first sorted point of every cell
+    int32_t* key_start = nullptr;    // nkeys + 1 (nullptr: sub-chunk kernels)
+    int nkeys = 0;
 };
 
 namespace mlb {

@@ -155,6 +155,74 @@ def test_banded_d2_spread_matches_oracle(grouped, layout):
     assert rel(y_band, y_full) < 1e-14
 
 
+@pytest.mark.parametrize("layout", ["uniform", "clustered"])
+def test_streaming_d1_kernels_match_oracle(layout):
+    """The streaming d = 1 spread / gather (contiguous warp ranges, per-cell
+    start table; used from 2^16 points): spread grid and gather against the
+    oracle, the fused Laplacian in node and cell order and with accumulation
+    against the sub-chunk kernels (MLB_D1_STREAM=0), repeated spreads bitwise."""
+    import os
+
+    import torch
+    from paper_2007_05239_b200 import KernelSpec, bind_points, build_plan
+    from paper_2007_05239_b200 import _lib
+    rng = np.random.default_rng(91)
+    n = 150_001
+    if layout == "uniform":
+        pts = rng.uniform(-0.2, 0.2, size=(n, 1))
+    else:   # empty cells, light cells and heavy ones
+        c = np.array([-0.15, -0.02, 0.0, 0.11])
+        pts = np.clip(c[rng.integers(0, 4, n)] + 0.004 * rng.standard_normal(n), -0.2, 0.2)[:, None]
+        pts[:40, 0] = np.linspace(-0.2, 0.2, 40)
+    v = rng.standard_normal(n)
+    plan = build_plan(KernelSpec("gaussian", 0.1), d=1, N=64, m_nfft=4, p_nfft=8)
+    b = bind_points(plan, pts)
+    L, ulo = b._plan_handle.L, b._plan_handle.ulo
+    lib = _lib.lib()
+    sp = _lib.stream_ptr()
+    vd = torch.from_numpy(v).cuda()
+    g1, g2 = (torch.zeros(L, dtype=torch.float64, device="cuda") for _ in range(2))
+    _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(vd), _lib.ptr(g1), 0, sp))
+    _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(vd), _lib.ptr(g2), 0, sp))
+    assert torch.equal(g1, g2)
+    op = fo.OraclePlan("gaussian", 0.1, 1, 64, 4, p=8)
+    ob = fo.bind(op, pts)
+    full = fo.spread(ob, v)
+    idx = np.mod(np.arange(ulo, ulo + L), op.ng)
+    assert rel(g1.cpu().numpy(), full[idx]) < 1e-13
+    conv = fo.convolve_grid(op, full)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    src = torch.from_numpy(np.ascontiguousarray(conv[idx])).cuda()
+    _lib.check(lib.mlb_gather(b.ptr, _lib.ptr(src), _lib.ptr(y), 0, sp))
+    assert rel(y.cpu().numpy(), fo.gather(ob, conv)) < 1e-13
+    # the fused Laplacian (node order, cell order, accumulate) vs the sub-chunk kernels
+    isd = torch.from_numpy(rng.uniform(0.5, 2.0, n)).cuda()
+    os.environ["MLB_D1_STREAM"] = "0"
+    try:
+        b0 = bind_points(plan, pts)
+    finally:
+        del os.environ["MLB_D1_STREAM"]
+    outs = []
+    for bb in (b, b0):
+        _lib.check(lib.mlb_binding_set_isd(bb.ptr, _lib.ptr(isd), sp))
+        r = []
+        for flags in (_lib.MLB_USE_ISD, _lib.MLB_USE_ISD | _lib.MLB_ACCUMULATE):
+            yy = torch.ones(n, dtype=torch.float64, device="cuda")
+            _lib.check(lib.mlb_apply(bb.ptr, _lib.ptr(vd), _lib.ptr(yy), 1.7, -1.0, 1.0, flags, sp))
+            r.append(yy.cpu().numpy())
+        vs = torch.empty_like(vd)
+        _lib.check(lib.mlb_to_sorted(bb.ptr, _lib.ptr(vd), _lib.ptr(vs), sp))
+        ys = torch.empty_like(vd)
+        _lib.check(lib.mlb_apply(bb.ptr, _lib.ptr(vs), _lib.ptr(ys), 1.7, -1.0, 1.0,
+                                 _lib.MLB_USE_ISD | _lib.MLB_SORTED, sp))
+        yn = torch.empty_like(vd)
+        _lib.check(lib.mlb_to_node(bb.ptr, _lib.ptr(ys), _lib.ptr(yn), 0, sp))
+        r.append(yn.cpu().numpy())
+        outs.append(r)
+    for a_, b_ in zip(*outs):
+        assert rel(a_, b_) < 1e-14
+
+
 def test_laplacian_matches_reference_golden():
     from paper_2007_05239_b200 import KernelSpec, build_plan
     from paper_2007_05239_b200.graphs import KernelWeights, apply_sym_laplacian, build_layer, with_shift
