@@ -91,7 +91,10 @@ struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
         cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
+        // a failed switch must not leave cudaErrorInvalidDevice as the
+        // runtime's last error: libcudart is shared with torch, whose next
+        // launch check would report it
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) (void)cudaGetLastError();
     }
     ~DeviceGuard() {
         int cur = -1;
@@ -232,7 +235,9 @@ int mlb_plan_destroy(mlb_plan* p) {
 
 int mlb_binding_destroy(mlb_binding* b) {
     if (!b) return MLB_OK;
-    DeviceGuard guard(b->plan->device);
+    // the binding's own copy of the device: a plan may be destroyed first
+    // (finalizer order inside a collected reference cycle is arbitrary)
+    DeviceGuard guard(b->device);
     dev_free(b->perm);
     dev_free(b->frac);
     dev_free(b->chunk_start);
@@ -693,6 +698,7 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     }
     mlb_binding* b = new mlb_binding();
     b->plan = plan;
+    b->device = plan->device;
     b->n = n;
     b->nchunks = nch;
     b->ngrp = ngrp;

@@ -115,6 +115,7 @@ struct mlb_plan {
 
 struct mlb_binding {
     const mlb_plan* plan;
+    int device = 0;                  // plan->device, kept for destroy
     int64_t n;
     int nchunks, nseg, nbricks;
     // device tables

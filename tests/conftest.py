@@ -46,3 +46,25 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _no_stale_cuda_error(request):
+    """GPU tests must not leave an error in the CUDA runtime's last-error slot:
+    libmlb shares libcudart with torch, whose next launch check would report
+    it inside an unrelated test."""
+    yield
+    if "gpu" not in request.node.keywords or not gpu_available():
+        return
+    import ctypes
+    import gc
+
+    import torch
+    gc.collect()   # finalizers (binding / plan destroy) run inside this test
+    torch.cuda.synchronize()
+    rt = ctypes.CDLL("libcudart.so.12")   # the loaded runtime (matched by soname)
+    code = rt.cudaPeekAtLastError()
+    if code != 0:
+        rt.cudaGetLastError()
+        rt.cudaGetErrorString.restype = ctypes.c_char_p
+        pytest.fail(f"test left CUDA error {code} ({rt.cudaGetErrorString(code).decode()}) in the runtime")
