@@ -53,6 +53,8 @@ def test_pipeline_matches_frozen_reference(tag, config, side):
     assert rel.max() <= 1e-7, rel
     Z = np.random.default_rng(12345).standard_normal((wl.n, 2))   # oracle/gen_golden_cfg.sketch_seeds
     P = basis.vectors @ (basis.vectors.T @ Z)
+    if "sketch_idx" in g:   # large fixtures keep a strided row subset of the sketch
+        P = P[g["sketch_idx"]]
     sk = g["sketch"].astype(np.float64)
     perr = np.linalg.norm(P - sk) / np.linalg.norm(sk)
     print(f"{tag}: projector sketch rel err {perr:.2e}")
