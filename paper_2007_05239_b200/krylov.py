@@ -596,10 +596,16 @@ def _ab_ld(dim):
     return 2 * dim + 5
 
 
-def _device_coeffs_ok(dim):
+def _device_coeffs_ok(dim, T):
     """Lockstep PKSM coefficients on the device (mlb_tridiag_fn_batched):
-    dim <= 64; MLB_PKSM_DEVICE_COEFFS=0 keeps the host's batched eigh."""
-    return dim <= 64 and os.environ.get("MLB_PKSM_DEVICE_COEFFS", "1") != "0"
+    dim <= 64 and at least 2 chains -- one chain's host eigh is cheaper than
+    the QL kernel's latency on the step's critical path (config 2's per-layer
+    graphs: eigensolve 0.29 -> 0.41 s with it).  MLB_PKSM_DEVICE_COEFFS=0 /
+    1 forces the host / device."""
+    env = os.environ.get("MLB_PKSM_DEVICE_COEFFS")
+    if env is not None:
+        return dim <= 64 and env != "0"
+    return dim <= 64 and T >= 2
 
 
 def _issue_coeffs(P, T, j, dim, p, sp):
@@ -681,7 +687,7 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
         x.V = _krylov_basis(dev, t, dim, n)
         scale_by(x.vs, x.V[0], vv, -0.5)
     use_graphs = _graphs_enabled()
-    dev_coeffs = _device_coeffs_ok(dim)
+    dev_coeffs = _device_coeffs_ok(dim, T)
     gkey = (dev.index, _VPOOL_DEPTH[0], dim, n, tuple(int(x.b.ptr.value) for x in st),
             tuple((x.a, x.K0) for x in st), tuple(x.V.data_ptr() for x in st), AB.data_ptr(),
             _batched_cgs_ok(dim, n), dev_coeffs, float(p) if dev_coeffs else None)
