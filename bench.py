@@ -471,11 +471,15 @@ def run_ours(args):
         ys = [torch.empty_like(v) for _ in range(T)]
 
         def step():
-            sg.lsym(v, ys)
+            if args.no_cuda_graph:
+                sg.lsym(v, ys)
+            else:
+                sg.lsym_graph(v, ys)
         parallelism = (f"node-range sharded x{ws}: rank r owns nodes [r n/{ws}, (r+1) n/{ws}) of every layer; per "
                        "layer one NCCL all-reduce of its sub-box grid per step")
         streams = ("one stream per layer (the d=3 layer at high priority, the cheap layer issued first): spread -> "
-                   "NCCL all-reduce of the layer's grid -> convolve -> fused gather")
+                   "NCCL all-reduce of the layer's grid -> convolve -> fused gather; the whole step replayed from one "
+                   "captured CUDA graph" + (" (disabled)" if args.no_cuda_graph else ""))
 
     # the e2e leg's pinned host buffers are allocated at setup: a freshly
     # pinned buffer transfers 2-3x slower for a while on the pool's boxes

@@ -593,6 +593,44 @@ class ShardedKernelGraph:
         """ys[t] = D^-1/2 W D^-1/2 v (the apply_one_minus_L1 term, powermean.py:75-76)."""
         return self._step(v, ys, [(0.0, 1.0, -k0) for k0 in self.K0], _lib.MLB_USE_ISD)
 
+    def lsym_graph(self, v, ys):
+        """`lsym` replayed from a CUDA graph captured once per (v, ys) buffer
+        set: the per-layer streams, the NCCL all-reduces (NCCL supports stream
+        capture; the communicator is warmed up by one eager step on a side
+        stream first) and every kernel, with no host issue gaps (projected
+        per-rank step at N = 8: 0.57 -> 0.53 ms).  Falls back to the eager
+        step (and remembers it) if the capture fails."""
+        torch = _torch()
+        if getattr(self, "_graphs", None) is None:
+            self._graphs = {}
+        key = (v.data_ptr(), tuple(y.data_ptr() for y in ys))
+        ent = self._graphs.get(key)
+        if ent is None:
+            lib = _lib.lib()
+            main = torch.cuda.current_stream(self.dev)
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.lsym(v, ys)
+            main.wait_stream(side)
+            torch.cuda.synchronize(self.dev)
+            try:
+                g = torch.cuda.CUDAGraph()
+                l0 = lib.mlb_launch_count()
+                with torch.cuda.graph(g):
+                    self.lsym(v, ys)
+                ent = (g, int(lib.mlb_launch_count() - l0))
+            except Exception:   # capture unsupported here: eager from now on
+                torch.cuda.synchronize(self.dev)
+                ent = (None, 0)
+            self._graphs[key] = ent
+        g, cnt = ent
+        if g is None:
+            return self.lsym(v, ys)
+        g.replay()
+        _lib.lib().mlb_note_launches(cnt)
+        return ys
+
     def lsym_many(self, V, out=None):
         """(k, T, n_local): `lsym` of k host vectors (rows of V, this rank's
         slices), streamed like LaplacianBatch.apply_many: vector i+1's H2D and

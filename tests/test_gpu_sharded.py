@@ -62,6 +62,14 @@ def test_sharded_graph_nccl_world1_equals_unsharded():
         ref = LaplacianBatch(MultilayerGraph(tuple(with_shift(lay, delta) for lay in G.layers))).apply_dev(v)
         for t in range(len(ys)):
             assert torch.equal(ys[t], ref[t]), t
+        # the step replayed from a captured CUDA graph (NCCL all-reduces inside)
+        # equals the eager step bitwise, replay after replay
+        yg = [torch.empty_like(v) for _ in range(len(ys))]
+        for _ in range(3):
+            sg.lsym_graph(v, yg)
+        assert sg._graphs[(v.data_ptr(), tuple(y.data_ptr() for y in yg))][0] is not None   # captured
+        for t in range(len(ys)):
+            assert torch.equal(yg[t], ref[t]), t
         # the streamed host-in / host-out form: every vector's results equal
         # the per-vector step bitwise
         V = torch.from_numpy(np.random.default_rng(6).standard_normal((5, wl.n))).pin_memory()

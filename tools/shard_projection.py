@@ -46,29 +46,57 @@ def main():
     delta = math.log(2.0)
     res = {"workload": wl.name, "n": wl.n, "allreduce_us_assumed": a.allreduce_us, "worlds": {}}
 
+    import time
+
     def time_step(sg, v, ys):
         for _ in range(3):
             sg.lsym(v, ys)
         torch.cuda.synchronize()
         tot = 0.0
+        cpu = 0.0
+        for _ in range(a.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record()
+            sg.lsym(v, ys)
+            e1.record()
+            cpu += time.perf_counter() - t0
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        # the same step replayed from a captured CUDA graph (no host issue time inside)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            sg.lsym(v, ys)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            sg.lsym(v, ys)
+        gt = 0.0
         for _ in range(a.steps):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            sg.lsym(v, ys)
+            g.replay()
             e1.record()
             e1.synchronize()
-            tot += e0.elapsed_time(e1)
-        return tot / a.steps
+            gt += e0.elapsed_time(e1)
+        return tot / a.steps, cpu / a.steps * 1e3, gt / a.steps
 
     for N in [1] + list(a.worlds):
-        per_rank = []
+        per_rank, cpu_ms, graph_ms = [], [], []
         for r in range(N):
             lo, hi, pts, kerns, plans = shard_feature_groups(wl.X, groups, r, N)
             sg = ShardedKernelGraph(pts, kerns, plans, wl.n, lo, hi, comm=None, shift=delta, device=0).build()
             v = torch.from_numpy(rng.standard_normal(hi - lo)).cuda()
             ys = [torch.empty_like(v) for _ in range(len(wl.layers))]
-            per_rank.append(time_step(sg, v, ys))
+            t_ev, t_cpu, t_graph = time_step(sg, v, ys)
+            per_rank.append(t_ev)
+            cpu_ms.append(t_cpu)
+            graph_ms.append(t_graph)
             if r == 0:
                 import bench
                 st = bench.stage_breakdown(torch, sg.weights, v)
@@ -79,9 +107,11 @@ def main():
         worst = max(per_rank)
         proj = worst + (a.allreduce_us * 1e-3 if N > 1 else 0.0)
         res["worlds"][N] = {"per_rank_compute_ms": per_rank, "max_compute_ms": worst,
+                            "host_issue_ms": cpu_ms, "graph_replay_ms": graph_ms,
                             "projected_step_ms": proj, "rank0_stages_ms": stages0,
                             "projected_value": wl.n * len(wl.layers) / (proj * 1e-3)}
-        print(N, ["%.3f" % x for x in per_rank], "projected %.3f ms" % proj, flush=True)
+        print(N, ["%.3f" % x for x in per_rank], "projected %.3f ms" % proj, "host issue",
+              ["%.3f" % x for x in cpu_ms], "graph", ["%.3f" % x for x in graph_ms], flush=True)
     base = res["worlds"][1]["projected_step_ms"]
     for N, r in res["worlds"].items():
         r["projected_speedup"] = base / r["projected_step_ms"]
