@@ -507,7 +507,7 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
         if (const char* env = std::getenv("MLB_D2_BANDED")) banded = d == 2 && env[0] == '1';  // tests / A/B
         if (banded && nseg > 0) {
             const int S = 2 * g.m + 1;
-            const int nc = std::min(nsm * 3, std::max(1, nseg / kBandWarps));
+            const int nc = std::min(nsm * kBandCtasPerSm, std::max(1, nseg / kBandWarps));
             std::vector<int32_t> cs(nc + 1), r0(nc), r1(nc);
             int rows = 0;
             for (int c = 0; c <= nc; ++c) cs[c] = (int32_t)((int64_t)nseg * c / nc);

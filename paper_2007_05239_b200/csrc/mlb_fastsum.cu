@@ -177,7 +177,8 @@ __device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps
 }
 
 template <int D, int M, bool PERSIST, bool GROUPED = false>
-__global__ void __launch_bounds__(PERSIST ? 256 : 64) spread_kernel(FsArgs a, WinCoef wc,
+__global__ void __launch_bounds__(PERSIST ? (GROUPED ? 32 * kBandWarps : 256) : 64, GROUPED ? kBandCtasPerSm : 1)
+spread_kernel(FsArgs a, WinCoef wc,
                                                                     const double* __restrict__ v, unsigned flags,
                                                                     int* __restrict__ work) {
     using C = SpreadCfg<D, M>;
@@ -1517,15 +1518,15 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
             a.cta_seg = b->cta_seg;
             a.tile_cells = b->band_tile;
         }
-        int nw = banded ? kBandWarps : 8;
+        bool grouped = D == 2 && b->n >= (1 << 20);
+        if (const char* env = std::getenv("MLB_D2_GROUPED")) grouped = D == 2 && env[0] == '1';  // tests / tuning
+        int nw = (banded || grouped) ? kBandWarps : 8;   // (the grouped kernel's launch bounds: kBandWarps warps)
         while (!banded && nw > 1 && spread_smem<D, M>(nw, b->tile_cells) > 110 * 1024) --nw;
         const size_t smem = spread_smem<D, M>(nw, a.tile_cells);
         if (smem > 220 * 1024) return fail(MLB_ERR_CONFIG, "spread tile too large for shared memory");
         // grouped d = 2 lanes pay off on large layers (config 4: 622 -> 498
         // us); at config-2 size the plain lane blocks leave more room for
         // the concurrently running d = 3 layer (step 3.96 vs 3.86e9)
-        bool grouped = D == 2 && b->n >= (1 << 20);
-        if (const char* env = std::getenv("MLB_D2_GROUPED")) grouped = D == 2 && env[0] == '1';  // tests / tuning
         auto kern = grouped ? spread_kernel<D, M, true, true> : spread_kernel<D, M, true, false>;
         MLB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int blocks = banded ? b->ncta_band : std::min(b->spread_parts_max, (b->nseg + nw - 1) / nw);

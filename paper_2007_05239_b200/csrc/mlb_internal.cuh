@@ -72,6 +72,10 @@ constexpr int kChunk = 64;        // points per chunk (<= 2 per warp lane)
 constexpr int kItemInts = 32;   // d = 3 spread item row: nb + 3 x (<= 8) entries, padded
 constexpr int kCellWarps = 8;   // warps per d = 3 spread CTA
 constexpr int kBandWarps = 4;    // warps per banded d = 2 spread CTA
+#ifndef MLB_BAND_CTAS
+#define MLB_BAND_CTAS 3
+#endif
+constexpr int kBandCtasPerSm = MLB_BAND_CTAS;   // resident banded spread CTAs per SM (launch bounds, grid; 4 = 128 registers: spills, d=2 spread 0.35 -> 0.56 ms)
 constexpr int64_t kStream1MinN = 1 << 16;  // d = 1: streaming kernels from this many points
 constexpr int kSegPoints = 256;   // points per spread work unit (one warp)
 constexpr int kMaxWinCoef = 17;   // monomial degree <= 16
