@@ -318,3 +318,33 @@ def masks_from_labels(labels, shapes):
         raise ConfigError(f"label vector length {labels.shape[0]} does not match shapes {shapes}")
     starts = np.concatenate([[0], ends[:-1]])
     return [labels[a:b].reshape(h, w) for a, b, (h, w) in zip(starts, ends, shapes)]
+
+
+# ------------------------------------------------------------- file formats --
+# The reference keeps its CSV readers / writers in datapipe (datapipe.py:392-
+# 470); here they live in csvio and are re-exported under the same names.
+from .csvio import load_features_csv, load_labels_csv, write_predictions_csv  # noqa: E402
+from .csvio import write_matrix_csv as write_scores_csv  # noqa: E402
+from .csvio import write_matrix_csv as write_values_csv  # noqa: E402
+
+
+# ------------------------------------------------- out of scope --
+# Stochastic block models (datapipe.py:178-279) build edge-list layers with no
+# NFFT kernel path; the names exist so a drop-in `from multilap.datapipe
+# import ...` resolves, and using them raises ConfigError.
+def _sbm_unsupported(*_args, **_kwargs):
+    raise ConfigError("stochastic block models are not part of the B200 backend "
+                      "(edge-list layers have no NFFT kernel path; use the reference package)")
+
+
+class SbmLayerSpec:
+    def __init__(self, *args, **kwargs):
+        _sbm_unsupported()
+
+
+class SbmSpec:
+    def __init__(self, *args, **kwargs):
+        _sbm_unsupported()
+
+
+sbm_generate = noisy_pair_sbm = complementary_sbm = _sbm_unsupported

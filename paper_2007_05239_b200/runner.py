@@ -379,15 +379,21 @@ def run_fastsum_bench(cfg, seed, out_dir=".", threads=1):
         fh.write("d,n,rel_error,t_fast,t_direct\n")
         for r in accuracy:
             fh.write(f"{r['d']},{r['n']},{r['rel_error']:.3e},{r['t_fast']:.6f},{r['t_direct']:.6f}\n")
+    # the reference's CSV exactly (a drop-in consumer parses it); the device
+    # times go to their own file and report.json
     scale_path = os.path.join(out_dir, "fastsum_scaling.csv")
     with open(scale_path, "w", encoding="utf-8") as fh:
-        fh.write("n,t_fast_median" + (",t_direct_median" if with_direct else "") + ",t_fast_device_median\n")
+        fh.write("n,t_fast_median" + (",t_direct_median" if with_direct else "") + "\n")
         for i, n in enumerate(sizes):
             cols = [f"{n}", f"{scaling['t_fast'][i]:.6f}"]
             if with_direct:
                 cols.append(f"{scaling['t_direct'][i]:.6f}")
-            cols.append(f"{scaling['t_fast_device'][i]:.6f}")
             fh.write(",".join(cols) + "\n")
+    dev_path = os.path.join(out_dir, "fastsum_scaling_device.csv")
+    with open(dev_path, "w", encoding="utf-8") as fh:
+        fh.write("n,t_fast_device_median\n")
+        for i, n in enumerate(sizes):
+            fh.write(f"{n},{scaling['t_fast_device'][i]:.6f}\n")
     txt_path = os.path.join(out_dir, "fastsum_bench.txt")
     with open(txt_path, "w", encoding="utf-8") as fh:
         fh.write(f"kernel {kernel.family}, sigma {kernel.sigma:g} (box units), N={params['N']}, "
@@ -402,7 +408,8 @@ def run_fastsum_bench(cfg, seed, out_dir=".", threads=1):
                 line += f"  direct {scaling['t_direct'][i]:.4f}s"
             fh.write(line + "\n")
     report = {"command": "fastsum-bench", "seed": seed, "accuracy": accuracy, "scaling": scaling, "config": cfg}
-    return _finish(out_dir, report, clock, {"accuracy_csv": acc_path, "scaling_csv": scale_path, "table": txt_path})
+    return _finish(out_dir, report, clock, {"accuracy_csv": acc_path, "scaling_csv": scale_path,
+                                            "scaling_device_csv": dev_path, "table": txt_path})
 
 
 def _unsupported(name):

@@ -151,5 +151,7 @@ def test_cli_fastsum_bench(tmp_path):
     assert errs[1] < 1e-6 and errs[2] < 1e-5 and errs[3] < 1e-3
     assert len(rep["scaling"]["t_fast"]) == 2 and all(t > 0 for t in rep["scaling"]["t_fast_device"])
     head = (tmp_path / "fastsum_scaling.csv").read_text().splitlines()[0]
-    assert head == "n,t_fast_median,t_direct_median,t_fast_device_median"
+    assert head == "n,t_fast_median,t_direct_median"   # the reference's format (ref test_cli.py:215)
+    dev = (tmp_path / "fastsum_scaling_device.csv").read_text().splitlines()
+    assert dev[0] == "n,t_fast_device_median" and len(dev) == 3
     assert os.path.exists(tmp_path / "fastsum_bench.txt")
