@@ -623,6 +623,8 @@ class ShardedKernelGraph:
             except Exception:   # capture unsupported here: eager from now on
                 torch.cuda.synchronize(self.dev)
                 ent = (None, 0)
+            if len(self._graphs) >= 4:   # a few buffer sets at most (each graph pins its buffers' addresses)
+                self._graphs.pop(next(iter(self._graphs)))
             self._graphs[key] = ent
         g, cnt = ent
         if g is None:
