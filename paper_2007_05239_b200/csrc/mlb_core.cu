@@ -153,7 +153,7 @@ int mlb_plan_create(const mlb_plan_desc* desc, int device, mlb_plan** out) {
         return fail(MLB_ERR_CONFIG, "m_nfft must lie in [2, " + std::to_string(kMaxM) + "] on the GPU path");
     if (ng < N + 2 || ng % 2) return fail(MLB_ERR_CONFIG, "invalid oversampled grid size");
     if (desc->bin_hi < desc->bin_lo) return fail(MLB_ERR_CONFIG, "empty bin range");
-    const int want_deg = (m <= 3) ? 16 : 14;
+    const int want_deg = (m <= 3) ? 15 : 13;   // mlb_window.cuh WinDeg
     if (desc->win_deg != want_deg)
         return fail(MLB_ERR_CONFIG, "window polynomial degree must be " + std::to_string(want_deg));
     DeviceGuard guard(device);

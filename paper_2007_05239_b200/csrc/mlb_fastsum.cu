@@ -555,18 +555,28 @@ __global__ void __launch_bounds__(256, 2) spread1_kernel(FsArgs a, WinCoef wc, c
     if (lo < hi) {
         int cur = key_of(a, lo);
         int64_t cstart = __ldg(a.key_start + cur), nxt = __ldg(a.key_start + cur + 1);
-        double acc[S];
+        // the current cell's even / odd pair sums and the o = -m sum (kb_accumulate_k)
+        double ae[M], ao[M], a0 = 0.0;
 #pragma unroll
-        for (int o = 0; o < S; ++o) acc[o] = 0.0;
+        for (int q = 0; q < M; ++q) ae[q] = ao[q] = 0.0;
         auto flush = [&]() {
+            double acc[S];
+            acc[0] = a0;
+#pragma unroll
+            for (int q = 1; q <= M; ++q) {
+                acc[q + M] = ae[q - 1] + ao[q - 1];
+                acc[1 - q + M] = ae[q - 1] - ao[q - 1];
+            }
 #pragma unroll
             for (int o = 0; o < S; ++o) {
                 double t = acc[o];
 #pragma unroll
                 for (int sh = 16; sh > 0; sh >>= 1) t += __shfl_xor_sync(0xffffffffu, t, sh);
                 if (lane == 0) my_tile[cur + o] += t;
-                acc[o] = 0.0;
             }
+#pragma unroll
+            for (int q = 0; q < M; ++q) ae[q] = ao[q] = 0.0;
+            a0 = 0.0;
         };
         auto ld_node = [&](int64_t base, int (&nd)[K1]) {
 #pragma unroll
@@ -603,7 +613,7 @@ __global__ void __launch_bounds__(256, 2) spread1_kernel(FsArgs a, WinCoef wc, c
             if (base + 2 * K1STEP < hi) ld_node(base + 2 * K1STEP, nd);   // and the indices after it
             const int64_t last = (base + K1STEP < hi ? base + K1STEP : hi) - 1;
             if (last < nxt) {
-                kb_accumulate_k<M, K1>(fc, svc, wc, acc);
+                kb_accumulate_k<M, K1>(fc, svc, wc, ae, ao, a0);
                 continue;
             }
 #pragma unroll 1
@@ -622,7 +632,7 @@ __global__ void __launch_bounds__(256, 2) spread1_kernel(FsArgs a, WinCoef wc, c
                 const double fu[1] = {fsel};
                 while (true) {
                     const double su[1] = {(p <= g1 && p >= cstart && p < nxt) ? ssel : 0.0};
-                    kb_accumulate_k<M, 1>(fu, su, wc, acc);
+                    kb_accumulate_k<M, 1>(fu, su, wc, ae, ao, a0);
                     if (g1 < nxt) break;
                     flush();
                     cstart = nxt;   // the next non-empty cell starts here
@@ -652,11 +662,23 @@ template <int M>
 __global__ void __launch_bounds__(256, 2) gather1_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
                                                          const double* __restrict__ v, double* __restrict__ y,
                                                          double alpha, double beta, double gamma, unsigned flags) {
-    extern __shared__ double gs[];
+    constexpr int TS = 2 * M + 1;
+    extern __shared__ double gs[];   // the grid (L), then per cell c: g[c], (GS, GD) per q (kb_dot_k)
+    double* tab = gs + a.g.L;
     const int lane = threadIdx.x & 31;
     const bool sorted = (flags & MLB_SORTED) != 0, use_isd = (flags & MLB_USE_ISD) != 0;
     pdl_wait();  // the grid (convolution) and v come from stream predecessors
     for (int i = threadIdx.x; i < a.g.L; i += blockDim.x) gs[i] = __ldcg(grid + i);
+    __syncthreads();
+    for (int c = threadIdx.x; c < a.nkeys; c += blockDim.x) {
+        tab[c * TS] = gs[c];
+#pragma unroll
+        for (int q = 1; q <= M; ++q) {
+            const double hi_ = gs[c + q + M], lo_ = gs[c + 1 - q + M];
+            tab[c * TS + 2 * q - 1] = hi_ + lo_;
+            tab[c * TS + 2 * q] = hi_ - lo_;
+        }
+    }
     __syncthreads();
     int64_t lo, hi;
     warp_range(a.n, lo, hi);
@@ -707,7 +729,7 @@ __global__ void __launch_bounds__(256, 2) gather1_kernel(FsArgs a, WinCoef wc, c
             double acc[K1];
 #pragma unroll
             for (int u = 0; u < K1; ++u) acc[u] = 0.0;
-            kb_dot_k<M, K1>(fc, wc, gs, cell, acc);
+            kb_dot_k<M, K1>(fc, wc, tab, cell, acc);
 #pragma unroll
             for (int u = 0; u < K1; ++u) {
                 const int64_t p = base + 32 * u + lane;
@@ -1583,7 +1605,7 @@ static int gather_dm(mlb_binding* b, const double* grid, const double* v, double
     if constexpr (D == 1) {
         if (b->key_start && b->n >= kStream1MinN) {   // streaming d = 1 gather
             FsArgs a = make_args(b);
-            const size_t smem = (size_t)b->plan->g.L * sizeof(double);
+            const size_t smem = ((size_t)b->plan->g.L + (size_t)b->nkeys * (2 * M + 1)) * sizeof(double);
             if (int rc = ensure_max_smem((const void*)gather1_kernel<M>, smem)) return rc;
             const int nsm = device_sms();
             const int blocks = std::max(1, std::min(2 * nsm, (int)((b->n + 8 * K1STEP - 1) / (8 * K1STEP))));

@@ -3,7 +3,7 @@
 // phi(t) = sinh(b sqrt(m^2-t^2)) / (pi sqrt(m^2-t^2)) (and its sin / b/pi
 // branches) is ONE entire function of z = m^2 - t^2, so for the 2m+1 stencil
 // offsets o = -m..m the values phi(f - o), f in [0,1), are entire functions
-// of s = 2f - 1 and are reproduced to ~1e-15 of max(phi) by degree-14/16
+// of s = 2f - 1 and are reproduced to ~1e-15 of max(phi) by degree-13/15
 // polynomials (fitted on the host, checked at plan build).  The symmetry
 // phi(t) = phi(-t) gives P_{1-q}(s) = P_q(-s), so q = 1..m share one even
 // part E_q(s^2) and one odd part O_q(s^2): two windows for one polynomial.
@@ -12,11 +12,14 @@
 
 namespace mlb {
 
+// Odd degrees: P = E(s^2) + s O(s^2) with equally many even and odd terms.
+// Degree 13 (m >= 4) / 15 (m <= 3) fits as tightly as 14 / 16 did (<= 5e-15
+// of max phi through float64 Horner) and saves one FMA per polynomial.
 template <int M>
 struct WinDeg {
-    static constexpr int deg = (M <= 3) ? 16 : 14;
-    static constexpr int ne = deg / 2 + 1;  // s^0, s^2, ..., s^deg
-    static constexpr int no = deg / 2;      // s^1, s^3, ..., s^(deg-1)
+    static constexpr int deg = (M <= 3) ? 15 : 13;
+    static constexpr int ne = deg / 2 + 1;        // s^0, s^2, ..., s^(deg-1)
+    static constexpr int no = (deg + 1) / 2;      // s^1, s^3, ..., s^deg
 };
 
 // w[o + M] = phi(f - o), o = -M..M
@@ -102,20 +105,25 @@ __device__ __forceinline__ void kb_windows_k(const double (&f)[K], const WinCoef
     for (int k = 0; k < K; ++k) w[k][0] = pm[k];
 }
 
-// acc[o] += sum_k phi(f_k - o) sv_k for K points of a lane, windows consumed
-// as they are formed (no K x (2m+1) window array held): the d = 1 streaming
-// spread.  Same per-point window arithmetic as kb_windows.
+// The d = 1 streaming kernels never need the window VALUES, only their sums
+// against sv (spread) or the grid (gather), and the pair P_q(s) = E_q + s O_q,
+// P_{1-q}(s) = E_q - s O_q shares E_q and O_q.  So the spread keeps the even
+// and odd sums apart -- ae[q] += E_q sv, ao[q] += O_q (s sv), a0 += P_{-m} sv:
+// two FMAs per pair instead of the product, two adds and two FMAs -- and the
+// cell's window sums are formed at the flush: acc[q+m] = ae + ao, acc[1-q+m]
+// = ae - ao.  Same arithmetic as kb_windows up to that association.
 template <int M, int K>
 __device__ __forceinline__ void kb_accumulate_k(const double (&f)[K], const double (&sv)[K], const WinCoef& c,
-                                                double (&acc)[2 * M + 1]) {
+                                                double (&ae)[M], double (&ao)[M], double& a0) {
     constexpr int NE = WinDeg<M>::ne;
     constexpr int NO = WinDeg<M>::no;
     constexpr int DM = WinDeg<M>::deg;
-    double s[K], s2[K];
+    double s[K], s2[K], ssv[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         s[k] = 2.0 * f[k] - 1.0;
         s2[k] = s[k] * s[k];
+        ssv[k] = s[k] * sv[k];
     }
 #pragma unroll
     for (int q = 1; q <= M; ++q) {
@@ -139,9 +147,8 @@ __device__ __forceinline__ void kb_accumulate_k(const double (&f)[K], const doub
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const double o = od[k] * s[k];
-            acc[q + M] = fma(e[k] + o, sv[k], acc[q + M]);
-            acc[1 - q + M] = fma(e[k] - o, sv[k], acc[1 - q + M]);
+            ae[q - 1] = fma(e[k], sv[k], ae[q - 1]);
+            ao[q - 1] = fma(od[k], ssv[k], ao[q - 1]);
         }
     }
     double pm[K];
@@ -154,23 +161,27 @@ __device__ __forceinline__ void kb_accumulate_k(const double (&f)[K], const doub
         for (int k = 0; k < K; ++k) pm[k] = fma(pm[k], s[k], cj);
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[0] = fma(pm[k], sv[k], acc[0]);
+    for (int k = 0; k < K; ++k) a0 = fma(pm[k], sv[k], a0);
 }
 
-// acc[k] += sum_o phi(f_k - o) g_k[o] for K points of a lane (g_k: the
-// (2m+1) grid values of point k's stencil), windows consumed as formed: the
-// d = 1 streaming gather.
+// Gather counterpart: acc_k = P_{-m} g[c] + sum_q E_q GS[c][q] + s sum_q O_q
+// GD[c][q] with the per-cell pair sums GS = g[c+q+m] + g[c+1-q+m] and
+// differences GD = g[c+q+m] - g[c+1-q+m] precomputed (tab: per cell, 2m + 1
+// doubles: g[c], then (GS, GD) per q).  2m + 3 FP64 ops per point besides the
+// Horner steps, instead of 5m + 1.
 template <int M, int K>
-__device__ __forceinline__ void kb_dot_k(const double (&f)[K], const WinCoef& c, const double* __restrict__ gbase,
+__device__ __forceinline__ void kb_dot_k(const double (&f)[K], const WinCoef& c, const double* __restrict__ tab,
                                          const int (&cell)[K], double (&acc)[K]) {
     constexpr int NE = WinDeg<M>::ne;
     constexpr int NO = WinDeg<M>::no;
     constexpr int DM = WinDeg<M>::deg;
-    double s[K], s2[K];
+    constexpr int TS = 2 * M + 1;
+    double s[K], s2[K], ao[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         s[k] = 2.0 * f[k] - 1.0;
         s2[k] = s[k] * s[k];
+        ao[k] = 0.0;
     }
 #pragma unroll
     for (int q = 1; q <= M; ++q) {
@@ -194,9 +205,9 @@ __device__ __forceinline__ void kb_dot_k(const double (&f)[K], const WinCoef& c,
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const double o = od[k] * s[k];
-            acc[k] = fma(e[k] + o, gbase[cell[k] + q + M], acc[k]);
-            acc[k] = fma(e[k] - o, gbase[cell[k] + 1 - q + M], acc[k]);
+            const double* t = tab + cell[k] * TS + 2 * q - 1;
+            acc[k] = fma(e[k], t[0], acc[k]);
+            ao[k] = fma(od[k], t[1], ao[k]);
         }
     }
     double pm[K];
@@ -209,7 +220,7 @@ __device__ __forceinline__ void kb_dot_k(const double (&f)[K], const WinCoef& c,
         for (int k = 0; k < K; ++k) pm[k] = fma(pm[k], s[k], cj);
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = fma(pm[k], gbase[cell[k]], acc[k]);
+    for (int k = 0; k < K; ++k) acc[k] = fma(s[k], ao[k], fma(pm[k], tab[cell[k] * TS], acc[k]));
 }
 
 }  // namespace mlb

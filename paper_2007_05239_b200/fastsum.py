@@ -153,7 +153,7 @@ def window_polynomials(m, b):
     extended-precision samples, converted to the monomial basis; the fit is
     checked against the reference's float64 formula.
     """
-    deg = 16 if m <= 3 else 14
+    deg = 15 if m <= 3 else 13   # odd: as many even as odd terms (csrc/mlb_window.cuh WinDeg)
     nodes = np.cos(np.pi * (np.arange(deg + 1) + 0.5) / (deg + 1))
     coef = np.empty((2 * m + 1, deg + 1))
     f_chk = np.linspace(0.0, 1.0, 513)
@@ -254,7 +254,7 @@ class FastsumPlan:
     _fused: np.ndarray = field(default=None, repr=False, compare=False)
     K0: float = 1.0
     win_coef: np.ndarray = field(default=None, repr=False)
-    win_deg: int = 14
+    win_deg: int = 13
     _device: dict = field(default_factory=dict, repr=False, compare=False)
 
     @property
@@ -402,7 +402,7 @@ def build_plan(kernel, d, N=DEFAULT_N, m_nfft=DEFAULT_M, eps_b=DEFAULT_EPS_B, p_
     leak = np.max(np.abs(coeffs.imag)) if coeffs.size else 0.0
     if leak > 1e-12 * max(1.0, np.max(np.abs(coeffs.real))):
         raise NumericalError("kernel coefficients are not real; kernel not even?")
-    win_coef, win_deg = (None, 14)
+    win_coef, win_deg = (None, 13)
     if m_nfft <= 6:
         win_coef, win_deg = window_polynomials(m_nfft, b)
     return FastsumPlan(kernel=kernel, d=d, N=N, m_nfft=m_nfft, eps_b=eps_b, p_nfft=p_nfft, rho=rho,
