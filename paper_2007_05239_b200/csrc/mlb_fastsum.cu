@@ -1521,8 +1521,8 @@ static int spread_dm(mlb_binding* b, const double* v, unsigned flags, cudaStream
     const int nsm = device_sms();
     (void)nsm;
     if constexpr (D == 1) {
-        if (b->key_start && b->n >= kStream1MinN) {   // streaming d = 1 spread
-            const size_t smem = (size_t)8 * b->tile_cells * sizeof(double);
+        const size_t smem = (size_t)8 * b->tile_cells * sizeof(double);
+        if (b->key_start && b->n >= kStream1MinN && smem <= 200 * 1024) {   // streaming d = 1 spread (fits: N <~ 3000)
             if (int rc = ensure_max_smem((const void*)spread1_kernel<M>, smem)) return rc;
             const int blocks = std::max(1, std::min(2 * nsm, (int)((b->n + 8 * K1STEP - 1) / (8 * K1STEP))));
             b->spread_parts = blocks;
@@ -1603,9 +1603,9 @@ template <int D, int M>
 static int gather_dm(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                      double beta, double gamma, unsigned flags, cudaStream_t st) {
     if constexpr (D == 1) {
-        if (b->key_start && b->n >= kStream1MinN) {   // streaming d = 1 gather
+        const size_t smem = ((size_t)b->plan->g.L + (size_t)b->nkeys * (2 * M + 1)) * sizeof(double);
+        if (b->key_start && b->n >= kStream1MinN && smem <= 200 * 1024) {   // streaming d = 1 gather
             FsArgs a = make_args(b);
-            const size_t smem = ((size_t)b->plan->g.L + (size_t)b->nkeys * (2 * M + 1)) * sizeof(double);
             if (int rc = ensure_max_smem((const void*)gather1_kernel<M>, smem)) return rc;
             const int nsm = device_sms();
             const int blocks = std::max(1, std::min(2 * nsm, (int)((b->n + 8 * K1STEP - 1) / (8 * K1STEP))));
