@@ -605,7 +605,12 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
         std::vector<int> iord(items.size());
         for (size_t i = 0; i < items.size(); ++i) iord[i] = (int)i;
         std::stable_sort(iord.begin(), iord.end(), [&](int x, int y) { return items[x].cost > items[y].cost; });
-        ncta_cells = std::min<int>((int)items.size(), nsm * 2);
+        // item lists for as many CTAs as can be resident (m >= 5: one 8-warp
+        // CTA per SM; m <= 4: two): one wave, so the LPT balance holds (two
+        // waves of 148 at m = 5 cost config-4 rank shards at N = 8 +7 %)
+        int cpsm = (g.m >= 5) ? 1 : 2;
+        if (const char* env = std::getenv("MLB_CELL_CTAS")) cpsm = std::max(1, std::atoi(env));  // tuning
+        ncta_cells = std::min<int>((int)items.size(), nsm * cpsm);
         // longest-processing-time-first: each item goes to the least loaded CTA
         std::vector<std::vector<int>> cta_items(ncta_cells);
         {
