@@ -631,7 +631,7 @@ def main():
     # CPU legs: bounded node samples of the workload (the full config-4 layers
     # would need a 213 GB reference binding): ~0.4 s per step on 16 cores
     ap.add_argument("--cpu-sample", type=int, default=131072, help="nodes in the CPU baseline sample")
-    ap.add_argument("--cpu-reps", type=int, default=30)
+    ap.add_argument("--cpu-reps", type=int, default=40)   # ~12 s of the 16-core port
     ap.add_argument("--cpu-single-sample", type=int, default=16384,
                     help="nodes in the single-thread ('as shipped') sample")
     ap.add_argument("--ref-sample", type=int, default=131072, help="nodes in the reference arm's sample")
