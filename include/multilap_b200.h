@@ -151,6 +151,17 @@ int mlb_apply(mlb_binding* b, const double* v_dev, double* y_dev, double alpha, 
  * t's mlb_apply of v with coefficients alpha[t], beta[t], gamma[t] (host
  * arrays).  The layers run concurrently on library-owned streams forked
  * from and joined back into `stream`; all bindings on one device. */
+/* The fused Laplacian of T layers with one launch per stage (blockIdx.y =
+ * layer) -- for many small layers of one (d, m), e.g. config 3's 52, whose
+ * per-layer launches are latency-bound (graphs.py:197-201 per layer).
+ * b: HOST array of T bindings (d = 2, same m <= 5, same grid and windows,
+ * < 2^20 points each, separable convolution); v_dev / y_dev: DEVICE arrays
+ * of T device pointers; abg_dev: DEVICE array alpha[T] | beta[T] | gamma[T].
+ * y_t (=|+=) alpha_t v_t + s_t (beta_t W~ (s_t v_t) + gamma_t s_t v_t) as
+ * mlb_apply.  MLB_ERR_CONFIG when the layers are not eligible (the caller
+ * falls back to mlb_apply per layer). */
+int mlb_apply_multi(mlb_binding* const* b, int T, const double* const* v_dev, double* const* y_dev,
+                    const double* abg_dev, unsigned flags, void* stream);
 int mlb_apply_batched(mlb_binding* const* b, int T, const double* v_dev, double* const* y_dev, const double* alpha,
                       const double* beta, const double* gamma, unsigned flags, void* stream);
 

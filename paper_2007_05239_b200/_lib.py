@@ -80,6 +80,7 @@ SIGNATURES = {
     "mlb_cgs2_batched_work_size": (I64, [I]),
     "mlb_cgs2_batched": (I, [I, P, I64, I64, I, P, P, P, P, P, P, P]),
     "mlb_tridiag_fn_batched": (I, [I, P, I64, I, I, D, P, P, P]),
+    "mlb_apply_multi": (I, [P, I, P, P, P, U, P]),
     "mlb_gemm_vs": (I, [P, I64, I64, I, P, I, P, I64, P]),
     "mlb_dot": (I, [P, P, I64, P, P, P]),
     "mlb_axpby": (I, [D, P, D, P, I64, P]),

@@ -704,6 +704,8 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     mlb_binding* b = new mlb_binding();
     b->plan = plan;
     b->device = plan->device;
+    static std::atomic<uint64_t> next_uid{1};
+    b->uid = next_uid++;
     b->n = n;
     b->nchunks = nch;
     b->ngrp = ngrp;
@@ -986,6 +988,16 @@ int mlb_apply(mlb_binding* b, const double* v, double* y, double alpha, double b
     if (rc == MLB_OK) rc = launch_convolve(b, b->grid, b->grid2, st);
     if (rc == MLB_OK) rc = launch_gather(b, b->grid2, v, y, alpha, beta, gamma, flags, st);
     return rc;
+}
+
+int mlb_apply_multi(mlb_binding* const* b, int T, const double* const* v_dev, double* const* y_dev,
+                    const double* abg_dev, unsigned flags, void* stream) {
+    if (T < 1 || !b || !v_dev || !y_dev || !abg_dev) return fail(MLB_ERR_ARG, "null argument");
+    for (int t = 0; t < T; ++t)
+        if (!b[t]) return fail(MLB_ERR_ARG, "null binding");
+    DeviceGuard guard(b[0]->plan->device);
+    flags &= (MLB_USE_ISD | MLB_ACCUMULATE | MLB_SORTED);
+    return launch_apply_multi(b, T, v_dev, y_dev, abg_dev, flags, (cudaStream_t)stream);
 }
 
 int mlb_apply_batched(mlb_binding* const* b, int T, const double* v, double* const* y, const double* alpha,

@@ -498,8 +498,8 @@ __device__ __forceinline__ void sep_line4(const double* __restrict__ sc, int u0,
 }
 
 // whole sub-box in smem, one CTA, all passes (d <= 2 and small grids)
-__global__ void sep_small_kernel(const double* __restrict__ gin, double* __restrict__ gout,
-                                 const double* __restrict__ c, int L, int d) {
+__device__ __forceinline__ void sep_small_body(const double* __restrict__ gin, double* __restrict__ gout,
+                                               const double* __restrict__ c, int L, int d) {
     extern __shared__ double sm[];
     const int cells = (d == 1) ? L : L * L;
     const int rows = cells / L;
@@ -540,6 +540,17 @@ __global__ void sep_small_kernel(const double* __restrict__ gin, double* __restr
             if (4 * q + j < L) gout[(4 * q + j) * L + col] = o[j];
     }
     pdl_launch();
+}
+
+__global__ void sep_small_kernel(const double* __restrict__ gin, double* __restrict__ gout,
+                                 const double* __restrict__ c, int L, int d) {
+    sep_small_body(gin, gout, c, L, d);
+}
+
+// one CTA per layer of mlb_apply_multi (same L and d for every layer)
+__global__ void sep_small_multi_kernel(const ConvJob* __restrict__ jobs, int L, int d) {
+    const ConvJob& J = jobs[blockIdx.x];
+    sep_small_body(J.gin, J.gout, J.c, L, d);
 }
 
 // one pass over a contiguous axis (rows of length L): CTA = 8 rows
@@ -733,6 +744,16 @@ static int convolve_separable(mlb_binding* b, const double* gin, double* gout, c
         sep_cols_kernel<<<dim3((unsigned)((B + 31) / 32), (unsigned)A), 256, scol, st>>>(src, dst, c, L, (int)B);
         note_launches(1);
     }
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int launch_sep_small_multi(const ConvJob* jobs_dev, int T, int L, int d, cudaStream_t st) {
+    const int cells = (d == 1) ? L : L * L;
+    const size_t smem = (size_t)(2 * cells + 2 * L + 8) * sizeof(double);
+    if (int rc = ensure_max_smem((const void*)sep_small_multi_kernel, smem)) return rc;
+    MLB_CUDA_TRY(launch_k(sep_small_multi_kernel, dim3(T), dim3(512), smem, st, jobs_dev, L, d));
+    note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
     return MLB_OK;
 }

@@ -15,6 +15,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
 #include <cstdlib>
 
 #include "mlb_internal.cuh"
@@ -176,11 +180,11 @@ __device__ __forceinline__ SubPos sub_next(const FsArgs& a, SubPos p, int nwarps
     return sub_first(a, p.seg + nwarps, seg_end);
 }
 
-template <int D, int M, bool PERSIST, bool GROUPED = false>
-__global__ void __launch_bounds__(PERSIST ? (GROUPED ? 32 * kBandWarps : 256) : 64, GROUPED ? kBandCtasPerSm : 1)
-spread_kernel(FsArgs a, WinCoef wc,
-                                                                    const double* __restrict__ v, unsigned flags,
-                                                                    int* __restrict__ work) {
+// body of spread_kernel; `bid` / `nblk` stand for blockIdx.x / gridDim.x (the
+// multi-layer launch gives every layer its own block count along x)
+template <int D, int M, bool PERSIST, bool GROUPED>
+__device__ __forceinline__ void spread_body(const FsArgs& a, const WinCoef& wc, const double* __restrict__ v,
+                                            unsigned flags, int bid, int nblk) {
     using C = SpreadCfg<D, M>;
     constexpr int S = C::S;
     constexpr int SPAD = StageCfg<D, M>::pad;
@@ -204,9 +208,9 @@ spread_kernel(FsArgs a, WinCoef wc,
     const int TL1 = (D >= 2) ? TL : 1;
     // segment walk: banded CTAs own a contiguous range, else global round-robin
     const bool banded = a.cta_seg != nullptr;
-    const int gwarp = banded ? __ldg(a.cta_seg + blockIdx.x) + warp : blockIdx.x * nw + warp;
-    const int nwarps = banded ? nw : gridDim.x * nw;
-    const int seg_end = banded ? __ldg(a.cta_seg + blockIdx.x + 1) : a.nseg;
+    const int gwarp = banded ? __ldg(a.cta_seg + bid) + warp : bid * nw + warp;
+    const int nwarps = banded ? nw : nblk * nw;
+    const int seg_end = banded ? __ldg(a.cta_seg + bid + 1) : a.nseg;
     const bool sorted = (flags & MLB_SORTED) != 0;
     const bool use_isd = (flags & MLB_USE_ISD) != 0;
 
@@ -494,13 +498,20 @@ spread_kernel(FsArgs a, WinCoef wc,
     pdl_launch();
     if (PERSIST) {
         __syncthreads();
-        double* out = a.partial + (size_t)blockIdx.x * tile;
+        double* out = a.partial + (size_t)bid * tile;
         for (int i = threadIdx.x; i < tile; i += blockDim.x) {
             double t = 0.0;
             for (int w = 0; w < nw; ++w) t += smem[(size_t)w * tile + i];
             out[i] = t;
         }
     }
+}
+
+template <int D, int M, bool PERSIST, bool GROUPED = false>
+__global__ void __launch_bounds__(PERSIST ? (GROUPED ? 32 * kBandWarps : 256) : 64, GROUPED ? kBandCtasPerSm : 1)
+spread_kernel(FsArgs a, WinCoef wc, const double* __restrict__ v, unsigned flags, int* __restrict__ work) {
+    (void)work;
+    spread_body<D, M, PERSIST, GROUPED>(a, wc, v, flags, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------- d = 1: streaming kernels --
@@ -1052,9 +1063,10 @@ __global__ void __launch_bounds__(MergeCfg<M>::MT, 2048 / MergeCfg<M>::MT) brick
 // d <= 2: grid[u] = sum over the spread CTAs' partial grids.  Block = 8
 // cells x 32 slices; slice k sums partials k, k+32, ...; the 32 slice sums
 // combine through a fixed shuffle tree -> deterministic.
-__global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, int cells, PeerOut grid) {
+__device__ __forceinline__ void grid_sum_body(const double* __restrict__ partial, int nparts, int cells,
+                                              const PeerOut& grid, int bid) {
     const int slice = threadIdx.x & 31;
-    const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int cell = bid * 8 + (threadIdx.x >> 5);
     double s = 0.0;
     pdl_wait();  // the partial grids come from the spread
     if (cell < cells) {
@@ -1075,6 +1087,10 @@ __global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, 
     pdl_launch();
     if (slice == 0 && cell < cells) po_store(grid, cell, s);
     if (grid.n > 1) __threadfence_system();  // peer stores ordered before the exchange barrier
+}
+
+__global__ void grid_sum_kernel(const double* __restrict__ partial, int nparts, int cells, PeerOut grid) {
+    grid_sum_body(partial, nparts, cells, grid, blockIdx.x);
 }
 
 // d = 2 banded spread: grid[u0, u1] = sum over the CTAs whose band covers
@@ -1219,10 +1235,11 @@ struct GatherCfg {
     static constexpr int NB = (D == 1) ? S : (D == 2 ? S * S : S * S * SR);
 };
 
+// body of gather_kernel; `bid` / `nblk` stand for blockIdx.x / gridDim.x
 template <int D, int M, bool PK>
-__global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel(FsArgs a, WinCoef wc, const double* __restrict__ grid,
-                                                     const double* __restrict__ v, double* __restrict__ y,
-                                                     double alpha, double beta, double gamma, unsigned flags) {
+__device__ __forceinline__ void gather_body(const FsArgs& a, const WinCoef& wc, const double* __restrict__ grid,
+                                            const double* __restrict__ v, double* __restrict__ y, double alpha,
+                                            double beta, double gamma, unsigned flags, int bid, int nblk) {
     constexpr int S = 2 * M + 1;
     constexpr int SR = GatherCfg<D, M, PK>::SR;  // staged row length (d = 3 packed: a pencil of <= Tb cells)
     constexpr int NB = GatherCfg<D, M, PK>::NB;
@@ -1232,8 +1249,8 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     double* nb = nbs + wl * NB;
     double* w0s = nbs + 8 * NB + (wl * 32 + lane) * W0S;  // [0,S): point A, [S,2S): point B
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwt = (gridDim.x * blockDim.x) >> 5;
+    const int gw = (bid * (int)blockDim.x + (int)threadIdx.x) >> 5;
+    const int nwt = (nblk * (int)blockDim.x) >> 5;
     const int nunits = (D == 3 && PK) ? a.ngrp : a.nchunks;  // pencil groups, or one-cell chunks
     const int c_lo = (int)(((long long)nunits * gw) / nwt);
     const int c_hi = (int)(((long long)nunits * (gw + 1)) / nwt);
@@ -1467,6 +1484,60 @@ __global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel
         }
     }
     pdl_launch();
+}
+
+template <int D, int M, bool PK>
+__global__ void __launch_bounds__(256, (D == 3 && M >= 5) ? 1 : 2) gather_kernel(FsArgs a, WinCoef wc,
+                                                                                 const double* __restrict__ grid,
+                                                                                 const double* __restrict__ v,
+                                                                                 double* __restrict__ y, double alpha,
+                                                                                 double beta, double gamma,
+                                                                                 unsigned flags) {
+    gather_body<D, M, PK>(a, wc, grid, v, y, alpha, beta, gamma, flags, blockIdx.x, gridDim.x);
+}
+
+// ------------------------------------------------------ many small layers --
+// mlb_apply_multi: T layers' fused Laplacians in one launch per stage,
+// blockIdx.y = layer, each layer with its own block count along x (the CTAs
+// past it exit at once).  For many small layers of one (d, m) -- config 3's
+// 52 of 40,000 points -- whose per-layer launches are latency-bound.
+struct MultiLayer {
+    FsArgs a;
+    double* grid;        // the layer's spread sum
+    double* grid2;       // the convolved grid
+    int spread_blocks;
+    int gather_blocks;
+    int cells;
+};
+
+// (the grouped d = 2 lanes: a small layer's few CTAs each walk thousands of points)
+template <int D, int M>
+__global__ void __launch_bounds__(32 * kBandWarps, kBandCtasPerSm) spread_multi_kernel(
+    const MultiLayer* __restrict__ ml, WinCoef wc, const double* const* __restrict__ v, unsigned flags) {
+    const MultiLayer& L = ml[blockIdx.y];
+    if ((int)blockIdx.x >= L.spread_blocks) return;
+    spread_body<D, M, true, true>(L.a, wc, v[blockIdx.y], flags, blockIdx.x, L.spread_blocks);
+}
+
+__global__ void grid_sum_multi_kernel(const MultiLayer* __restrict__ ml) {
+    const MultiLayer& L = ml[blockIdx.y];
+    if ((int)blockIdx.x * 8 >= L.cells) return;
+    PeerOut out{};
+    out.p[0] = L.grid;
+    out.n = 1;
+    grid_sum_body(L.a.partial, L.spread_blocks, L.cells, out, blockIdx.x);
+}
+
+template <int D, int M>
+__global__ void __launch_bounds__(256, 2) gather_multi_kernel(const MultiLayer* __restrict__ ml, WinCoef wc,
+                                                              const double* const* __restrict__ v,
+                                                              double* const* __restrict__ y,
+                                                              const double* __restrict__ abg, int T, unsigned flags) {
+    const MultiLayer& L = ml[blockIdx.y];
+    if ((int)blockIdx.x >= L.gather_blocks) return;
+    const int t = blockIdx.y;
+    gather_body<D, M, false>(L.a, wc, L.grid2, v[t], y[t], abg[t], abg[T + t], abg[2 * T + t], flags, blockIdx.x,
+                             L.gather_blocks);
 }
 
 // --------------------------------------------------------------- launchers --
@@ -1737,6 +1808,111 @@ int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y
     if (b->nchunks == 0) return MLB_OK;
     const Geom& g = b->plan->g;
     MLB_DISPATCH_DM(gather_dm, g.d, g.m, b, grid, v, y, alpha, beta, gamma, flags, st);
+}
+
+// ---------------------------------------------------------- many layers --
+namespace {
+struct MultiTab {
+    MultiLayer* ml = nullptr;   // device, T entries
+    ConvJob* jobs = nullptr;    // device, T entries
+    int nw = 0, maxs = 0, maxg = 0, maxcells = 0;
+};
+std::mutex g_multi_mu;
+std::map<std::vector<uint64_t>, MultiTab> g_multi;   // per binding set (binding uids)
+}  // namespace
+
+template <int M>
+static int apply_multi_m(mlb_binding* const* b, int T, const double* const* v, double* const* y, const double* abg,
+                         unsigned flags, cudaStream_t st) {
+    constexpr int D = 2;
+    constexpr int S = 2 * M + 1;
+    constexpr int NB = GatherCfg<D, M, false>::NB;
+    const int nsm = device_sms();
+    const int tile = b[0]->tile_cells;
+    int nw = kBandWarps;   // (spread_multi_kernel's launch bounds)
+    while (nw > 1 && spread_smem<D, M>(nw, tile) > 72 * 1024) --nw;
+    const size_t smem_s = spread_smem<D, M>(nw, tile);
+    const size_t smem_g = ((size_t)8 * NB + (size_t)256 * (2 * S + 1)) * sizeof(double);
+    auto ks = spread_multi_kernel<D, M>;
+    auto kg = gather_multi_kernel<D, M>;
+    if (int rc = ensure_max_smem((const void*)ks, smem_s)) return rc;
+    if (int rc = ensure_max_smem((const void*)kg, smem_g)) return rc;
+    std::vector<uint64_t> key(T);
+    for (int t = 0; t < T; ++t) key[t] = b[t]->uid;
+    MultiTab tab;
+    {
+        std::lock_guard<std::mutex> lk(g_multi_mu);
+        auto it = g_multi.find(key);
+        if (it != g_multi.end()) tab = it->second;
+    }
+    if (!tab.ml) {
+        const int per_sm = occupancy_per_sm((const void*)kg, 256, smem_g);
+        std::vector<MultiLayer> hml(T);
+        std::vector<ConvJob> hjobs(T);
+        for (int t = 0; t < T; ++t) {
+            MultiLayer& L = hml[t];
+            L.a = make_args(b[t]);
+            L.grid = b[t]->grid;
+            L.grid2 = b[t]->grid2;
+            // the layers share the GPU: about two resident waves of CTAs in
+            // total, so small layers get few CTAs (each spread CTA zeroes and
+            // writes a whole sub-box tile: one CTA per segment would make the
+            // tiles, not the points, the work)
+            const int sshare = std::max(1, (2 * nsm + T - 1) / T);
+            const int gshare = std::max(1, (2 * nsm * per_sm + T - 1) / T);
+            L.spread_blocks = std::max(1, std::min(sshare, (b[t]->nseg + nw - 1) / nw));
+            L.gather_blocks = std::max(1, std::min(gshare, (b[t]->nchunks + 7) / 8));
+            L.cells = (int)b[t]->grid_cells;
+            b[t]->spread_parts = L.spread_blocks;
+            hjobs[t] = ConvJob{b[t]->grid, b[t]->grid2, b[t]->plan->sep};
+            tab.maxs = std::max(tab.maxs, L.spread_blocks);
+            tab.maxg = std::max(tab.maxg, L.gather_blocks);
+            tab.maxcells = std::max(tab.maxcells, L.cells);
+        }
+        tab.nw = nw;
+        MLB_CUDA_TRY(cudaMalloc(&tab.ml, sizeof(MultiLayer) * T));
+        MLB_CUDA_TRY(cudaMalloc(&tab.jobs, sizeof(ConvJob) * T));
+        MLB_CUDA_TRY(cudaMemcpy(tab.ml, hml.data(), sizeof(MultiLayer) * T, cudaMemcpyHostToDevice));
+        MLB_CUDA_TRY(cudaMemcpy(tab.jobs, hjobs.data(), sizeof(ConvJob) * T, cudaMemcpyHostToDevice));
+        std::lock_guard<std::mutex> lk(g_multi_mu);
+        g_multi[key] = tab;
+    }
+    const Geom& g = b[0]->plan->g;
+    MLB_CUDA_TRY(launch_k(ks, dim3(tab.maxs, T), dim3(32 * tab.nw), smem_s, st, (const MultiLayer*)tab.ml,
+                          b[0]->plan->wc, v, flags));
+    MLB_CUDA_TRY(launch_k(grid_sum_multi_kernel, dim3((tab.maxcells + 7) / 8, T), dim3(256), 0, st,
+                          (const MultiLayer*)tab.ml));
+    if (int rc = launch_sep_small_multi(tab.jobs, T, g.L, D, st)) return rc;
+    MLB_CUDA_TRY(launch_k(kg, dim3(tab.maxg, T), dim3(256), smem_g, st, (const MultiLayer*)tab.ml, b[0]->plan->wc,
+                          v, y, abg, T, flags));
+    note_launches(3);
+    MLB_CUDA_TRY(cudaGetLastError());
+    return MLB_OK;
+}
+
+int launch_apply_multi(mlb_binding* const* b, int T, const double* const* v, double* const* y, const double* abg,
+                       unsigned flags, cudaStream_t st) {
+    // eligibility: one device, d = 2, one m, full-tile spreads (n < 2^20),
+    // the separable one-CTA convolution, identical windows and tile sizes
+    const mlb_plan* p0 = b[0]->plan;
+    const int d = p0->g.d, m = p0->g.m, L = p0->g.L;
+    const int64_t cells = b[0]->grid_cells;
+    if (d != 2 || m < 2 || m > 5) return fail(MLB_ERR_CONFIG, "multi-layer apply covers d = 2, m <= 5");
+    if ((2 * cells + 2 * L + 8) * 8 > 96 * 1024) return fail(MLB_ERR_CONFIG, "multi-layer apply: grid too large");
+    for (int t = 0; t < T; ++t) {
+        const mlb_binding* bt = b[t];
+        const mlb_plan* p = bt->plan;
+        if (p->device != p0->device || p->g.d != d || p->g.m != m || p->g.L != L || !p->sep ||
+            bt->tile_cells != b[0]->tile_cells || bt->grid_cells != cells || bt->n < 1 || bt->n >= (1 << 20) ||
+            bt->ncta_band > 0 || bt->spread_atomic || std::memcmp(&p->wc, &p0->wc, sizeof(WinCoef)) != 0)
+            return fail(MLB_ERR_CONFIG, "multi-layer apply: layers differ in (d, m, grid, windows) or are large");
+    }
+    switch (m) {
+        case 2: return apply_multi_m<2>(b, T, v, y, abg, flags, st);
+        case 3: return apply_multi_m<3>(b, T, v, y, abg, flags, st);
+        case 4: return apply_multi_m<4>(b, T, v, y, abg, flags, st);
+        default: return apply_multi_m<5>(b, T, v, y, abg, flags, st);
+    }
 }
 
 }  // namespace mlb

@@ -90,6 +90,14 @@ struct WinCoef {
     int deg;
 };
 
+// one layer's convolution in the multi-layer launch (mlb_apply_multi)
+struct ConvJob {
+    const double* gin;
+    double* gout;
+    const double* c;   // the plan's separable kernel (2L - 1 taps)
+};
+int launch_sep_small_multi(const ConvJob* jobs_dev, int T, int L, int d, cudaStream_t st);
+
 // Geometry shared by all kernels of one plan.
 struct Geom {
     int d, N, m, ng;
@@ -120,6 +128,7 @@ struct mlb_plan {
 struct mlb_binding {
     const mlb_plan* plan;
     int device = 0;                  // plan->device, kept for destroy
+    uint64_t uid = 0;                // unique per binding (multi-layer table cache key)
     int64_t n;
     int nchunks, nseg, nbricks;
     // device tables
@@ -217,4 +226,6 @@ int launch_slot_sum(const double* recv, int world, int64_t cells, double* grid, 
 int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_t st);
 int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                   double beta, double gamma, unsigned flags, cudaStream_t st);
+int launch_apply_multi(mlb_binding* const* b, int T, const double* const* v, double* const* y, const double* abg,
+                       unsigned flags, cudaStream_t st);
 }  // namespace mlb

@@ -635,6 +635,49 @@ def _issue_cgs_batched(P, p_V, T, j, dim, n, sp):
         C.c_void_p(p_V.data_ptr()) if j + 1 < dim else None, C.c_void_p(P["bwork"].data_ptr()), sp))
 
 
+_MULTI_OK = {}
+
+
+def _multi_matvec(st, P, dim, n, dev, stream):
+    """Whether the lockstep step issues all layers' matvecs with ONE
+    mlb_apply_multi per stage (many small layers of one (d, m): config 3's
+    52 of 40,000 points, whose per-layer launches are latency-bound).  The
+    pointer tables live in the pool; eligibility is probed once per binding
+    set by an eager call (it also builds the library's per-set tables outside
+    any capture).  MLB_PKSM_MULTI=0 keeps the per-layer launches."""
+    if os.environ.get("MLB_PKSM_MULTI", "1") == "0" or len(st) < 2:
+        return False
+    bkey = tuple(int(x.b.ptr.value) for x in st)
+    if len(set(bkey)) != len(bkey):   # a binding twice: its scratch grids would be shared
+        return False
+    torch = _torch()
+    T = len(st)
+    if "p_x" not in P:
+        rows = [[x.V.data_ptr() + 8 * n * j for x in st] for j in range(dim)]
+        P["p_x"] = torch.tensor(rows, dtype=torch.int64, device=dev)
+    abg = [x.a for x in st] + [-1.0] * T + [x.K0 for x in st]
+    if P.get("abg_key") != abg:
+        P["abg"] = torch.tensor(abg, dtype=torch.float64, device=dev)
+        P["abg_key"] = abg
+    P["b_host"] = (C.c_void_p * T)(*[x.b.ptr.value for x in st])
+    ok = _MULTI_OK.get(bkey)
+    if ok is None:
+        rc = _lib.lib().mlb_apply_multi(P["b_host"], T, C.c_void_p(P["p_x"][0].data_ptr()),
+                                        C.c_void_p(P["p_w"].data_ptr()), C.c_void_p(P["abg"].data_ptr()),
+                                        _lib.MLB_USE_ISD | _lib.MLB_SORTED, C.c_void_p(stream.cuda_stream))
+        ok = _MULTI_OK[bkey] = rc == 0
+        for x in st:   # forget the probe result when a binding dies (its address may be reused)
+            weakref.finalize(x.b, _MULTI_OK.pop, bkey, None)
+    return ok
+
+
+def _issue_multi(P, T, j, sp):
+    """w_t = (L_t + delta) V_t[j] for every chain t: mlb_apply_multi."""
+    _lib.check(_lib.lib().mlb_apply_multi(P["b_host"], T, C.c_void_p(P["p_x"][j].data_ptr()),
+                                          C.c_void_p(P["p_w"].data_ptr()), C.c_void_p(P["abg"].data_ptr()),
+                                          _lib.MLB_USE_ISD | _lib.MLB_SORTED, sp))
+
+
 def _issue_layer_step(x, t, j, P, dim, n, sp):
     """Step j of layer t's chain on stream `sp`: matvec of V[j] (fused
     Laplacian, sorted order), CGS2 against V[:j+1] (alpha_j and ||w||^2 into
@@ -690,7 +733,8 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
     dev_coeffs = _device_coeffs_ok(dim, T)
     gkey = (dev.index, _VPOOL_DEPTH[0], dim, n, tuple(int(x.b.ptr.value) for x in st),
             tuple((x.a, x.K0) for x in st), tuple(x.V.data_ptr() for x in st), AB.data_ptr(),
-            _batched_cgs_ok(dim, n), dev_coeffs, float(p) if dev_coeffs else None)
+            _batched_cgs_ok(dim, n), dev_coeffs, float(p) if dev_coeffs else None,
+            os.environ.get("MLB_PKSM_MULTI", "1"))
     graphs = None
     if use_graphs:
         graphs = _LOCK_GRAPHS.get(gkey)
@@ -712,7 +756,9 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
         elif P["p_V_key"] != vptrs:
             P["p_V"].copy_(torch.tensor(vptrs, dtype=torch.int64))
             P["p_V_key"] = vptrs
+            P.pop("p_x", None)
         p_V = P["p_V"]
+    multi = batched and use_graphs and _multi_matvec(st, P, dim, n, dev, stream)
 
     def issue(j):
         if not use_graphs:
@@ -738,7 +784,9 @@ def _pksm_layers_dev(layers, p, v_node, out, out_scale=1.0, krylov_dim=50, tol=1
                     # one stream per binding: a binding's scratch grids must not be shared by
                     # concurrent chains (the same layer may appear twice in a layer set)
                     slot = {}
-                    for t, x in enumerate(st):
+                    if multi:   # every layer's matvec in one launch per stage
+                        _issue_multi(P, T, j, C.c_void_p(cap.cuda_stream))
+                    for t, x in enumerate(st if not multi else ()):
                         s_ = ss[slot.setdefault(int(x.b.ptr.value), len(slot)) % len(ss)]
                         if batched:    # the layers' matvecs concurrently, then ONE batched CGS2
                             _issue_matvec(x, t, j, P, n, C.c_void_p(s_.cuda_stream))

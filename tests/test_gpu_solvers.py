@@ -298,3 +298,53 @@ def test_binary_allen_cahn_and_energy_match_golden():
     lab64 = LabelData.from_class_ids(ids[:64], int(ids.max()) + 1, 1000.0)
     e64 = ginzburg_landau_energy(gs["ac_scores"][:64], gb["L_dense64"], lab64, 5e-3)
     assert abs(e64 - gb["energy_dense64"][0]) <= 1e-10 * abs(gb["energy_dense64"][0])
+
+
+def test_multi_layer_apply_matches_per_layer_apply():
+    """mlb_apply_multi (one launch per stage for T small layers: config 3's
+    lockstep matvec) against mlb_apply per layer, to rounding; the lockstep
+    PKSM with and without it (MLB_PKSM_MULTI=0) agree to 1e-13."""
+    import ctypes as C
+    import os
+
+    import torch
+
+    import synth
+    from paper_2007_05239_b200 import _lib, with_shift
+    from paper_2007_05239_b200.krylov import pksm_layers_dev
+    wl = synth.CONFIGS[3](seed=0)
+    G = synth.build_graph(wl, device=0)
+    layers = [with_shift(lay, math.log(2.0)) for lay in G.layers[:12]]
+    T, n = len(layers), wl.n
+    lib = _lib.lib()
+    rng = np.random.default_rng(3)
+    xs = [torch.from_numpy(rng.standard_normal(n)).cuda() for _ in range(T)]
+    bs = [lay.weights._bindings[0] for lay in layers]
+    for lay in layers:
+        w = lay.weights
+        if w._isd_dev is None:
+            w.set_isd(lay.isd_device(w.device))
+    ys = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(T)]
+    ref = [torch.empty_like(y) for y in ys]
+    abg = [1.0 + lay.shift for lay in layers] + [-1.0] * T + [lay.weights.kernel.value_at_zero() for lay in layers]
+    flags = _lib.MLB_USE_ISD
+    for t, b in enumerate(bs):
+        _lib.check(lib.mlb_apply(b.ptr, _lib.ptr(xs[t]), _lib.ptr(ref[t]), abg[t], -1.0, abg[2 * T + t], flags,
+                                 _lib.stream_ptr()))
+    px = torch.tensor([x.data_ptr() for x in xs], dtype=torch.int64, device="cuda")
+    py = torch.tensor([y.data_ptr() for y in ys], dtype=torch.int64, device="cuda")
+    pabg = torch.tensor(abg, dtype=torch.float64, device="cuda")
+    bh = (C.c_void_p * T)(*[b.ptr.value for b in bs])
+    _lib.check(lib.mlb_apply_multi(bh, T, _lib.ptr(px), _lib.ptr(py), _lib.ptr(pabg), flags, _lib.stream_ptr()))
+    for t in range(T):   # (its own CTA partition of each layer: summation order differs)
+        assert rel(ys[t].cpu().numpy(), ref[t].cpu().numpy()) < 1e-14, t
+    v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    out = torch.zeros_like(v)
+    pksm_layers_dev(layers, -1.0, v, out, 1.0)
+    os.environ["MLB_PKSM_MULTI"] = "0"
+    try:
+        out0 = torch.zeros_like(v)
+        pksm_layers_dev(layers, -1.0, v, out0, 1.0)
+    finally:
+        del os.environ["MLB_PKSM_MULTI"]
+    assert rel(out.cpu().numpy(), out0.cpu().numpy()) < 1e-13
