@@ -423,6 +423,66 @@ __global__ void __launch_bounds__(32) tridiag_fn_kernel(double* __restrict__ AB,
         be[j] = sqrt(fmax(ab[dim + j], 0.0));
     }
     __syncwarp();
+    if (p == -1.0) {
+        // f(T) e1 = T^{-1} e1: one LDL^T (Thomas) solve, O(s), instead of the
+        // eigendecomposition.  All pivots positive <=> T SPD (Sylvester
+        // inertia), then lmin is reported as the smallest pivot (> 0: the
+        // host only tests its sign); otherwise the QL path below yields the
+        // real minimum eigenvalue for the host's error.
+        int spd = 1;
+        double pmin = 0.0;
+        if (lane == 0) {
+            double piv = al[0];
+            pmin = piv;
+            dg[0] = piv;   // pivots in dg, the forward-eliminated right-hand side in of
+            spd = piv > 0.0;
+            double z = 1.0;
+            of[0] = z;
+            for (int i = 1; i < s && spd; ++i) {
+                const double l = be[i - 1] / piv;
+                piv = al[i] - l * be[i - 1];
+                z = -l * z;
+                dg[i] = piv;
+                of[i] = z;
+                pmin = fmin(pmin, piv);
+                spd = piv > 0.0;
+            }
+        }
+        spd = __shfl_sync(0xffffffffu, spd, 0);
+        if (spd) {
+            const double nv = sqrt(ab[2 * dim]);
+            double* c = Cc + ((size_t)t * dim + j) * dim;
+            const double* cp = Cc + ((size_t)t * dim + (j > 0 ? j - 1 : 0)) * dim;
+            if (lane == 0) {   // back substitution: x_i = (z_i - be_i x_{i+1}) / piv_i
+                double x = of[s - 1] / dg[s - 1];
+                c[s - 1] = nv * x;
+                for (int i = s - 2; i >= 0; --i) {
+                    x = (of[i] - be[i] * x) / dg[i];
+                    c[i] = nv * x;
+                }
+            }
+            __syncwarp();
+            double c2 = 0.0, d2 = 0.0;
+            for (int i = lane; i < s; i += 32) {
+                const double ci = c[i];
+                const double di = ci - ((j > 0 && i < s - 1) ? cp[i] : 0.0);
+                c2 = fma(ci, ci, c2);
+                d2 = fma(di, di, d2);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+                d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+            }
+            if (lane == 0) {
+                ab[2 * dim + 1] = pmin;
+                ab[2 * dim + 2] = c2;
+                ab[2 * dim + 3] = d2;
+                ab[2 * dim + 4] = 0.0;
+            }
+            return;
+        }
+        __syncwarp();
+    }
     for (int i = lane; i < s; i += 32) {
         dg[i] = al[i];
         of[i] = (i + 1 < s) ? be[i] : 0.0;

@@ -132,7 +132,12 @@ def test_device_tridiagonal_coefficients_match_host_eigh(p):
         lam = np.array([np.linalg.eigvalsh(np.diag(al[t, :s]) + np.diag(be[t, :s - 1], 1) + np.diag(be[t, :s - 1], -1))
                         for t in range(T)])
         assert np.all(out[:, 2 * dim + 4] == 0)
-        assert np.allclose(out[:, 2 * dim + 1], lam.min(axis=1), rtol=0, atol=1e-13 * np.abs(lam).max())
+        if p == -1.0:   # T^{-1} e1 by one LDL^T solve: SPD chains report a positive pivot, others the QL minimum
+            spd = lam.min(axis=1) > 0
+            assert np.all(out[spd, 2 * dim + 1] > 0)
+            assert np.allclose(out[~spd, 2 * dim + 1], lam.min(axis=1)[~spd], rtol=0, atol=1e-13 * np.abs(lam).max())
+        else:
+            assert np.allclose(out[:, 2 * dim + 1], lam.min(axis=1), rtol=0, atol=1e-13 * np.abs(lam).max())
         ok = [t for t in range(T) if lam[t].min() > 1e-3]   # the power is defined on these chains
         ref = _coeffs(al[ok], be[ok], s, np.sqrt(vv[ok]), fn)
         got = Cc[ok, j, :s].cpu().numpy()
