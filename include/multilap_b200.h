@@ -131,6 +131,11 @@ int mlb_binding_perm(const mlb_binding* b, int32_t* perm_host);
 /* binding statistics: [n, nchunks, nsegments, nbricks, tile_cells, grid_cells,
    band_ctas (d = 2 banded spread CTAs, 0 = full tiles), band_tile_cells] */
 int mlb_binding_stats(const mlb_binding* b, int64_t* out8);
+/* d = 2 lattice items (image layers: the points of a cell form an R x C
+   product set; spread / gather as two small contractions per cell, see
+   DESIGN.md 3.3b): [items (0 = the general kernels), points in lattice cells].
+   Bind-time env MLB_LATTICE=0 / 1 turns the mode off / on regardless of size. */
+int mlb_binding_lattice(const mlb_binding* b, int64_t* out2);
 
 /* Store D^-1/2 (graphs.py:159-165) for the fused Laplacian; node order, device. */
 int mlb_binding_set_isd(mlb_binding* b, const double* isd_dev, void* stream);

@@ -56,6 +56,7 @@ SIGNATURES = {
     "mlb_binding_n": (I64, [P]),
     "mlb_binding_perm": (I, [P, P]),
     "mlb_binding_stats": (I, [P, P]),
+    "mlb_binding_lattice": (I, [P, P]),
     "mlb_binding_set_isd": (I, [P, P, P]),
     "mlb_apply": (I, [P, P, P, D, D, D, U, P]),
     "mlb_grid_cells": (I, [P, P, P, P]),

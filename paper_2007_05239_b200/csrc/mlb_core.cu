@@ -272,6 +272,9 @@ int mlb_binding_destroy(mlb_binding* b) {
     dev_free(b->grid2);
     dev_free(b->stage_a);
     dev_free(b->stage_b);
+    dev_free(b->lat_items);
+    dev_free(b->lat_bin_off);
+    dev_free(b->lat_blocks);
     delete b;
     return MLB_OK;
 }
@@ -780,6 +783,13 @@ static int bind_impl(const mlb_plan* plan, const BindPointsIn& in, mlb_binding**
     if (rc == MLB_OK) rc = dev_upload<double>(&b->grid2, nullptr, (size_t)b->grid_cells + 2);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_a, nullptr, (size_t)b->stage_elems);
     if (rc == MLB_OK) rc = dev_upload<double>(&b->stage_b, nullptr, (size_t)b->stage_elems);
+    if (rc == MLB_OK && d == 2 && n > 0) {   // lattice items (image layers): MLB_LATTICE=0 off, 1 forced
+        int mode = -1;
+        if (const char* env = std::getenv("MLB_LATTICE")) mode = env[0] == '1' ? 1 : (env[0] == '0' ? 0 : -1);
+        std::vector<int32_t> key_gcell((size_t)nkeys);
+        for (int64_t k = 0; k < nkeys; ++k) key_gcell[k] = gcell_of(k);
+        rc = build_lattice(b, cnt, key_gcell, mode, (cudaStream_t)in.stream);
+    }
     if (rc != MLB_OK) {
         std::string msg = g_err;
         mlb_binding_destroy(b);
@@ -808,6 +818,13 @@ int mlb_binding_stats(const mlb_binding* b, int64_t* o) {
     o[5] = b->grid_cells;
     o[6] = b->ncta_band;
     o[7] = b->band_tile;
+    return MLB_OK;
+}
+
+int mlb_binding_lattice(const mlb_binding* b, int64_t* out2) {
+    if (!b || !out2) return fail(MLB_ERR_ARG, "null argument");
+    out2[0] = b->lat_nitems;
+    out2[1] = b->lat_points;
     return MLB_OK;
 }
 

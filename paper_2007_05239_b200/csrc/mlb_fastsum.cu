@@ -1713,6 +1713,7 @@ static int gather_dm(mlb_binding* b, const double* grid, const double* v, double
 
 int launch_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st) {
     if (b->nseg == 0) return MLB_OK;
+    if (b->lat_nitems > 0) return launch_lat_spread(b, v, flags, st);
     const Geom& g = b->plan->g;
     MLB_DISPATCH_DM(spread_dm, g.d, g.m, b, v, flags, st);
 }
@@ -1727,6 +1728,7 @@ int launch_reduce(mlb_binding* b, double* grid_local, cudaStream_t st, const Pee
         grid.n = 1;
     }
     const Geom& G = b->plan->g;
+    if (b->lat_nitems > 0) return launch_lat_reduce(b, grid, st);
     if (G.d == 2 && b->ncta_band > 0) {
         // the banded spread left one band tile per CTA
         const int cells = (int)b->grid_cells;
@@ -1806,6 +1808,7 @@ int launch_slot_sum(const double* recv, int world, int64_t cells, double* grid, 
 int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha, double beta,
                   double gamma, unsigned flags, cudaStream_t st) {
     if (b->nchunks == 0) return MLB_OK;
+    if (b->lat_nitems > 0) return launch_lat_gather(b, grid, v, y, alpha, beta, gamma, flags, st);
     const Geom& g = b->plan->g;
     MLB_DISPATCH_DM(gather_dm, g.d, g.m, b, grid, v, y, alpha, beta, gamma, flags, st);
 }
@@ -1904,7 +1907,7 @@ int launch_apply_multi(mlb_binding* const* b, int T, const double* const* v, dou
         const mlb_plan* p = bt->plan;
         if (p->device != p0->device || p->g.d != d || p->g.m != m || p->g.L != L || !p->sep ||
             bt->tile_cells != b[0]->tile_cells || bt->grid_cells != cells || bt->n < 1 || bt->n >= (1 << 20) ||
-            bt->ncta_band > 0 || bt->spread_atomic || std::memcmp(&p->wc, &p0->wc, sizeof(WinCoef)) != 0)
+            bt->ncta_band > 0 || bt->lat_nitems > 0 || bt->spread_atomic || std::memcmp(&p->wc, &p0->wc, sizeof(WinCoef)) != 0)
             return fail(MLB_ERR_CONFIG, "multi-layer apply: layers differ in (d, m, grid, windows) or are large");
     }
     switch (m) {

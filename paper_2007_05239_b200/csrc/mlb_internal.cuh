@@ -193,6 +193,15 @@ struct mlb_binding {
     // d = 1 streaming spread / gather: first sorted point of every cell
     int32_t* key_start = nullptr;    // nkeys + 1 (nullptr: sub-chunk kernels)
     int nkeys = 0;
+    // d = 2 lattice items (mlb_lattice.cu; 0 items: the kernels above)
+    int lat_nitems = 0;
+    int64_t lat_points = 0;          // points in lattice cells of >= 2 x 2
+    int lat_nf_max = 0;              // widest fast-axis window table of an item
+    int lat_r_max = 0;               // most rows of an item
+    int lat_sv_max = 0;              // largest staged s v block (rows at an odd stride)
+    int32_t* lat_items = nullptr;    // nitems x {first point, rows, C | fast << 16 | diag << 17, sub-box cell}
+    int32_t* lat_bin_off = nullptr;  // nb^2 + 1: CSR of items per bin (items stored in bin order)
+    double* lat_blocks = nullptr;    // nitems x (2m+1)^2
 };
 
 namespace mlb {
@@ -226,6 +235,22 @@ int launch_slot_sum(const double* recv, int world, int64_t cells, double* grid, 
 int launch_convolve(mlb_binding* b, const double* gin, double* gout, cudaStream_t st);
 int launch_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha,
                   double beta, double gamma, unsigned flags, cudaStream_t st);
+// d = 2 lattice (separable-per-cell) kernels (mlb_lattice.cu)
+#ifndef MLB_LAT_THREADS
+#define MLB_LAT_THREADS 256
+#endif
+constexpr int kLatRowsMax = MLB_LAT_THREADS;   // rows per lattice item (<= one per thread)
+constexpr int kLatThreads = MLB_LAT_THREADS;   // threads per lattice CTA
+constexpr int kLatCols = kLatThreads;          // widest lattice run C (a gather thread owns a column)
+constexpr int kLatPts = 8 * kLatThreads;       // points per lattice item (8 per spread thread)
+constexpr int kLatGatherSlots = 8;             // points per gather thread and item
+constexpr int64_t kLatMinN = 1 << 16;     // auto mode: layers from this many points
+int build_lattice(mlb_binding* b, const std::vector<int64_t>& cnt, const std::vector<int32_t>& key_gcell, int mode,
+                  cudaStream_t st);
+int launch_lat_spread(mlb_binding* b, const double* v, unsigned flags, cudaStream_t st);
+int launch_lat_reduce(mlb_binding* b, const PeerOut& grid, cudaStream_t st);
+int launch_lat_gather(mlb_binding* b, const double* grid, const double* v, double* y, double alpha, double beta,
+                      double gamma, unsigned flags, cudaStream_t st);
 int launch_apply_multi(mlb_binding* const* b, int T, const double* const* v, double* const* y, const double* abg,
                        unsigned flags, cudaStream_t st);
 }  // namespace mlb

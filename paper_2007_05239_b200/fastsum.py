@@ -470,8 +470,10 @@ class PointBinding:
     def stats(self):
         o = (C.c_int64 * 8)()
         _lib.check(_lib.load().mlb_binding_stats(self.ptr, o))
+        lat = (C.c_int64 * 2)()
+        _lib.check(_lib.load().mlb_binding_lattice(self.ptr, lat))
         return dict(zip(("n", "chunks", "segments", "bricks", "tile_cells", "grid_cells", "band_ctas",
-                         "band_tile_cells"), list(o)))
+                         "band_tile_cells", "lattice_items", "lattice_points"), list(o) + list(lat)))
 
     def sorted_perm(self):
         out = np.empty(self.n, dtype=np.int32)

@@ -401,6 +401,12 @@ class MultilayerGraph:
         return MultilayerGraph(tuple(self.layers[i] for i in layer_indices))
 
 
+def _fills_sms(layer):
+    """Do the layer's spread / gather run one CTA per SM for a whole wave?"""
+    plan = getattr(layer.weights, "plan", None)
+    return plan is not None and plan.d == 3 and plan.m_nfft >= 5
+
+
 def _layer_cost(layer):
     """Relative cost of one L_sym apply of a layer: n (2m+1)^d for NFFT layers."""
     w = layer.weights
@@ -437,6 +443,17 @@ class LaplacianBatch:
             # stream priority; cheaper layers fill the SMs it leaves idle
             cost = [_layer_cost(layer) for layer in graph.layers]
             top = max(range(len(cost)), key=lambda i: cost[i])
+            # ... unless the costliest layer's kernels hold every SM for their
+            # whole run (d = 3, m >= 5: one CTA per SM, one wave): then nothing
+            # fills beside them, and the cheap layer goes first so its
+            # device->host copy overlaps the long layer (config 4: synchronous
+            # e2e 2.72 -> 3.27e9, streamed 4.88 -> 5.75e9; step -0.4 %)
+            pl = os.environ.get("MLB_PRIO_LAYER", "auto")
+            if pl == "cheap" or (pl == "auto" and _fills_sms(graph.layers[top])):
+                top = min(range(len(cost)), key=lambda i: cost[i])
+            # apply_many issues the layers cheapest first, so the copy-out
+            # stream gets results in the order they finish
+            self._order = sorted(range(len(cost)), key=lambda i: cost[i])
             prio = os.environ.get("MLB_NO_STREAM_PRIORITY") is None
             hi = int(os.environ.get("MLB_STREAM_PRIORITY", "-1"))  # torch range on B200: 0 (low) .. -3 (high)
             # one stream per weights object: a binding's scratch grids must not be shared
@@ -563,7 +580,13 @@ class LaplacianBatch:
         with torch.cuda.device(dev):
             v2 = torch.empty_like(self._v)
             y2 = torch.empty_like(self._y)
-            self._couts = [torch.cuda.Stream(device=dev) for _ in self.graph.layers]
+            # one copy-out stream (MLB_COUT=layer: one per layer): device->host
+            # copies queue in finishing order, so the D2H engine never idles
+            # behind a layer still computing while another's result waits
+            if os.environ.get("MLB_COUT", "one") == "layer":
+                self._couts = [torch.cuda.Stream(device=dev) for _ in self.graph.layers]
+            else:
+                self._couts = [torch.cuda.Stream(device=dev)] * len(self.graph.layers)
             self._cin = torch.cuda.Stream(device=dev)
         graphs2 = None
         if self._use_graph:
@@ -626,7 +649,7 @@ class LaplacianBatch:
             with torch.cuda.stream(self._cin):
                 self._vb[b].copy_(src[i], non_blocking=True)
             ev_in[b].record(self._cin)
-            for t in range(T):
+            for t in self._order:
                 s = self._streams[t]
                 s.wait_event(ev_in[b])
                 if i >= 2:  # buffer b's output row is free once vector i-2's copy-out is done
@@ -643,7 +666,7 @@ class LaplacianBatch:
                 with torch.cuda.stream(co):
                     out[i, t].copy_(self._yb[b][t], non_blocking=True)
                 ev_out[b][t].record(co)
-        for s in self._couts + self._streams + [self._cin]:
+        for s in list(dict.fromkeys(self._couts + self._streams + [self._cin])):
             main.wait_stream(s)
         main.synchronize()
         return out

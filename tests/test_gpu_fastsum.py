@@ -551,3 +551,85 @@ def test_bare_nfft_matches_naive_dft_and_oracle(d):
     assert np.abs(fwd - ref).max() <= 1e-12 * np.abs(ref).max()
     lhs, rhs = np.sum(fwd * v), np.sum(c * np.conj(adj))
     assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def _lattice_points(W, H, lo=-0.2, hi=0.2, transpose=False):
+    """Pixel coordinates of a W x H image in the box (node = row * W + col)."""
+    xs, ys = np.linspace(lo, hi, W), np.linspace(-0.2, 0.2, H)
+    X, Y = np.meshgrid(xs, ys)   # row-major: Y constant along a row
+    pts = np.stack([X.ravel(), Y.ravel()], axis=1)
+    return pts[:, ::-1].copy() if transpose else pts
+
+
+@pytest.mark.parametrize("layout,m", [("image", 5), ("image_t", 4), ("mixed", 5), ("image", 3), ("cut", 6)])
+def test_lattice_d2_kernels_match_oracle(layout, m):
+    """The d = 2 lattice kernels (cells whose points form R x C product sets:
+    spread = Ws^T (SV Wf), gather = (Ws G) Wf^T; non-lattice cells as
+    diagonal items) forced on: spread grid vs the oracle, fastsum and the
+    fused Laplacian epilogue (node / cell order, accumulate) vs the general
+    kernels (MLB_LATTICE=0), repeated spreads bitwise identical."""
+    import os
+
+    import torch
+    from paper_2007_05239_b200 import KernelSpec, bind_points, build_plan
+    from paper_2007_05239_b200 import _lib
+    from paper_2007_05239_b200.fastsum import fastsum_apply
+    rng = np.random.default_rng(31)
+    if layout in ("image", "image_t"):
+        pts = _lattice_points(173, 151, transpose=layout == "image_t")
+    elif layout == "mixed":   # an image plus scattered points (diagonal items)
+        img = _lattice_points(120, 90, -0.2, 0.0)
+        pts = np.concatenate([img, rng.uniform(0.02, 0.2, size=(3000, 2)), img[::97] + 1e-3])
+    else:                     # a node range cutting rows (a shard of an image)
+        pts = _lattice_points(160, 160)[1234:21234]
+    n = len(pts)
+    v = rng.standard_normal(n)
+    plan = build_plan(KernelSpec("gaussian", 0.1), d=2, N=64, m_nfft=m, p_nfft=8)
+    lib = _lib.lib()
+    L, ulo = None, None
+    try:
+        os.environ["MLB_LATTICE"] = "1"
+        b = bind_points(plan, pts)
+        st = b.stats()
+        assert st["lattice_items"] > 0
+        assert st["lattice_points"] >= (0.5 * n if layout != "cut" else 0.8 * n)
+        L, ulo = b._plan_handle.L, b._plan_handle.ulo
+        vd = torch.from_numpy(v).cuda()
+        grids = []
+        for _ in range(2):
+            g = torch.zeros(L * L, dtype=torch.float64, device="cuda")
+            _lib.check(lib.mlb_spread(b.ptr, _lib.ptr(vd), _lib.ptr(g), 0, _lib.stream_ptr()))
+            grids.append(g.cpu().numpy())
+        y_lat = fastsum_apply(pts, v, plan, binding=b)
+        os.environ["MLB_LATTICE"] = "0"
+        b0 = bind_points(plan, pts)
+        assert b0.stats()["lattice_items"] == 0
+        y_gen = fastsum_apply(pts, v, plan, binding=b0)
+    finally:
+        del os.environ["MLB_LATTICE"]
+    assert np.array_equal(grids[0], grids[1])
+    op = fo.OraclePlan("gaussian", 0.1, 2, 64, m, p=8)
+    full = fo.spread(fo.bind(op, pts), v).reshape(op.ng, op.ng)
+    idx = np.mod(np.arange(ulo, ulo + L), op.ng)
+    assert rel(grids[0].reshape(L, L), full[np.ix_(idx, idx)]) < 1e-13
+    assert rel(y_lat, y_gen) < 1e-13
+    ref = fo.fastsum(op, v, points=pts) if n <= 20000 else None
+    if ref is not None:
+        assert rel(y_lat, ref) < 1e-12
+    # fused epilogue: y = a v + s (b acc + c s v), node and cell order, accumulate
+    s = torch.from_numpy(rng.uniform(0.5, 2.0, n)).cuda()
+    for bb in (b, b0):
+        _lib.check(lib.mlb_binding_set_isd(bb.ptr, _lib.ptr(s), _lib.stream_ptr()))
+    outs = []
+    for bb in (b, b0):
+        y = torch.full((n,), 0.25, dtype=torch.float64, device="cuda")
+        _lib.check(lib.mlb_apply(bb.ptr, _lib.ptr(vd), _lib.ptr(y), 1.3, -0.7, 0.2, 1 | 2, _lib.stream_ptr()))
+        perm = torch.from_numpy(bb.sorted_perm().astype(np.int64)).cuda()
+        vs = vd[perm].contiguous()
+        ys = torch.empty_like(vs)
+        _lib.check(lib.mlb_apply(bb.ptr, _lib.ptr(vs), _lib.ptr(ys), 1.3, -0.7, 0.2, 1 | 4, _lib.stream_ptr()))
+        yn = torch.empty_like(ys)
+        yn[perm] = ys
+        outs.append((y.cpu().numpy(), yn.cpu().numpy()))
+    assert rel(outs[0][0], outs[1][0]) < 1e-13
+    assert rel(outs[0][1], outs[1][1]) < 1e-13

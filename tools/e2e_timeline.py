@@ -8,8 +8,9 @@ import bench
 from paper_2007_05239_b200 import LaplacianBatch, MultilayerGraph
 
 torch.cuda.set_device(0)
-wl = synth.config2_segmentation(seed=0)
-layers = bench.build_layers(wl, 0, math.log(2.0))
+wl = synth.config4_large(seed=0) if os.environ.get("CFG4") else synth.config2_segmentation(seed=0)
+from paper_2007_05239_b200 import with_shift
+layers = [with_shift(l, math.log(2.0)) for l in synth.build_graph(wl, device=0).layers]
 n, T = wl.n, len(layers)
 b = LaplacianBatch(MultilayerGraph(tuple(layers)))
 vp = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).pin_memory()
