@@ -18,6 +18,10 @@ OUT = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 def kernel_key(name):
     if "spread_cells_kernel" in name:
         return "spread_d3"
+    if "lat_spread_kernel" in name:
+        return "spread_d2"
+    if "lat_gather_kernel" in name:
+        return "gather_d2"
     for kern in ("spread_kernel<", "gather_kernel<"):
         if kern in name:
             d = name.split(kern)[1].split(",")[0].replace("(int)", "").strip()
