@@ -55,59 +55,86 @@ namespace mlb {
 
 
 // ------------------------------------------------------------- detection --
-// One warp per cell (key): is the cell's point list an R x C product set in
-// row-major order?  Axis a is "slow" if the first run holds its offset fixed.
-// out[k] = C | fast << 16 (lattice), 0 (empty cell), -1 (not a lattice).
+// First index in [i0, i1) (step dir = +1) or last index in [i1, i0] (dir =
+// -1, scanning down from i0) where f differs from f[i0]; returns the run
+// length of the constant value starting at i0 in that direction.
+__device__ __forceinline__ int lat_run(const double* __restrict__ f, int i0, int len, int dir, int lane) {
+    const double f0 = f[i0];
+    for (int base = 0; base < len; base += 32) {
+        const int i = base + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, i < len && f[i0 + dir * i] != f0);
+        if (m) return base + __ffs(m) - 1;
+    }
+    return len;
+}
+
+// Is [q0, q0 + Q) an (Q / C) x C product set with `fast` varying along runs of C?
+__device__ __forceinline__ bool lat_check(const double* __restrict__ frac, int64_t n, int q0, int Q, int C, int fast,
+                                          int lane) {
+    const double* ff = frac + fast * n + q0;
+    const double* fs = frac + (1 - fast) * n + q0;
+    bool bad = false;
+    for (int i = lane; i < Q; i += 32) {
+        const int r = i / C, c = i - r * C;
+        bad |= (ff[i] != ff[c]) || (fs[i] != fs[r * C]);
+    }
+    return !__any_sync(0xffffffffu, bad);
+}
+
+// One warp per cell (key): is the cell's point list (cell-sorted = node
+// order, i.e. row-major for an image) an R x C product set, or -- a node
+// range cutting the image's rows (a shard) -- a partial run, an R x C
+// product set and a partial run?  out[4k..4k+3] = {code, fast | C << 1, a, b}:
+// code 0 empty cell, -1 not a lattice, 1 one R x C lattice (all P points),
+// 3 segments [0, a) (one run), [a, b) (runs of C), [b, P) (one run).
 __global__ void lat_detect_kernel(const double* __restrict__ frac, int64_t n, const int32_t* __restrict__ ks,
                                   int nkeys, int cmax, int32_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (k >= nkeys) return;
     const int p0 = ks[k], P = ks[k + 1] - p0;
+    int code = -1, fastC = 0, a = 0, b = 0;
     if (P == 0) {
-        if (lane == 0) out[k] = 0;
-        return;
-    }
-    // run lengths of a constant axis-0 / axis-1 offset from the first point
-    int run[2];
-#pragma unroll
-    for (int ax = 0; ax < 2; ++ax) {
-        const double* f = frac + ax * n + p0;
-        const double f0 = f[0];
-        int r = P;
-        for (int base = 0; base < P; base += 32) {
-            const int i = base + lane;
-            const unsigned m = __ballot_sync(0xffffffffu, i < P && f[i] != f0);
-            if (m) {
-                r = base + __ffs(m) - 1;
-                break;
+        code = 0;
+    } else {
+        // whole cell: axis 0 fixed along the first run -> axis 1 is fast
+        const int run0 = lat_run(frac + p0, 0, P, 1, lane);
+        const int run1 = lat_run(frac + n + p0, 0, P, 1, lane);
+        const int fast = run0 >= 2 ? 1 : (run1 >= 2 ? 0 : 1);
+        const int C = run0 >= 2 ? run0 : (run1 >= 2 ? run1 : 1);
+        if (P % C == 0 && C <= cmax && lat_check(frac, n, p0, P, C, fast, lane)) {
+            code = 1;
+            fastC = fast | (C << 1);
+        } else {
+            // a partial first / last run around a lattice (either axis slow)
+            for (int fa = 1; fa >= 0 && code < 0; --fa) {
+                const double* fs = frac + (1 - fa) * n + p0;
+                const int ra = lat_run(fs, 0, P, 1, lane);               // first run
+                if (ra >= P) continue;
+                const int rb = lat_run(fs, P - 1, P - ra, -1, lane);     // last run
+                const int A = ra, B = P - rb;
+                if (A > cmax || rb > cmax) continue;
+                int Cm = 1;
+                bool ok = true;
+                if (B > A) {
+                    Cm = lat_run(fs, A, B - A, 1, lane);
+                    ok = (B - A) % Cm == 0 && Cm <= cmax && lat_check(frac, n, p0 + A, B - A, Cm, fa, lane);
+                }
+                if (ok) {
+                    code = 3;
+                    fastC = fa | (Cm << 1);
+                    a = A;
+                    b = B;
+                }
             }
         }
-        run[ax] = r;
     }
-    int fast, C;
-    if (run[0] >= 2) {          // axis 0 fixed along the run: axis 1 is fast
-        fast = 1;
-        C = run[0];
-    } else if (run[1] >= 2) {
-        fast = 0;
-        C = run[1];
-    } else {
-        fast = 1;
-        C = 1;                  // a single point, or not a lattice (checked below)
+    if (lane == 0) {
+        out[4 * k] = code;
+        out[4 * k + 1] = fastC;
+        out[4 * k + 2] = a;
+        out[4 * k + 3] = b;
     }
-    bool ok = (P % C == 0) && C <= cmax;
-    if (ok) {
-        const double* ff = frac + fast * n + p0;
-        const double* fs = frac + (1 - fast) * n + p0;
-        bool bad = false;
-        for (int i = lane; i < P; i += 32) {
-            const int r = i / C, c = i - r * C;
-            bad |= (ff[i] != ff[c]) || (fs[i] != fs[r * C]);
-        }
-        ok = !__any_sync(0xffffffffu, bad);
-    }
-    if (lane == 0) out[k] = ok ? (C | (fast << 16)) : -1;
 }
 
 // ------------------------------------------------------------ the kernels --
@@ -484,7 +511,7 @@ int build_lattice(mlb_binding* b, const std::vector<int64_t>& cnt, const std::ve
     std::vector<int32_t> ks(cnt.begin(), cnt.end());
     int32_t *ks_d = nullptr, *out_d = nullptr;
     MLB_CUDA_TRY(cudaMalloc(&ks_d, ks.size() * sizeof(int32_t)));
-    MLB_CUDA_TRY(cudaMalloc(&out_d, (size_t)nkeys * sizeof(int32_t)));
+    MLB_CUDA_TRY(cudaMalloc(&out_d, (size_t)nkeys * 4 * sizeof(int32_t)));
     struct Free {
         int32_t *a, *b;
         ~Free() {
@@ -496,17 +523,36 @@ int build_lattice(mlb_binding* b, const std::vector<int64_t>& cnt, const std::ve
     lat_detect_kernel<<<(nkeys + 7) / 8, 256, 0, st>>>(b->frac, b->n, ks_d, nkeys, kLatCols, out_d);
     note_launches(1);
     MLB_CUDA_TRY(cudaGetLastError());
-    std::vector<int32_t> lat(nkeys);
-    MLB_CUDA_TRY(cudaMemcpyAsync(lat.data(), out_d, (size_t)nkeys * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> lat((size_t)nkeys * 4);
+    MLB_CUDA_TRY(cudaMemcpyAsync(lat.data(), out_d, lat.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     MLB_CUDA_TRY(cudaStreamSynchronize(st));
+    // segments of a cell: {first point, rows, C, fast}; lattice = runs of C
+    struct Seg { int64_t p0, R; int C, fast, diag; };
+    auto segments = [&](int k, std::vector<Seg>& out) {
+        out.clear();
+        const int64_t p0 = cnt[k], P = cnt[k + 1] - p0;
+        const int code = lat[4 * k], fast = lat[4 * k + 1] & 1, C = lat[4 * k + 1] >> 1;
+        if (P == 0) return;
+        if (code == 1) {
+            out.push_back({p0, P / C, C, fast, 0});
+        } else if (code == 3) {
+            const int64_t a = lat[4 * k + 2], bb = lat[4 * k + 3];
+            if (a > 0) out.push_back({p0, 1, (int)a, fast, 0});
+            if (bb > a) out.push_back({p0 + a, (bb - a) / C, C, fast, 0});
+            if (P > bb) out.push_back({p0 + bb, 1, (int)(P - bb), fast, 0});
+        } else {
+            out.push_back({p0, P, 1, 1, 1});   // diagonal: one row per point
+        }
+    };
+    std::vector<Seg> segs;
     int64_t lat_pts = 0;
     for (int k = 0; k < nkeys; ++k) {
-        const int64_t P = cnt[k + 1] - cnt[k];
-        const int C = lat[k] & 0xffff;
-        if (lat[k] > 0 && C >= 2 && P / C >= 2) lat_pts += P;
+        segments(k, segs);
+        for (const Seg& sg : segs)
+            if (!sg.diag && sg.C >= 2 && sg.R >= 2) lat_pts += sg.R * sg.C;
     }
     if (mode < 0 && 2 * lat_pts < b->n) return MLB_OK;
-    // items: <= rows_cap rows of one cell (about a CTA's share of the points)
+    // items: <= rows_cap rows of one segment (about a CTA's share of the points)
     const int nsm = b->plan->nsm;
     int64_t tgt = std::min<int64_t>(kLatPts, std::max<int64_t>(512, b->n / (nsm * 8)));
     if (const char* env = std::getenv("MLB_LAT_TGT")) tgt = std::max<int64_t>(64, std::min<int64_t>(kLatPts, std::atoll(env)));   // tuning
@@ -514,32 +560,28 @@ int build_lattice(mlb_binding* b, const std::vector<int64_t>& cnt, const std::ve
     std::vector<std::vector<int32_t>> bin_items((size_t)g.nb * g.nb);
     int nf_max = 1, r_max = 1, sv_max = 1;
     for (int k = 0; k < nkeys; ++k) {
-        const int64_t p0 = cnt[k], P = cnt[k + 1] - p0;
-        if (P == 0) continue;
+        segments(k, segs);
+        if (segs.empty()) continue;
         const int gc = key_gcell[k];
         const int bin = (gc / g.L) * g.nb + gc % g.L;
-        int C = 1, fast = 1, diag = 1;
-        int64_t R = P;
-        if (lat[k] > 0) {
-            C = lat[k] & 0xffff;
-            fast = (lat[k] >> 16) & 1;
-            diag = 0;
-            R = P / C;
-        }
-        int64_t rows_cap = diag ? kLatRowsMax : std::max<int64_t>(1, std::min<int64_t>(kLatRowsMax, tgt / C));
-        if (!diag) rows_cap = std::min<int64_t>(rows_cap, (int64_t)kLatGatherSlots * (kLatThreads / C));   // gather slots
-        const int64_t nparts = (R + rows_cap - 1) / rows_cap;
-        rows_cap = (R + nparts - 1) / nparts;   // even parts
-        for (int64_t r0 = 0; r0 < R; r0 += rows_cap) {
-            const int64_t rn = std::min(rows_cap, R - r0);
-            bin_items[bin].push_back((int32_t)(items.size() / 4));
-            items.push_back((int32_t)(p0 + r0 * (diag ? 1 : C)));
-            items.push_back((int32_t)rn);
-            items.push_back(C | (fast << 16) | (diag << 17));
-            items.push_back(gc);
-            nf_max = std::max<int>(nf_max, diag ? (int)rn : C);
-            r_max = std::max<int>(r_max, (int)rn);
-            sv_max = std::max<int>(sv_max, diag ? (int)rn : (int)rn * (C | 1));
+        for (const Seg& sg : segs) {
+            const int C = sg.C, fast = sg.fast, diag = sg.diag;
+            const int64_t R = sg.R;
+            int64_t rows_cap = diag ? kLatRowsMax : std::max<int64_t>(1, std::min<int64_t>(kLatRowsMax, tgt / C));
+            if (!diag) rows_cap = std::min<int64_t>(rows_cap, (int64_t)kLatGatherSlots * (kLatThreads / C));   // gather slots
+            const int64_t nparts = (R + rows_cap - 1) / rows_cap;
+            rows_cap = (R + nparts - 1) / nparts;   // even parts
+            for (int64_t r0 = 0; r0 < R; r0 += rows_cap) {
+                const int64_t rn = std::min(rows_cap, R - r0);
+                bin_items[bin].push_back((int32_t)(items.size() / 4));
+                items.push_back((int32_t)(sg.p0 + r0 * (diag ? 1 : C)));
+                items.push_back((int32_t)rn);
+                items.push_back(C | (fast << 16) | (diag << 17));
+                items.push_back(gc);
+                nf_max = std::max<int>(nf_max, diag ? (int)rn : C);
+                r_max = std::max<int>(r_max, (int)rn);
+                sv_max = std::max<int>(sv_max, diag ? (int)rn : (int)rn * (C | 1));
+            }
         }
     }
     // items sorted by bin (CSR) so the reduction walks each bin's items in order
