@@ -438,18 +438,25 @@ def test_peer_grid_exchange_two_emulated_ranks():
     import torch
     from paper_2007_05239_b200 import KernelSpec, build_plan, bind_points, _lib
     from paper_2007_05239_b200.dist import PeerGridExchange
+    import os
     rng = np.random.default_rng(8)
     n = 4000
-    for d, N, m in ((3, 32, 4), (2, 32, 4)):
-        pts = np.clip(rng.normal(0, 0.07, size=(n, d)), -0.21875, 0.21875)
+    for d, N, m, lattice in ((3, 32, 4, False), (2, 32, 4, False), (2, 64, 5, True)):
+        if lattice:   # an image's pixels, ranks cutting its rows: lattice items + shard-cut segments
+            pts = _lattice_points(80, 50)
+            os.environ["MLB_LATTICE"] = "1"
+        else:
+            pts = np.clip(rng.normal(0, 0.07, size=(n, d)), -0.21875, 0.21875)
+        n = len(pts)
         v = rng.standard_normal(n)
         plan = build_plan(KernelSpec("gaussian", 0.12), d=d, N=N, m_nfft=m, p_nfft=8)
         full = bind_points(plan, pts)
+        assert (full.stats()["lattice_items"] > 0) == lattice
         cells = full.stats()["grid_cells"]
         ref = torch.zeros(cells, dtype=torch.float64, device="cuda")
         _lib.check(_lib.lib().mlb_spread(full.ptr, _lib.ptr(torch.from_numpy(v).cuda()), _lib.ptr(ref), 0,
                                          _lib.stream_ptr()))
-        halves = [(0, n // 2), (n // 2, n)]
+        halves = [(0, n // 2 + 17), (n // 2 + 17, n)]
         recv = [torch.full((2 * cells,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(2)]
         grids = []
         for r, (lo, hi) in enumerate(halves):
@@ -465,6 +472,7 @@ def test_peer_grid_exchange_two_emulated_ranks():
             g = torch.empty(cells, dtype=torch.float64, device="cuda")
             _lib.check(_lib.lib().mlb_grid_sum_slots(_lib.ptr(recv[r]), 2, cells, _lib.ptr(g), _lib.stream_ptr()))
             out.append(g.cpu().numpy())
+        os.environ.pop("MLB_LATTICE", None)
         assert np.array_equal(out[0], out[1])
         assert rel(out[0], ref.cpu().numpy()) < 1e-13
 
