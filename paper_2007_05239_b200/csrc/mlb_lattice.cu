@@ -33,7 +33,9 @@
 // config 4 (d = 2 spread / gather us): CTAs per SM of the spread (2: 143 /
 // 3: 124 / 4: 116) and gather (2: 98 / 3: 83), window polynomials as
 // per-thread tasks (spread 166 -> 124 at 3 CTAs; gather 98 -> 137: divergent
-// constant-bank reads), gather epilogue loads hoisted (123 -> 98 at 2 CTAs)
+// constant-bank reads), gather epilogue loads hoisted (123 -> 98 at 2 CTAs),
+// the spread's two contractions on the fp64 tensor cores (DMMA m8n8k4: 116 ->
+// 112 us; the FMA path with column-group partials stays as MLB_LAT_DMMA=0)
 #ifndef MLB_LAT_SPREAD_MINB
 #define MLB_LAT_SPREAD_MINB 4
 #endif
@@ -46,11 +48,22 @@
 #ifndef MLB_LAT_WTASK_G
 #define MLB_LAT_WTASK_G 0
 #endif
+#ifndef MLB_LAT_DMMA
+#define MLB_LAT_DMMA 1
+#endif
 #ifndef MLB_LAT_GHOIST
 #define MLB_LAT_GHOIST 1
 #endif
 
 namespace mlb {
+
+// fp64 tensor-core MMA (one warp): D(8x8) += A(8x4, row) B(4x8, col); lane l
+// holds A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) .. 2(l%4)+1]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 
 
@@ -223,8 +236,8 @@ __global__ void __launch_bounds__(kLatThreads, MLB_LAT_SPREAD_MINB)
     double* SV = sm;
     double* Wf = SV + lay.sv_max;
     double* Ws = Wf + lay.nf_max * S;
-    double* Tp = Ws + lay.r_max * S;
-    double* T = Tp + kLatThreads * S;
+    double* Tp = Ws + lay.r_max * S;                          // column-group partials (FMA path)
+    double* T = Tp + (MLB_LAT_DMMA ? 0 : kLatThreads * S);
     const bool sorted = (flags & MLB_SORTED) != 0, use_isd = (flags & MLB_USE_ISD) != 0;
     const int tid = threadIdx.x;
     int nd[KP];
@@ -257,6 +270,59 @@ __global__ void __launch_bounds__(kLatThreads, MLB_LAT_SPREAD_MINB)
         }
     }
     __syncthreads();
+#if MLB_LAT_DMMA
+    const int lane = tid & 31, warp = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;   // fragment row / column group of the lane
+    constexpr int NT = (S + 7) / 8;            // 8-wide tiles over the S window offsets
+    if (!diag) {
+        // T = SV Wf on the fp64 tensor cores: warp w owns 8 x 8 tiles
+        // (row tile, offset tile) w, w + 8, ...; K = C columns in steps of 4
+        const int MT = (R + 7) / 8;
+        for (int tile = warp; tile < MT * NT; tile += kLatThreads / 32) {
+            const int r0 = (tile / NT) * 8, q0 = (tile % NT) * 8;
+            double d0 = 0.0, d1 = 0.0;
+            const int ra = r0 + gq, qb = q0 + gq;
+            for (int c0 = 0; c0 < C; c0 += 4) {
+                const int c = c0 + tq;
+                const double av = (ra < R && c < C) ? SV[ra * Cp + c] : 0.0;
+                const double bv = (c < C && qb < S) ? Wf[c * S + qb] : 0.0;
+                dmma884(d0, d1, av, bv);
+            }
+            const int q = q0 + 2 * tq;
+            if (ra < R) {
+                if (q < S) T[ra * S + q] = d0;
+                if (q + 1 < S) T[ra * S + q + 1] = d1;
+            }
+        }
+    } else {
+        for (int r = tid; r < R; r += kLatThreads) {
+            const double xv = SV[r];
+#pragma unroll
+            for (int q = 0; q < S; ++q) T[r * S + q] = xv * Wf[r * S + q];
+        }
+    }
+    __syncthreads();
+    // B = Ws^T T (S x S) on the tensor cores: one warp per 8 x 8 tile, K = R
+    double* out = blocks + (int64_t)blockIdx.x * S * S;
+    for (int tile = warp; tile < NT * NT; tile += kLatThreads / 32) {
+        const int ks0 = (tile / NT) * 8, kf0 = (tile % NT) * 8;
+        double d0 = 0.0, d1 = 0.0;
+        const int ksa = ks0 + gq, kfb = kf0 + gq;
+        for (int r0 = 0; r0 < R; r0 += 4) {
+            const int r = r0 + tq;
+            const double av = (r < R && ksa < S) ? Ws[r * S + ksa] : 0.0;
+            const double bv = (r < R && kfb < S) ? T[r * S + kfb] : 0.0;
+            dmma884(d0, d1, av, bv);
+        }
+        const int kf = kf0 + 2 * tq;
+        if (ksa < S) {
+            if (kf < S) out[fast ? ksa * S + kf : kf * S + ksa] = d0;
+            if (kf + 1 < S) out[fast ? ksa * S + kf + 1 : (kf + 1) * S + ksa] = d1;
+        }
+    }
+    pdl_launch();
+    (void)Tp;
+#else
     if (!diag) {
         // Tp[cg][r] = sum over column group cg of SV[r][c] Wf[c]: thread
         // (r, cg), r fastest, so a warp reads one Wf row (broadcast) per step
@@ -299,6 +365,7 @@ __global__ void __launch_bounds__(kLatThreads, MLB_LAT_SPREAD_MINB)
         out[fast ? q : kf * S + ks] = s;
     }
     pdl_launch();
+#endif
 }
 
 // grid cell (u0, u1) = sum over the bins (u0 - i, u1 - j), i, j < S, of their
@@ -431,7 +498,7 @@ static LatLayout lat_layout(const mlb_binding* b) {
 static size_t lat_smem(int M, const LatLayout& l, bool gather) {
     const int S = 2 * M + 1;
     if (gather) return ((size_t)(l.nf_max + 2 * l.r_max) * S + (size_t)S * S) * sizeof(double);
-    return ((size_t)l.sv_max + (size_t)(l.nf_max + 2 * l.r_max + kLatThreads) * S) * sizeof(double);
+    return ((size_t)l.sv_max + (size_t)(l.nf_max + 2 * l.r_max + (MLB_LAT_DMMA ? 0 : kLatThreads)) * S) * sizeof(double);
 }
 
 template <int M>
