@@ -35,9 +35,12 @@
 // per-thread tasks (spread 166 -> 124 at 3 CTAs; gather 98 -> 137: divergent
 // constant-bank reads), gather epilogue loads hoisted (123 -> 98 at 2 CTAs),
 // the spread's two contractions on the fp64 tensor cores (DMMA m8n8k4: 116 ->
-// 112 us; the FMA path with column-group partials stays as MLB_LAT_DMMA=0)
+// 112 us; the FMA path with column-group partials stays as MLB_LAT_DMMA=0),
+// the spread's window coefficients copied to shared memory (112 -> 102 us),
+// then 5 spread CTAs per SM (51 registers, no spill: 102 -> 97 us; 6: spills,
+// 119 us; per-value windows at 5: spills, 124 us)
 #ifndef MLB_LAT_SPREAD_MINB
-#define MLB_LAT_SPREAD_MINB 4
+#define MLB_LAT_SPREAD_MINB 5
 #endif
 #ifndef MLB_LAT_GATHER_MINB
 #define MLB_LAT_GATHER_MINB 3
@@ -50,6 +53,9 @@
 #endif
 #ifndef MLB_LAT_DMMA
 #define MLB_LAT_DMMA 1
+#endif
+#ifndef MLB_LAT_WSMEM
+#define MLB_LAT_WSMEM 1
 #endif
 #ifndef MLB_LAT_GHOIST
 #define MLB_LAT_GHOIST 1
@@ -249,12 +255,26 @@ __global__ void __launch_bounds__(kLatThreads, MLB_LAT_SPREAD_MINB)
         sc[k] = (idx < P && use_isd) ? __ldg(isd + p0 + idx) : 1.0;
     }
     const int nf = diag ? R : C;
-    lat_windows_range<M, MLB_LAT_WTASK_S>(it, frac, n, wc, Wf, Ws, 0, nf);
+#if MLB_LAT_WSMEM
+    // the window coefficients in shared memory: the per-thread polynomial
+    // tasks read different rows (divergent constant-bank reads serialise)
+    __shared__ WinCoef wcs;
+    {
+        const double* src = reinterpret_cast<const double*>(&wc);
+        double* dst = reinterpret_cast<double*>(&wcs);
+        for (int i = tid; i < (int)(sizeof(WinCoef) / sizeof(double)); i += kLatThreads) dst[i] = src[i];
+        __syncthreads();
+    }
+    const WinCoef& wq = wcs;
+#else
+    const WinCoef& wq = wc;
+#endif
+    lat_windows_range<M, MLB_LAT_WTASK_S>(it, frac, n, wq, Wf, Ws, 0, nf);
     pdl_wait();   // v comes from stream predecessors
     double x[KP];
 #pragma unroll
     for (int k = 0; k < KP; ++k) x[k] = nd[k] >= 0 ? __ldg(v + nd[k]) * sc[k] : 0.0;
-    lat_windows_range<M, MLB_LAT_WTASK_S>(it, frac, n, wc, Wf, Ws, nf, nf + R);
+    lat_windows_range<M, MLB_LAT_WTASK_S>(it, frac, n, wq, Wf, Ws, nf, nf + R);
     {   // point idx = tid + k * kLatThreads sits at (r, c) of the item: step by (dr, dc)
         int r = tid / Cw, c = tid - r * Cw;
         const int dr = kLatThreads / Cw, dc = kLatThreads - dr * Cw;
@@ -432,7 +452,19 @@ __global__ void __launch_bounds__(kLatThreads, MLB_LAT_GATHER_MINB)
             sc[k] = (ok && use_isd) ? __ldg(isd + p) : 1.0;
         }
     }
-    lat_windows_range<M, MLB_LAT_WTASK_G>(it, frac, n, wc, Wf, Ws, 0, (diag ? R : C) + R);
+#if MLB_LAT_WTASK_G && MLB_LAT_WSMEM
+    __shared__ WinCoef wcs;
+    {
+        const double* src = reinterpret_cast<const double*>(&wc);
+        double* dst = reinterpret_cast<double*>(&wcs);
+        for (int i = tid; i < (int)(sizeof(WinCoef) / sizeof(double)); i += kLatThreads) dst[i] = src[i];
+        __syncthreads();
+    }
+    const WinCoef& wq = wcs;
+#else
+    const WinCoef& wq = wc;
+#endif
+    lat_windows_range<M, MLB_LAT_WTASK_G>(it, frac, n, wq, Wf, Ws, 0, (diag ? R : C) + R);
     pdl_wait();   // the grid and v come from stream predecessors
     if (MLB_LAT_GHOIST) {
 #pragma unroll
