@@ -13,6 +13,8 @@ the host only reads the two maxima of the stopping rule each iteration.
 import ctypes as C
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -134,22 +136,45 @@ def allen_cahn_solve(basis, labels, params, callback=None, device=None, return_d
     lib = _lib.lib()
     work = torch.empty(int(lib.mlb_ac_work_size(n, k, m)), dtype=torch.float64, device=U.device)
     stats = torch.empty(2, dtype=torch.float64, device=U.device)
+    # The device runs one iteration ahead of the host's stopping test (the
+    # test of iteration t reads its two maxima from pinned memory while
+    # iteration t+1 computes into the other buffer; a stop at t discards
+    # t+1).  Iterates are bitwise those of the one-at-a-time loop.
+    # MLB_AC_DEPTH=1 (or a callback, which needs every iterate) disables it.
+    depth = 1 if callback is not None else max(1, min(2, int(os.environ.get("MLB_AC_DEPTH", "2"))))
+    bufs = (U, Un)
+    pin = torch.empty((2, 2), dtype=torch.float64, pin_memory=True)
+    evs = (torch.cuda.Event(), torch.cuda.Event())
+    stream = torch.cuda.current_stream(U.device)
+
+    def launch(it):
+        src, dst = bufs[(it - 1) % 2], bufs[it % 2]
+        _lib.check(lib.mlb_ac_step2(_lib.ptr(Phi), n, k, m, _lib.ptr(src), _lib.ptr(F), _lib.ptr(fid),
+                                    _lib.ptr(denom), 1.0 + c * dt, dt / (2.0 * eps), dt, int(it == 1), _lib.ptr(dst),
+                                    _lib.ptr(stats), _lib.ptr(work), _lib.stream_ptr()))
+        pin[it % 2].copy_(stats, non_blocking=True)
+        evs[it % 2].record(stream)
+
     converged = False
     iterations = 0
+    launch(1)
     for it in range(1, params.max_iter + 1):
-        _lib.check(lib.mlb_ac_step2(_lib.ptr(Phi), n, k, m, _lib.ptr(U), _lib.ptr(F), _lib.ptr(fid),
-                                    _lib.ptr(denom), 1.0 + c * dt, dt / (2.0 * eps), dt, int(it == 1), _lib.ptr(Un),
-                                    _lib.ptr(stats), _lib.ptr(work), _lib.stream_ptr()))
-        num, den = stats.cpu().numpy()
+        if depth > 1 and it < params.max_iter:
+            launch(it + 1)   # speculative: writes the other buffer
+        evs[it % 2].synchronize()
+        num, den = (float(x) for x in pin[it % 2])
         if den <= 0 or not np.isfinite(num):
             raise NumericalError("Allen-Cahn iterate degenerated")
-        U, Un = Un, U
+        U = bufs[it % 2]
         iterations = it
         if callback is not None:
             callback(it, U.cpu().numpy())
         if num / den <= params.tolerance:
             converged = True
             break
+        if depth == 1 and it < params.max_iter:
+            launch(it + 1)
+    stream.synchronize()   # (a discarded speculative step may still run)
     scores = U if return_device else U.cpu().numpy()
     return AllenCahnResult(scores=scores, iterations=iterations, converged=converged)
 

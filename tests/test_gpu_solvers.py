@@ -181,6 +181,22 @@ def test_allen_cahn_matches_golden():
     assert [res.iterations, int(res.converged)] == list(g["ac_iters"])
     assert np.abs(res.scores - g["ac_scores"]).max() < 1e-9
     assert np.array_equal(predict_labels(res.scores), g["ac_pred"])
+    # the device runs one iteration ahead of the stopping test: the same
+    # iterates as one at a time, and as with a callback (which sees each)
+    import os
+    seen = []
+    os.environ["MLB_AC_DEPTH"] = "1"
+    try:
+        one = allen_cahn_solve(basis, labels, AllenCahnParams())
+    finally:
+        del os.environ["MLB_AC_DEPTH"]
+    cb = allen_cahn_solve(basis, labels, AllenCahnParams(), callback=lambda it, U: seen.append(it))
+    for other in (one, cb):
+        assert other.iterations == res.iterations and other.converged == res.converged
+        assert np.array_equal(other.scores, res.scores)
+    assert seen == list(range(1, res.iterations + 1))
+    capped = allen_cahn_solve(basis, labels, AllenCahnParams(max_iter=3))
+    assert capped.iterations == 3 and not capped.converged
 
 
 def test_end_to_end_labels_match_oracle():
