@@ -235,7 +235,11 @@ def kernel_table(stages, workload, hbm_peak, fp64_peak):
             gbs = nbytes / (ms * 1e-3) / 1e9
             tfs = nflops / (ms * 1e-3) / 1e12
             traffic, src = _traffic(workload, name, d)
-            rows.append({"kernel": name, "layer": st["layer"], "d": d, "N": st["N"], "m": m, "n": nl, "ms": ms,
+            st_ = st["stats"]
+            path = ("lattice" if st_.get("lattice_items", 0) > 0 else
+                    ("cells" if d == 3 else ("banded" if st_.get("band_ctas", 0) > 0 else "tiles")))
+            rows.append({"kernel": name, "path": path, "layer": st["layer"], "d": d, "N": st["N"], "m": m, "n": nl,
+                         "ms": ms,
                          "alg_bytes": nbytes, "alg_flops": nflops, "gbs": gbs, "hbm_frac": gbs / hbm_peak,
                          "fp64_tflops": tfs, "fp64_frac": tfs / fp64_peak if fp64_peak else None,
                          "traffic": traffic, "traffic_source": src})
@@ -575,8 +579,8 @@ def run_ours(args):
                           "hbm_frac": step_bytes * ws / (ms_step * 1e-3) / 1e9 / hbm_peak / ws,
                           "fp64_flops_per_step": step_flops * ws,
                           "fp64_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak if fp64_peak else None},
-        "kernels": [{k: r[k] for k in ("kernel", "d", "m", "n", "ms", "gbs", "hbm_frac", "fp64_tflops", "fp64_frac",
-                                       "traffic")} for r in rows if r["kernel"] in ("spread", "gather")],
+        "kernels": [{k: r[k] for k in ("kernel", "path", "d", "m", "n", "ms", "gbs", "hbm_frac", "fp64_tflops",
+                                       "fp64_frac", "traffic")} for r in rows if r["kernel"] in ("spread", "gather")],
         "stages_ms": [{k: st[k] for k in ("layer", "d", "N", "m", "n", "spread_ms", "reduce_ms", "convolve_ms",
                                           "gather_ms")} for st in stages],
         **extra,
