@@ -20,6 +20,7 @@ formed once at the end.  Borderline steps (ratio within
 
 import ctypes as C
 import os
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -44,7 +45,8 @@ class _Work:
     def get(cls, device, cols):
         torch = _torch()
         need = int(_lib.lib().mlb_krylov_work_size(0, int(cols) + 2))
-        key = int(device)
+        # per (device, stream): chains on concurrent streams keep their own scratch
+        key = (int(device), torch.cuda.current_stream(int(device)).cuda_stream)
         buf = cls._cache.get(key)
         if buf is None or buf.numel() < need:
             buf = torch.empty(max(need, 1 << 16), dtype=torch.float64, device=f"cuda:{device}")
@@ -293,7 +295,8 @@ def _pinned_snapshots(shape, device):
     solve at the same level is safe: every read waits for its own step's
     event, which follows any earlier copy into the buffer on the stream."""
     torch = _torch()
-    key = (int(device.index if hasattr(device, "index") else device), _VPOOL_DEPTH[0], tuple(shape))
+    di = int(device.index if hasattr(device, "index") else device)
+    key = (di, _VPOOL_DEPTH[0], tuple(shape), torch.cuda.current_stream(di).cuda_stream)
     buf = _PINNED.get(key)
     if buf is None:
         buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
@@ -302,7 +305,24 @@ def _pinned_snapshots(shape, device):
 
 
 _VPOOL = {}
-_VPOOL_DEPTH = [0]  # nesting level of running solves (an operator may itself run a solve)
+
+
+class _Depth(threading.local):
+    """Nesting level of running solves (an operator may itself run a solve),
+    per thread: concurrent per-layer solves (apply_Lp_power_dev) each count
+    their own; the pools below are keyed by it and by the current stream."""
+
+    def __init__(self):
+        self.v = 0
+
+    def __getitem__(self, i):
+        return self.v
+
+    def __setitem__(self, i, x):
+        self.v = x
+
+
+_VPOOL_DEPTH = _Depth()
 
 
 def _krylov_basis(device, slot, dim, n):
@@ -311,7 +331,8 @@ def _krylov_basis(device, slot, dim, n):
     previous solve's basis (stream order); allocating ~100 MB per solve made
     the caching allocator release and re-allocate (device syncs)."""
     torch = _torch()
-    key = (int(device.index if hasattr(device, "index") else device), _VPOOL_DEPTH[0], slot)
+    di = int(device.index if hasattr(device, "index") else device)
+    key = (di, _VPOOL_DEPTH[0], slot, torch.cuda.current_stream(di).cuda_stream)
     buf = _VPOOL.get(key)
     if buf is None or buf.numel() < dim * n:
         _VPOOL[key] = buf = torch.empty(dim * n, dtype=torch.float64, device=device)

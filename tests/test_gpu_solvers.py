@@ -169,6 +169,20 @@ def test_power_mean_eigs_match_golden():
     again = power_mean_eigs(G, PowerMeanConfig(p=-1.0), k=5, seed=0)
     assert np.array_equal(again.values, basis.values)
     assert np.array_equal(again.vectors, basis.vectors)
+    # the per-layer solves of large layers, one after the other and run
+    # concurrently (a stream and a host thread each): bitwise the same
+    from paper_2007_05239_b200 import powermean as pm
+    saved = pm._SEQ_GRAPHS, pm._CONCURRENT
+    try:
+        got = {}
+        for conc in (False, True):
+            pm._SEQ_GRAPHS, pm._CONCURRENT = False, conc
+            got[conc] = power_mean_eigs(G, PowerMeanConfig(p=-1.0), k=5, seed=0)
+    finally:
+        pm._SEQ_GRAPHS, pm._CONCURRENT = saved
+    assert np.array_equal(got[True].values, got[False].values)
+    assert np.array_equal(got[True].vectors, got[False].vectors)
+    assert_allclose(got[True].values, g["eig_m1_values"], rtol=1e-7)
 
 
 def test_allen_cahn_matches_golden():
