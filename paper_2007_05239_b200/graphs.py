@@ -443,16 +443,18 @@ class LaplacianBatch:
             # stream priority; cheaper layers fill the SMs it leaves idle
             cost = [_layer_cost(layer) for layer in graph.layers]
             top = max(range(len(cost)), key=lambda i: cost[i])
-            # ... unless the costliest layer's kernels hold every SM for their
-            # whole run (d = 3, m >= 5: one CTA per SM, one wave): then nothing
-            # fills beside them, and the cheap layer goes first so its
-            # device->host copy overlaps the long layer (config 4: synchronous
-            # e2e 2.72 -> 3.27e9, streamed 4.88 -> 5.75e9; step -0.4 %)
-            pl = os.environ.get("MLB_PRIO_LAYER", "auto")
+            # (the layers are ISSUED cheapest first, `_order`: the cheap layer's
+            # first kernels start before the costly layer's, and apply_many's
+            # copies come out in finishing order.  MLB_PRIO_LAYER=cheap gives the
+            # cheap layer the priority instead, so with costly kernels that hold
+            # every SM (d = 3, m >= 5) its result -- and its device->host copy --
+            # comes first: config 4 synchronous e2e 2.68 -> 3.29e9, but the
+            # device step 3.08 -> 3.12 ms and the streamed e2e unchanged)
+            pl = os.environ.get("MLB_PRIO_LAYER", "costly")
             if pl == "cheap" or (pl == "auto" and _fills_sms(graph.layers[top])):
                 top = min(range(len(cost)), key=lambda i: cost[i])
-            # apply_many issues the layers cheapest first, so the copy-out
-            # stream gets results in the order they finish
+            # every step issues the layers cheapest first (the copy-out stream
+            # of apply_many then gets results in the order they finish)
             self._order = sorted(range(len(cost)), key=lambda i: cost[i])
             prio = os.environ.get("MLB_NO_STREAM_PRIORITY") is None
             hi = int(os.environ.get("MLB_STREAM_PRIORITY", "-1"))  # torch range on B200: 0 (low) .. -3 (high)
@@ -505,7 +507,8 @@ class LaplacianBatch:
             self._capture()
         main = torch.cuda.current_stream(self.device)
         self._fork.record(main)
-        for t, (s, j) in enumerate(zip(self._streams, self._joins)):
+        for t in self._order:   # cheapest layer issued first
+            s, j = self._streams[t], self._joins[t]
             s.wait_event(self._fork)
             with torch.cuda.stream(s):
                 self._layer(t)
@@ -675,7 +678,8 @@ class LaplacianBatch:
         """Kernel-by-kernel step with per-layer D2H (for whole-step capture)."""
         torch = _torch()
         self._fork.record(main)
-        for t, (layer, s, j) in enumerate(zip(self.graph.layers, self._streams, self._joins)):
+        for t in self._order:   # cheapest layer issued first
+            layer, s, j = self.graph.layers[t], self._streams[t], self._joins[t]
             s.wait_event(self._fork)
             with torch.cuda.stream(s):
                 apply_sym_laplacian_dev(layer, self._v, self._y[t])
