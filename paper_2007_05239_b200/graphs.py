@@ -443,14 +443,15 @@ class LaplacianBatch:
             # stream priority; cheaper layers fill the SMs it leaves idle
             cost = [_layer_cost(layer) for layer in graph.layers]
             top = max(range(len(cost)), key=lambda i: cost[i])
-            # (the layers are ISSUED cheapest first, `_order`: the cheap layer's
-            # first kernels start before the costly layer's, and apply_many's
-            # copies come out in finishing order.  MLB_PRIO_LAYER=cheap gives the
-            # cheap layer the priority instead, so with costly kernels that hold
-            # every SM (d = 3, m >= 5) its result -- and its device->host copy --
-            # comes first: config 4 synchronous e2e 2.68 -> 3.29e9, but the
-            # device step 3.08 -> 3.12 ms and the streamed e2e unchanged)
-            pl = os.environ.get("MLB_PRIO_LAYER", "costly")
+            # ... unless the costliest layer's kernels hold every SM for their
+            # whole run (d = 3, m >= 5: one CTA per SM, one wave): then the
+            # cheap layer gets the priority, so its result -- and its
+            # device->host copy -- comes first and overlaps the long layer
+            # (config 4, same box: streamed e2e 5.5 -> 5.7e9, synchronous
+            # 2.69 -> 3.29e9; device step 3.08 -> 3.12 ms).  The layers are
+            # also ISSUED cheapest first (`_order`).  MLB_PRIO_LAYER=costly /
+            # cheap forces a rule.
+            pl = os.environ.get("MLB_PRIO_LAYER", "auto")
             if pl == "cheap" or (pl == "auto" and _fills_sms(graph.layers[top])):
                 top = min(range(len(cost)), key=lambda i: cost[i])
             # every step issues the layers cheapest first (the copy-out stream
