@@ -172,14 +172,14 @@ def test_power_mean_eigs_match_golden():
     # the per-layer solves of large layers, one after the other and run
     # concurrently (a stream and a host thread each): bitwise the same
     from paper_2007_05239_b200 import powermean as pm
-    saved = pm._SEQ_GRAPHS, pm._CONCURRENT
+    saved = pm._SEQ_GRAPHS, pm._CONCURRENT, pm._CONC_MIN_N
     try:
         got = {}
         for conc in (False, True):
-            pm._SEQ_GRAPHS, pm._CONCURRENT = False, conc
+            pm._SEQ_GRAPHS, pm._CONCURRENT, pm._CONC_MIN_N = False, conc, 0
             got[conc] = power_mean_eigs(G, PowerMeanConfig(p=-1.0), k=5, seed=0)
     finally:
-        pm._SEQ_GRAPHS, pm._CONCURRENT = saved
+        pm._SEQ_GRAPHS, pm._CONCURRENT, pm._CONC_MIN_N = saved
     assert np.array_equal(got[True].values, got[False].values)
     assert np.array_equal(got[True].vectors, got[False].vectors)
     assert_allclose(got[True].values, g["eig_m1_values"], rtol=1e-7)
