@@ -15,11 +15,14 @@
 // lattices (node-range shard cuts, stray points) run as "diagonal" items:
 // the same two contractions with one row per point (Wf per row).
 //
-// Work items (bind time, mlb_core.cu): <= kLatRows rows of one cell, one CTA
-// each.  The spread writes one S x S block per item; lat_reduce_kernel sums,
-// per grid cell, the blocks covering it in (bin, item) order -- no atomics,
-// bitwise reproducible.  The gather fuses the L_sym epilogue like
-// gather_kernel (y = alpha v + s (beta acc + gamma s v)).
+// Work items (bind time, build_lattice below; lat_detect_kernel checks the
+// structure and splits a cell cut by a node range into partial run +
+// lattice + partial run): <= kLatRowsMax rows / kLatPts points of one cell
+// segment, one CTA each.  The spread forms both contractions on the fp64
+// tensor cores (mma.sync m8n8k4) and writes one S x S block per item;
+// lat_reduce_kernel sums, per grid cell, the blocks covering it in (bin,
+// item) order -- no atomics, bitwise reproducible.  The gather fuses the
+// L_sym epilogue like gather_kernel (y = alpha v + s (beta acc + gamma s v)).
 #include <cuda_runtime.h>
 
 #include <algorithm>
