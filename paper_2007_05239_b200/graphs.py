@@ -442,32 +442,40 @@ class LaplacianBatch:
             # the costliest layer (the step's critical path) gets the highest
             # stream priority; cheaper layers fill the SMs it leaves idle
             cost = [_layer_cost(layer) for layer in graph.layers]
-            top = max(range(len(cost)), key=lambda i: cost[i])
-            # ... unless the costliest layer's kernels hold every SM for their
-            # whole run (d = 3, m >= 5: one CTA per SM, one wave): then the
-            # cheap layer gets the priority, so its result -- and its
+            # Stream priorities.  Results that stay on the device (`_run()`,
+            # `apply_dev`): the costliest layer -- the step's critical path -- first
+            # in line for free SMs.  Results copied to the host (`apply` with host
+            # buffers, `apply_many`): when the costliest layer's kernels hold every
+            # SM for their whole run (d = 3, m >= 5: one CTA per SM, one wave) the
+            # CHEAP layer gets the priority instead, so its result -- and its
             # device->host copy -- comes first and overlaps the long layer
-            # (config 4, same box: streamed e2e 5.5 -> 5.7e9, synchronous
-            # 2.69 -> 3.29e9; device step 3.08 -> 3.12 ms).  The layers are
-            # also ISSUED cheapest first (`_order`).  MLB_PRIO_LAYER=costly /
-            # cheap forces a rule.
+            # (config 4, same box: device step 3.08 ms with the costly priority vs
+            # 3.12; streamed e2e 5.5 -> 5.7e9, synchronous 2.69 -> 3.29e9 with the
+            # cheap one).  Every step issues the layers cheapest first (`_order`;
+            # apply_many's copy-out stream then gets results in finishing order).
+            # MLB_PRIO_LAYER=costly / cheap forces one rule for both.
+            costly = max(range(len(cost)), key=lambda i: cost[i])
+            cheap = min(range(len(cost)), key=lambda i: cost[i])
             pl = os.environ.get("MLB_PRIO_LAYER", "auto")
-            if pl == "cheap" or (pl == "auto" and _fills_sms(graph.layers[top])):
-                top = min(range(len(cost)), key=lambda i: cost[i])
-            # every step issues the layers cheapest first (the copy-out stream
-            # of apply_many then gets results in the order they finish)
+            top_dev = cheap if pl == "cheap" else costly
+            top_host = cheap if (pl == "cheap" or (pl == "auto" and _fills_sms(graph.layers[costly]))) else costly
             self._order = sorted(range(len(cost)), key=lambda i: cost[i])
             prio = os.environ.get("MLB_NO_STREAM_PRIORITY") is None
             hi = int(os.environ.get("MLB_STREAM_PRIORITY", "-1"))  # torch range on B200: 0 (low) .. -3 (high)
-            # one stream per weights object: a binding's scratch grids must not be shared
-            # by concurrent layers (a graph may hold the same weights twice)
-            by_w = {}
-            self._streams = []
-            for i, layer in enumerate(graph.layers):
-                key = id(layer.weights)
-                if key not in by_w:
-                    by_w[key] = torch.cuda.Stream(device=dev, priority=(hi if (prio and i == top) else 0))
-                self._streams.append(by_w[key])
+
+            def stream_set(top):
+                # one stream per weights object: a binding's scratch grids must not be
+                # shared by concurrent layers (a graph may hold the same weights twice)
+                by_w, out = {}, []
+                for i, layer in enumerate(graph.layers):
+                    key = id(layer.weights)
+                    if key not in by_w:
+                        by_w[key] = torch.cuda.Stream(device=dev, priority=(hi if (prio and i == top) else 0))
+                    out.append(by_w[key])
+                return out
+
+            self._streams = stream_set(top_host)
+            self._streams_dev = self._streams if top_dev == top_host else stream_set(top_dev)
             self._fork = torch.cuda.Event()
             self._joins = [torch.cuda.Event() for _ in graph.layers]
         self._pin_in = None
@@ -482,20 +490,26 @@ class LaplacianBatch:
         for t, layer in enumerate(self.graph.layers):  # warm-up: kernel attributes, D^-1/2
             apply_sym_laplacian_dev(layer, self._v, self._y[t])
         torch.cuda.synchronize(self.device)
-        graphs, counts = [], []
-        for t, layer in enumerate(self.graph.layers):
-            l0 = _lib.lib().mlb_launch_count()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self._streams[t]):
-                apply_sym_laplacian_dev(layer, self._v, self._y[t])
-            counts.append(int(_lib.lib().mlb_launch_count() - l0))
-            graphs.append(g)
-        torch.cuda.synchronize(self.device)
-        self._graphs, self._graph_launches = graphs, counts
+        def capture(streams):
+            graphs, counts = [], []
+            for t, layer in enumerate(self.graph.layers):
+                l0 = _lib.lib().mlb_launch_count()
+                g = torch.cuda.CUDAGraph()
+                # (a captured kernel keeps the priority of its capture stream)
+                with torch.cuda.graph(g, stream=streams[t]):
+                    apply_sym_laplacian_dev(layer, self._v, self._y[t])
+                counts.append(int(_lib.lib().mlb_launch_count() - l0))
+                graphs.append(g)
+            return graphs, counts
 
-    def _layer(self, t):
+        self._graphs, self._graph_launches = capture(self._streams)
+        self._graphs_dev = (self._graphs if self._streams_dev is self._streams
+                            else capture(self._streams_dev)[0])
+        torch.cuda.synchronize(self.device)
+
+    def _layer(self, t, dev=False):
         if self._use_graph:
-            self._graphs[t].replay()
+            (self._graphs_dev if dev else self._graphs)[t].replay()
             _lib.lib().mlb_note_launches(self._graph_launches[t])
         else:
             apply_sym_laplacian_dev(self.graph.layers[t], self._v, self._y[t])
@@ -508,11 +522,12 @@ class LaplacianBatch:
             self._capture()
         main = torch.cuda.current_stream(self.device)
         self._fork.record(main)
+        streams = self._streams if out is not None else self._streams_dev
         for t in self._order:   # cheapest layer issued first
-            s, j = self._streams[t], self._joins[t]
+            s, j = streams[t], self._joins[t]
             s.wait_event(self._fork)
             with torch.cuda.stream(s):
-                self._layer(t)
+                self._layer(t, dev=out is None)
                 if out is not None:
                     out[t].copy_(self._y[t], non_blocking=True)
             j.record(s)
