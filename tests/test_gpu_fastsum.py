@@ -570,7 +570,7 @@ def _lattice_points(W, H, lo=-0.2, hi=0.2, transpose=False):
 
 
 @pytest.mark.parametrize("layout,m", [("image", 5), ("image_t", 4), ("mixed", 5), ("image", 3), ("cut", 6),
-                                      ("cut_t", 5)])
+                                      ("cut_t", 5), ("image", 2)])
 def test_lattice_d2_kernels_match_oracle(layout, m):
     """The d = 2 lattice kernels (cells whose points form R x C product sets:
     spread = Ws^T (SV Wf), gather = (Ws G) Wf^T; non-lattice cells as

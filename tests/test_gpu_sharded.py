@@ -82,17 +82,25 @@ def test_sharded_graph_nccl_world1_equals_unsharded():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_graph_emulated_ranks_match_oracle(world):
+@pytest.mark.parametrize("world,lattice", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_graph_emulated_ranks_match_oracle(world, lattice):
+    """(lattice: the xy layer on the d = 2 lattice items, forced at this size;
+    the rank boundaries cut image rows -> partial-run segments)"""
     import torch
 
     from paper_2007_05239_b200.dist import ShardedKernelGraph, shard_feature_groups
     wl = _small_cfg4(side=80)
     delta = math.log(2.0)
     ranks = []
-    for r in range(world):
-        lo, hi, pts, kerns, plans = shard_feature_groups(wl.X, _groups(wl), r, world)
-        ranks.append(ShardedKernelGraph(pts, kerns, plans, wl.n, lo, hi, comm=None, shift=delta, device=0))
+    os.environ["MLB_LATTICE"] = "1" if lattice else "0"
+    try:
+        for r in range(world):
+            lo, hi, pts, kerns, plans = shard_feature_groups(wl.X, _groups(wl), r, world)
+            ranks.append(ShardedKernelGraph(pts, kerns, plans, wl.n, lo, hi, comm=None, shift=delta, device=0))
+    finally:
+        del os.environ["MLB_LATTICE"]
+    for sg in ranks:   # the d = 2 (xy) layer runs on lattice items exactly when forced
+        assert [w._bindings[0].stats()["lattice_items"] > 0 for w in sg.weights] == [False, lattice]
     T = len(wl.layers)
 
     def emulated_step(vs, coef_of, flags):
